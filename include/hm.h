@@ -1,0 +1,208 @@
+/*
+ * hm.h — C-ABI of the B200-native static FKS hash map (libhm.so).
+ *
+ * Method: "Towards Efficient Hash Maps in Functional Array Languages"
+ * (arXiv 2508.11443).  Citations are PAPER.md line numbers (the LaTeX source)
+ * with the section they fall in; R<k> are the readings of the paper listed in
+ * DESIGN.md §2.
+ *
+ * The library builds the two-level FKS hash set of §2.2 —
+ *   g k = (hash const k) mod n,  shape = hist of g (squared: s_b^2 slots),
+ *   offsets = presum shape,      h k = offsets[g k] + (hash consts[g k] k mod s_b^2)
+ * — extended to a hash map by an accompanying value per slot,
+ * and answers batched lookups (PAPER.md:244-245 membership test, §3.2 lookup).
+ *
+ * Conventions for every entry point:
+ *  - All pointers are DEVICE pointers of the map's device unless stated
+ *    otherwise.  The build and lookup entry points also accept HOST pointers
+ *    (pageable or pinned) for their array arguments; they are detected with
+ *    cudaPointerGetAttributes and staged through device memory inside the call
+ *    (this is the end-to-end path bench.py times).  Mixing host and device
+ *    arrays in one call is allowed.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = the legacy default
+ *    stream).  Kernels run on that stream only.
+ *  - Sizes are element counts unless named *_bytes.
+ *  - No entry point ever falls back to a CPU implementation.  Errors are
+ *    returned as hm_status; a human-readable detail for the last failure on the
+ *    calling thread is available from hm_last_error().
+ *  - Every result is a deterministic function of (seed, key set[, context
+ *    order for byte keys]); internal parallel order never changes it (R13).
+ */
+#ifndef HM_H_
+#define HM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HM_SPEC_VERSION 1u
+#define HM_MAGIC 0x31544D48u /* "HMT1" little-endian */
+
+typedef enum {
+  HM_OK = 0,
+  HM_ERR_INVALID_ARG = 1,    /* NULL where required, bad offsets, both outputs NULL ... */
+  HM_ERR_EMPTY = 2,          /* n == 0: K is a non-empty set (§2.2)        */
+  HM_ERR_DUPLICATE_KEY = 3,  /* from_array_nodup precondition violated  */
+  HM_ERR_SEED_EXHAUSTED = 4, /* level one: t1 reached 16 (R7); or a bucket reached t = 256 (R8) */
+  HM_ERR_FP_EXHAUSTED = 5,   /* byte keys: fingerprint redraw t0 reached 16 (R5)          */
+  HM_ERR_TOO_LARGE = 6,      /* n > 2^30, or a byte key longer than 65535 bytes (R23)     */
+  HM_ERR_OOM = 7,            /* device allocation failed                                   */
+  HM_ERR_CUDA = 8,           /* a CUDA runtime error (detail in hm_last_error)             */
+  HM_ERR_NCCL = 9,           /* reserved for the fused multi-GPU path                     */
+  HM_ERR_NO_DEVICE = 10      /* no CUDA device / wrong architecture                       */
+} hm_status;
+
+typedef struct hm_map hm_map; /* opaque; immutable after build; bound to its device */
+
+/* Build options.  NULL means all defaults. */
+typedef struct {
+  uint64_t seed;       /* table seed: selects the constant schedule (R6). default 0  */
+  uint32_t log2_bp;    /* 0 = auto. log2 of the level-1 buckets per build partition   */
+  uint32_t flags;      /* reserved, must be 0                                         */
+} hm_opts;
+
+/* Table header, 56 bytes, little-endian (DESIGN.md §4 "Table layout"). */
+typedef struct {
+  uint32_t magic;        /* HM_MAGIC                                   */
+  uint32_t spec_version; /* HM_SPEC_VERSION                            */
+  uint32_t key_kind;     /* 0 = u64 keys, 1 = byte-string keys         */
+  uint32_t reserved;     /* 0                                          */
+  uint64_t n;            /* number of keys = number of level-1 buckets (R3) */
+  uint64_t S;            /* total slots = sum over buckets of s_b^2    */
+  uint64_t seed;         /* table seed                                 */
+  uint32_t t1;           /* level-1 attempt (first with S <= 4n, R7)   */
+  uint32_t t0;           /* byte keys: fingerprint attempt (R5); 0 for u64 */
+  uint64_t ctx_bytes;    /* byte keys: size of the map's context copy  */
+} hm_header;
+
+/* ------------------------------------------------------------------ build
+ * hm_build_u64 — from_array_nodup for 64-bit integer keys (PAPER.md:608-609,
+ * 623-624; construction §2.2-§2.5).
+ *   keys[n], vals[n]: the key/value pairs (u64 each).  Keys must be pairwise
+ *                     distinct; violations are detected and reported as
+ *                     HM_ERR_DUPLICATE_KEY (never a hang, never a wrong table).
+ *   opts:   NULL or build options.
+ *   stream: the stream all work is ordered on.
+ *   out:    receives the new map (NULL on failure).
+ * Synchronous: the call waits on `stream` once at the end to learn the total
+ * slot count and the device-detected error flags; inputs may be freed when it
+ * returns.  The map owns its directory u64[n] and its slot array {key,value}[S]
+ * (16 B per slot), allocated with cudaMallocAsync on `stream`.
+ * Errors: HM_ERR_EMPTY (n==0), HM_ERR_TOO_LARGE (n>2^30), HM_ERR_INVALID_ARG
+ * (NULL keys/vals/out), HM_ERR_DUPLICATE_KEY, HM_ERR_SEED_EXHAUSTED,
+ * HM_ERR_OOM, HM_ERR_CUDA.  Precedence (R26): level-1 exhaustion,
+ * then duplicates, then level-2 exhaustion. */
+hm_status hm_build_u64(const uint64_t* keys, const uint64_t* vals, uint64_t n,
+                       const hm_opts* opts, void* stream, hm_map** out);
+
+/* hm_build_bytes — from_array_nodup for byte-string keys (slices of a flat
+ * context, §3.1; slice keys PAPER.md:726-746).
+ *   bytes:   the flat context; key i is bytes[offsets[i] .. offsets[i+1]).
+ *   offsets: u64[n+1], CSR, non-decreasing; offsets[0] need not be 0.
+ *   vals:    u64[n].
+ * The map stores a COPY of bytes[offsets[0] .. offsets[n])
+ * and 32-byte slots {u64 fp, u64 value, u64 ctx_off, u32 len, u32 0}[S], with
+ * ctx_off relative to offsets[0].  Keys are hashed through a 61-bit polynomial
+ * fingerprint (R5); two different keys with equal fingerprints trigger a
+ * redraw of the fingerprint point (t0), equal keys are DUPLICATE_KEY.
+ * Errors: as hm_build_u64, plus HM_ERR_TOO_LARGE for a key longer than 65535
+ * bytes and HM_ERR_FP_EXHAUSTED.  Synchronous like hm_build_u64. */
+hm_status hm_build_bytes(const uint8_t* bytes, const uint64_t* offsets, const uint64_t* vals,
+                         uint64_t n, const hm_opts* opts, void* stream, hm_map** out);
+
+/* ----------------------------------------------------------------- lookup
+ * hm_lookup_u64 — batched lookup: for each query
+ * q[i], b = g q; probe the directory dir[b]; an empty bucket misses (R9);
+ * j = soff_b + (hash consts_b q mod s_b^2) (singletons: j = soff_b, R12);
+ * hit iff slot[j].key == q.
+ *   out_vals[nq]:  value on a hit, 0 on a miss (R24).  May be NULL
+ *                  (membership only).
+ *   out_found[nq]: 1 on a hit, 0 on a miss.  May be NULL.  Not both NULL.
+ * Asynchronous and stream-ordered when all arrays are device memory; when any
+ * array is host memory the call stages it and returns after the results are
+ * on the host.  A map may serve concurrent lookups from several streams.
+ * Errors: HM_ERR_INVALID_ARG (NULL map/q with nq>0, both outputs NULL, wrong
+ * key kind), HM_ERR_CUDA. */
+hm_status hm_lookup_u64(const hm_map* map, const uint64_t* q, uint64_t nq, uint64_t* out_vals,
+                        uint8_t* out_found, void* stream);
+
+/* hm_lookup_bytes — batched lookup of byte-string needles given in their OWN
+ * context: needle i is
+ * qbytes[qoffsets[i] .. qoffsets[i+1]).  A hit requires equal fingerprint,
+ * equal length and equal bytes against the map's context copy.  Outputs and
+ * errors as hm_lookup_u64. */
+hm_status hm_lookup_bytes(const hm_map* map, const uint8_t* qbytes, const uint64_t* qoffsets,
+                          uint64_t nq, uint64_t* out_vals, uint8_t* out_found, void* stream);
+
+/* ---------------------------------------------------------------- lifetime */
+void hm_free(hm_map* map); /* NULL-safe; waits for the map's pending work */
+
+/* Header of the (logical) table.  host_out: host pointer. */
+hm_status hm_info(const hm_map* map, hm_header* host_out);
+
+/* hm_export — copy the table to HOST memory for parity checks:
+ *   host_dir:   u64[n]  entry b = soff_b | s_b<<40 | t_b<<56 (may be NULL)
+ *   host_slots: S slots of 16 B (u64 keys) or 32 B (byte keys) (may be NULL)
+ *   host_ctx:   ctx_bytes bytes of the map's context copy (byte keys; may be NULL)
+ * For a shard (hm_build_u64_shard) the directory covers the shard's bucket
+ * range and soff is GLOBAL (the shard's slot base is added). Synchronous. */
+hm_status hm_export(const hm_map* map, uint64_t* host_dir, void* host_slots, uint8_t* host_ctx);
+
+const char* hm_status_str(hm_status s);
+const char* hm_last_error(void); /* thread-local; "" if none */
+const char* hm_version(void);
+
+/* ------------------------------------------------- multi-GPU building blocks
+ * Bucket-range sharding: with G ranks and the
+ * global key count n (= number of level-1 buckets), rank r owns buckets
+ * [lo_r, lo_{r+1}) with lo_r = ceil(r*n/G), i.e. owner(b) = floor(b*G/n).
+ * The exchange between the two steps is done by the caller (NCCL all-to-all
+ * through torch.distributed); these entry points are the kernels on each side. */
+
+/* hm_route_u64 — level-1 hash each (key, value) with the level-1 constants of
+ * attempt t1 and partition the pairs by owner rank (stable within a rank is
+ * NOT guaranteed).
+ *   keys/vals[n_local]: this rank's input pairs.
+ *   n_global: the global n (the level-1 modulus).
+ *   send_keys/send_vals[n_local]: output, grouped by destination rank.
+ *   send_counts[world]: output (device, u64): pairs destined to each rank.
+ * Asynchronous. */
+hm_status hm_route_u64(const uint64_t* keys, const uint64_t* vals, uint64_t n_local,
+                       uint64_t n_global, uint64_t seed, uint32_t t1, int world,
+                       uint64_t* send_keys, uint64_t* send_vals, uint64_t* send_counts,
+                       void* stream);
+
+/* hm_build_u64_shard — build the shard of the global table that holds level-1
+ * buckets [b_lo, b_hi) of a table with n_global keys, from exactly the keys
+ * routed to it, with level-1 attempt t1 fixed by the caller.  The caller
+ * checks the global space bound sum_r S_r <= 4 n_global (R7) and redraws t1
+ * if it fails.  On return *S_local holds the shard's slot count.  The shard's
+ * global slot base (exclusive prefix of S_r over ranks) is set with
+ * hm_shard_set_base.  Errors as hm_build_u64 (duplicates within the shard are
+ * reported; SEED_EXHAUSTED only for level-2 exhaustion). Synchronous. */
+hm_status hm_build_u64_shard(const uint64_t* keys, const uint64_t* vals, uint64_t n_recv,
+                             uint64_t n_global, uint64_t b_lo, uint64_t b_hi, uint32_t t1,
+                             const hm_opts* opts, void* stream, hm_map** out, uint64_t* S_local);
+
+hm_status hm_shard_set_base(hm_map* map, uint64_t slot_base);
+
+/* hm_route_queries_u64 — partition queries by owner rank of their level-1
+ * bucket. send_q[nq] grouped by rank, perm[nq] (u64): position in send_q of
+ * query i, send_counts[world] (u64, device). Asynchronous. */
+hm_status hm_route_queries_u64(const hm_map* map, const uint64_t* q, uint64_t nq, int world,
+                               uint64_t* send_q, uint64_t* perm, uint64_t* send_counts,
+                               void* stream);
+
+/* hm_unroute_u64 — out_vals[i] = vals_routed[perm[i]], out_found likewise
+ * (either output may be NULL). Asynchronous. */
+hm_status hm_unroute_u64(const uint64_t* vals_routed, const uint8_t* found_routed,
+                         const uint64_t* perm, uint64_t nq, uint64_t* out_vals,
+                         uint8_t* out_found, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HM_H_ */

@@ -1,0 +1,786 @@
+// build.cu — FKS construction on sm_100a (§2.2-§2.5, 220-499).
+//
+// The paper's flattened construction runs make2 for all buckets in bulk rounds
+// (segrandom / seghashes / segcollisions / segresult).  This
+// is the B200 design of DESIGN.md §6 instead — two kernels per level-1 attempt:
+//
+//   K_A  k_partition : stream (key, value), hash every key to its level-1
+//        bucket g k = hash(c1, k) mod n and append it to the
+//        build partition that owns a contiguous range of 2^log2_bp buckets.
+//        A per-CTA shared-memory histogram ranks the tile's keys per partition
+//        so that only one global atomic per (tile, partition) reserves space.
+//   K_B  k_bucket    : one CTA per partition, everything else in shared memory:
+//        hist of the partition's buckets, exclusive scans of s
+//        and s^2 (presum, PAPER.md:229-230 with R1/R2), groupby
+//        as a counting scatter of (key, index) into bucket order, the level-2
+//        seed search make2 per bucket — thread-per-bucket
+//        with a register occupancy bitmap for s <= 16, warp-per-bucket with
+//        __match_any_sync for 16 < s <= 32 — then a decoupled look-back across
+//        partitions for the global slot base, and the coalesced write of the
+//        directory and of the s^2 slots of every bucket (members + filler, R10).
+//
+// One host synchronisation per attempt reads the device status (total S for
+// the space bound R7, duplicate / exhaustion flags).
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "hm_internal.cuh"
+
+namespace hm {
+
+constexpr int kAThreads = 512;
+constexpr int kBThreads = 512;
+constexpr int kBWarps = kBThreads / 32;
+constexpr int kMaxBig = 64;  // buckets with 16 < s <= 32 per partition (expected ~1e-12)
+constexpr unsigned long long kFlagAgg = 1ull << 62, kFlagInc = 2ull << 62, kValMask = (1ull << 62) - 1;
+
+// ----------------------------------------------------------------- sources
+struct SrcU64 {
+  const uint64_t* keys;
+  const uint64_t* vals;
+  __device__ __forceinline__ KV16 load(uint64_t i) const {
+    KV16 e;
+    e.key = __ldg(keys + i);
+    e.value = __ldg(vals + i);
+    return e;
+  }
+};
+struct SrcBytes {
+  const uint64_t* fp;
+  const uint64_t* vals;
+  const uint64_t* offs;
+  uint64_t off0;
+  __device__ __forceinline__ KV32 load(uint64_t i) const {
+    KV32 e;
+    const uint64_t o = __ldg(offs + i), o1 = __ldg(offs + i + 1);
+    e.key = __ldg(fp + i);
+    e.value = __ldg(vals + i);
+    e.ctx_off = o - off0;
+    e.len = uint32_t(o1 - o);
+    e.reserved = 0;
+    return e;
+  }
+};
+// Equal hashed keys: the same key (duplicate) or a fingerprint collision?
+struct SameU64 {
+  __device__ __forceinline__ bool same(const KV16&, const KV16&) const { return true; }
+};
+struct SameBytes {
+  const uint8_t* bytes;  // original context, element ctx_off is relative to off0
+  uint64_t off0;
+  __device__ bool same(const KV32& a, const KV32& b) const {
+    if (a.len != b.len) return false;
+    const uint8_t* pa = bytes + off0 + a.ctx_off;
+    const uint8_t* pb = bytes + off0 + b.ctx_off;
+    for (uint32_t i = 0; i < a.len; i++)
+      if (pa[i] != pb[i]) return false;
+    return true;
+  }
+};
+
+// ------------------------------------------------------------- primitives
+__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Block-wide exclusive scan of u64 (kBThreads threads); also returns the total.
+__device__ __forceinline__ unsigned long long block_excl_scan(unsigned long long v, unsigned long long* total,
+                                                              unsigned long long* s_red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned long long x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_red[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    unsigned long long w = lane < kBWarps ? s_red[lane] : 0ull;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      unsigned long long y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < kBWarps) s_red[lane] = w;
+  }
+  __syncthreads();
+  const unsigned long long before = warp ? s_red[warp - 1] : 0ull;
+  *total = s_red[kBWarps - 1];
+  __syncthreads();
+  return before + x - v;
+}
+
+__device__ __forceinline__ uint32_t cur_get(const uint32_t* scur, uint32_t lb) {
+  const uint32_t w = scur[lb >> 1];
+  return (lb & 1) ? (w >> 16) : (w & 0xFFFFu);
+}
+
+// 256-bit occupancy bitmap in four registers (s^2 <= 256).
+struct Bits256 {
+  uint64_t w0, w1, w2, w3;
+  __device__ __forceinline__ void clear() { w0 = w1 = w2 = w3 = 0; }
+  __device__ __forceinline__ bool test_set(uint32_t h) {
+    const uint64_t bit = 1ull << (h & 63);
+    const uint32_t k = h >> 6;
+    const uint64_t w = k == 0 ? w0 : k == 1 ? w1 : k == 2 ? w2 : w3;
+    const bool was = (w & bit) != 0;
+    if (k == 0) w0 |= bit;
+    else if (k == 1) w1 |= bit;
+    else if (k == 2) w2 |= bit;
+    else w3 |= bit;
+    return was;
+  }
+  __device__ __forceinline__ bool test(uint32_t h) const {
+    const uint32_t k = h >> 6;
+    const uint64_t w = k == 0 ? w0 : k == 1 ? w1 : k == 2 ? w2 : w3;
+    return (w >> (h & 63)) & 1;
+  }
+};
+
+// make2 for 2 <= s <= 16: first attempt t whose level-2
+// hashes mod s^2 are pairwise distinct (`collision`, as a
+// register bitmap).  Returns kT2Cap when exhausted (R8).
+__device__ uint32_t search_small(uint64_t smix, uint64_t b, const uint64_t* keys, uint32_t s, uint64_t m2) {
+  const FastMod fm{uint64_t(s) * s, m2};
+  for (uint32_t t = 0; t < kT2Cap; t++) {
+    const Consts c = derive(smix, 2, b, t);
+    Bits256 bm;
+    bm.clear();
+    bool ok = true;
+    for (uint32_t j = 0; j < s; j++) {
+      const uint32_t h = uint32_t(fastmod(hash64(c, keys[j]), fm));
+      if (bm.test_set(h)) {
+        ok = false;
+        break;
+      }
+    }
+    if (ok) return t;
+  }
+  return kT2Cap;
+}
+
+// ------------------------------------------------------------------ K_A
+template <class Src, class E, int KPT, bool kSmemHist>
+__global__ void __launch_bounds__(kAThreads) k_partition(Src src, BuildParams bp, E* __restrict__ pbuf,
+                                                         unsigned int* __restrict__ pcount,
+                                                         DevStatus* __restrict__ stt) {
+  extern __shared__ unsigned int s_hist[];
+  const uint32_t tid = threadIdx.x;
+  if (kSmemHist) {
+    for (uint32_t i = tid; i < bp.np; i += kAThreads) s_hist[i] = 0;
+    __syncthreads();
+  }
+  const uint64_t T = uint64_t(kAThreads) * KPT;
+  const uint64_t ntiles = (bp.n_in + T - 1) / T;
+  bool ovf = false, bad = false;
+  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    E e[KPT];
+    uint32_t pp[KPT], rk[KPT];
+    const uint64_t base = tile * T;
+#pragma unroll
+    for (int j = 0; j < KPT; j++) {
+      const uint64_t idx = base + uint64_t(j) * kAThreads + tid;
+      pp[j] = 0xFFFFFFFFu;
+      rk[j] = 0;
+      if (idx < bp.n_in) e[j] = src.load(idx);
+    }
+#pragma unroll
+    for (int j = 0; j < KPT; j++) {
+      const uint64_t idx = base + uint64_t(j) * kAThreads + tid;
+      if (idx < bp.n_in) {
+        const uint64_t lb = level1_bucket(bp.l1, e[j].key) - bp.b_lo;
+        if (lb >= bp.nb) {
+          bad = true;
+          continue;
+        }
+        pp[j] = uint32_t(lb >> bp.log2_bp);
+        rk[j] = kSmemHist ? atomicAdd(&s_hist[pp[j]], 1u) : atomicAdd(&pcount[pp[j]], 1u);
+      }
+    }
+    if (kSmemHist) {
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < KPT; j++)
+        if (pp[j] != 0xFFFFFFFFu && rk[j] == 0) s_hist[pp[j]] = atomicAdd(&pcount[pp[j]], s_hist[pp[j]]);
+      __syncthreads();
+    }
+#pragma unroll
+    for (int j = 0; j < KPT; j++) {
+      if (pp[j] == 0xFFFFFFFFu) continue;
+      const uint32_t pos = (kSmemHist ? s_hist[pp[j]] : 0u) + rk[j];
+      if (pos < bp.cap) pbuf[size_t(pp[j]) * bp.cap + pos] = e[j];
+      else ovf = true;
+    }
+    if (kSmemHist) {
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < KPT; j++)
+        if (pp[j] != 0xFFFFFFFFu && rk[j] == 0) s_hist[pp[j]] = 0;
+      __syncthreads();
+    }
+  }
+  if (ovf) atomicOr(&stt->part_overflow, 1u);
+  if (bad) atomicOr(&stt->pad, 1u);
+}
+
+// ------------------------------------------------------------------ K_B
+template <class E, class Same>
+__global__ void __launch_bounds__(kBThreads, 1)
+    k_bucket(BuildParams bp, const E* __restrict__ pbuf, const unsigned int* __restrict__ pcount,
+             unsigned long long* __restrict__ lbstate, uint64_t* __restrict__ dir, E* __restrict__ slots,
+             DevStatus* __restrict__ stt, Same same) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ uint64_t s_m2[33];
+  __shared__ uint32_t s_p, s_nbig;
+  __shared__ uint32_t s_big[kMaxBig];
+  __shared__ uint64_t s_bigsoff[kMaxBig];
+  __shared__ unsigned long long s_red[kBWarps];
+  __shared__ unsigned long long s_base;
+  __shared__ uint32_t s_bits[kBWarps][32];
+
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    s_p = atomicAdd(&stt->ticket, 1u);
+    s_nbig = 0;
+  }
+  if (tid < 33) s_m2[tid] = tid ? ~0ull / (uint64_t(tid) * tid) : 0ull;
+  __syncthreads();
+  const uint32_t p = s_p;
+  const uint32_t cap = bp.cap;
+  const uint32_t BP = 1u << bp.log2_bp;
+  const uint64_t lb0 = uint64_t(p) << bp.log2_bp;
+  const uint32_t nbp = uint32_t(bp.nb - lb0 < uint64_t(BP) ? bp.nb - lb0 : uint64_t(BP));
+  const uint32_t cnt_raw = pcount[p];
+  const bool ovf = cnt_raw > cap;
+  const uint32_t cnt = ovf ? 0u : cnt_raw;
+
+  uint64_t* skeys = reinterpret_cast<uint64_t*>(smem);
+  uint16_t* sidx = reinterpret_cast<uint16_t*>(smem + ((size_t(cap) * 8 + 15) & ~size_t(15)));
+  uint32_t* scur = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(sidx) + ((size_t(cap) * 2 + 15) & ~size_t(15)));
+  const uint32_t ncw = BP / 2 + 1;
+  uint8_t* s_t = reinterpret_cast<uint8_t*>(scur) + ((size_t(ncw) * 4 + 15) & ~size_t(15));
+
+  for (uint32_t w = tid; w < ncw; w += kBThreads) scur[w] = 0;
+  __syncthreads();
+  const E* part = pbuf + size_t(p) * cap;
+  const uint64_t bbase = bp.b_lo + lb0;  // global id of local bucket 0 of this partition
+
+  // pass 1 — hist n hashes (rep n 1) restricted to this partition
+  for (uint32_t i = tid; i < cnt; i += kBThreads) {
+    const uint64_t k = part[i].key;
+    const uint32_t lb = uint32_t(level1_bucket(bp.l1, k) - bbase);
+    atomicAdd(&scur[lb >> 1], 1u << ((lb & 1) * 16));
+  }
+  __syncthreads();
+
+  // exclusive scan of s (grouping offsets) and sum of s^2
+  const uint32_t CH = max(2u, BP / kBThreads);
+  const uint32_t c0 = tid * CH, c1 = min(c0 + CH, nbp);
+  uint32_t lcnt = 0, maxs = 0;
+  unsigned long long lsq = 0;
+  for (uint32_t j = c0; j < c1; j += 2) {
+    const uint32_t w = scur[j >> 1], a = w & 0xFFFFu, b2 = w >> 16;
+    lcnt += a + b2;
+    lsq += uint64_t(a) * a + uint64_t(b2) * b2;
+    maxs = max(maxs, max(a, b2));
+  }
+  unsigned long long tot_cnt, S_p;
+  const unsigned long long excl = block_excl_scan(lcnt, &tot_cnt, s_red);
+  (void)block_excl_scan(lsq, &S_p, s_red);
+  {
+    uint32_t run = uint32_t(excl);
+    for (uint32_t j = c0; j < c1; j += 2) {
+      const uint32_t w = scur[j >> 1], a = w & 0xFFFFu, b2 = w >> 16;
+      scur[j >> 1] = run | ((run + a) << 16);
+      run += a + b2;
+    }
+  }
+  if (uint64_t(maxs) * maxs > bp.bound4n) atomicOr(&stt->bound_fail, 1u);
+  // publish this partition's aggregate early (decoupled look-back)
+  if (tid == 0) st_release(&lbstate[p], (p == 0 ? kFlagInc : kFlagAgg) | (S_p & kValMask));
+  __syncthreads();
+
+  // pass 2 — groupby: counting scatter of (key, index) into bucket order
+  for (uint32_t i = tid; i < cnt; i += kBThreads) {
+    const uint64_t k = part[i].key;
+    const uint32_t lb = uint32_t(level1_bucket(bp.l1, k) - bbase);
+    const uint32_t sh = (lb & 1) * 16;
+    const uint32_t old = atomicAdd(&scur[lb >> 1], 1u << sh);
+    const uint32_t pos = (old >> sh) & 0xFFFFu;
+    skeys[pos] = k;
+    sidx[pos] = uint16_t(i);
+  }
+  __syncthreads();
+  // from here: end(lb) = cur_get(lb), start(lb) = end(lb-1)
+
+  // level-2 seed search, map make2 over the buckets
+  for (uint32_t lb = tid; lb < nbp; lb += kBThreads) {
+    const uint32_t st0 = lb ? cur_get(scur, lb - 1) : 0u, s = cur_get(scur, lb) - st0;
+    uint32_t t = 0;
+    if (s >= 2 && uint64_t(s) * s <= bp.bound4n) {
+      if (s <= 16) {
+        // equal keys never separate: record and skip (§8(c) step 3)
+        bool skip = false;
+        for (uint32_t i = 0; i < s && !skip; i++)
+          for (uint32_t j = i + 1; j < s; j++)
+            if (skeys[st0 + i] == skeys[st0 + j]) {
+              const bool d = same.same(part[sidx[st0 + i]], part[sidx[st0 + j]]);
+              atomicOr(d ? &stt->dup : &stt->fpcoll, 1u);
+              skip = true;
+              break;
+            }
+        if (!skip) {
+          t = search_small(bp.smix, bbase + lb, skeys + st0, s, s_m2[s]);
+          if (t >= kT2Cap) {
+            atomicOr(&stt->exhausted, 1u);
+            t = 0;
+          }
+        }
+      } else if (s <= 32) {
+        const uint32_t k = atomicAdd(&s_nbig, 1u);
+        if (k < kMaxBig) s_big[k] = lb;
+        else atomicOr(&stt->huge, 1u);
+      } else {
+        atomicOr(&stt->huge, 1u);
+      }
+    }
+    s_t[lb] = uint8_t(t);
+  }
+  __syncthreads();
+  const uint32_t nbig = min(s_nbig, uint32_t(kMaxBig));
+  // warp per bucket for 16 < s <= 32: lanes hold the members, match.any finds collisions
+  for (uint32_t bi = warp; bi < nbig; bi += kBWarps) {
+    const uint32_t lb = s_big[bi];
+    const uint32_t st0 = lb ? cur_get(scur, lb - 1) : 0u, s = cur_get(scur, lb) - st0;
+    const uint32_t mask = s == 32 ? 0xffffffffu : ((1u << s) - 1u);
+    uint32_t t = 0;
+    if (lane < s) {
+      const uint64_t k = skeys[st0 + lane];
+      const uint32_t m = __match_any_sync(mask, k);
+      const uint32_t leader = __ffs(m) - 1;
+      if (__popc(m) > 1 && leader != lane) {
+        const bool d = same.same(part[sidx[st0 + lane]], part[sidx[st0 + leader]]);
+        atomicOr(d ? &stt->dup : &stt->fpcoll, 1u);
+      }
+      const bool anydup = __any_sync(mask, __popc(m) > 1);
+      if (!anydup) {
+        const FastMod fm{uint64_t(s) * s, s_m2[s]};
+        for (t = 0; t < kT2Cap; t++) {
+          const Consts c = derive(bp.smix, 2, bbase + lb, t);
+          const uint32_t h = uint32_t(fastmod(hash64(c, k), fm));
+          const uint32_t mh = __match_any_sync(mask, h);
+          if (!__any_sync(mask, __popc(mh) > 1)) break;
+        }
+        if (t >= kT2Cap) {
+          if (lane == 0) atomicOr(&stt->exhausted, 1u);
+          t = 0;
+        }
+      }
+      if (lane == 0) s_t[lb] = uint8_t(t);
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+
+  // look-back: exclusive prefix of S over the partitions before p
+  if (tid == 0) {
+    unsigned long long base = 0;
+    if (p > 0) {
+      int64_t q = int64_t(p) - 1;
+      while (true) {
+        const unsigned long long v = ld_acquire(&lbstate[q]);
+        const unsigned long long f = v & ~kValMask;
+        if (f == 0) continue;
+        base += v & kValMask;
+        if (f == kFlagInc) break;
+        q--;
+      }
+      st_release(&lbstate[p], kFlagInc | ((base + S_p) & kValMask));
+    }
+    if (p == bp.np - 1) stt->S = base + S_p;
+    s_base = base;
+  }
+  __syncthreads();
+  const unsigned long long base = s_base;
+  if (ovf) {
+    if (tid == 0) atomicOr(&stt->part_overflow, 1u);
+    return;
+  }
+  if (base + S_p > bp.slot_cap) {
+    if (tid == 0) atomicOr(&stt->slot_overflow, 1u);
+    return;
+  }
+
+  // write the directory (coalesced) and the s^2 slots of every bucket
+  unsigned long long running = base;
+  for (uint32_t cb = 0; cb < nbp; cb += kBThreads) {
+    const uint32_t lb = cb + tid;
+    uint32_t st0 = 0, s = 0, t = 0;
+    if (lb < nbp) {
+      st0 = lb ? cur_get(scur, lb - 1) : 0u;
+      s = cur_get(scur, lb) - st0;
+      t = s_t[lb];
+    }
+    unsigned long long tot;
+    const unsigned long long ex = block_excl_scan(uint64_t(s) * s, &tot, s_red);
+    if (lb < nbp) {
+      const uint64_t soff = running + ex;
+      dir[lb0 + lb] = dir_entry(soff, s, t);
+      if (s == 1) {
+        slots[soff] = part[sidx[st0]];  // R12: singleton at soff
+      } else if (s >= 2 && s <= 16 && uint64_t(s) * s <= bp.bound4n) {
+        const Consts c = derive(bp.smix, 2, bbase + lb, t);
+        const FastMod fm{uint64_t(s) * s, s_m2[s]};
+        Bits256 bm;
+        bm.clear();
+        uint32_t hmin = 0xFFFFFFFFu, jmin = 0;
+        for (uint32_t j = 0; j < s; j++) {
+          const uint32_t h = uint32_t(fastmod(hash64(c, skeys[st0 + j]), fm));
+          bm.test_set(h);
+          if (h < hmin) {
+            hmin = h;
+            jmin = j;
+          }
+          slots[soff + h] = part[sidx[st0 + j]];
+        }
+        // R10: unused slots of the bucket hold the lowest-slot member, value 0
+        E f = part[sidx[st0 + jmin]];
+        f.value = 0;
+        const uint32_t s2 = s * s;
+        for (uint32_t e = 0; e < s2; e++)
+          if (!bm.test(e)) slots[soff + e] = f;
+      } else if (s > 16 && s <= 32) {
+        for (uint32_t bi = 0; bi < nbig; bi++)
+          if (s_big[bi] == lb) s_bigsoff[bi] = soff;
+      }
+    }
+    running += tot;
+  }
+  __syncthreads();
+  // slots of the 16 < s <= 32 buckets, warp per bucket
+  for (uint32_t bi = warp; bi < nbig; bi += kBWarps) {
+    const uint32_t lb = s_big[bi];
+    const uint32_t st0 = lb ? cur_get(scur, lb - 1) : 0u, s = cur_get(scur, lb) - st0;
+    const uint32_t s2 = s * s, t = s_t[lb];
+    const uint64_t soff = s_bigsoff[bi];
+    s_bits[warp][lane] = 0;
+    __syncwarp();
+    uint32_t h = 0xFFFFFFFFu;
+    if (lane < s) {
+      const Consts c = derive(bp.smix, 2, bbase + lb, t);
+      const FastMod fm{uint64_t(s2), s_m2[s]};
+      h = uint32_t(fastmod(hash64(c, skeys[st0 + lane]), fm));
+      atomicOr(&s_bits[warp][h >> 5], 1u << (h & 31));
+      slots[soff + h] = part[sidx[st0 + lane]];
+    }
+    const uint32_t hmin = __reduce_min_sync(0xffffffffu, h);
+    const uint32_t who = __ffs(__ballot_sync(0xffffffffu, h == hmin)) - 1;
+    __syncwarp();
+    E f = part[sidx[st0 + who]];
+    f.value = 0;
+    for (uint32_t e = lane; e < s2; e += 32)
+      if (!((s_bits[warp][e >> 5] >> (e & 31)) & 1)) slots[soff + e] = f;
+    __syncwarp();
+  }
+}
+
+// ------------------------------------------------------------- host side
+static size_t bucket_smem_bytes(uint32_t cap, uint32_t log2_bp) {
+  const size_t BP = size_t(1) << log2_bp;
+  return ((size_t(cap) * 8 + 15) & ~size_t(15)) + ((size_t(cap) * 2 + 15) & ~size_t(15)) +
+         (((BP / 2 + 1) * 4 + 15) & ~size_t(15)) + ((BP + 15) & ~size_t(15));
+}
+
+struct Plan {
+  uint32_t log2_bp, np, cap;
+  size_t smemB;
+};
+
+static Plan make_plan(uint64_t n_in, uint64_t nb, uint32_t log2_req, size_t smem_limit) {
+  Plan pl{};
+  const int sms = num_sms();
+  uint32_t lg = log2_req ? log2_req : 14;
+  if (!log2_req) {
+    while (lg > 6 && (nb >> lg) < uint64_t(2 * sms)) lg--;
+  }
+  for (;; lg--) {
+    const double BP = double(uint64_t(1) << lg);
+    const double m = double(n_in) * BP / double(std::max<uint64_t>(nb, 1));
+    double c = m + 8.0 * std::sqrt(std::max(m, 1.0)) + 64.0;
+    uint32_t cap = uint32_t(std::min(65535.0, std::ceil(c / 32.0) * 32.0));
+    if (cap > 65535u) cap = 65535u;
+    const size_t sm = bucket_smem_bytes(cap, lg);
+    if ((sm <= smem_limit && c <= 65535.0) || lg <= 1) {
+      pl.log2_bp = lg;
+      pl.cap = cap;
+      pl.smemB = sm;
+      break;
+    }
+  }
+  pl.np = uint32_t((nb + (uint64_t(1) << pl.log2_bp) - 1) >> pl.log2_bp);
+  return pl;
+}
+
+template <class T>
+static hm_status dmalloc(T** p, size_t bytes, cudaStream_t st) {
+  void* v = nullptr;
+  cudaError_t e = cudaMallocAsync(&v, std::max<size_t>(bytes, 16), st);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    set_error(std::string("cudaMallocAsync(") + std::to_string(bytes) + ") failed: " + cudaGetErrorString(e));
+    return HM_ERR_OOM;
+  }
+  *p = reinterpret_cast<T*>(v);
+  return HM_OK;
+}
+
+struct Scratch {
+  cudaStream_t st;
+  std::vector<void*> ptrs;
+  ~Scratch() {
+    for (void* p : ptrs) cudaFreeAsync(p, st);
+  }
+  template <class T>
+  hm_status alloc(T** p, size_t bytes) {
+    hm_status s = dmalloc(p, bytes, st);
+    if (s == HM_OK) ptrs.push_back(*p);
+    return s;
+  }
+};
+
+// Builds one table for buckets [b_lo, b_lo+nb) of a level-1 function mod
+// n_global from the n_in elements produced by `src`.
+template <class Src, class E, class Same>
+static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global, uint64_t b_lo, uint64_t nb,
+                            int t1_fixed, uint64_t seed, uint32_t log2_req, cudaStream_t st, BuildOut* out,
+                            bool* fpcoll) {
+  *fpcoll = false;
+  int dev = 0;
+  HM_CUDA_TRY(cudaGetDevice(&dev));
+  int smem_optin = 0;
+  HM_CUDA_TRY(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  const size_t static_smem_B = 4096;  // upper bound for k_bucket's static shared memory
+  const Plan pl = make_plan(n_in, nb, log2_req, size_t(smem_optin) - static_smem_B);
+  if (pl.smemB + static_smem_B > size_t(smem_optin)) {
+    set_error("build plan does not fit in shared memory");
+    return HM_ERR_TOO_LARGE;
+  }
+  const int sms = num_sms();
+  const uint64_t smix = seed_mix(seed);
+
+  Scratch sc{st, {}};
+  E* pbuf = nullptr;
+  unsigned int* pcount = nullptr;
+  unsigned long long* lbstate = nullptr;
+  DevStatus* dstat = nullptr;
+  hm_status s;
+  if ((s = sc.alloc(&pbuf, size_t(pl.np) * pl.cap * sizeof(E))) != HM_OK) return s;
+  if ((s = sc.alloc(&pcount, size_t(pl.np) * 4)) != HM_OK) return s;
+  if ((s = sc.alloc(&lbstate, size_t(pl.np) * 8)) != HM_OK) return s;
+  if ((s = sc.alloc(&dstat, sizeof(DevStatus))) != HM_OK) return s;
+
+  uint64_t* dir = nullptr;
+  E* slots = nullptr;
+  if ((s = dmalloc(&dir, nb * 8, st)) != HM_OK) return s;
+  const double sn = double(n_in);
+  uint64_t slot_cap = uint64_t(2.0 * sn + 8.0 * std::sqrt(2.0 * sn + 1.0) + 1024.0);
+  if (n_in <= 4096) slot_cap = std::max<uint64_t>(slot_cap, 4 * std::max<uint64_t>(n_in, 1));
+  if ((s = dmalloc(&slots, slot_cap * sizeof(E), st)) != HM_OK) {
+    cudaFreeAsync(dir, st);
+    return s;
+  }
+  auto fail = [&](hm_status code) {
+    cudaFreeAsync(dir, st);
+    cudaFreeAsync(slots, st);
+    return code;
+  };
+
+  // kernel configuration
+  constexpr int KPT = sizeof(E) == 16 ? 16 : 8;
+  const size_t smemA = size_t(pl.np) * 4;
+  const bool smemHist = smemA <= size_t(smem_optin) - 1024;
+  auto kA_s = k_partition<Src, E, KPT, true>;
+  auto kA_g = k_partition<Src, E, KPT, false>;
+  auto kB = k_bucket<E, Same>;
+  if (smemHist) HM_CUDA_TRY(cudaFuncSetAttribute(kA_s, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smemA)));
+  HM_CUDA_TRY(cudaFuncSetAttribute(kB, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smemB)));
+  int occA = 1;
+  if (smemHist) HM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occA, kA_s, kAThreads, smemA));
+  else HM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occA, kA_g, kAThreads, 0));
+  occA = std::max(occA, 1);
+  const uint64_t T = uint64_t(kAThreads) * KPT;
+  const uint64_t ntiles = (n_in + T - 1) / T;
+  const unsigned gridA = unsigned(std::max<uint64_t>(1, std::min<uint64_t>(ntiles, uint64_t(sms) * occA)));
+
+  BuildParams bp{};
+  bp.smix = smix;
+  bp.b_lo = b_lo;
+  bp.nb = nb;
+  bp.n_in = n_in;
+  bp.bound4n = 4 * n_global;
+  bp.log2_bp = pl.log2_bp;
+  bp.np = pl.np;
+  bp.cap = pl.cap;
+
+  DevStatus hs{};
+  const uint32_t t1_lo = t1_fixed >= 0 ? uint32_t(t1_fixed) : 0u;
+  const uint32_t t1_hi = t1_fixed >= 0 ? uint32_t(t1_fixed) + 1 : kT1Cap;
+  for (uint32_t t1 = t1_lo; t1 < t1_hi; t1++) {
+    bp.l1 = make_l1(smix, t1, n_global);
+    bp.slot_cap = slot_cap;
+    HM_CUDA_TRY(cudaMemsetAsync(pcount, 0, size_t(pl.np) * 4, st));
+    bool run_a = true;
+    for (int pass = 0; pass < 3; pass++) {
+      HM_CUDA_TRY(cudaMemsetAsync(lbstate, 0, size_t(pl.np) * 8, st));
+      HM_CUDA_TRY(cudaMemsetAsync(dstat, 0, sizeof(DevStatus), st));
+      if (run_a && ntiles > 0) {
+        if (smemHist) kA_s<<<gridA, kAThreads, smemA, st>>>(src, bp, pbuf, pcount, dstat);
+        else kA_g<<<gridA, kAThreads, 0, st>>>(src, bp, pbuf, pcount, dstat);
+        HM_CUDA_TRY(cudaGetLastError());
+      }
+      run_a = false;
+      kB<<<pl.np, kBThreads, pl.smemB, st>>>(bp, pbuf, pcount, lbstate, dir, slots, dstat, same);
+      HM_CUDA_TRY(cudaGetLastError());
+      HM_CUDA_TRY(cudaMemcpyAsync(&hs, dstat, sizeof(hs), cudaMemcpyDeviceToHost, st));
+      HM_CUDA_TRY(cudaStreamSynchronize(st));
+      if (hs.pad) {
+        set_error("a routed key does not belong to this shard's bucket range");
+        return fail(HM_ERR_INVALID_ARG);
+      }
+      if (hs.part_overflow) {
+        set_error("build partition overflow (degenerate key distribution); not supported in this version");
+        return fail(HM_ERR_TOO_LARGE);
+      }
+      if (t1_fixed < 0 && (hs.S > 4 * n_global || hs.bound_fail)) break;  // R7: redraw level one
+      if (hs.slot_overflow && !(hs.bound_fail)) {
+        // more slots than the allocation: grow to exactly S and rerun K_B
+        cudaFreeAsync(slots, st);
+        slots = nullptr;
+        slot_cap = hs.S;
+        bp.slot_cap = slot_cap;
+        if ((s = dmalloc(&slots, slot_cap * sizeof(E), st)) != HM_OK) {
+          cudaFreeAsync(dir, st);
+          return s;
+        }
+        continue;
+      }
+      break;
+    }
+    if (t1_fixed < 0 && (hs.S > 4 * n_global || hs.bound_fail)) continue;
+    if (hs.huge) {
+      set_error("a level-1 bucket with more than 32 keys (degenerate input); not supported in this version");
+      if (hs.dup) return fail(HM_ERR_DUPLICATE_KEY);
+      return fail(HM_ERR_TOO_LARGE);
+    }
+    if (hs.dup) {
+      set_error("duplicate keys in from_array_nodup input");
+      return fail(HM_ERR_DUPLICATE_KEY);
+    }
+    if (hs.fpcoll) {
+      *fpcoll = true;
+      return fail(HM_OK);
+    }
+    if (hs.exhausted) {
+      set_error("a level-2 bucket exhausted 256 attempts");
+      return fail(HM_ERR_SEED_EXHAUSTED);
+    }
+    if (hs.slot_overflow) {
+      set_error("slot allocation overflow");
+      return fail(HM_ERR_CUDA);
+    }
+    out->dir = dir;
+    out->slots = slots;
+    out->S = hs.S;
+    out->t1 = t1;
+    return HM_OK;
+  }
+  set_error("level one exhausted 16 attempts without meeting the space bound S <= 4n");
+  return fail(HM_ERR_SEED_EXHAUSTED);
+}
+
+hm_status build_u64_core(const uint64_t* keys, const uint64_t* vals, uint64_t n_in, uint64_t n_global,
+                         uint64_t b_lo, uint64_t nb, int t1_fixed, uint64_t seed, uint32_t log2_bp,
+                         cudaStream_t st, BuildOut* out) {
+  bool fpc = false;
+  return build_core<SrcU64, KV16, SameU64>(SrcU64{keys, vals}, SameU64{}, n_in, n_global, b_lo, nb, t1_fixed, seed,
+                                           log2_bp, st, out, &fpc);
+}
+
+// ------------------------------------------------------------ byte keys
+__global__ void k_fingerprint(const uint8_t* __restrict__ bytes, const uint64_t* __restrict__ offs, uint64_t n,
+                              uint64_t r, uint64_t* __restrict__ fp) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t o = offs[i], o1 = offs[i + 1];
+    fp[i] = fingerprint_dev(bytes, o, o1 - o, r);
+  }
+}
+
+__global__ void k_check_offsets(const uint64_t* __restrict__ offs, uint64_t n, unsigned int* bad) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t o = offs[i], o1 = offs[i + 1];
+    if (o1 < o) atomicOr(bad, 1u);
+    else if (o1 - o > 65535) atomicOr(bad, 2u);
+  }
+}
+
+void launch_fingerprint(const uint8_t* bytes, const uint64_t* offs, uint64_t n, uint64_t r, uint64_t* fp,
+                        cudaStream_t st) {
+  const unsigned grid = unsigned(std::min<uint64_t>((n + 255) / 256, uint64_t(num_sms()) * 16));
+  k_fingerprint<<<std::max(grid, 1u), 256, 0, st>>>(bytes, offs, n, r, fp);
+}
+
+hm_status build_bytes_core(const uint8_t* bytes, const uint64_t* offsets, const uint64_t* vals, uint64_t n,
+                           uint64_t seed, uint32_t log2_bp, cudaStream_t st, BuildOut* out, uint32_t* t0_out,
+                           uint64_t* r_out) {
+  Scratch sc{st, {}};
+  uint64_t* fp = nullptr;
+  unsigned int* bad = nullptr;
+  hm_status s;
+  if ((s = sc.alloc(&fp, n * 8)) != HM_OK) return s;
+  if ((s = sc.alloc(&bad, 4)) != HM_OK) return s;
+  HM_CUDA_TRY(cudaMemsetAsync(bad, 0, 4, st));
+  {
+    const unsigned grid = unsigned(std::min<uint64_t>((n + 255) / 256, uint64_t(num_sms()) * 16));
+    k_check_offsets<<<std::max(grid, 1u), 256, 0, st>>>(offsets, n, bad);
+    HM_CUDA_TRY(cudaGetLastError());
+  }
+  unsigned int hbad = 0;
+  uint64_t off0 = 0;
+  HM_CUDA_TRY(cudaMemcpyAsync(&hbad, bad, 4, cudaMemcpyDeviceToHost, st));
+  HM_CUDA_TRY(cudaMemcpyAsync(&off0, offsets, 8, cudaMemcpyDeviceToHost, st));
+  HM_CUDA_TRY(cudaStreamSynchronize(st));
+  if (hbad & 1u) {
+    set_error("offsets are not non-decreasing");
+    return HM_ERR_INVALID_ARG;
+  }
+  if (hbad & 2u) {
+    set_error("a byte key is longer than 65535 bytes");
+    return HM_ERR_TOO_LARGE;
+  }
+  const uint64_t smix = seed_mix(seed);
+  for (uint32_t t0 = 0; t0 < kT0Cap; t0++) {
+    const uint64_t r = derive(smix, 0, 0, t0).a1;
+    launch_fingerprint(bytes, offsets, n, r, fp, st);
+    HM_CUDA_TRY(cudaGetLastError());
+    bool fpc = false;
+    s = build_core<SrcBytes, KV32, SameBytes>(SrcBytes{fp, vals, offsets, off0}, SameBytes{bytes, off0}, n, n, 0, n,
+                                               -1, seed, log2_bp, st, out, &fpc);
+    if (s != HM_OK) return s;
+    if (!fpc) {
+      *t0_out = t0;
+      *r_out = r;
+      return HM_OK;
+    }
+  }
+  set_error("fingerprint redraws exhausted (16)");
+  return HM_ERR_FP_EXHAUSTED;
+}
+
+}  // namespace hm

@@ -1,0 +1,466 @@
+// capi.cu — the extern "C" boundary of libhm (include/hm.h).
+//
+// Argument validation, host-buffer staging for the end-to-end path, map
+// lifetime, export for parity, and the multi-GPU building blocks.  Every
+// compute step is one of the kernels in build.cu / lookup.cu; nothing here
+// computes on the CPU.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "hm_internal.cuh"
+
+namespace hm {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& s) { g_last_error = s; }
+
+hm_status cuda_fail(cudaError_t e, const char* where) {
+  cudaGetLastError();  // clear sticky-free errors
+  set_error(std::string(where) + ": " + cudaGetErrorString(e));
+  if (e == cudaErrorMemoryAllocation) return HM_ERR_OOM;
+  if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver || e == cudaErrorNoKernelImageForDevice)
+    return HM_ERR_NO_DEVICE;
+  return HM_ERR_CUDA;
+}
+
+L1Params make_l1(uint64_t smix, uint32_t t1, uint64_t n_global) {
+  L1Params p{};
+  p.c1 = derive(smix, 1, 0, t1);
+  p.n = n_global;
+  p.mmagic = ~0ull / n_global;
+  p.pow2 = (n_global & (n_global - 1)) == 0;
+  p.mask = p.pow2 ? n_global - 1 : 0;
+  return p;
+}
+
+int num_sms() {
+  static int cache[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!cache[dev]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = v > 0 ? v : 148;
+    // keep freed scratch in the stream-ordered pool between builds (warm pool)
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
+  return cache[dev];
+}
+
+static hm_status check_device() {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    set_error("no CUDA device visible");
+    return HM_ERR_NO_DEVICE;
+  }
+  int dev = 0, major = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  if (major != 10) {
+    set_error("libhm is built for sm_100a (B200) only");
+    return HM_ERR_NO_DEVICE;
+  }
+  return HM_OK;
+}
+
+static bool is_device_ptr(const void* p) {
+  if (!p) return true;
+  cudaPointerAttributes a{};
+  cudaError_t e = cudaPointerGetAttributes(&a, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// Device view of a caller array: the pointer itself, or a staged copy.
+struct Staged {
+  cudaStream_t st;
+  std::vector<void*> tmp;
+  ~Staged() {
+    for (void* p : tmp) cudaFreeAsync(p, st);
+  }
+  template <class T>
+  hm_status in(const T* host_or_dev, size_t count, const T** dev) {
+    if (!host_or_dev || is_device_ptr(host_or_dev)) {
+      *dev = host_or_dev;
+      return HM_OK;
+    }
+    void* d = nullptr;
+    HM_CUDA_TRY(cudaMallocAsync(&d, std::max<size_t>(count * sizeof(T), 16), st));
+    tmp.push_back(d);
+    HM_CUDA_TRY(cudaMemcpyAsync(d, host_or_dev, count * sizeof(T), cudaMemcpyHostToDevice, st));
+    *dev = reinterpret_cast<const T*>(d);
+    return HM_OK;
+  }
+  template <class T>
+  hm_status out(T* host_or_dev, size_t count, T** dev, bool* staged) {
+    *staged = false;
+    if (!host_or_dev || is_device_ptr(host_or_dev)) {
+      *dev = host_or_dev;
+      return HM_OK;
+    }
+    void* d = nullptr;
+    HM_CUDA_TRY(cudaMallocAsync(&d, std::max<size_t>(count * sizeof(T), 16), st));
+    tmp.push_back(d);
+    *dev = reinterpret_cast<T*>(d);
+    *staged = true;
+    return HM_OK;
+  }
+};
+
+static hm_map* new_map() {
+  hm_map* m = new hm_map;
+  std::memset(m, 0, sizeof(*m));
+  cudaGetDevice(&m->device);
+  return m;
+}
+
+}  // namespace hm
+
+using namespace hm;
+
+extern "C" {
+
+const char* hm_version(void) { return "hm 0.1 (sm_100a, spec v1)"; }
+
+const char* hm_last_error(void) { return g_last_error.c_str(); }
+
+const char* hm_status_str(hm_status s) {
+  switch (s) {
+    case HM_OK: return "OK";
+    case HM_ERR_INVALID_ARG: return "INVALID_ARG";
+    case HM_ERR_EMPTY: return "EMPTY";
+    case HM_ERR_DUPLICATE_KEY: return "DUPLICATE_KEY";
+    case HM_ERR_SEED_EXHAUSTED: return "SEED_EXHAUSTED";
+    case HM_ERR_FP_EXHAUSTED: return "FP_EXHAUSTED";
+    case HM_ERR_TOO_LARGE: return "TOO_LARGE";
+    case HM_ERR_OOM: return "OOM";
+    case HM_ERR_CUDA: return "CUDA";
+    case HM_ERR_NCCL: return "NCCL";
+    case HM_ERR_NO_DEVICE: return "NO_DEVICE";
+  }
+  return "UNKNOWN";
+}
+
+hm_status hm_build_u64(const uint64_t* keys, const uint64_t* vals, uint64_t n, const hm_opts* opts, void* stream,
+                       hm_map** out) {
+  g_last_error.clear();
+  if (!out) return HM_ERR_INVALID_ARG;
+  *out = nullptr;
+  if (n == 0) return HM_ERR_EMPTY;
+  if (!keys || !vals) return HM_ERR_INVALID_ARG;
+  if (n > (1ull << 30)) return HM_ERR_TOO_LARGE;
+  if (opts && opts->flags) return HM_ERR_INVALID_ARG;
+  hm_status s = check_device();
+  if (s != HM_OK) return s;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  Staged sg{st, {}};
+  const uint64_t *dk, *dv;
+  if ((s = sg.in(keys, n, &dk)) != HM_OK) return s;
+  if ((s = sg.in(vals, n, &dv)) != HM_OK) return s;
+  const uint64_t seed = opts ? opts->seed : 0;
+  BuildOut bo;
+  s = build_u64_core(dk, dv, n, n, 0, n, -1, seed, opts ? opts->log2_bp : 0, st, &bo);
+  if (s != HM_OK) return s;
+  hm_map* m = new_map();
+  m->key_kind = 0;
+  m->n_global = n;
+  m->b_lo = 0;
+  m->nb = n;
+  m->S = bo.S;
+  m->seed = seed;
+  m->t1 = bo.t1;
+  m->smix = seed_mix(seed);
+  m->l1 = make_l1(m->smix, bo.t1, n);
+  m->dir = bo.dir;
+  m->slots = bo.slots;
+  *out = m;
+  return HM_OK;
+}
+
+hm_status hm_build_bytes(const uint8_t* bytes, const uint64_t* offsets, const uint64_t* vals, uint64_t n,
+                         const hm_opts* opts, void* stream, hm_map** out) {
+  g_last_error.clear();
+  if (!out) return HM_ERR_INVALID_ARG;
+  *out = nullptr;
+  if (n == 0) return HM_ERR_EMPTY;
+  if (!offsets || !vals) return HM_ERR_INVALID_ARG;
+  if (n > (1ull << 30)) return HM_ERR_TOO_LARGE;
+  if (opts && opts->flags) return HM_ERR_INVALID_ARG;
+  hm_status s = check_device();
+  if (s != HM_OK) return s;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  Staged sg{st, {}};
+  const uint64_t *doff, *dv;
+  if ((s = sg.in(offsets, n + 1, &doff)) != HM_OK) return s;
+  if ((s = sg.in(vals, n, &dv)) != HM_OK) return s;
+  // context extent: offsets[0] .. offsets[n]
+  uint64_t o0 = 0, on = 0;
+  HM_CUDA_TRY(cudaMemcpyAsync(&o0, doff, 8, cudaMemcpyDeviceToHost, st));
+  HM_CUDA_TRY(cudaMemcpyAsync(&on, doff + n, 8, cudaMemcpyDeviceToHost, st));
+  HM_CUDA_TRY(cudaStreamSynchronize(st));
+  if (on < o0) return HM_ERR_INVALID_ARG;
+  if (on > o0 && !bytes) return HM_ERR_INVALID_ARG;
+  const uint8_t* db = bytes;
+  if (bytes && !is_device_ptr(bytes)) {
+    // stage exactly the used extent, keeping absolute offsets valid
+    void* d = nullptr;
+    HM_CUDA_TRY(cudaMallocAsync(&d, std::max<uint64_t>(on + 16, 16), st));
+    sg.tmp.push_back(d);
+    if (on > o0)
+      HM_CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(d) + o0, bytes + o0, on - o0, cudaMemcpyHostToDevice, st));
+    db = reinterpret_cast<const uint8_t*>(d);
+  }
+  const uint64_t seed = opts ? opts->seed : 0;
+  BuildOut bo;
+  uint32_t t0 = 0;
+  uint64_t r = 0;
+  s = build_bytes_core(db, doff, dv, n, seed, opts ? opts->log2_bp : 0, st, &bo, &t0, &r);
+  if (s != HM_OK) return s;
+  hm_map* m = new_map();
+  m->key_kind = 1;
+  m->n_global = n;
+  m->nb = n;
+  m->S = bo.S;
+  m->seed = seed;
+  m->t1 = bo.t1;
+  m->t0 = t0;
+  m->r_fp = r;
+  m->smix = seed_mix(seed);
+  m->l1 = make_l1(m->smix, bo.t1, n);
+  m->dir = bo.dir;
+  m->slots = bo.slots;
+  m->ctx_bytes = on - o0;
+  void* c = nullptr;
+  cudaError_t e = cudaMallocAsync(&c, std::max<uint64_t>(m->ctx_bytes + 16, 16), st);
+  if (e != cudaSuccess) {
+    hm_free(m);
+    return cuda_fail(e, "context copy");
+  }
+  m->ctx = reinterpret_cast<uint8_t*>(c);
+  if (m->ctx_bytes) {
+    e = cudaMemcpyAsync(m->ctx, db + o0, m->ctx_bytes, cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) {
+      hm_free(m);
+      return cuda_fail(e, "context copy");
+    }
+  }
+  e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) {
+    hm_free(m);
+    return cuda_fail(e, "build_bytes");
+  }
+  *out = m;
+  return HM_OK;
+}
+
+static hm_status lookup_common(const hm_map* map, uint64_t nq, uint64_t* out_vals, uint8_t* out_found,
+                               cudaStream_t st, Staged& sg, uint64_t** dvo, uint8_t** dfo, bool* sv, bool* sf) {
+  hm_status s;
+  if ((s = sg.out(out_vals, nq, dvo, sv)) != HM_OK) return s;
+  if ((s = sg.out(out_found, nq, dfo, sf)) != HM_OK) return s;
+  (void)map;
+  (void)st;
+  return HM_OK;
+}
+
+static hm_status finish_outputs(uint64_t nq, uint64_t* out_vals, uint8_t* out_found, uint64_t* dvo, uint8_t* dfo,
+                                bool sv, bool sf, cudaStream_t st) {
+  if (sv) HM_CUDA_TRY(cudaMemcpyAsync(out_vals, dvo, nq * 8, cudaMemcpyDeviceToHost, st));
+  if (sf) HM_CUDA_TRY(cudaMemcpyAsync(out_found, dfo, nq, cudaMemcpyDeviceToHost, st));
+  if (sv || sf) HM_CUDA_TRY(cudaStreamSynchronize(st));
+  return HM_OK;
+}
+
+hm_status hm_lookup_u64(const hm_map* map, const uint64_t* q, uint64_t nq, uint64_t* out_vals, uint8_t* out_found,
+                        void* stream) {
+  if (!map || (!q && nq) || (!out_vals && !out_found) || map->key_kind != 0) return HM_ERR_INVALID_ARG;
+  if (nq == 0) return HM_OK;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  Staged sg{st, {}};
+  const uint64_t* dq;
+  uint64_t* dvo;
+  uint8_t* dfo;
+  bool sv, sf;
+  hm_status s;
+  if ((s = sg.in(q, nq, &dq)) != HM_OK) return s;
+  if ((s = lookup_common(map, nq, out_vals, out_found, st, sg, &dvo, &dfo, &sv, &sf)) != HM_OK) return s;
+  if ((s = lookup_u64_launch(map, dq, nq, dvo, dfo, st)) != HM_OK) return s;
+  return finish_outputs(nq, out_vals, out_found, dvo, dfo, sv, sf, st);
+}
+
+hm_status hm_lookup_bytes(const hm_map* map, const uint8_t* qbytes, const uint64_t* qoffsets, uint64_t nq,
+                          uint64_t* out_vals, uint8_t* out_found, void* stream) {
+  if (!map || (!qoffsets && nq) || (!out_vals && !out_found) || map->key_kind != 1) return HM_ERR_INVALID_ARG;
+  if (nq == 0) return HM_OK;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  Staged sg{st, {}};
+  const uint64_t* dqo;
+  hm_status s;
+  if ((s = sg.in(qoffsets, nq + 1, &dqo)) != HM_OK) return s;
+  const uint8_t* dqb = qbytes;
+  if (qbytes && !is_device_ptr(qbytes)) {
+    uint64_t o0 = 0, on = 0;
+    HM_CUDA_TRY(cudaMemcpyAsync(&o0, dqo, 8, cudaMemcpyDeviceToHost, st));
+    HM_CUDA_TRY(cudaMemcpyAsync(&on, dqo + nq, 8, cudaMemcpyDeviceToHost, st));
+    HM_CUDA_TRY(cudaStreamSynchronize(st));
+    void* d = nullptr;
+    HM_CUDA_TRY(cudaMallocAsync(&d, on + 16, st));
+    sg.tmp.push_back(d);
+    if (on > o0)
+      HM_CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(d) + o0, qbytes + o0, on - o0, cudaMemcpyHostToDevice, st));
+    dqb = reinterpret_cast<const uint8_t*>(d);
+  }
+  uint64_t* dvo;
+  uint8_t* dfo;
+  bool sv, sf;
+  if ((s = lookup_common(map, nq, out_vals, out_found, st, sg, &dvo, &dfo, &sv, &sf)) != HM_OK) return s;
+  if ((s = lookup_bytes_launch(map, dqb, dqo, nq, dvo, dfo, st)) != HM_OK) return s;
+  return finish_outputs(nq, out_vals, out_found, dvo, dfo, sv, sf, st);
+}
+
+void hm_free(hm_map* map) {
+  if (!map) return;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (cur != map->device) cudaSetDevice(map->device);
+  cudaDeviceSynchronize();
+  if (map->dir) cudaFree(map->dir);
+  if (map->slots) cudaFree(map->slots);
+  if (map->ctx) cudaFree(map->ctx);
+  if (cur != map->device) cudaSetDevice(cur);
+  delete map;
+}
+
+hm_status hm_info(const hm_map* map, hm_header* h) {
+  if (!map || !h) return HM_ERR_INVALID_ARG;
+  std::memset(h, 0, sizeof(*h));
+  h->magic = HM_MAGIC;
+  h->spec_version = HM_SPEC_VERSION;
+  h->key_kind = map->key_kind;
+  h->n = map->is_shard ? map->nb : map->n_global;
+  h->S = map->S;
+  h->seed = map->seed;
+  h->t1 = map->t1;
+  h->t0 = map->t0;
+  h->ctx_bytes = map->ctx_bytes;
+  return HM_OK;
+}
+
+hm_status hm_export(const hm_map* map, uint64_t* host_dir, void* host_slots, uint8_t* host_ctx) {
+  if (!map) return HM_ERR_INVALID_ARG;
+  if (host_dir) {
+    HM_CUDA_TRY(cudaMemcpy(host_dir, map->dir, map->nb * 8, cudaMemcpyDeviceToHost));
+    if (map->slot_base)
+      for (uint64_t i = 0; i < map->nb; i++) {
+        const uint64_t d = host_dir[i];
+        host_dir[i] = (d & ~kMask40) | ((d & kMask40) + map->slot_base);
+      }
+  }
+  if (host_slots && map->S)
+    HM_CUDA_TRY(cudaMemcpy(host_slots, map->slots, map->S * (map->key_kind ? 32 : 16), cudaMemcpyDeviceToHost));
+  if (host_ctx && map->ctx_bytes) HM_CUDA_TRY(cudaMemcpy(host_ctx, map->ctx, map->ctx_bytes, cudaMemcpyDeviceToHost));
+  return HM_OK;
+}
+
+// ------------------------------------------------------------- multi-GPU
+hm_status hm_route_u64(const uint64_t* keys, const uint64_t* vals, uint64_t n_local, uint64_t n_global, uint64_t seed,
+                       uint32_t t1, int world, uint64_t* send_keys, uint64_t* send_vals, uint64_t* send_counts,
+                       void* stream) {
+  if ((!keys || !vals || !send_keys || !send_vals) && n_local) return HM_ERR_INVALID_ARG;
+  if (!send_counts || world < 1 || world > 64 || n_global == 0 || t1 >= kT1Cap) return HM_ERR_INVALID_ARG;
+  hm_status s = check_device();
+  if (s != HM_OK) return s;
+  const L1Params l1 = make_l1(seed_mix(seed), t1, n_global);
+  return route_u64_launch(keys, vals, n_local, l1, world, send_keys, send_vals, send_counts,
+                          reinterpret_cast<cudaStream_t>(stream));
+}
+
+hm_status hm_build_u64_shard(const uint64_t* keys, const uint64_t* vals, uint64_t n_recv, uint64_t n_global,
+                             uint64_t b_lo, uint64_t b_hi, uint32_t t1, const hm_opts* opts, void* stream,
+                             hm_map** out, uint64_t* S_local) {
+  g_last_error.clear();
+  if (!out || !S_local) return HM_ERR_INVALID_ARG;
+  *out = nullptr;
+  if (n_global == 0) return HM_ERR_EMPTY;
+  if (n_global > (1ull << 30)) return HM_ERR_TOO_LARGE;
+  if (b_hi < b_lo || b_hi > n_global || t1 >= kT1Cap) return HM_ERR_INVALID_ARG;
+  if (n_recv && (!keys || !vals)) return HM_ERR_INVALID_ARG;
+  hm_status s = check_device();
+  if (s != HM_OK) return s;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const uint64_t seed = opts ? opts->seed : 0;
+  const uint64_t nb = b_hi - b_lo;
+  BuildOut bo;
+  if (nb == 0) {
+    // an empty bucket range: nothing to build, an empty shard
+    hm_map* m = new_map();
+    m->is_shard = true;
+    m->n_global = n_global;
+    m->b_lo = b_lo;
+    m->seed = seed;
+    m->t1 = t1;
+    m->smix = seed_mix(seed);
+    m->l1 = make_l1(m->smix, t1, n_global);
+    HM_CUDA_TRY(cudaMalloc(&m->dir, 16));
+    HM_CUDA_TRY(cudaMalloc(&m->slots, 16));
+    *S_local = 0;
+    *out = m;
+    return HM_OK;
+  }
+  s = build_u64_core(keys, vals, n_recv, n_global, b_lo, nb, int(t1), seed, opts ? opts->log2_bp : 0, st, &bo);
+  if (s != HM_OK) return s;
+  hm_map* m = new_map();
+  m->is_shard = true;
+  m->key_kind = 0;
+  m->n_global = n_global;
+  m->b_lo = b_lo;
+  m->nb = nb;
+  m->S = bo.S;
+  m->seed = seed;
+  m->t1 = t1;
+  m->smix = seed_mix(seed);
+  m->l1 = make_l1(m->smix, t1, n_global);
+  m->dir = bo.dir;
+  m->slots = bo.slots;
+  *S_local = bo.S;
+  *out = m;
+  return HM_OK;
+}
+
+hm_status hm_shard_set_base(hm_map* map, uint64_t slot_base) {
+  if (!map) return HM_ERR_INVALID_ARG;
+  map->slot_base = slot_base;
+  return HM_OK;
+}
+
+hm_status hm_route_queries_u64(const hm_map* map, const uint64_t* q, uint64_t nq, int world, uint64_t* send_q,
+                               uint64_t* perm, uint64_t* send_counts, void* stream) {
+  if (!map || (nq && (!q || !send_q || !perm)) || !send_counts || world < 1 || world > 64) return HM_ERR_INVALID_ARG;
+  return route_queries_launch(map->l1, q, nq, world, send_q, perm, send_counts,
+                              reinterpret_cast<cudaStream_t>(stream));
+}
+
+hm_status hm_unroute_u64(const uint64_t* vals_routed, const uint8_t* found_routed, const uint64_t* perm, uint64_t nq,
+                         uint64_t* out_vals, uint8_t* out_found, void* stream) {
+  if (nq && (!perm || (out_vals && !vals_routed) || (out_found && !found_routed))) return HM_ERR_INVALID_ARG;
+  return unroute_launch(vals_routed, found_routed, perm, nq, out_vals, out_found,
+                        reinterpret_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,124 @@
+// hm_internal.cuh — shared host/device declarations of libhm (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "../../include/hm.h"
+#include "hm_math.cuh"
+
+namespace hm {
+
+// Partition-buffer elements double as slot records: the first
+// u64 is the hashed key (the key itself, or the fingerprint of a byte key).
+struct __align__(16) KV16 {  // u64 keys: {key, value}
+  uint64_t key, value;
+};
+struct __align__(32) KV32 {  // byte keys: {fp, value, ctx_off, len, 0}
+  uint64_t key, value, ctx_off;
+  uint32_t len, reserved;
+};
+
+// Device-detected conditions of one build pass (all zero-initialised).
+struct DevStatus {
+  unsigned int dup;            // two equal keys (DUPLICATE_KEY)
+  unsigned int exhausted;      // some bucket needed 256 attempts
+  unsigned int fpcoll;         // equal fingerprints, different bytes (redraw t0)
+  unsigned int part_overflow;  // a build partition exceeded its capacity
+  unsigned int slot_overflow;  // S exceeded the slot allocation
+  unsigned int huge;           // a bucket with s > 32 and s^2 <= 4n (fallback path)
+  unsigned int bound_fail;     // some bucket has s^2 > 4n (=> S > 4n)
+  unsigned int ticket;         // partition ticket for the ordered look-back
+  unsigned long long S;        // total slots of this pass
+  unsigned long long max_count;// largest partition count
+  unsigned int nhuge;          // entries in the huge-bucket list
+  unsigned int pad;
+};
+
+constexpr int kMaxHuge = 1024;
+
+struct BuildParams {
+  L1Params l1;
+  uint64_t smix;      // seed_mix(seed)
+  uint64_t b_lo;      // first global bucket of this (shard) table
+  uint64_t nb;        // local bucket count
+  uint64_t n_in;      // number of input elements
+  uint64_t slot_cap;  // allocated slots
+  uint64_t bound4n;   // 4 * n_global (R7)
+  uint32_t log2_bp;   // buckets per partition = 1 << log2_bp
+  uint32_t np;        // partitions
+  uint32_t cap;       // partition capacity (elements)
+  uint32_t pad;
+};
+
+struct LookupParams {
+  L1Params l1;
+  uint64_t smix;
+  uint64_t b_lo, nb;
+  const uint64_t* dir;
+  const void* slots;
+  // byte keys
+  const uint8_t* ctx;
+  uint64_t r_fp;
+};
+
+}  // namespace hm
+
+struct hm_map {
+  int device;
+  uint32_t key_kind;     // 0 u64, 1 bytes
+  uint64_t n_global;     // level-1 modulus
+  uint64_t b_lo, nb;     // bucket range held
+  uint64_t S;            // local slots
+  uint64_t slot_base;    // global base of the local slots (shards)
+  uint64_t seed;
+  uint32_t t1, t0;
+  bool is_shard;
+  hm::L1Params l1;
+  uint64_t smix;
+  uint64_t r_fp;         // byte keys: fingerprint point (a1 of derive(seed,0,0,t0))
+  uint64_t* dir;         // nb entries, local soff
+  void* slots;           // S records
+  uint8_t* ctx;          // byte keys: context copy
+  uint64_t ctx_bytes;
+};
+
+namespace hm {
+void set_error(const std::string& s);
+hm_status cuda_fail(cudaError_t e, const char* where);
+L1Params make_l1(uint64_t smix, uint32_t t1, uint64_t n_global);
+int num_sms();
+
+// build.cu
+struct BuildOut {
+  uint64_t* dir = nullptr;
+  void* slots = nullptr;
+  uint64_t S = 0;
+  uint32_t t1 = 0;
+};
+// t1_fixed < 0: search t1 = 0..15 with the space bound of this table.
+hm_status build_u64_core(const uint64_t* keys, const uint64_t* vals, uint64_t n_in, uint64_t n_global,
+                         uint64_t b_lo, uint64_t nb, int t1_fixed, uint64_t seed, uint32_t log2_bp,
+                         cudaStream_t st, BuildOut* out);
+hm_status build_bytes_core(const uint8_t* bytes, const uint64_t* offsets, const uint64_t* vals, uint64_t n,
+                           uint64_t seed, uint32_t log2_bp, cudaStream_t st, BuildOut* out, uint32_t* t0_out,
+                           uint64_t* r_out);
+// lookup.cu
+hm_status lookup_u64_launch(const hm_map* m, const uint64_t* q, uint64_t nq, uint64_t* out_vals,
+                            uint8_t* out_found, cudaStream_t st);
+hm_status lookup_bytes_launch(const hm_map* m, const uint8_t* qb, const uint64_t* qo, uint64_t nq,
+                              uint64_t* out_vals, uint8_t* out_found, cudaStream_t st);
+hm_status route_u64_launch(const uint64_t* keys, const uint64_t* vals, uint64_t n, const L1Params& l1,
+                           int world, uint64_t* sk, uint64_t* sv, uint64_t* counts, cudaStream_t st);
+hm_status route_queries_launch(const L1Params& l1, const uint64_t* q, uint64_t nq, int world, uint64_t* sq,
+                               uint64_t* perm, uint64_t* counts, cudaStream_t st);
+hm_status unroute_launch(const uint64_t* vr, const uint8_t* fr, const uint64_t* perm, uint64_t nq,
+                         uint64_t* ov, uint8_t* of, cudaStream_t st);
+}  // namespace hm
+
+#define HM_CUDA_TRY(expr)                                              \
+  do {                                                                 \
+    cudaError_t e__ = (expr);                                          \
+    if (e__ != cudaSuccess) return ::hm::cuda_fail(e__, #expr);        \
+  } while (0)

@@ -1,0 +1,169 @@
+// hm_math.cuh — device arithmetic of the FKS hot path (sm_100a).
+//
+//  * constant schedule  `random` made deterministic as
+//    the counter schedule of DESIGN.md R6;
+//  * the universal family `hash` of DESIGN.md R4:
+//    hash((a1,a2,b), x) = (a1*(x mod 2^32) + a2*(x >> 32) + b) mod (2^61-1);
+//  * exact range reduction `mod n` / `mod s^2` (R22) with a
+//    precomputed reciprocal instead of the 64-bit division subroutine;
+//  * the 61-bit polynomial fingerprint of byte keys (R5).
+//
+// Everything is integer arithmetic; 64x64->128 products use __umul64hi, and
+// the Mersenne modulus is reduced with shifts and masks (no division).
+#pragma once
+#include <cstdint>
+
+namespace hm {
+
+constexpr uint64_t kP = (1ull << 61) - 1;          // Mersenne prime (R4)
+constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ull;  // splitmix64 increment (R6)
+constexpr uint64_t kSeedSalt = 0xD6E8FEB86659FD93ull;
+constexpr uint32_t kT1Cap = 16, kT2Cap = 256, kT0Cap = 16;
+constexpr uint64_t kMask40 = (1ull << 40) - 1;
+
+struct Consts {  // (a1, a2, b)
+  uint64_t a1, a2, b;
+};
+
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__host__ __device__ __forceinline__ uint64_t field_of(uint64_t z) {
+  uint64_t v = z >> 3;
+  return v == kP ? 0 : v;
+}
+
+// seed_mix = mix64(seed ^ kSeedSalt) is hoisted per table (one per build).
+__host__ __device__ __forceinline__ uint64_t seed_mix(uint64_t seed) { return mix64(seed ^ kSeedSalt); }
+
+// derive(seed, level, bucket, attempt) -> (a1, a2, b)   (R6)
+__host__ __device__ __forceinline__ Consts derive(uint64_t smix, uint32_t level, uint64_t bucket,
+                                                  uint32_t attempt) {
+  const uint64_t ctr = (uint64_t(level) << 60) | (bucket << 8) | uint64_t(attempt);
+  const uint64_t u = mix64(smix ^ ctr);
+  Consts c;
+  c.a1 = field_of(mix64(u + kGamma));
+  c.a2 = field_of(mix64(u + 2 * kGamma));
+  c.b = field_of(mix64(u + 3 * kGamma));
+  if (c.a1 == 0) c.a1 = 1;
+  if (c.a2 == 0) c.a2 = 1;
+  return c;
+}
+
+__host__ __device__ __forceinline__ uint64_t umulhi(uint64_t a, uint64_t b) {
+#if defined(__CUDA_ARCH__)
+  return __umul64hi(a, b);
+#else
+  return (uint64_t)(((unsigned __int128)a * b) >> 64);
+#endif
+}
+
+// Reduce the 128-bit value hi*2^64 + lo (hi < 2^40) modulo P = 2^61-1,
+// using 2^61 == 1 (mod P), hence 2^64 == 8.
+__host__ __device__ __forceinline__ uint64_t mod_p128(uint64_t hi, uint64_t lo) {
+  uint64_t x = (lo & kP) + (lo >> 61) + (hi << 3);
+  x = (x & kP) + (x >> 61);
+  return x >= kP ? x - kP : x;
+}
+
+// The universal family (R4).  a1, a2 < 2^61, limbs < 2^32: the sum of the two
+// products and b is < 2^95, so hi < 2^31.
+__host__ __device__ __forceinline__ uint64_t hash64(const Consts& c, uint64_t x) {
+  const uint64_t xl = x & 0xFFFFFFFFull, xh = x >> 32;
+  const uint64_t l1 = c.a1 * xl, h1 = umulhi(c.a1, xl);
+  const uint64_t l2 = c.a2 * xh, h2 = umulhi(c.a2, xh);
+  uint64_t lo = l1 + l2;
+  uint64_t hi = h1 + h2 + (lo < l1);
+  const uint64_t lo2 = lo + c.b;
+  hi += (lo2 < lo);
+  return mod_p128(hi, lo2);
+}
+
+// (a*b) mod P for a, b < 2^62.
+__host__ __device__ __forceinline__ uint64_t mulmod_p(uint64_t a, uint64_t b) {
+  const uint64_t lo = a * b, hi = umulhi(a, b);
+  // value = hi*2^64 + lo < 2^124: fold the top: hi*2^64 = hi*8 (mod P), hi < 2^60
+  uint64_t x = (lo & kP) + (lo >> 61);
+  // hi*8 may be up to 2^63: fold it separately
+  uint64_t h8 = hi << 3;                 // < 2^63
+  uint64_t y = (h8 & kP) + (h8 >> 61);   // < 2^61 + 4
+  x += y;                                // < 2^62 + small
+  x = (x & kP) + (x >> 61);
+  return x >= kP ? x - kP : x;
+}
+
+// Exact x mod d for x < 2^62 and 1 <= d < 2^32, with m = floor((2^64-1)/d):
+// q = umulhi(x, m) underestimates floor(x/d) by at most 1 (x/2^64 < 1/4), so
+// one or two corrections give the exact remainder (R22).
+struct FastMod {
+  uint64_t d, m;
+};
+__host__ __device__ __forceinline__ FastMod make_fastmod(uint64_t d) {
+  FastMod f;
+  f.d = d;
+  f.m = ~0ull / d;
+  return f;
+}
+__host__ __device__ __forceinline__ uint64_t fastmod(uint64_t x, const FastMod& f) {
+  const uint64_t q = umulhi(x, f.m);
+  uint64_t r = x - q * f.d;
+  if (r >= f.d) r -= f.d;
+  if (r >= f.d) r -= f.d;
+  return r;
+}
+
+// Level-one range reduction `mod n`: mask when n is a power of
+// two (all benchmark configs), reciprocal otherwise.
+struct L1Params {
+  Consts c1;
+  uint64_t n;       // level-1 modulus (global key count)
+  uint64_t mmagic;  // ~0 / n
+  uint64_t mask;    // n-1 when n is a power of two, else 0
+  int pow2;
+};
+__host__ __device__ __forceinline__ uint64_t level1_bucket(const L1Params& p, uint64_t key) {
+  const uint64_t h = hash64(p.c1, key);
+  if (p.pow2) return h & p.mask;
+  FastMod f{p.n, p.mmagic};
+  return fastmod(h, f);
+}
+
+// Directory entry: soff | s<<40 | t<<56.
+__host__ __device__ __forceinline__ uint64_t dir_entry(uint64_t soff, uint64_t s, uint64_t t) {
+  return soff | (s << 40) | (t << 56);
+}
+
+#if defined(__CUDACC__)
+// Fingerprint (R5): acc = (acc + w_i) * r mod P over little-endian u32 words
+// (zero padded), fp = acc + len mod P.  Thread per key; the words are
+// assembled from 4-byte aligned loads with a funnel shift.
+__device__ __forceinline__ uint32_t ld_u32(const uint8_t* p) { return __ldg(reinterpret_cast<const uint32_t*>(p)); }
+
+__device__ __forceinline__ uint64_t fingerprint_dev(const uint8_t* bytes, uint64_t off, uint64_t len, uint64_t r) {
+  uint64_t acc = 0;
+  if (len == 0) return 0;
+  const uint64_t abase = off & ~uint64_t(3);
+  const uint32_t sh = uint32_t(off & 3) * 8;
+  const uint64_t last_aligned = (off + len - 1) & ~uint64_t(3);
+  const uint64_t nw = (len + 3) >> 2;
+  uint32_t cur = ld_u32(bytes + abase);
+  for (uint64_t i = 0; i < nw; i++) {
+    const uint64_t na = abase + 4 * (i + 1);
+    const uint32_t nxt = na <= last_aligned ? ld_u32(bytes + na) : 0u;
+    uint32_t w = sh ? __funnelshift_r(cur, nxt, sh) : cur;
+    const uint64_t rem = len - 4 * i;
+    if (rem < 4) w &= (1u << (8 * rem)) - 1u;
+    acc = mulmod_p(acc + w, r);
+    cur = nxt;
+  }
+  uint64_t f = acc + len;
+  f = (f & kP) + (f >> 61);
+  return f >= kP ? f - kP : f;
+}
+
+#endif
+
+}  // namespace hm

@@ -1,0 +1,296 @@
+// lookup.cu — batched lookups and multi-GPU routing kernels (sm_100a).
+//
+// lookup is the membership test of PAPER.md:244-245
+// extended to a map: two dependent random probes (directory entry, slot) and a
+// key compare.  Each thread keeps QPT independent queries in flight so that the
+// chip has enough outstanding 32-byte sectors to cover DRAM latency (Little's
+// law).
+#include <algorithm>
+
+#include "hm_internal.cuh"
+
+namespace hm {
+
+constexpr int kLThreads = 256;
+
+__device__ __forceinline__ uint64_t ld_stream_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint64_t ld_dir(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ KV16 ld_slot16(const KV16* p) {
+  KV16 e;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u64 {%0, %1}, [%2];" : "=l"(e.key), "=l"(e.value) : "l"(p));
+  return e;
+}
+__device__ __forceinline__ void st_stream_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.global.L1::no_allocate.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// level-2 range reduction mod s^2 (R22): reciprocal table for s <= 32
+__device__ __forceinline__ uint64_t mod_s2(uint64_t h, uint32_t s, const uint64_t* s_m2) {
+  const uint64_t d = uint64_t(s) * s;
+  if (s <= 32) {
+    const FastMod fm{d, s_m2[s]};
+    return fastmod(h, fm);
+  }
+  return h % d;
+}
+
+// probe-2 slot index of key k in bucket b (global id) with directory entry d
+__device__ __forceinline__ uint64_t slot_index(uint64_t smix, uint64_t b, uint64_t d, uint64_t k,
+                                               const uint64_t* s_m2) {
+  const uint32_t s = uint32_t((d >> 40) & 0xFFFF);
+  const uint64_t soff = d & kMask40;
+  if (s <= 1) return soff;  // R12
+  const Consts c = derive(smix, 2, b, uint32_t(d >> 56));
+  return soff + mod_s2(hash64(c, k), s, s_m2);
+}
+
+template <int QPT>
+__global__ void __launch_bounds__(kLThreads) k_lookup_u64(LookupParams lp, const uint64_t* __restrict__ q,
+                                                          uint64_t nq, uint64_t* __restrict__ ov,
+                                                          uint8_t* __restrict__ of) {
+  __shared__ uint64_t s_m2[33];
+  if (threadIdx.x < 33) s_m2[threadIdx.x] = threadIdx.x ? ~0ull / (uint64_t(threadIdx.x) * threadIdx.x) : 0ull;
+  __syncthreads();
+  const KV16* __restrict__ slots = reinterpret_cast<const KV16*>(lp.slots);
+  const uint64_t per = uint64_t(kLThreads) * QPT;
+  for (uint64_t base = blockIdx.x * per; base < nq; base += uint64_t(gridDim.x) * per) {
+    uint64_t key[QPT], b[QPT], d[QPT];
+#pragma unroll
+    for (int j = 0; j < QPT; j++) {
+      const uint64_t idx = base + uint64_t(j) * kLThreads + threadIdx.x;
+      key[j] = idx < nq ? ld_stream_u64(q + idx) : 0ull;
+    }
+    // L1 + L2: g q and the directory probe
+#pragma unroll
+    for (int j = 0; j < QPT; j++) {
+      const uint64_t idx = base + uint64_t(j) * kLThreads + threadIdx.x;
+      b[j] = level1_bucket(lp.l1, key[j]) - lp.b_lo;
+      d[j] = (idx < nq && b[j] < lp.nb) ? ld_dir(lp.dir + b[j]) : 0ull;
+    }
+    // L3 + L4: slot index and the slot probe
+    KV16 e[QPT];
+#pragma unroll
+    for (int j = 0; j < QPT; j++) {
+      const bool live = ((d[j] >> 40) & 0xFFFF) != 0;
+      e[j].key = ~key[j];
+      e[j].value = 0;
+      if (live) e[j] = ld_slot16(slots + slot_index(lp.smix, b[j] + lp.b_lo, d[j], key[j], s_m2));
+    }
+#pragma unroll
+    for (int j = 0; j < QPT; j++) {
+      const uint64_t idx = base + uint64_t(j) * kLThreads + threadIdx.x;
+      if (idx < nq) {
+        const bool hit = e[j].key == key[j];
+        if (ov) st_stream_u64(ov + idx, hit ? e[j].value : 0ull);
+        if (of) of[idx] = hit ? 1 : 0;
+      }
+    }
+  }
+}
+
+hm_status lookup_u64_launch(const hm_map* m, const uint64_t* q, uint64_t nq, uint64_t* out_vals,
+                            uint8_t* out_found, cudaStream_t st) {
+  if (nq == 0) return HM_OK;
+  LookupParams lp{};
+  lp.l1 = m->l1;
+  lp.smix = m->smix;
+  lp.b_lo = m->b_lo;
+  lp.nb = m->nb;
+  lp.dir = m->dir;
+  lp.slots = m->slots;
+  constexpr int QPT = 4;
+  const uint64_t per = uint64_t(kLThreads) * QPT;
+  const uint64_t blocks = (nq + per - 1) / per;
+  const unsigned grid = unsigned(std::min<uint64_t>(blocks, uint64_t(num_sms()) * 8));
+  k_lookup_u64<QPT><<<grid, kLThreads, 0, st>>>(lp, q, nq, out_vals, out_found);
+  HM_CUDA_TRY(cudaGetLastError());
+  return HM_OK;
+}
+
+// ------------------------------------------------------------ byte keys
+
+template <int QPT>
+__global__ void __launch_bounds__(kLThreads) k_lookup_bytes(LookupParams lp, const uint8_t* __restrict__ qb,
+                                                            const uint64_t* __restrict__ qo, uint64_t nq,
+                                                            uint64_t* __restrict__ ov, uint8_t* __restrict__ of) {
+  __shared__ uint64_t s_m2[33];
+  if (threadIdx.x < 33) s_m2[threadIdx.x] = threadIdx.x ? ~0ull / (uint64_t(threadIdx.x) * threadIdx.x) : 0ull;
+  __syncthreads();
+  const KV32* __restrict__ slots = reinterpret_cast<const KV32*>(lp.slots);
+  const uint64_t per = uint64_t(kLThreads) * QPT;
+  for (uint64_t base = blockIdx.x * per; base < nq; base += uint64_t(gridDim.x) * per) {
+    uint64_t fp[QPT], b[QPT], d[QPT], off[QPT], len[QPT];
+#pragma unroll
+    for (int j = 0; j < QPT; j++) {
+      const uint64_t idx = base + uint64_t(j) * kLThreads + threadIdx.x;
+      off[j] = 0;
+      len[j] = 0;
+      fp[j] = 0;
+      if (idx < nq) {
+        off[j] = qo[idx];
+        len[j] = qo[idx + 1] - off[j];
+        fp[j] = fingerprint_dev(qb, off[j], len[j], lp.r_fp);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < QPT; j++) {
+      const uint64_t idx = base + uint64_t(j) * kLThreads + threadIdx.x;
+      b[j] = level1_bucket(lp.l1, fp[j]) - lp.b_lo;
+      d[j] = (idx < nq && b[j] < lp.nb) ? ld_dir(lp.dir + b[j]) : 0ull;
+    }
+#pragma unroll
+    for (int j = 0; j < QPT; j++) {
+      const uint64_t idx = base + uint64_t(j) * kLThreads + threadIdx.x;
+      if (idx >= nq) continue;
+      bool hit = false;
+      uint64_t v = 0;
+      if (((d[j] >> 40) & 0xFFFF) != 0) {
+        const KV32 e = slots[slot_index(lp.smix, b[j] + lp.b_lo, d[j], fp[j], s_m2)];
+        if (e.key == fp[j] && e.len == len[j]) {
+          const uint8_t* a = lp.ctx + e.ctx_off;
+          const uint8_t* c = qb + off[j];
+          hit = true;
+          for (uint32_t i = 0; i < e.len; i++)
+            if (a[i] != c[i]) {
+              hit = false;
+              break;
+            }
+          if (hit) v = e.value;
+        }
+      }
+      if (ov) ov[idx] = v;
+      if (of) of[idx] = hit ? 1 : 0;
+    }
+  }
+}
+
+hm_status lookup_bytes_launch(const hm_map* m, const uint8_t* qb, const uint64_t* qo, uint64_t nq,
+                              uint64_t* out_vals, uint8_t* out_found, cudaStream_t st) {
+  if (nq == 0) return HM_OK;
+  LookupParams lp{};
+  lp.l1 = m->l1;
+  lp.smix = m->smix;
+  lp.b_lo = m->b_lo;
+  lp.nb = m->nb;
+  lp.dir = m->dir;
+  lp.slots = m->slots;
+  lp.ctx = m->ctx;
+  lp.r_fp = m->r_fp;
+  constexpr int QPT = 2;
+  const uint64_t per = uint64_t(kLThreads) * QPT;
+  const uint64_t blocks = (nq + per - 1) / per;
+  const unsigned grid = unsigned(std::min<uint64_t>(blocks, uint64_t(num_sms()) * 8));
+  k_lookup_bytes<QPT><<<grid, kLThreads, 0, st>>>(lp, qb, qo, nq, out_vals, out_found);
+  HM_CUDA_TRY(cudaGetLastError());
+  return HM_OK;
+}
+
+// ------------------------------------------------------- multi-GPU routing
+// owner(b) = floor(b * G / n): contiguous bucket ranges.
+__device__ __forceinline__ uint32_t owner_of(uint64_t b, uint64_t n, int world) {
+  return uint32_t((b * uint64_t(world)) / n);
+}
+
+__global__ void k_route_count(const uint64_t* __restrict__ keys, uint64_t n, L1Params l1, int world,
+                              unsigned long long* __restrict__ counts) {
+  __shared__ unsigned long long s_c[64];
+  if (threadIdx.x < 64) s_c[threadIdx.x] = 0;
+  __syncthreads();
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+    atomicAdd(&s_c[owner_of(level1_bucket(l1, keys[i]), l1.n, world)], 1ull);
+  __syncthreads();
+  if (threadIdx.x < world && s_c[threadIdx.x]) atomicAdd(&counts[threadIdx.x], s_c[threadIdx.x]);
+}
+
+__global__ void k_route_prefix(const unsigned long long* counts, int world, unsigned long long* cursors) {
+  if (threadIdx.x == 0) {
+    unsigned long long acc = 0;
+    for (int r = 0; r < world; r++) {
+      cursors[r] = acc;
+      acc += counts[r];
+    }
+  }
+}
+
+// Scatter by owner rank; warp-aggregated cursor reservation per destination.
+__global__ void k_route_scatter(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ vals, uint64_t n,
+                                L1Params l1, int world, unsigned long long* __restrict__ cursors,
+                                uint64_t* __restrict__ sk, uint64_t* __restrict__ sv, uint64_t* __restrict__ perm) {
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint64_t base = (blockIdx.x * uint64_t(blockDim.x)) & ~uint64_t(31); base < n;
+       base += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t i = base + (threadIdx.x & ~31u) + lane;
+    const bool live = i < n;
+    uint64_t k = live ? keys[i] : 0;
+    const uint32_t r = live ? owner_of(level1_bucket(l1, k), l1.n, world) : 0xFFFFFFFFu;
+    const uint32_t peers = __match_any_sync(0xffffffffu, r);
+    const uint32_t leader = __ffs(peers) - 1;
+    const uint32_t rank_in = __popc(peers & ((1u << lane) - 1u));
+    unsigned long long pos0 = 0;
+    if (live && lane == leader) pos0 = atomicAdd(&cursors[r], (unsigned long long)__popc(peers));
+    pos0 = __shfl_sync(0xffffffffu, pos0, leader);
+    if (live) {
+      const uint64_t pos = pos0 + rank_in;
+      sk[pos] = k;
+      if (sv) sv[pos] = vals[i];
+      if (perm) perm[i] = pos;
+    }
+  }
+}
+
+static hm_status route_common(const uint64_t* keys, const uint64_t* vals, uint64_t n, const L1Params& l1, int world,
+                              uint64_t* sk, uint64_t* sv, uint64_t* perm, uint64_t* counts, cudaStream_t st) {
+  if (world < 1 || world > 64) return HM_ERR_INVALID_ARG;
+  unsigned long long* cur = nullptr;
+  HM_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&cur), 64 * 8, st));
+  cudaError_t e = cudaMemsetAsync(counts, 0, size_t(world) * 8, st);
+  const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, uint64_t(num_sms()) * 8)));
+  if (e == cudaSuccess && n) {
+    k_route_count<<<grid, 256, 0, st>>>(keys, n, l1, world, reinterpret_cast<unsigned long long*>(counts));
+    k_route_prefix<<<1, 32, 0, st>>>(reinterpret_cast<unsigned long long*>(counts), world, cur);
+    k_route_scatter<<<grid, 256, 0, st>>>(keys, vals, n, l1, world, cur, sk, sv, perm);
+    e = cudaGetLastError();
+  }
+  cudaFreeAsync(cur, st);
+  if (e != cudaSuccess) return cuda_fail(e, "route");
+  return HM_OK;
+}
+
+hm_status route_u64_launch(const uint64_t* keys, const uint64_t* vals, uint64_t n, const L1Params& l1, int world,
+                           uint64_t* sk, uint64_t* sv, uint64_t* counts, cudaStream_t st) {
+  return route_common(keys, vals, n, l1, world, sk, sv, nullptr, counts, st);
+}
+
+hm_status route_queries_launch(const L1Params& l1, const uint64_t* q, uint64_t nq, int world, uint64_t* sq,
+                               uint64_t* perm, uint64_t* counts, cudaStream_t st) {
+  return route_common(q, nullptr, nq, l1, world, sq, nullptr, perm, counts, st);
+}
+
+__global__ void k_unroute(const uint64_t* __restrict__ vr, const uint8_t* __restrict__ fr,
+                          const uint64_t* __restrict__ perm, uint64_t nq, uint64_t* __restrict__ ov,
+                          uint8_t* __restrict__ of) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < nq; i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t p = perm[i];
+    if (ov) ov[i] = vr[p];
+    if (of) of[i] = fr[p];
+  }
+}
+
+hm_status unroute_launch(const uint64_t* vr, const uint8_t* fr, const uint64_t* perm, uint64_t nq, uint64_t* ov,
+                         uint8_t* of, cudaStream_t st) {
+  if (!nq) return HM_OK;
+  const unsigned grid = unsigned(std::min<uint64_t>((nq + 255) / 256, uint64_t(num_sms()) * 8));
+  k_unroute<<<grid, 256, 0, st>>>(vr, fr, perm, nq, ov, of);
+  HM_CUDA_TRY(cudaGetLastError());
+  return HM_OK;
+}
+
+}  // namespace hm

@@ -1,0 +1,314 @@
+"""Thin ctypes binding of libhm.so (include/hm.h) — argument marshalling only.
+
+Every step of the hot path runs in the CUDA kernels behind the C-ABI; this
+module converts torch tensors / numpy arrays into pointers and sizes, passes
+the current CUDA stream, and turns statuses into exceptions.  There is no CPU
+fallback: if libhm.so is missing or the device is not a B200 the calls raise.
+
+Names follow include/hm.h: build_u64 / build_bytes (from_array_nodup,
+PAPER.md:608-609), lookup / lookup_bytes, free.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libhm.so")
+
+STATUS = {
+    0: "OK", 1: "INVALID_ARG", 2: "EMPTY", 3: "DUPLICATE_KEY", 4: "SEED_EXHAUSTED",
+    5: "FP_EXHAUSTED", 6: "TOO_LARGE", 7: "OOM", 8: "CUDA", 9: "NCCL", 10: "NO_DEVICE",
+}
+
+HEADER_DTYPE = np.dtype(
+    [
+        ("magic", "<u4"), ("spec_version", "<u4"), ("key_kind", "<u4"), ("reserved", "<u4"),
+        ("n", "<u8"), ("S", "<u8"), ("seed", "<u8"), ("t1", "<u4"), ("t0", "<u4"),
+        ("ctx_bytes", "<u8"),
+    ]
+)
+SLOT_U64_DTYPE = np.dtype([("key", "<u8"), ("value", "<u8")])
+SLOT_BYTES_DTYPE = np.dtype(
+    [("fp", "<u8"), ("value", "<u8"), ("ctx_off", "<u8"), ("len", "<u4"), ("reserved", "<u4")]
+)
+
+
+class HMError(RuntimeError):
+    def __init__(self, code: int, detail: str = ""):
+        self.code = code
+        self.name = STATUS.get(code, "?")
+        super().__init__(f"hm status {code} ({self.name}){': ' + detail if detail else ''}")
+
+
+class _Opts(C.Structure):
+    _fields_ = [("seed", C.c_uint64), ("log2_bp", C.c_uint32), ("flags", C.c_uint32)]
+
+
+class _Header(C.Structure):
+    _fields_ = [(n, C.c_uint32 if d.kind == "u" and d.itemsize == 4 else C.c_uint64)
+                for n, (d, _) in HEADER_DTYPE.fields.items()]
+
+
+_lib = None
+
+
+def lib():
+    """Load libhm.so; raises if it has not been built (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = C.CDLL(LIB_PATH)
+        p, u64, u32, i32 = C.c_void_p, C.c_uint64, C.c_uint32, C.c_int
+        L.hm_build_u64.argtypes = [p, p, u64, C.POINTER(_Opts), p, C.POINTER(p)]
+        L.hm_build_bytes.argtypes = [p, p, p, u64, C.POINTER(_Opts), p, C.POINTER(p)]
+        L.hm_lookup_u64.argtypes = [p, p, u64, p, p, p]
+        L.hm_lookup_bytes.argtypes = [p, p, p, u64, p, p, p]
+        L.hm_free.argtypes = [p]
+        L.hm_free.restype = None
+        L.hm_info.argtypes = [p, C.POINTER(_Header)]
+        L.hm_export.argtypes = [p, p, p, p]
+        L.hm_status_str.restype = C.c_char_p
+        L.hm_status_str.argtypes = [i32]
+        L.hm_last_error.restype = C.c_char_p
+        L.hm_version.restype = C.c_char_p
+        L.hm_route_u64.argtypes = [p, p, u64, u64, u64, u32, i32, p, p, p, p]
+        L.hm_build_u64_shard.argtypes = [p, p, u64, u64, u64, u64, u32, C.POINTER(_Opts), p, C.POINTER(p),
+                                         C.POINTER(u64)]
+        L.hm_shard_set_base.argtypes = [p, u64]
+        L.hm_route_queries_u64.argtypes = [p, p, u64, i32, p, p, p, p]
+        L.hm_unroute_u64.argtypes = [p, p, p, u64, p, p, p]
+        for f in ("hm_build_u64", "hm_build_bytes", "hm_lookup_u64", "hm_lookup_bytes", "hm_info", "hm_export",
+                  "hm_route_u64", "hm_build_u64_shard", "hm_shard_set_base", "hm_route_queries_u64",
+                  "hm_unroute_u64"):
+            getattr(L, f).restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def _check(code: int):
+    if code != 0:
+        raise HMError(code, lib().hm_last_error().decode(errors="replace"))
+
+
+# ------------------------------------------------------------- marshalling
+
+def _ptr(x):
+    """Pointer + keep-alive for a torch tensor (any device) or numpy array."""
+    if x is None:
+        return None, None
+    try:
+        import torch
+        if isinstance(x, torch.Tensor):
+            if not x.is_contiguous():
+                x = x.contiguous()
+            return C.c_void_p(x.data_ptr()), x
+    except ImportError:  # pragma: no cover
+        pass
+    a = np.ascontiguousarray(x)
+    return a.ctypes.data_as(C.c_void_p), a
+
+
+def _numel(x) -> int:
+    return int(x.numel()) if hasattr(x, "numel") else int(np.asarray(x).size)
+
+
+def _stream(stream=None):
+    if stream is not None:
+        return C.c_void_p(int(stream))
+    try:
+        import torch
+        if torch.cuda.is_available():
+            return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    except ImportError:  # pragma: no cover
+        pass
+    return C.c_void_p(0)
+
+
+def _opts(seed: int, log2_bp: int = 0):
+    return _Opts(seed & ((1 << 64) - 1), log2_bp, 0)
+
+
+@dataclass
+class Info:
+    key_kind: int
+    n: int
+    S: int
+    seed: int
+    t1: int
+    t0: int
+    ctx_bytes: int
+
+
+class HashMap:
+    """An immutable FKS hash map living on one GPU (owned by libhm)."""
+
+    def __init__(self, handle: int, key_kind: int):
+        self._h = C.c_void_p(handle)
+        self.key_kind = key_kind
+
+    # -- build
+    @classmethod
+    def build_u64(cls, keys, vals, seed: int = 0, stream=None, log2_bp: int = 0) -> "HashMap":
+        kp, kk = _ptr(keys)
+        vp, vk = _ptr(vals)
+        n = _numel(keys)
+        if _numel(vals) != n:
+            raise ValueError("keys and vals differ in length")
+        h = C.c_void_p()
+        o = _opts(seed, log2_bp)
+        _check(lib().hm_build_u64(kp, vp, n, C.byref(o), _stream(stream), C.byref(h)))
+        return cls(h.value, 0)
+
+    @classmethod
+    def build_bytes(cls, ctx, offsets, vals, seed: int = 0, stream=None, log2_bp: int = 0) -> "HashMap":
+        cp, ck = _ptr(ctx)
+        op, ok = _ptr(offsets)
+        vp, vk = _ptr(vals)
+        n = _numel(offsets) - 1
+        if _numel(vals) != n:
+            raise ValueError("offsets and vals disagree on n")
+        h = C.c_void_p()
+        o = _opts(seed, log2_bp)
+        _check(lib().hm_build_bytes(cp, op, vp, n, C.byref(o), _stream(stream), C.byref(h)))
+        return cls(h.value, 1)
+
+    # -- lookup
+    def lookup(self, q, out_vals=None, out_found=None, stream=None):
+        """Batched lookup of u64 queries; fills/returns (vals, found).
+
+        With torch CUDA inputs and no outputs given, allocates device outputs."""
+        nq = _numel(q)
+        out_vals, out_found = self._outputs(q, nq, out_vals, out_found)
+        qp, qk = _ptr(q)
+        vp, vk = _ptr(out_vals)
+        fp, fk = _ptr(out_found)
+        _check(lib().hm_lookup_u64(self._h, qp, nq, vp, fp, _stream(stream)))
+        return out_vals, out_found
+
+    def contains(self, q, out_found=None, stream=None):
+        """Membership only: no value is read or written."""
+        nq = _numel(q)
+        _, out_found = self._outputs(q, nq, False, out_found)
+        qp, qk = _ptr(q)
+        fp, fk = _ptr(out_found)
+        _check(lib().hm_lookup_u64(self._h, qp, nq, None, fp, _stream(stream)))
+        return out_found
+
+    def lookup_bytes(self, qctx, qoffsets, out_vals=None, out_found=None, stream=None):
+        nq = _numel(qoffsets) - 1
+        out_vals, out_found = self._outputs(qoffsets, nq, out_vals, out_found)
+        cp, ck = _ptr(qctx)
+        op, ok = _ptr(qoffsets)
+        vp, vk = _ptr(out_vals)
+        fp, fk = _ptr(out_found)
+        _check(lib().hm_lookup_bytes(self._h, cp, op, nq, vp, fp, _stream(stream)))
+        return out_vals, out_found
+
+    @staticmethod
+    def _outputs(like, nq, out_vals, out_found):
+        try:
+            import torch
+            is_t = isinstance(like, torch.Tensor)
+        except ImportError:  # pragma: no cover
+            is_t = False
+        if is_t:
+            import torch
+            dev = like.device
+            if out_vals is None:
+                out_vals = torch.empty(nq, dtype=torch.int64, device=dev)
+            if out_found is None:
+                out_found = torch.empty(nq, dtype=torch.uint8, device=dev)
+        else:
+            if out_vals is None:
+                out_vals = np.empty(nq, np.uint64)
+            if out_found is None:
+                out_found = np.empty(nq, np.uint8)
+        if out_vals is False:
+            out_vals = None
+        return out_vals, out_found
+
+    # -- introspection
+    def info(self) -> Info:
+        h = _Header()
+        _check(lib().hm_info(self._h, C.byref(h)))
+        return Info(h.key_kind, h.n, h.S, h.seed, h.t1, h.t0, h.ctx_bytes)
+
+    def header_bytes(self) -> bytes:
+        h = _Header()
+        _check(lib().hm_info(self._h, C.byref(h)))
+        return bytes(h)
+
+    def export(self):
+        """Host copies (dir uint64[n], slots structured[S], ctx uint8[] | None)."""
+        inf = self.info()
+        d = np.empty(inf.n, np.uint64)
+        sd = SLOT_U64_DTYPE if self.key_kind == 0 else SLOT_BYTES_DTYPE
+        raw = np.empty(max(1, inf.S) * sd.itemsize, np.uint8)
+        ctx = np.empty(max(1, inf.ctx_bytes), np.uint8) if self.key_kind == 1 else None
+        _check(lib().hm_export(self._h, d.ctypes.data_as(C.c_void_p), raw.ctypes.data_as(C.c_void_p),
+                               ctx.ctypes.data_as(C.c_void_p) if ctx is not None else None))
+        slots = raw[: inf.S * sd.itemsize].view(sd)
+        if ctx is not None:
+            ctx = ctx[: inf.ctx_bytes]
+        return d, slots, ctx
+
+    def free(self):
+        if self._h and self._h.value:
+            lib().hm_free(self._h)
+            self._h = C.c_void_p(0)
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+    # -- shards (multi-GPU)
+    def set_base(self, slot_base: int):
+        _check(lib().hm_shard_set_base(self._h, slot_base))
+
+    def route_queries(self, q, world: int, send_q, perm, counts, stream=None):
+        qp, qk = _ptr(q)
+        sp, sk = _ptr(send_q)
+        pp, pk = _ptr(perm)
+        cp, ck = _ptr(counts)
+        _check(lib().hm_route_queries_u64(self._h, qp, _numel(q), world, sp, pp, cp, _stream(stream)))
+
+
+def route_u64(keys, vals, n_global: int, seed: int, t1: int, world: int, send_keys, send_vals, counts, stream=None):
+    kp, kk = _ptr(keys)
+    vp, vk = _ptr(vals)
+    sk, skk = _ptr(send_keys)
+    sv, svk = _ptr(send_vals)
+    cp, ck = _ptr(counts)
+    _check(lib().hm_route_u64(kp, vp, _numel(keys), n_global, seed, t1, world, sk, sv, cp, _stream(stream)))
+
+
+def build_u64_shard(keys, vals, n_global: int, b_lo: int, b_hi: int, t1: int, seed: int = 0, stream=None,
+                    log2_bp: int = 0):
+    kp, kk = _ptr(keys)
+    vp, vk = _ptr(vals)
+    h = C.c_void_p()
+    S = C.c_uint64()
+    o = _opts(seed, log2_bp)
+    _check(lib().hm_build_u64_shard(kp, vp, _numel(keys), n_global, b_lo, b_hi, t1, C.byref(o), _stream(stream),
+                                    C.byref(h), C.byref(S)))
+    return HashMap(h.value, 0), int(S.value)
+
+
+def unroute_u64(vals_routed, found_routed, perm, out_vals, out_found, stream=None):
+    a, ak = _ptr(vals_routed)
+    b, bk = _ptr(found_routed)
+    p, pk = _ptr(perm)
+    v, vk = _ptr(out_vals)
+    f, fk = _ptr(out_found)
+    _check(lib().hm_unroute_u64(a, b, p, _numel(perm), v, f, _stream(stream)))
+
+
+def version() -> str:
+    return lib().hm_version().decode()

@@ -1,0 +1,179 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle.
+
+Bit-exact on every byte of the exported table (header fields, directory,
+slots, context copy) and on every lookup output — all integer work
+(DESIGN.md §5).  Sizes span many build partitions plus ragged tails; the
+edge cases are the method's degenerate ones (n=1, tiny n with level-1
+redraws, duplicates, empty strings).
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from workloads import gen
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def _hm():
+    from paper_2508_11443_b200 import hm
+    return hm
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a).view(np.int64)).cuda()
+
+
+def host(t):
+    return t.cpu().numpy().view(np.uint64) if t.dtype == torch.int64 else t.cpu().numpy()
+
+
+def assert_table_equal(m, ot):
+    d, slots, ctx = m.export()
+    inf = m.info()
+    assert inf.n == ot.n and inf.S == ot.S
+    assert inf.t1 == int(ot.header["t1"]) and inf.t0 == int(ot.header["t0"])
+    assert inf.seed == int(ot.header["seed"])
+    assert m.header_bytes() == ot.header_bytes()
+    bad = np.nonzero(d != ot.dir)[0]
+    assert len(bad) == 0, f"dir differs at {bad[:10]} gpu={d[bad[:3]]} oracle={ot.dir[bad[:3]]}"
+    assert slots.tobytes() == ot.slots.tobytes(), "slots differ"
+    if ctx is not None:
+        assert ctx.tobytes() == ot.ctx.tobytes()
+
+
+U64_CASES = [
+    (1, 0, 0), (2, 0, 0), (5, 0, 0), (7, 3, 0), (100, 1, 0), (1000, 2, 0), (4133, 5, 0),
+    (1 << 14, 0, 0), (50_000, 7, 0), (1 << 16, 0, 0), (1 << 16, 11, 0),
+    # forced small partitions: many CTAs, long look-back chains, ragged last partition
+    (70_001, 3, 6), (1 << 17, 4, 9), (300_007, 0, 12),
+]
+
+
+@pytest.mark.parametrize("n,seed,log2_bp", U64_CASES)
+def test_u64_build_and_lookup_parity(n, seed, log2_bp):
+    hm = _hm()
+    keys, vals = gen.u64_keys(n), gen.u64_values(n)
+    ot = O.build_u64(keys, vals, seed)
+    m = hm.HashMap.build_u64(dev(keys), dev(vals), seed=seed, log2_bp=log2_bp)
+    assert_table_equal(m, ot)
+    nq = max(2 * n, 1000)
+    q, exp_found, exp_vals = gen.u64_queries(n, nq)
+    ov, of = O.lookup_u64(ot, q)
+    assert np.array_equal(of.astype(bool), exp_found) and np.array_equal(ov, exp_vals)
+    gv, gf = m.lookup(dev(q))
+    torch.cuda.synchronize()
+    assert np.array_equal(host(gv), ov) and np.array_equal(host(gf), of)
+    # membership only (no values)
+    gf2 = m.contains(dev(q))
+    assert np.array_equal(host(gf2), of)
+    m.free()
+
+
+def test_u64_many_seeds_small():
+    hm = _hm()
+    for n in (3, 6, 8, 13, 31):
+        keys, vals = gen.u64_keys(n, lo=n * 1000), gen.u64_values(n)
+        for seed in range(0, 60):
+            ot = O.build_u64(keys, vals, seed)
+            m = hm.HashMap.build_u64(dev(keys), dev(vals), seed=seed)
+            assert_table_equal(m, ot)
+            m.free()
+
+
+def test_u64_order_invariance_and_host_path():
+    hm = _hm()
+    n = 123_457
+    keys, vals = gen.u64_keys(n), gen.u64_values(n)
+    perm = np.random.default_rng(0).permutation(n)
+    m1 = hm.HashMap.build_u64(dev(keys), dev(vals), seed=9)
+    m2 = hm.HashMap.build_u64(dev(keys[perm]), dev(vals[perm]), seed=9)
+    m3 = hm.HashMap.build_u64(keys[perm], vals[perm], seed=9)  # host (numpy) buffers
+    d1, s1, _ = m1.export()
+    for m in (m2, m3):
+        d, s, _ = m.export()
+        assert d.tobytes() == d1.tobytes() and s.tobytes() == s1.tobytes()
+    q, f, v = gen.u64_queries(n, 10_000)
+    hv, hf = m3.lookup(q)  # host in, host out
+    assert np.array_equal(hv, v) and np.array_equal(hf.astype(bool), f)
+
+
+def test_u64_error_cases():
+    hm = _hm()
+    with pytest.raises(hm.HMError) as e:
+        hm.HashMap.build_u64(dev(np.array([7, 7], np.uint64)), dev(np.array([1, 2], np.uint64)))
+    assert e.value.name == "DUPLICATE_KEY"
+    with pytest.raises(hm.HMError) as e:
+        hm.HashMap.build_u64(dev(np.full(5, 9, np.uint64)), dev(np.arange(5, dtype=np.uint64)))
+    assert e.value.name == "SEED_EXHAUSTED"
+    keys = gen.u64_keys(100_000)
+    keys[77_777] = keys[12]
+    with pytest.raises(hm.HMError) as e:
+        hm.HashMap.build_u64(dev(keys), dev(gen.u64_values(100_000)))
+    assert e.value.name == "DUPLICATE_KEY"
+    with pytest.raises(O.OracleError) as eo:
+        O.build_u64(keys, gen.u64_values(100_000), 0)
+    assert eo.value.name == "DUPLICATE_KEY"
+    with pytest.raises(hm.HMError) as e:
+        hm.HashMap.build_u64(dev(np.zeros(0, np.uint64)), dev(np.zeros(0, np.uint64)))
+    assert e.value.name == "EMPTY"
+
+
+def test_u64_adversarial_values_and_keys():
+    """Keys at the edges of u64 (0, 2^64-1, P, P+5, 2^32 boundaries)."""
+    hm = _hm()
+    P = (1 << 61) - 1
+    special = [0, 1, (1 << 64) - 1, P, P + 5, 1 << 32, (1 << 32) - 1, (1 << 63), 5]
+    keys = np.array(special + list(gen.u64_keys(991)), np.uint64)
+    vals = np.array([(1 << 64) - 1 - i for i in range(len(keys))], np.uint64)
+    for seed in range(5):
+        ot = O.build_u64(keys, vals, seed)
+        m = hm.HashMap.build_u64(dev(keys), dev(vals), seed=seed)
+        assert_table_equal(m, ot)
+        gv, gf = m.lookup(dev(keys))
+        assert host(gf).all() and np.array_equal(host(gv), vals)
+
+
+# ------------------------------------------------------------------ strings
+
+STR_CASES = [(1, 0), (2, 1), (50, 0), (1000, 3), (20_000, 0), (70_000, 5)]
+
+
+@pytest.mark.parametrize("n,seed", STR_CASES)
+def test_bytes_build_and_lookup_parity(n, seed):
+    hm = _hm()
+    ctx, offs = gen.string_keys(n)
+    vals = gen.u64_values(n) + np.uint64(1)
+    ot = O.build_bytes(ctx, offs, vals, seed)
+    m = hm.HashMap.build_bytes(torch.from_numpy(ctx).cuda(), dev(offs), dev(vals), seed=seed)
+    assert_table_equal(m, ot)
+    qctx, qoffs, f, v = gen.string_queries(n, max(2 * n, 500))
+    ov, of = O.lookup_bytes(ot, qctx, qoffs)
+    gv, gf = m.lookup_bytes(torch.from_numpy(qctx).cuda(), dev(qoffs))
+    assert np.array_equal(host(gv), ov) and np.array_equal(host(gf), of)
+    m.free()
+
+
+def test_bytes_edge_strings_and_offsets():
+    hm = _hm()
+    strs = [b"", b"ab", b"ab\0", b"\0", b"\0\0\0\0", b"\0\0\0\0\0", b"x" * 64, b"y" * 1000, b"abc", b"abcd"]
+    ctx, offs = gen.pack_bytes_list(strs)
+    # non-zero first offset: the map copies bytes[offsets[0]..offsets[n])
+    pre = np.frombuffer(b"PREFIX!", np.uint8)
+    ctx2 = np.concatenate([pre, ctx])
+    offs2 = offs + np.uint64(len(pre))
+    vals = np.arange(10, 10 + len(strs), dtype=np.uint64)
+    for seed in range(6):
+        ot = O.build_bytes(ctx2, offs2, vals, seed)
+        m = hm.HashMap.build_bytes(torch.from_numpy(ctx2).cuda(), dev(offs2), dev(vals), seed=seed)
+        assert_table_equal(m, ot)
+        needles = strs + [b"a", b"ab\0\0", b"x" * 63, b"y" * 999 + b"z", b"PREFIX!"]
+        qc, qo = gen.pack_bytes_list(needles)
+        ov, of = O.lookup_bytes(ot, qc, qo)
+        gv, gf = m.lookup_bytes(qc, qo)  # host needles
+        assert np.array_equal(gv, ov) and np.array_equal(gf, of)
+    with pytest.raises(hm.HMError) as e:
+        c, o = gen.pack_bytes_list([b"hello", b"world", b"hello"])
+        hm.HashMap.build_bytes(torch.from_numpy(c).cuda(), dev(o), dev(np.arange(3, dtype=np.uint64)))
+    assert e.value.name == "DUPLICATE_KEY"
