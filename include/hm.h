@@ -154,6 +154,9 @@ hm_status hm_export(const hm_map* map, uint64_t* host_dir, void* host_slots, uin
 const char* hm_status_str(hm_status s);
 const char* hm_last_error(void); /* thread-local; "" if none */
 const char* hm_version(void);
+/* Number of CUDA kernels this library has launched in this process (all
+ * devices, all threads): the evidence bench.py reports as gpu_launches. */
+uint64_t hm_kernel_launches(void);
 
 /* ------------------------------------------------- multi-GPU building blocks
  * Bucket-range sharding: with G ranks and the

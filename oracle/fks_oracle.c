@@ -315,11 +315,11 @@ static int or_same_u64(void* ctx, uint64_t i, uint64_t j) {
 /* Fill the table (R10): every key at h k, every unused slot
  * of a non-empty bucket gets the bucket member at its lowest occupied slot
  * (value 0).  `occupant[j]` = item index + 1 at slot j, 0 if unused. */
-static void or_occupancy(const uint64_t* dir, uint64_t n, const uint64_t* member_slot,
-                         uint64_t S, uint64_t* occupant) {
+static void or_occupancy(const uint64_t* dir, uint64_t nb, const uint64_t* member_slot,
+                         uint64_t nkeys, uint64_t S, uint64_t* occupant) {
   for (uint64_t j = 0; j < S; j++) occupant[j] = 0;
-  for (uint64_t i = 0; i < n; i++) occupant[member_slot[i]] = i + 1;
-  for (uint64_t b = 0; b < n; b++) {
+  for (uint64_t i = 0; i < nkeys; i++) occupant[member_slot[i]] = i + 1;
+  for (uint64_t b = 0; b < nb; b++) {
     uint64_t s = (dir[b] >> 40) & 0xFFFF;
     if (s == 0) continue;
     uint64_t soff = dir[b] & ((1ULL << 40) - 1);
@@ -364,7 +364,7 @@ int or_build_u64(const uint64_t* keys, const uint64_t* vals, uint64_t n, uint64_
   if (st != OR_OK) { free(dir); free(mslot); return st; }
   uint64_t* occ = (uint64_t*)malloc(sizeof(uint64_t) * S);
   or_slot_u64* slots = (or_slot_u64*)calloc(S ? S : 1, sizeof(or_slot_u64));
-  or_occupancy(dir, n, mslot, S, occ);
+  or_occupancy(dir, n, mslot, n, S, occ);
   for (uint64_t j = 0; j < S; j++) {
     uint64_t o = occ[j];
     uint64_t i = (o & ~(1ULL << 63)) - 1;
@@ -467,7 +467,7 @@ int or_build_bytes(const uint8_t* bytes, const uint64_t* offsets, const uint64_t
   }
   uint64_t* occ = (uint64_t*)malloc(sizeof(uint64_t) * S);
   or_slot_bytes* slots = (or_slot_bytes*)calloc(S ? S : 1, sizeof(or_slot_bytes));
-  or_occupancy(dir, n, mslot, S, occ);
+  or_occupancy(dir, n, mslot, n, S, occ);
   for (uint64_t j = 0; j < S; j++) {
     uint64_t o = occ[j];
     uint64_t i = (o & ~(1ULL << 63)) - 1;
@@ -551,4 +551,95 @@ uint64_t or_level1_S(const uint64_t* keys, uint64_t n, uint64_t seed, uint32_t t
   uint64_t S = or_level1(seed, t1, keys, n, hashes, shape_out);
   free(hashes);
   return S;
+}
+
+/* ------------------------------------------------------------ shards
+ * The bucket-range shard of the logical table:
+ * buckets [b_lo, b_hi) of g k = hash(derive(seed,1,0,t1), k) mod n_global,
+ * built from exactly the keys whose bucket falls in the range, with the same
+ * steps 2-3 as or_fks (presum of s^2 over the range, make2 per bucket, R10
+ * filler).  dir has b_hi-b_lo entries with soff relative to the shard;
+ * concatenating the shards of all ranks, each soff shifted by the slot count of
+ * the ranks before it, gives the single table.  No level-1 loop: the caller
+ * checks the GLOBAL bound sum S_r <= 4 n_global (R7). */
+int or_build_u64_shard(const uint64_t* keys, const uint64_t* vals, uint64_t n_recv, uint64_t n_global,
+                       uint64_t b_lo, uint64_t b_hi, uint32_t t1, uint64_t seed, or_table** out) {
+  *out = NULL;
+  if (n_global == 0) return OR_ERR_EMPTY;
+  if (b_hi < b_lo || b_hi > n_global) return OR_ERR_INVALID_ARG;
+  uint64_t nb = b_hi - b_lo;
+  uint64_t c1[3];
+  or_derive(seed, 1, 0, t1, c1);
+  uint64_t* lb = (uint64_t*)malloc(sizeof(uint64_t) * (n_recv ? n_recv : 1));
+  for (uint64_t i = 0; i < n_recv; i++) {
+    uint64_t g = or_hash(c1, keys[i]) % n_global;
+    if (g < b_lo || g >= b_hi) { free(lb); return OR_ERR_INVALID_ARG; }
+    lb[i] = g - b_lo;
+  }
+  uint64_t* shape = (uint64_t*)calloc(nb ? nb : 1, sizeof(uint64_t));
+  uint64_t* ones = (uint64_t*)malloc(sizeof(uint64_t) * (n_recv ? n_recv : 1));
+  for (uint64_t i = 0; i < n_recv; i++) ones[i] = 1;
+  or_hist(nb, lb, ones, n_recv, shape);
+  free(ones);
+  uint64_t* sq = (uint64_t*)malloc(sizeof(uint64_t) * (nb ? nb : 1));
+  uint64_t* offsets = (uint64_t*)malloc(sizeof(uint64_t) * (nb + 1));
+  uint64_t* gstart = (uint64_t*)malloc(sizeof(uint64_t) * (nb + 1));
+  uint64_t* gitems = (uint64_t*)malloc(sizeof(uint64_t) * (n_recv ? n_recv : 1));
+  for (uint64_t b = 0; b < nb; b++) sq[b] = shape[b] * shape[b];
+  or_presum(sq, nb, offsets);
+  or_groupby(nb, lb, n_recv, gstart, gitems);
+  uint64_t S = offsets[nb];
+  uint64_t* dir = (uint64_t*)malloc(sizeof(uint64_t) * (nb ? nb : 1));
+  uint64_t* mslot = (uint64_t*)malloc(sizeof(uint64_t) * (n_recv ? n_recv : 1));
+  uint64_t* bkeys = (uint64_t*)malloc(sizeof(uint64_t) * (n_recv ? n_recv : 1));
+  uint64_t* bhs = (uint64_t*)malloc(sizeof(uint64_t) * (n_recv ? n_recv : 1));
+  int dup = 0, exhausted = 0, bound = 0;
+  for (uint64_t b = 0; b < nb; b++) {
+    uint64_t s = shape[b], soff = offsets[b];
+    const uint64_t* items = gitems + gstart[b];
+    dir[b] = OR_DIR(soff, s, 0);
+    if (s == 0) continue;
+    if (s * s > 4 * n_global) { bound = 1; continue; }
+    int skip = 0;
+    for (uint64_t i = 0; i < s; i++)
+      for (uint64_t j = i + 1; j < s; j++)
+        if (keys[items[i]] == keys[items[j]]) { dup = 1; skip = 1; }
+    if (skip) continue;
+    if (s == 1) { mslot[items[0]] = soff; continue; }
+    for (uint64_t i = 0; i < s; i++) bkeys[i] = keys[items[i]];
+    int t = or_make2(seed, b_lo + b, bkeys, s, bhs);
+    if (t < 0) { exhausted = 1; continue; }
+    for (uint64_t i = 0; i < s; i++) mslot[items[i]] = soff + bhs[i];
+    dir[b] = OR_DIR(soff, s, (uint64_t)t);
+  }
+  free(bkeys); free(bhs); free(lb); free(shape); free(sq); free(offsets); free(gstart); free(gitems);
+  or_table* tb = (or_table*)calloc(1, sizeof(or_table));
+  tb->hdr.magic = OR_MAGIC;
+  tb->hdr.spec_version = OR_SPEC_VERSION;
+  tb->hdr.n = nb;
+  tb->hdr.S = S;
+  tb->hdr.seed = seed;
+  tb->hdr.t1 = t1;
+  tb->dir = dir;
+  if (!dup && !exhausted && !bound && S <= 4 * n_global) {
+    uint64_t* occ = (uint64_t*)malloc(sizeof(uint64_t) * (S ? S : 1));
+    or_slot_u64* slots = (or_slot_u64*)calloc(S ? S : 1, sizeof(or_slot_u64));
+    or_occupancy(dir, nb, mslot, n_recv, S, occ);
+    for (uint64_t j = 0; j < S; j++) {
+      uint64_t o = occ[j];
+      uint64_t i = (o & ~(1ULL << 63)) - 1;
+      slots[j].key = keys[i];
+      slots[j].value = (o >> 63) ? 0 : vals[i];
+    }
+    free(occ);
+    tb->slots = slots;
+  } else {
+    tb->slots = calloc(1, sizeof(or_slot_u64));
+    tb->hdr.S = (bound && S <= 4 * n_global) ? 4 * n_global + 1 : S;
+  }
+  free(mslot);
+  *out = tb;
+  if (dup) return OR_ERR_DUPLICATE_KEY;
+  if (exhausted) return OR_ERR_SEED_EXHAUSTED;
+  return OR_OK;
 }

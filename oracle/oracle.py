@@ -85,6 +85,8 @@ def lib():
         L.or_build_bytes.argtypes = [p, p, p, u64, u64, C.POINTER(p)]
         L.or_lookup_u64.argtypes = [p, p, u64, p, p]
         L.or_lookup_bytes.argtypes = [p, p, p, u64, p, p]
+        L.or_build_u64_shard.restype = C.c_int
+        L.or_build_u64_shard.argtypes = [p, p, u64, u64, u64, u64, u32, u64, C.POINTER(p)]
         L.or_table_free.argtypes = [p]
         L.or_table_header.argtypes = [p, p]
         L.or_table_dir.restype = p
@@ -222,6 +224,21 @@ def build_u64(keys, vals, seed: int = 0) -> Table:
     if st != 0:
         raise OracleError(st)
     return _wrap(h.value, 0)
+
+
+def build_u64_shard(keys, vals, n_global: int, b_lo: int, b_hi: int, t1: int, seed: int = 0):
+    """(status_name, Table) of one bucket-range shard (fks_oracle.c or_build_u64_shard)."""
+    keys, vals = _u64(keys), _u64(vals)
+    h = C.c_void_p()
+    kb = keys if len(keys) else np.zeros(1, np.uint64)
+    vb = vals if len(vals) else np.zeros(1, np.uint64)
+    st = lib().or_build_u64_shard(_ptr(kb), _ptr(vb), len(keys), n_global, b_lo, b_hi, t1, seed, C.byref(h))
+    if not h.value:
+        raise OracleError(st)
+    t = _wrap(h.value, 0)
+    if st != 0:
+        t.slots = t.slots[:0]
+    return STATUS[st], t
 
 
 def lookup_u64(t: Table, q):

@@ -13,16 +13,18 @@
 //        hist of the partition's buckets, exclusive scans of s
 //        and s^2 (presum, PAPER.md:229-230 with R1/R2), groupby
 //        as a counting scatter of (key, index) into bucket order, the level-2
-//        seed search make2 per bucket — thread-per-bucket
-//        with a register occupancy bitmap for s <= 16, warp-per-bucket with
-//        __match_any_sync for 16 < s <= 32 — then a decoupled look-back across
-//        partitions for the global slot base, and the coalesced write of the
-//        directory and of the s^2 slots of every bucket (members + filler, R10).
+//        seed search make2 per bucket — a group of G lanes
+//        per bucket (G = 2/4/8/32 by size class), one attempt per loop
+//        iteration, __match_any_sync as the injectivity test — then a
+//        decoupled look-back across partitions for the global slot base, and
+//        the write of the directory and of the s^2 slots of every bucket
+//        (members + filler, R10).
 //
 // One host synchronisation per attempt reads the device status (total S for
 // the space bound R7, duplicate / exhaustion flags).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "hm_internal.cuh"
@@ -122,55 +124,12 @@ __device__ __forceinline__ uint32_t cur_get(const uint32_t* scur, uint32_t lb) {
   return (lb & 1) ? (w >> 16) : (w & 0xFFFFu);
 }
 
-// 256-bit occupancy bitmap in four registers (s^2 <= 256).
-struct Bits256 {
-  uint64_t w0, w1, w2, w3;
-  __device__ __forceinline__ void clear() { w0 = w1 = w2 = w3 = 0; }
-  __device__ __forceinline__ bool test_set(uint32_t h) {
-    const uint64_t bit = 1ull << (h & 63);
-    const uint32_t k = h >> 6;
-    const uint64_t w = k == 0 ? w0 : k == 1 ? w1 : k == 2 ? w2 : w3;
-    const bool was = (w & bit) != 0;
-    if (k == 0) w0 |= bit;
-    else if (k == 1) w1 |= bit;
-    else if (k == 2) w2 |= bit;
-    else w3 |= bit;
-    return was;
-  }
-  __device__ __forceinline__ bool test(uint32_t h) const {
-    const uint32_t k = h >> 6;
-    const uint64_t w = k == 0 ? w0 : k == 1 ? w1 : k == 2 ? w2 : w3;
-    return (w >> (h & 63)) & 1;
-  }
-};
-
-// make2 for 2 <= s <= 16: first attempt t whose level-2
-// hashes mod s^2 are pairwise distinct (`collision`, as a
-// register bitmap).  Returns kT2Cap when exhausted (R8).
-__device__ uint32_t search_small(uint64_t smix, uint64_t b, const uint64_t* keys, uint32_t s, uint64_t m2) {
-  const FastMod fm{uint64_t(s) * s, m2};
-  for (uint32_t t = 0; t < kT2Cap; t++) {
-    const Consts c = derive(smix, 2, b, t);
-    Bits256 bm;
-    bm.clear();
-    bool ok = true;
-    for (uint32_t j = 0; j < s; j++) {
-      const uint32_t h = uint32_t(fastmod(hash64(c, keys[j]), fm));
-      if (bm.test_set(h)) {
-        ok = false;
-        break;
-      }
-    }
-    if (ok) return t;
-  }
-  return kT2Cap;
-}
-
 // ------------------------------------------------------------------ K_A
 template <class Src, class E, int KPT, bool kSmemHist>
 __global__ void __launch_bounds__(kAThreads) k_partition(Src src, BuildParams bp, E* __restrict__ pbuf,
                                                          unsigned int* __restrict__ pcount,
                                                          DevStatus* __restrict__ stt) {
+  constexpr uint32_t kNone = 0x7FFFFFFFu, kLead = 0x80000000u;
   extern __shared__ unsigned int s_hist[];
   const uint32_t tid = threadIdx.x;
   if (kSmemHist) {
@@ -187,10 +146,11 @@ __global__ void __launch_bounds__(kAThreads) k_partition(Src src, BuildParams bp
 #pragma unroll
     for (int j = 0; j < KPT; j++) {
       const uint64_t idx = base + uint64_t(j) * kAThreads + tid;
-      pp[j] = 0xFFFFFFFFu;
+      pp[j] = kNone;
       rk[j] = 0;
       if (idx < bp.n_in) e[j] = src.load(idx);
     }
+    // g k = hash(c1, k) mod n -> owning partition; rank within the tile
 #pragma unroll
     for (int j = 0; j < KPT; j++) {
       const uint64_t idx = base + uint64_t(j) * kAThreads + tid;
@@ -205,15 +165,31 @@ __global__ void __launch_bounds__(kAThreads) k_partition(Src src, BuildParams bp
       }
     }
     if (kSmemHist) {
+      // one global reservation per (tile, partition), issued back to back by
+      // the rank-0 element of each partition: counts first, then independent
+      // atomics, then the bases
       __syncthreads();
 #pragma unroll
       for (int j = 0; j < KPT; j++)
-        if (pp[j] != 0xFFFFFFFFu && rk[j] == 0) s_hist[pp[j]] = atomicAdd(&pcount[pp[j]], s_hist[pp[j]]);
+        if (pp[j] != kNone && rk[j] == 0) {
+          rk[j] = s_hist[pp[j]];
+          pp[j] |= kLead;
+        }
+#pragma unroll
+      for (int j = 0; j < KPT; j++)
+        if (pp[j] & kLead) rk[j] = atomicAdd(&pcount[pp[j] & ~kLead], rk[j]);
+#pragma unroll
+      for (int j = 0; j < KPT; j++)
+        if (pp[j] & kLead) {
+          pp[j] &= ~kLead;
+          s_hist[pp[j]] = rk[j];
+          rk[j] = 0;
+        }
       __syncthreads();
     }
 #pragma unroll
     for (int j = 0; j < KPT; j++) {
-      if (pp[j] == 0xFFFFFFFFu) continue;
+      if (pp[j] == kNone) continue;
       const uint32_t pos = (kSmemHist ? s_hist[pp[j]] : 0u) + rk[j];
       if (pos < bp.cap) pbuf[size_t(pp[j]) * bp.cap + pos] = e[j];
       else ovf = true;
@@ -222,7 +198,7 @@ __global__ void __launch_bounds__(kAThreads) k_partition(Src src, BuildParams bp
       __syncthreads();
 #pragma unroll
       for (int j = 0; j < KPT; j++)
-        if (pp[j] != 0xFFFFFFFFu && rk[j] == 0) s_hist[pp[j]] = 0;
+        if (pp[j] != kNone && rk[j] == 0) s_hist[pp[j]] = 0;
       __syncthreads();
     }
   }
@@ -231,25 +207,55 @@ __global__ void __launch_bounds__(kAThreads) k_partition(Src src, BuildParams bp
 }
 
 // ------------------------------------------------------------------ K_B
+// Size classes of multi-key buckets and the lane-group width G that searches
+// one bucket: s=2 -> 2 lanes, s=3..4 -> 4, s=5..8 -> 8, s=9..32 -> 32.
+constexpr int kNCls = 4;
+__device__ __forceinline__ int size_class(uint32_t s) { return s == 2 ? 0 : s <= 4 ? 1 : s <= 8 ? 2 : s <= 32 ? 3 : 4; }
+__device__ __forceinline__ int class_log2g(int c) { return c == 0 ? 1 : c == 1 ? 2 : c == 2 ? 3 : 5; }
+
+template <class E>
+__device__ __forceinline__ E shfl_elem(const E& e, int src) {
+  constexpr int W = sizeof(E) / 8;
+  const uint64_t* p = reinterpret_cast<const uint64_t*>(&e);
+  E out;
+  uint64_t* q = reinterpret_cast<uint64_t*>(&out);
+#pragma unroll
+  for (int w = 0; w < W; w++) q[w] = __shfl_sync(0xffffffffu, p[w], src);
+  return out;
+}
+
+// Dynamic shared memory of k_bucket (all offsets 16-byte aligned).
+struct BucketSmem {
+  size_t sA, sidx, scur, ssoff, st, slist, total;
+};
+__host__ __device__ __forceinline__ size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
+__host__ __device__ __forceinline__ BucketSmem bucket_smem_layout(uint32_t cap, uint32_t BP) {
+  BucketSmem L;
+  L.sA = 0;                                            // u16[cap]: bucket of element i, later h of position
+  L.sidx = L.sA + al16(size_t(cap) * 2);               // u16[cap]: grouped position -> element index
+  L.scur = L.sidx + al16(size_t(cap) * 2);             // u32[BP/2+1]: packed u16 counts -> starts -> ends
+  L.ssoff = L.scur + al16((size_t(BP) / 2 + 1) * 4);   // u32[BP]: slot offset of the bucket within the partition
+  L.st = L.ssoff + al16(size_t(BP) * 4);               // u8[BP]: attempt t of the bucket
+  L.slist = L.st + al16(BP);                           // u16[cap/2+8]: multi-key buckets grouped by class
+  L.total = L.slist + al16((size_t(cap) / 2 + 8) * 2);
+  return L;
+}
+
 template <class E, class Same>
-__global__ void __launch_bounds__(kBThreads, 1)
+__global__ void __launch_bounds__(kBThreads, 2)
     k_bucket(BuildParams bp, const E* __restrict__ pbuf, const unsigned int* __restrict__ pcount,
              unsigned long long* __restrict__ lbstate, uint64_t* __restrict__ dir, E* __restrict__ slots,
              DevStatus* __restrict__ stt, Same same) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint64_t s_m2[33];
-  __shared__ uint32_t s_p, s_nbig;
-  __shared__ uint32_t s_big[kMaxBig];
-  __shared__ uint64_t s_bigsoff[kMaxBig];
+  __shared__ uint32_t s_p;
   __shared__ unsigned long long s_red[kBWarps];
   __shared__ unsigned long long s_base;
+  __shared__ uint32_t s_cls_off[kNCls + 1];
   __shared__ uint32_t s_bits[kBWarps][32];
 
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) {
-    s_p = atomicAdd(&stt->ticket, 1u);
-    s_nbig = 0;
-  }
+  if (tid == 0) s_p = atomicAdd(&stt->ticket, 1u);
   if (tid < 33) s_m2[tid] = tid ? ~0ull / (uint64_t(tid) * tid) : 0ull;
   __syncthreads();
   const uint32_t p = s_p;
@@ -260,132 +266,195 @@ __global__ void __launch_bounds__(kBThreads, 1)
   const uint32_t cnt_raw = pcount[p];
   const bool ovf = cnt_raw > cap;
   const uint32_t cnt = ovf ? 0u : cnt_raw;
-
-  uint64_t* skeys = reinterpret_cast<uint64_t*>(smem);
-  uint16_t* sidx = reinterpret_cast<uint16_t*>(smem + ((size_t(cap) * 8 + 15) & ~size_t(15)));
-  uint32_t* scur = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(sidx) + ((size_t(cap) * 2 + 15) & ~size_t(15)));
+  const BucketSmem SL = bucket_smem_layout(cap, BP);
+  uint16_t* sA = reinterpret_cast<uint16_t*>(smem + SL.sA);
+  uint16_t* sidx = reinterpret_cast<uint16_t*>(smem + SL.sidx);
+  uint32_t* scur = reinterpret_cast<uint32_t*>(smem + SL.scur);
+  uint32_t* ssoff = reinterpret_cast<uint32_t*>(smem + SL.ssoff);
+  uint8_t* s_t = smem + SL.st;
+  uint16_t* slist = reinterpret_cast<uint16_t*>(smem + SL.slist);
   const uint32_t ncw = BP / 2 + 1;
-  uint8_t* s_t = reinterpret_cast<uint8_t*>(scur) + ((size_t(ncw) * 4 + 15) & ~size_t(15));
-
   for (uint32_t w = tid; w < ncw; w += kBThreads) scur[w] = 0;
   __syncthreads();
   const E* part = pbuf + size_t(p) * cap;
-  const uint64_t bbase = bp.b_lo + lb0;  // global id of local bucket 0 of this partition
+  const uint64_t bbase = bp.b_lo + lb0;  // global id of the partition's first bucket
 
-  // pass 1 — hist n hashes (rep n 1) restricted to this partition
+  // pass 1 — hist n hashes (rep n 1) on this partition's buckets
   for (uint32_t i = tid; i < cnt; i += kBThreads) {
-    const uint64_t k = part[i].key;
-    const uint32_t lb = uint32_t(level1_bucket(bp.l1, k) - bbase);
+    const uint32_t lb = uint32_t(level1_bucket(bp.l1, part[i].key) - bbase);
+    sA[i] = uint16_t(lb);
     atomicAdd(&scur[lb >> 1], 1u << ((lb & 1) * 16));
   }
   __syncthreads();
 
-  // exclusive scan of s (grouping offsets) and sum of s^2
+  // scans over a contiguous chunk of CH buckets per thread: group starts
+  // (presum of s), slot offsets (presum of s^2, R1/R2),
+  // and the class lists of multi-key buckets in bucket order.
   const uint32_t CH = max(2u, BP / kBThreads);
   const uint32_t c0 = tid * CH, c1 = min(c0 + CH, nbp);
-  uint32_t lcnt = 0, maxs = 0;
-  unsigned long long lsq = 0;
-  for (uint32_t j = c0; j < c1; j += 2) {
-    const uint32_t w = scur[j >> 1], a = w & 0xFFFFu, b2 = w >> 16;
-    lcnt += a + b2;
-    lsq += uint64_t(a) * a + uint64_t(b2) * b2;
-    maxs = max(maxs, max(a, b2));
-  }
-  unsigned long long tot_cnt, S_p;
-  const unsigned long long excl = block_excl_scan(lcnt, &tot_cnt, s_red);
-  (void)block_excl_scan(lsq, &S_p, s_red);
-  {
-    uint32_t run = uint32_t(excl);
-    for (uint32_t j = c0; j < c1; j += 2) {
-      const uint32_t w = scur[j >> 1], a = w & 0xFFFFu, b2 = w >> 16;
-      scur[j >> 1] = run | ((run + a) << 16);
-      run += a + b2;
+  uint32_t lcnt = 0, lsq = 0, maxs = 0;
+  unsigned long long lcls = 0;
+  for (uint32_t j = c0; j < c1; j++) {
+    const uint32_t v = cur_get(scur, j);
+    lcnt += v;
+    lsq += v * v;
+    maxs = max(maxs, v);
+    if (v >= 2) {
+      const int c = size_class(v);
+      if (c < kNCls && uint64_t(v) * v <= bp.bound4n) lcls += 1ull << (16 * c);
     }
   }
-  if (uint64_t(maxs) * maxs > bp.bound4n) atomicOr(&stt->bound_fail, 1u);
-  // publish this partition's aggregate early (decoupled look-back)
+  unsigned long long totA, totB;
+  const unsigned long long exA = block_excl_scan(uint64_t(lcnt) | (uint64_t(lsq) << 32), &totA, s_red);
+  const unsigned long long exB = block_excl_scan(lcls, &totB, s_red);
+  const unsigned long long S_p = totA >> 32;
+  if (tid == 0) {
+    s_cls_off[0] = 0;
+    for (int c = 0; c < kNCls; c++) s_cls_off[c + 1] = s_cls_off[c] + uint32_t((totB >> (16 * c)) & 0xFFFF);
+  }
+  __syncthreads();
+  {
+    uint32_t run = uint32_t(exA & 0xFFFFFFFFu), fsq = uint32_t(exA >> 32);
+    uint32_t ccur[kNCls];
+#pragma unroll
+    for (int c = 0; c < kNCls; c++) ccur[c] = s_cls_off[c] + uint32_t((exB >> (16 * c)) & 0xFFFF);
+    bool huge = false, bfail = false;
+    for (uint32_t j = c0; j < c1; j += 2) {
+      const uint32_t w = scur[j >> 1], a = w & 0xFFFFu, b2 = w >> 16;
+      scur[j >> 1] = run | ((run + a) << 16);  // starts of buckets j, j+1
+      run += a + b2;
+#pragma unroll
+      for (int k = 0; k < 2; k++) {
+        const uint32_t jj = j + k, v = k ? b2 : a;
+        if (jj >= c1) break;
+        ssoff[jj] = fsq;
+        fsq += v * v;
+        s_t[jj] = 0;
+        if (v >= 2) {
+          const int c = size_class(v);
+          if (uint64_t(v) * v > bp.bound4n) bfail = true;  // S > 4n: level one redraws
+          else if (c >= kNCls) huge = true;
+          else slist[ccur[c]++] = uint16_t(jj);
+        }
+      }
+    }
+    if (huge) atomicOr(&stt->huge, 1u);
+    if (bfail || uint64_t(maxs) * maxs > bp.bound4n) atomicOr(&stt->bound_fail, 1u);
+  }
+  // publish the partition's aggregate early (decoupled look-back)
   if (tid == 0) st_release(&lbstate[p], (p == 0 ? kFlagInc : kFlagAgg) | (S_p & kValMask));
   __syncthreads();
 
-  // pass 2 — groupby: counting scatter of (key, index) into bucket order
+  // pass 2 — groupby: counting scatter of element indices into bucket order
   for (uint32_t i = tid; i < cnt; i += kBThreads) {
-    const uint64_t k = part[i].key;
-    const uint32_t lb = uint32_t(level1_bucket(bp.l1, k) - bbase);
+    const uint32_t lb = sA[i];
     const uint32_t sh = (lb & 1) * 16;
     const uint32_t old = atomicAdd(&scur[lb >> 1], 1u << sh);
-    const uint32_t pos = (old >> sh) & 0xFFFFu;
-    skeys[pos] = k;
-    sidx[pos] = uint16_t(i);
+    sidx[(old >> sh) & 0xFFFFu] = uint16_t(i);
   }
   __syncthreads();
-  // from here: end(lb) = cur_get(lb), start(lb) = end(lb-1)
+  // from here: end(lb) = cur_get(lb), start(lb) = end(lb-1); sA[pos] holds level-2 slots
 
-  // level-2 seed search, map make2 over the buckets
-  for (uint32_t lb = tid; lb < nbp; lb += kBThreads) {
-    const uint32_t st0 = lb ? cur_get(scur, lb - 1) : 0u, s = cur_get(scur, lb) - st0;
-    uint32_t t = 0;
-    if (s >= 2 && uint64_t(s) * s <= bp.bound4n) {
-      if (s <= 16) {
-        // equal keys never separate: record and skip (§8(c) step 3)
-        bool skip = false;
-        for (uint32_t i = 0; i < s && !skip; i++)
-          for (uint32_t j = i + 1; j < s; j++)
-            if (skeys[st0 + i] == skeys[st0 + j]) {
-              const bool d = same.same(part[sidx[st0 + i]], part[sidx[st0 + j]]);
-              atomicOr(d ? &stt->dup : &stt->fpcoll, 1u);
-              skip = true;
-              break;
-            }
-        if (!skip) {
-          t = search_small(bp.smix, bbase + lb, skeys + st0, s, s_m2[s]);
-          if (t >= kT2Cap) {
-            atomicOr(&stt->exhausted, 1u);
-            t = 0;
-          }
-        }
-      } else if (s <= 32) {
-        const uint32_t k = atomicAdd(&s_nbig, 1u);
-        if (k < kMaxBig) s_big[k] = lb;
-        else atomicOr(&stt->huge, 1u);
+  // level-2 seed search, map make2 over the multi-key buckets.
+  // A group of G lanes owns one bucket; each loop iteration is one attempt t
+  // for every group: derive(seed,2,b,t), hash every member mod s^2, and
+  // __match_any_sync on (group, slot) finds collisions (`collision`,
+  // PAPER.md:280-282).  A group that succeeds takes the next bucket of its
+  // class, so lanes stay busy whatever the attempt counts are.
+  for (int c = 0; c < kNCls; c++) {
+    const int lg = class_log2g(c);
+    const uint32_t G = 1u << lg;
+    const uint32_t L = s_cls_off[c + 1] - s_cls_off[c];
+    const uint16_t* list = slist + s_cls_off[c];
+    const uint32_t gpw = 32u >> lg, NG = kBWarps * gpw;
+    const uint32_t gbase = lane & ~(G - 1), r = lane & (G - 1);
+    const uint32_t gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << gbase;
+    uint32_t idx = warp * gpw + (lane >> lg);
+    bool have = false;
+    uint32_t lb = 0, st0 = 0, s = 2, t = 0;
+    uint64_t key = 0, b = 0;
+    auto load = [&]() {
+      have = idx < L;
+      t = 0;
+      if (have) {
+        lb = list[idx];
+        st0 = lb ? cur_get(scur, lb - 1) : 0u;
+        s = cur_get(scur, lb) - st0;
+        b = bbase + lb;
+        key = r < s ? part[sidx[st0 + r]].key : 0ull;
+      }
+    };
+    load();
+    while (__any_sync(0xffffffffu, have)) {
+      const bool mine = have && r < s;
+      const Consts cc = derive(bp.smix, 2, b, t);
+      const uint32_t s2 = have ? s * s : 4u;
+      const FastMod fm{s2, s_m2[have ? s : 2u]};
+      const uint32_t h = uint32_t(fastmod(hash64(cc, key), fm));
+      // injectivity of the group's slots: an OR-reduced occupancy bitmap
+      // (s^2 <= 64) for G <= 8, __match_any_sync for the rare G = 32 class
+      bool gcoll;
+      if (G < 32) {
+        uint64_t bits = mine ? (1ull << h) : 0ull;
+#pragma unroll
+        for (uint32_t o = 1; o < 8; o <<= 1)
+          if (o < G) bits |= __shfl_xor_sync(0xffffffffu, bits, o);
+        gcoll = have && uint32_t(__popcll(bits)) < s;
       } else {
-        atomicOr(&stt->huge, 1u);
+        const uint32_t mh = __match_any_sync(0xffffffffu, mine ? h : (0x80000000u | lane));
+        gcoll = __any_sync(0xffffffffu, mine && __popc(mh) > 1);
       }
-    }
-    s_t[lb] = uint8_t(t);
-  }
-  __syncthreads();
-  const uint32_t nbig = min(s_nbig, uint32_t(kMaxBig));
-  // warp per bucket for 16 < s <= 32: lanes hold the members, match.any finds collisions
-  for (uint32_t bi = warp; bi < nbig; bi += kBWarps) {
-    const uint32_t lb = s_big[bi];
-    const uint32_t st0 = lb ? cur_get(scur, lb - 1) : 0u, s = cur_get(scur, lb) - st0;
-    const uint32_t mask = s == 32 ? 0xffffffffu : ((1u << s) - 1u);
-    uint32_t t = 0;
-    if (lane < s) {
-      const uint64_t k = skeys[st0 + lane];
-      const uint32_t m = __match_any_sync(mask, k);
-      const uint32_t leader = __ffs(m) - 1;
-      if (__popc(m) > 1 && leader != lane) {
-        const bool d = same.same(part[sidx[st0 + lane]], part[sidx[st0 + leader]]);
-        atomicOr(d ? &stt->dup : &stt->fpcoll, 1u);
-      }
-      const bool anydup = __any_sync(mask, __popc(m) > 1);
-      if (!anydup) {
-        const FastMod fm{uint64_t(s) * s, s_m2[s]};
-        for (t = 0; t < kT2Cap; t++) {
-          const Consts c = derive(bp.smix, 2, bbase + lb, t);
-          const uint32_t h = uint32_t(fastmod(hash64(c, k), fm));
-          const uint32_t mh = __match_any_sync(mask, h);
-          if (!__any_sync(mask, __popc(mh) > 1)) break;
+      // equal keys collide under every t, so only a bucket whose first
+      // attempt collides can hold duplicates: check those pairwise, once
+      const bool suspect = have && gcoll && t == 0;
+      bool gdup = false;
+      if (__any_sync(0xffffffffu, suspect)) {
+        bool dupl = false;
+        uint32_t other = 0;
+        if (G < 32) {
+          for (uint32_t d = 1; d < G; d++) {
+            const uint32_t rp = (r + d) & (G - 1);
+            const uint64_t pk = __shfl_sync(0xffffffffu, key, gbase + rp);
+            if (mine && rp < s && pk == key && !dupl) {
+              dupl = true;
+              other = rp;
+            }
+          }
+        } else {
+          const uint32_t valid = __ballot_sync(0xffffffffu, mine);
+          const uint32_t dm = __match_any_sync(0xffffffffu, key) & valid & ~(1u << lane);
+          dupl = mine && dm != 0;
+          other = dm ? __ffs(dm) - 1 : 0;
         }
-        if (t >= kT2Cap) {
-          if (lane == 0) atomicOr(&stt->exhausted, 1u);
+        const uint32_t dball = __ballot_sync(0xffffffffu, dupl);  // all lanes: no short-circuit
+        gdup = suspect && (dball & gmask) != 0;
+        if (gdup && dupl) {
+          const bool d = same.same(part[sidx[st0 + r]], part[sidx[st0 + other]]);
+          atomicOr(d ? &stt->dup : &stt->fpcoll, 1u);
+        }
+      }
+      bool done = false;
+      if (have) {
+        if (gdup) {
           t = 0;
+          done = true;
+        } else if (!gcoll) {
+          if (mine) sA[st0 + r] = uint16_t(h);
+          done = true;
+        } else if (t + 1 >= kT2Cap) {
+          if (r == 0) atomicOr(&stt->exhausted, 1u);
+          t = 0;
+          done = true;
+        } else {
+          t++;
         }
+        if (done && r == 0) s_t[lb] = uint8_t(t);
       }
-      if (lane == 0) s_t[lb] = uint8_t(t);
+      if (done) {
+        idx += NG;
+        load();
+      }
     }
-    __syncwarp();
   }
   __syncthreads();
 
@@ -418,84 +487,78 @@ __global__ void __launch_bounds__(kBThreads, 1)
     return;
   }
 
-  // write the directory (coalesced) and the s^2 slots of every bucket
-  unsigned long long running = base;
-  for (uint32_t cb = 0; cb < nbp; cb += kBThreads) {
-    const uint32_t lb = cb + tid;
-    uint32_t st0 = 0, s = 0, t = 0;
-    if (lb < nbp) {
-      st0 = lb ? cur_get(scur, lb - 1) : 0u;
-      s = cur_get(scur, lb) - st0;
-      t = s_t[lb];
-    }
-    unsigned long long tot;
-    const unsigned long long ex = block_excl_scan(uint64_t(s) * s, &tot, s_red);
-    if (lb < nbp) {
-      const uint64_t soff = running + ex;
-      dir[lb0 + lb] = dir_entry(soff, s, t);
-      if (s == 1) {
-        slots[soff] = part[sidx[st0]];  // R12: singleton at soff
-      } else if (s >= 2 && s <= 16 && uint64_t(s) * s <= bp.bound4n) {
-        const Consts c = derive(bp.smix, 2, bbase + lb, t);
-        const FastMod fm{uint64_t(s) * s, s_m2[s]};
-        Bits256 bm;
-        bm.clear();
-        uint32_t hmin = 0xFFFFFFFFu, jmin = 0;
-        for (uint32_t j = 0; j < s; j++) {
-          const uint32_t h = uint32_t(fastmod(hash64(c, skeys[st0 + j]), fm));
-          bm.test_set(h);
-          if (h < hmin) {
-            hmin = h;
-            jmin = j;
+  // directory (coalesced) and singleton slots (R12: a singleton sits at soff)
+  for (uint32_t lb = tid; lb < nbp; lb += kBThreads) {
+    const uint32_t st0 = lb ? cur_get(scur, lb - 1) : 0u, s = cur_get(scur, lb) - st0;
+    const uint64_t soff = base + ssoff[lb];
+    dir[lb0 + lb] = dir_entry(soff, s, s_t[lb]);
+    if (s == 1) slots[soff] = part[sidx[st0]];
+  }
+  // multi-key buckets: members at soff + h, every unused slot gets the
+  // lowest-slot member with value 0 (R10)
+  for (int c = 0; c < kNCls; c++) {
+    const int lg = class_log2g(c);
+    const uint32_t G = 1u << lg;
+    const uint32_t L = s_cls_off[c + 1] - s_cls_off[c];
+    const uint16_t* list = slist + s_cls_off[c];
+    const uint32_t gpw = 32u >> lg, NG = kBWarps * gpw;
+    const uint32_t gbase = lane & ~(G - 1), r = lane & (G - 1);
+    const uint32_t gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << gbase;
+    for (uint32_t i0 = 0; i0 < L; i0 += NG) {
+      const uint32_t idx = i0 + warp * gpw + (lane >> lg);
+      const bool have = idx < L;
+      uint32_t st0 = 0, s = 0, h = 0xFFFFu;
+      uint64_t soff = 0;
+      E e;
+      if (have) {
+        const uint32_t lb = list[idx];
+        st0 = lb ? cur_get(scur, lb - 1) : 0u;
+        s = cur_get(scur, lb) - st0;
+        soff = base + ssoff[lb];
+      }
+      const bool mine = have && r < s;
+      if (mine) {
+        h = sA[st0 + r];
+        e = part[sidx[st0 + r]];
+        slots[soff + h] = e;
+      }
+      uint32_t hmin = h;
+      if (G < 32) {
+        uint64_t bits = mine ? (1ull << h) : 0ull;
+#pragma unroll
+        for (uint32_t o = 1; o < 8; o <<= 1) {
+          if (o < G) {
+            bits |= __shfl_xor_sync(0xffffffffu, bits, o);
+            hmin = min(hmin, __shfl_xor_sync(0xffffffffu, hmin, o));
           }
-          slots[soff + h] = part[sidx[st0 + j]];
         }
-        // R10: unused slots of the bucket hold the lowest-slot member, value 0
-        E f = part[sidx[st0 + jmin]];
+        const uint32_t who = __ffs(__ballot_sync(0xffffffffu, mine && h == hmin) & gmask);
+        E f = shfl_elem(e, who ? who - 1 : lane);
         f.value = 0;
-        const uint32_t s2 = s * s;
-        for (uint32_t e = 0; e < s2; e++)
-          if (!bm.test(e)) slots[soff + e] = f;
-      } else if (s > 16 && s <= 32) {
-        for (uint32_t bi = 0; bi < nbig; bi++)
-          if (s_big[bi] == lb) s_bigsoff[bi] = soff;
+        if (have)
+          for (uint32_t x = r; x < s * s; x += G)
+            if (!((bits >> x) & 1)) slots[soff + x] = f;
+      } else {
+        s_bits[warp][lane] = 0;
+        __syncwarp();
+        if (mine) atomicOr(&s_bits[warp][h >> 5], 1u << (h & 31));
+        hmin = __reduce_min_sync(0xffffffffu, h);
+        const uint32_t who = __ffs(__ballot_sync(0xffffffffu, mine && h == hmin));
+        E f = shfl_elem(e, who ? who - 1 : lane);
+        f.value = 0;
+        __syncwarp();
+        if (have)
+          for (uint32_t x = lane; x < s * s; x += 32)
+            if (!((s_bits[warp][x >> 5] >> (x & 31)) & 1)) slots[soff + x] = f;
+        __syncwarp();
       }
     }
-    running += tot;
-  }
-  __syncthreads();
-  // slots of the 16 < s <= 32 buckets, warp per bucket
-  for (uint32_t bi = warp; bi < nbig; bi += kBWarps) {
-    const uint32_t lb = s_big[bi];
-    const uint32_t st0 = lb ? cur_get(scur, lb - 1) : 0u, s = cur_get(scur, lb) - st0;
-    const uint32_t s2 = s * s, t = s_t[lb];
-    const uint64_t soff = s_bigsoff[bi];
-    s_bits[warp][lane] = 0;
-    __syncwarp();
-    uint32_t h = 0xFFFFFFFFu;
-    if (lane < s) {
-      const Consts c = derive(bp.smix, 2, bbase + lb, t);
-      const FastMod fm{uint64_t(s2), s_m2[s]};
-      h = uint32_t(fastmod(hash64(c, skeys[st0 + lane]), fm));
-      atomicOr(&s_bits[warp][h >> 5], 1u << (h & 31));
-      slots[soff + h] = part[sidx[st0 + lane]];
-    }
-    const uint32_t hmin = __reduce_min_sync(0xffffffffu, h);
-    const uint32_t who = __ffs(__ballot_sync(0xffffffffu, h == hmin)) - 1;
-    __syncwarp();
-    E f = part[sidx[st0 + who]];
-    f.value = 0;
-    for (uint32_t e = lane; e < s2; e += 32)
-      if (!((s_bits[warp][e >> 5] >> (e & 31)) & 1)) slots[soff + e] = f;
-    __syncwarp();
   }
 }
 
 // ------------------------------------------------------------- host side
 static size_t bucket_smem_bytes(uint32_t cap, uint32_t log2_bp) {
-  const size_t BP = size_t(1) << log2_bp;
-  return ((size_t(cap) * 8 + 15) & ~size_t(15)) + ((size_t(cap) * 2 + 15) & ~size_t(15)) +
-         (((BP / 2 + 1) * 4 + 15) & ~size_t(15)) + ((BP + 15) & ~size_t(15));
+  return bucket_smem_layout(cap, 1u << log2_bp).total;
 }
 
 struct Plan {
@@ -506,9 +569,11 @@ struct Plan {
 static Plan make_plan(uint64_t n_in, uint64_t nb, uint32_t log2_req, size_t smem_limit) {
   Plan pl{};
   const int sms = num_sms();
-  uint32_t lg = log2_req ? log2_req : 14;
+  // 8K buckets per partition (two CTAs of k_bucket per SM); 16K when that
+  // would make more than 32K partitions (k_partition's shared histogram)
+  uint32_t lg = log2_req ? log2_req : ((nb >> 13) > 32768 ? 14 : 13);
   if (!log2_req) {
-    while (lg > 6 && (nb >> lg) < uint64_t(2 * sms)) lg--;
+    while (lg > 6 && (nb >> lg) < uint64_t(4 * sms)) lg--;
   }
   for (;; lg--) {
     const double BP = double(uint64_t(1) << lg);
@@ -605,7 +670,7 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
   // kernel configuration
   constexpr int KPT = sizeof(E) == 16 ? 16 : 8;
   const size_t smemA = size_t(pl.np) * 4;
-  const bool smemHist = smemA <= size_t(smem_optin) - 1024;
+  const bool smemHist = smemA <= size_t(smem_optin) - 1024 && !getenv("HM_KA_GLOBAL");
   auto kA_s = k_partition<Src, E, KPT, true>;
   auto kA_g = k_partition<Src, E, KPT, false>;
   auto kB = k_bucket<E, Same>;
@@ -641,11 +706,13 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
       HM_CUDA_TRY(cudaMemsetAsync(lbstate, 0, size_t(pl.np) * 8, st));
       HM_CUDA_TRY(cudaMemsetAsync(dstat, 0, sizeof(DevStatus), st));
       if (run_a && ntiles > 0) {
+        count_launch();
         if (smemHist) kA_s<<<gridA, kAThreads, smemA, st>>>(src, bp, pbuf, pcount, dstat);
         else kA_g<<<gridA, kAThreads, 0, st>>>(src, bp, pbuf, pcount, dstat);
         HM_CUDA_TRY(cudaGetLastError());
       }
       run_a = false;
+      count_launch();
       kB<<<pl.np, kBThreads, pl.smemB, st>>>(bp, pbuf, pcount, lbstate, dir, slots, dstat, same);
       HM_CUDA_TRY(cudaGetLastError());
       HM_CUDA_TRY(cudaMemcpyAsync(&hs, dstat, sizeof(hs), cudaMemcpyDeviceToHost, st));
@@ -658,7 +725,7 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
         set_error("build partition overflow (degenerate key distribution); not supported in this version");
         return fail(HM_ERR_TOO_LARGE);
       }
-      if (t1_fixed < 0 && (hs.S > 4 * n_global || hs.bound_fail)) break;  // R7: redraw level one
+      if (hs.S > 4 * n_global || hs.bound_fail) break;  // R7: redraw level one
       if (hs.slot_overflow && !(hs.bound_fail)) {
         // more slots than the allocation: grow to exactly S and rerun K_B
         cudaFreeAsync(slots, st);
@@ -673,7 +740,15 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
       }
       break;
     }
-    if (t1_fixed < 0 && (hs.S > 4 * n_global || hs.bound_fail)) continue;
+    if (hs.S > 4 * n_global || hs.bound_fail) {
+      if (t1_fixed < 0) continue;
+      // a shard with a fixed t1: report the failed bound, the caller redraws
+      out->dir = dir;
+      out->slots = slots;
+      out->S = std::max<uint64_t>(hs.S, 4 * n_global + 1);
+      out->t1 = t1;
+      return HM_OK;
+    }
     if (hs.huge) {
       set_error("a level-1 bucket with more than 32 keys (degenerate input); not supported in this version");
       if (hs.dup) return fail(HM_ERR_DUPLICATE_KEY);
@@ -733,6 +808,7 @@ __global__ void k_check_offsets(const uint64_t* __restrict__ offs, uint64_t n, u
 void launch_fingerprint(const uint8_t* bytes, const uint64_t* offs, uint64_t n, uint64_t r, uint64_t* fp,
                         cudaStream_t st) {
   const unsigned grid = unsigned(std::min<uint64_t>((n + 255) / 256, uint64_t(num_sms()) * 16));
+  count_launch();
   k_fingerprint<<<std::max(grid, 1u), 256, 0, st>>>(bytes, offs, n, r, fp);
 }
 
@@ -748,6 +824,7 @@ hm_status build_bytes_core(const uint8_t* bytes, const uint64_t* offsets, const 
   HM_CUDA_TRY(cudaMemsetAsync(bad, 0, 4, st));
   {
     const unsigned grid = unsigned(std::min<uint64_t>((n + 255) / 256, uint64_t(num_sms()) * 16));
+    count_launch();
     k_check_offsets<<<std::max(grid, 1u), 256, 0, st>>>(offsets, n, bad);
     HM_CUDA_TRY(cudaGetLastError());
   }

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -17,6 +18,9 @@
 namespace hm {
 
 static thread_local std::string g_last_error;
+static std::atomic<uint64_t> g_launches{0};
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 void set_error(const std::string& s) { g_last_error = s; }
 
@@ -137,6 +141,8 @@ using namespace hm;
 extern "C" {
 
 const char* hm_version(void) { return "hm 0.1 (sm_100a, spec v1)"; }
+
+uint64_t hm_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
 
 const char* hm_last_error(void) { return g_last_error.c_str(); }
 

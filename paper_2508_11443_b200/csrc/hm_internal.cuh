@@ -89,6 +89,7 @@ void set_error(const std::string& s);
 hm_status cuda_fail(cudaError_t e, const char* where);
 L1Params make_l1(uint64_t smix, uint32_t t1, uint64_t n_global);
 int num_sms();
+void count_launch();  // one of our kernels was launched (hm_kernel_launches)
 
 // build.cu
 struct BuildOut {

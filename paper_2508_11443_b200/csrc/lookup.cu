@@ -18,14 +18,26 @@ __device__ __forceinline__ uint64_t ld_stream_u64(const uint64_t* p) {
   asm volatile("ld.global.nc.L1::no_allocate.u64 %0, [%1];" : "=l"(v) : "l"(p));
   return v;
 }
+// Random probes bypass L1 (.cg): an L1 miss would be promoted to a full
+// 128-byte line request, four times the one 32-byte sector a probe needs.
 __device__ __forceinline__ uint64_t ld_dir(const uint64_t* p) {
   uint64_t v;
-  asm volatile("ld.global.nc.L1::no_allocate.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  asm volatile("ld.global.cg.u64 %0, [%1];" : "=l"(v) : "l"(p));
   return v;
 }
 __device__ __forceinline__ KV16 ld_slot16(const KV16* p) {
   KV16 e;
-  asm volatile("ld.global.nc.L1::no_allocate.v2.u64 {%0, %1}, [%2];" : "=l"(e.key), "=l"(e.value) : "l"(p));
+  asm volatile("ld.global.cg.v2.u64 {%0, %1}, [%2];" : "=l"(e.key), "=l"(e.value) : "l"(p));
+  return e;
+}
+__device__ __forceinline__ KV32 ld_slot32(const KV32* p) {
+  KV32 e;
+  uint64_t w3;
+  asm volatile("ld.global.cg.v4.u64 {%0, %1, %2, %3}, [%4];"
+               : "=l"(e.key), "=l"(e.value), "=l"(e.ctx_off), "=l"(w3)
+               : "l"(p));
+  e.len = uint32_t(w3);
+  e.reserved = uint32_t(w3 >> 32);
   return e;
 }
 __device__ __forceinline__ void st_stream_u64(uint64_t* p, uint64_t v) {
@@ -110,6 +122,7 @@ hm_status lookup_u64_launch(const hm_map* m, const uint64_t* q, uint64_t nq, uin
   const uint64_t per = uint64_t(kLThreads) * QPT;
   const uint64_t blocks = (nq + per - 1) / per;
   const unsigned grid = unsigned(std::min<uint64_t>(blocks, uint64_t(num_sms()) * 8));
+  count_launch();
   k_lookup_u64<QPT><<<grid, kLThreads, 0, st>>>(lp, q, nq, out_vals, out_found);
   HM_CUDA_TRY(cudaGetLastError());
   return HM_OK;
@@ -153,7 +166,7 @@ __global__ void __launch_bounds__(kLThreads) k_lookup_bytes(LookupParams lp, con
       bool hit = false;
       uint64_t v = 0;
       if (((d[j] >> 40) & 0xFFFF) != 0) {
-        const KV32 e = slots[slot_index(lp.smix, b[j] + lp.b_lo, d[j], fp[j], s_m2)];
+        const KV32 e = ld_slot32(slots + slot_index(lp.smix, b[j] + lp.b_lo, d[j], fp[j], s_m2));
         if (e.key == fp[j] && e.len == len[j]) {
           const uint8_t* a = lp.ctx + e.ctx_off;
           const uint8_t* c = qb + off[j];
@@ -188,6 +201,7 @@ hm_status lookup_bytes_launch(const hm_map* m, const uint8_t* qb, const uint64_t
   const uint64_t per = uint64_t(kLThreads) * QPT;
   const uint64_t blocks = (nq + per - 1) / per;
   const unsigned grid = unsigned(std::min<uint64_t>(blocks, uint64_t(num_sms()) * 8));
+  count_launch();
   k_lookup_bytes<QPT><<<grid, kLThreads, 0, st>>>(lp, qb, qo, nq, out_vals, out_found);
   HM_CUDA_TRY(cudaGetLastError());
   return HM_OK;
@@ -254,8 +268,11 @@ static hm_status route_common(const uint64_t* keys, const uint64_t* vals, uint64
   cudaError_t e = cudaMemsetAsync(counts, 0, size_t(world) * 8, st);
   const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, uint64_t(num_sms()) * 8)));
   if (e == cudaSuccess && n) {
+    count_launch();
     k_route_count<<<grid, 256, 0, st>>>(keys, n, l1, world, reinterpret_cast<unsigned long long*>(counts));
+    count_launch();
     k_route_prefix<<<1, 32, 0, st>>>(reinterpret_cast<unsigned long long*>(counts), world, cur);
+    count_launch();
     k_route_scatter<<<grid, 256, 0, st>>>(keys, vals, n, l1, world, cur, sk, sv, perm);
     e = cudaGetLastError();
   }
@@ -288,6 +305,7 @@ hm_status unroute_launch(const uint64_t* vr, const uint8_t* fr, const uint64_t* 
                          uint8_t* of, cudaStream_t st) {
   if (!nq) return HM_OK;
   const unsigned grid = unsigned(std::min<uint64_t>((nq + 255) / 256, uint64_t(num_sms()) * 8));
+  count_launch();
   k_unroute<<<grid, 256, 0, st>>>(vr, fr, perm, nq, ov, of);
   HM_CUDA_TRY(cudaGetLastError());
   return HM_OK;

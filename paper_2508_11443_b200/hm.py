@@ -76,6 +76,7 @@ def lib():
         L.hm_status_str.argtypes = [i32]
         L.hm_last_error.restype = C.c_char_p
         L.hm_version.restype = C.c_char_p
+        L.hm_kernel_launches.restype = C.c_uint64
         L.hm_route_u64.argtypes = [p, p, u64, u64, u64, u32, i32, p, p, p, p]
         L.hm_build_u64_shard.argtypes = [p, p, u64, u64, u64, u64, u32, C.POINTER(_Opts), p, C.POINTER(p),
                                          C.POINTER(u64)]
@@ -308,6 +309,11 @@ def unroute_u64(vals_routed, found_routed, perm, out_vals, out_found, stream=Non
     v, vk = _ptr(out_vals)
     f, fk = _ptr(out_found)
     _check(lib().hm_unroute_u64(a, b, p, _numel(perm), v, f, _stream(stream)))
+
+
+def kernel_launches() -> int:
+    """Kernels launched by libhm so far in this process."""
+    return int(lib().hm_kernel_launches())
 
 
 def version() -> str:

@@ -6,6 +6,11 @@ from paper_2508_11443_b200 import hm
 from workloads import gen_cuda
 
 def main(log2n=26, reps=5):
+    if os.environ.get("L2FG"):
+        from cuda.bindings import runtime as cudart
+        torch.cuda.init(); torch.zeros(1, device='cuda')
+        print("set L2 fetch granularity", os.environ["L2FG"], cudart.cudaDeviceSetLimit(cudart.cudaLimit.cudaLimitMaxL2FetchGranularity, int(os.environ["L2FG"])),
+              cudart.cudaDeviceGetLimit(cudart.cudaLimit.cudaLimitMaxL2FetchGranularity))
     n = 1 << log2n
     k, v = gen_cuda.u64_keys(n)
     q, ev, ef = gen_cuda.u64_queries(n, n, with_expect=True)
