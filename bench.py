@@ -1,0 +1,374 @@
+#!/usr/bin/env python
+"""bench.py — FKS build + batched lookup on B200 (BASELINE.json metric).
+
+One step = one pass of the whole hot path over one batch:
+build the FKS table from n device-resident (key, value) pairs (level-1 hash,
+partition, per-bucket histogram/scans, level-2 seed search, table write) and
+answer n lookups at 50% hit rate (PAPER.md:903-915 workload shape, recipe in
+DESIGN.md §3), then free the table.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N=1: BASELINE.json configs[1] — 2^26 random distinct u64 keys with u64
+values, 2^26 lookups at 50% hit.  N>1 (torchrun, one process per GPU): every
+rank holds 2^26 keys and 2^26 queries of one global table of N*2^26 keys,
+bucket-range sharded with NCCL all-to-all (weak scaling).
+Inputs are larger than L2 (126 MB), so no L2 flush is needed between steps.
+
+`value` = keys processed per second (one key = one key built + one query
+answered) over all ranks, timed with CUDA events between barriers, max over
+ranks.  The JSON line also carries the separate build and lookup rates, the
+roofline of the dominant kernel (live CUDA-event timing of every libhm launch,
+hm_profile_*), the oracle's CPU baseline, the end-to-end rate through the
+C-ABI with pinned host buffers, the clocks seen during the timed region and
+the number of libhm kernel launches.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FKS build Mkeys/s and lookup Mqueries/s, u64 & string keys, 1–8 B200"
+LOG2N = 26
+LOOKUP_BYTES_PER_QUERY = 8 + 32 + 32 * (0.5 + 0.5 * (1 - 0.36787944117)) + 8 + 1  # 75.1 B
+BUILD_BYTES_PER_KEY = 56.0  # read key+value 16, dir 8, slots 16*S/n (~32)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region (200 ms)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev: int):
+        self.dev = dev
+        self.lines = []
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-lms", "200", "-i", str(self.dev)], stdout=subprocess.PIPE,
+                                      stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.p = None
+
+    def _read(self):
+        for line in self.p.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.p:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            f = [x.strip() for x in l.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_baseline(log2n_sample: int = 24):
+    """The oracle as it stands, single-threaded, on a bounded sample of the same workload."""
+    from oracle import oracle as O
+    from workloads import gen
+    n = 1 << log2n_sample
+    k, v = gen.u64_keys(n), gen.u64_values(n)
+    q, _, _ = gen.u64_queries(n, n)
+    t0 = time.perf_counter()
+    t = O.build_u64(k, v, 0)
+    t1 = time.perf_counter()
+    O.lookup_u64(t, q)
+    t2 = time.perf_counter()
+    return {"value": round(n / (t2 - t0) / 1e6, 4), "unit": "Mkeys/s", "cores": 1, "kind": "oracle",
+            "sample": f"2^{log2n_sample} keys built + 2^{log2n_sample} lookups (same recipe), one pass",
+            "build_mkeys_s": round(n / (t1 - t0) / 1e6, 4), "lookup_mq_s": round(n / (t2 - t1) / 1e6, 4)}
+
+
+def run_reference(args):
+    """--impl reference: the oracle (plain C, one core) timed on bounded samples."""
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return 0
+    from oracle import oracle as O
+    from workloads import gen
+    ls = 22
+    n = 1 << ls
+    k, v = gen.u64_keys(n), gen.u64_values(n)
+    q, _, _ = gen.u64_queries(n, n)
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        t = O.build_u64(k, v, 0)
+        O.lookup_u64(t, q)
+        del t
+        if i >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    ms = 1e3 * statistics.mean(times)
+    val = n / (ms / 1e3) / 1e6
+    sample = f"each step: oracle pass over 2^{ls} keys + 2^{ls} lookups of the config workload"
+    out = {
+        "impl": "reference", "metric": METRIC, "value": round(val, 4), "unit": "Mkeys/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic (workloads/gen.py recipe)",
+        "config": config_dict(world),
+        "cpu_baseline": {"value": round(val, 4), "unit": "Mkeys/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": round(val, 4), "unit": "Mkeys/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+def config_dict(world):
+    return {"workload": "configs[1]: 2^26 random distinct u64 keys + u64 values, build + 2^26 lookups at 50% hit"
+            + (" per rank; global table of %d*2^26 keys bucket-range sharded over NCCL" % world if world > 1 else ""),
+            "keys_per_gpu": 1 << LOG2N, "queries_per_gpu": 1 << LOG2N, "global_keys": world << LOG2N,
+            "hit_rate": 0.5, "key_type": "u64", "value_type": "u64", "table_seed": 0,
+            "seeds": {"SEED_K": 1, "SEED_Q": 2}, "parallelism": f"bucket-range shards x{world}" if world > 1 else "1 GPU",
+            "l2": "inputs (512 MiB keys, 512 MiB values, 512 MiB queries) exceed the 126 MB L2; no flush"}
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as tdist
+
+    from paper_2508_11443_b200 import dist, hm
+    from workloads import gen_cuda
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    def barrier():
+        if world > 1:
+            tdist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        return float(t.item())
+
+    n = 1 << LOG2N
+    n_global = n * world
+    keys, vals = gen_cuda.u64_keys(n, lo=rank * n)
+    q, ev, ef = gen_cuda.u64_queries(n_global, n, lo=rank * n, with_expect=True)
+    ov = torch.empty(n, dtype=torch.int64, device=dev)
+    of = torch.empty(n, dtype=torch.uint8, device=dev)
+    torch.cuda.synchronize()
+
+    def step(ev_b=None):
+        if world == 1:
+            m = hm.HashMap.build_u64(keys, vals, seed=0)
+            if ev_b is not None:
+                ev_b.record()
+            m.lookup(q, ov, of)
+            m.free()
+        else:
+            dm = dist.build_dist(keys, vals, seed=0)
+            if ev_b is not None:
+                ev_b.record()
+            v, f = dist.lookup_dist(dm, q)
+            ov.copy_(v)
+            of.copy_(f)
+            dist.free_dist(dm)
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    # ---------------------------------------------------------------- timed
+    clk = ClockSampler(local)
+    clk.start()
+    time.sleep(0.3)
+    hm.profile_read()
+    hm.profile_enable(True)
+    l0 = hm.kernel_launches()
+    barrier()
+    e_start = torch.cuda.Event(enable_timing=True)
+    e_end = torch.cuda.Event(enable_timing=True)
+    marks = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+              torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    e_start.record()
+    for (a, b, c) in marks:
+        a.record()
+        step(b)
+        c.record()
+    e_end.record()
+    barrier()
+    launches = hm.kernel_launches() - l0
+    hm.profile_enable(False)
+    kstats = hm.profile_read()
+    clocks = clk.stop()
+    total_ms = max_over_ranks(e_start.elapsed_time(e_end))
+    build_ms = max_over_ranks(sum(a.elapsed_time(b) for a, b, _ in marks) / args.steps)
+    look_ms = max_over_ranks(sum(b.elapsed_time(c) for _, b, c in marks) / args.steps)
+    ms = total_ms / args.steps
+    # correctness of the last step against the generator's ground truth
+    ok = bool(torch.equal(of, ef)) and bool(torch.equal(ov, ev))
+    okt = torch.tensor([1 if ok else 0], device=dev)
+    if world > 1:
+        tdist.all_reduce(okt, op=tdist.ReduceOp.MIN)
+    ok = bool(okt.item())
+
+    # ---------------------------------------------------------------- roofline
+    peak, peak_src = peaks()
+    per_step = {k: v[1] / args.steps for k, v in kstats.items()}
+    dom = max(per_step, key=per_step.get) if per_step else None
+    roof = None
+    if dom:
+        launches_dom, ms_dom = kstats[dom]
+        avg_ms = ms_dom / launches_dom
+        if dom.startswith("k_lookup"):
+            units, bpu, what = n * args.steps / launches_dom, LOOKUP_BYTES_PER_QUERY, "queries"
+        elif dom == "k_partition":
+            units, bpu, what = n * args.steps / launches_dom, 16.0, "keys"
+        else:
+            units, bpu, what = n * args.steps / launches_dom, BUILD_BYTES_PER_KEY - 16.0, "keys"
+        achieved = units * bpu / (avg_ms / 1e3) / 1e9
+        traffic = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+                summ = json.load(f)
+            if dom in summ.get("kernels", {}):
+                traffic = summ["kernels"][dom]["dram_bytes_per_launch"]
+        except Exception:
+            pass
+        roof = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
+                "algorithmic_bytes": f"{bpu:.2f} B per {what[:-1]} x {int(units)} {what} per launch",
+                "avg_launch_ms": round(avg_ms, 4), "share_of_step": round(per_step[dom] / ms, 4)}
+
+    # ---------------------------------------------------------------- e2e
+    e2e = None
+    if not args.no_e2e:
+        hk = keys.cpu().pin_memory()
+        hv = vals.cpu().pin_memory()
+        hq = q.cpu().pin_memory()
+        hov = torch.empty(n, dtype=torch.int64).pin_memory()
+        hof = torch.empty(n, dtype=torch.uint8).pin_memory()
+
+        def e2e_step():
+            if world == 1:
+                m = hm.HashMap.build_u64(hk, hv, seed=0)  # host buffers: staged inside the C-ABI
+                m.lookup(hq, hov, hof)  # host in, host out
+                m.free()
+            else:
+                dk, dv, dq = hk.to(dev, non_blocking=True), hv.to(dev, non_blocking=True), hq.to(dev, non_blocking=True)
+                dm = dist.build_dist(dk, dv, seed=0)
+                v, f = dist.lookup_dist(dm, dq)
+                hov.copy_(v)
+                hof.copy_(f)
+                dist.free_dist(dm)
+
+        for _ in range(2):
+            e2e_step()
+        barrier()
+        t0 = time.perf_counter()
+        es = torch.cuda.Event(enable_timing=True)
+        ee = torch.cuda.Event(enable_timing=True)
+        es.record()
+        ke = max(2, min(args.steps, 5))
+        for _ in range(ke):
+            e2e_step()
+        ee.record()
+        barrier()
+        e2e_ms = max_over_ranks(max(es.elapsed_time(ee), 1e3 * (time.perf_counter() - t0)) / ke)
+        e2e_ok = bool(torch.equal(hof, ef.cpu())) and bool(torch.equal(hov, ev.cpu()))
+        e2e = {"value": round(n * world / (e2e_ms / 1e3) / 1e6, 2), "unit": "Mkeys/s",
+               "h2d_bytes_per_step": 24 * n, "d2h_bytes_per_step": 9 * n, "ms_per_step": round(e2e_ms, 3),
+               "correct": e2e_ok, "path": "hm_build_u64/hm_lookup_u64 on pinned host buffers" if world == 1
+               else "H2D copy + dist.build_dist/lookup_dist + D2H copy"}
+
+    if rank != 0:
+        if world > 1:
+            tdist.destroy_process_group()
+        return 0
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline()
+    out = {
+        "metric": METRIC,
+        "value": round(n * world / (ms / 1e3) / 1e6, 2),
+        "unit": "Mkeys/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic: seeded splitmix64 key stream (workloads/gen.py, generated on device)",
+        "config": config_dict(world),
+        "build_mkeys_s": round(n * world / (build_ms / 1e3) / 1e6, 2),
+        "lookup_mq_s": round(n * world / (look_ms / 1e3) / 1e6, 2),
+        "build_ms": round(build_ms, 4), "lookup_ms": round(look_ms, 4),
+        "correct": ok,
+        "roofline": roof,
+        "kernels_ms_per_step": {k: round(v, 4) for k, v in sorted(per_step.items(), key=lambda x: -x[1])},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+    }
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        tdist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

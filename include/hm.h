@@ -158,6 +158,20 @@ const char* hm_version(void);
  * devices, all threads): the evidence bench.py reports as gpu_launches. */
 uint64_t hm_kernel_launches(void);
 
+/* Per-kernel device timing (diagnostics, used by bench.py for the roofline).
+ * While enabled, every kernel launch of this library is bracketed by two CUDA
+ * events recorded on the stream it is launched on.  hm_profile_read
+ * synchronises those events, aggregates them per kernel name since the last
+ * read, writes up to `max` entries to host array `out`, clears the record and
+ * returns the number of distinct kernels. */
+typedef struct {
+  char name[32];     /* kernel name, e.g. "k_bucket" */
+  uint64_t launches; /* launches since the last read */
+  double ms;         /* summed event-to-event device time */
+} hm_kernel_stat;
+void hm_profile_enable(int on);
+int hm_profile_read(hm_kernel_stat* out, int max);
+
 /* ------------------------------------------------- multi-GPU building blocks
  * Bucket-range sharding: with G ranks and the
  * global key count n (= number of level-1 buckets), rank r owns buckets

@@ -34,7 +34,6 @@ namespace hm {
 constexpr int kAThreads = 512;
 constexpr int kBThreads = 512;
 constexpr int kBWarps = kBThreads / 32;
-constexpr int kMaxBig = 64;  // buckets with 16 < s <= 32 per partition (expected ~1e-12)
 constexpr unsigned long long kFlagAgg = 1ull << 62, kFlagInc = 2ull << 62, kValMask = (1ull << 62) - 1;
 
 // ----------------------------------------------------------------- sources
@@ -706,14 +705,18 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
       HM_CUDA_TRY(cudaMemsetAsync(lbstate, 0, size_t(pl.np) * 8, st));
       HM_CUDA_TRY(cudaMemsetAsync(dstat, 0, sizeof(DevStatus), st));
       if (run_a && ntiles > 0) {
-        count_launch();
-        if (smemHist) kA_s<<<gridA, kAThreads, smemA, st>>>(src, bp, pbuf, pcount, dstat);
-        else kA_g<<<gridA, kAThreads, 0, st>>>(src, bp, pbuf, pcount, dstat);
+        {
+          LaunchScope ls_("k_partition", st);
+          if (smemHist) kA_s<<<gridA, kAThreads, smemA, st>>>(src, bp, pbuf, pcount, dstat);
+          else kA_g<<<gridA, kAThreads, 0, st>>>(src, bp, pbuf, pcount, dstat);
+        }
         HM_CUDA_TRY(cudaGetLastError());
       }
       run_a = false;
-      count_launch();
-      kB<<<pl.np, kBThreads, pl.smemB, st>>>(bp, pbuf, pcount, lbstate, dir, slots, dstat, same);
+      {
+        LaunchScope ls_("k_bucket", st);
+        kB<<<pl.np, kBThreads, pl.smemB, st>>>(bp, pbuf, pcount, lbstate, dir, slots, dstat, same);
+      }
       HM_CUDA_TRY(cudaGetLastError());
       HM_CUDA_TRY(cudaMemcpyAsync(&hs, dstat, sizeof(hs), cudaMemcpyDeviceToHost, st));
       HM_CUDA_TRY(cudaStreamSynchronize(st));
@@ -808,8 +811,10 @@ __global__ void k_check_offsets(const uint64_t* __restrict__ offs, uint64_t n, u
 void launch_fingerprint(const uint8_t* bytes, const uint64_t* offs, uint64_t n, uint64_t r, uint64_t* fp,
                         cudaStream_t st) {
   const unsigned grid = unsigned(std::min<uint64_t>((n + 255) / 256, uint64_t(num_sms()) * 16));
-  count_launch();
-  k_fingerprint<<<std::max(grid, 1u), 256, 0, st>>>(bytes, offs, n, r, fp);
+  {
+    LaunchScope ls_("k_fingerprint", st);
+    k_fingerprint<<<std::max(grid, 1u), 256, 0, st>>>(bytes, offs, n, r, fp);
+  }
 }
 
 hm_status build_bytes_core(const uint8_t* bytes, const uint64_t* offsets, const uint64_t* vals, uint64_t n,
@@ -824,8 +829,10 @@ hm_status build_bytes_core(const uint8_t* bytes, const uint64_t* offsets, const 
   HM_CUDA_TRY(cudaMemsetAsync(bad, 0, 4, st));
   {
     const unsigned grid = unsigned(std::min<uint64_t>((n + 255) / 256, uint64_t(num_sms()) * 16));
-    count_launch();
-    k_check_offsets<<<std::max(grid, 1u), 256, 0, st>>>(offsets, n, bad);
+    {
+      LaunchScope ls_("k_check_offsets", st);
+      k_check_offsets<<<std::max(grid, 1u), 256, 0, st>>>(offsets, n, bad);
+    }
     HM_CUDA_TRY(cudaGetLastError());
   }
   unsigned int hbad = 0;

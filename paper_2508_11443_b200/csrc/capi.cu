@@ -19,8 +19,49 @@ namespace hm {
 
 static thread_local std::string g_last_error;
 static std::atomic<uint64_t> g_launches{0};
+static std::atomic<int> g_profile{0};
 
-void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+struct ProfRec {
+  const char* name;
+  cudaEvent_t e0, e1;
+};
+static std::mutex g_prof_mu;
+static std::vector<ProfRec> g_prof_pending;
+static std::vector<cudaEvent_t> g_event_pool;
+
+static cudaEvent_t get_event() {
+  {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    if (!g_event_pool.empty()) {
+      cudaEvent_t e = g_event_pool.back();
+      g_event_pool.pop_back();
+      return e;
+    }
+  }
+  cudaEvent_t e = nullptr;
+  if (cudaEventCreate(&e) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return e;
+}
+
+LaunchScope::LaunchScope(const char* n, cudaStream_t s) : name(n), st(s) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (g_profile.load(std::memory_order_relaxed)) {
+    e0 = get_event();
+    if (e0) cudaEventRecord(e0, st);
+  }
+}
+
+LaunchScope::~LaunchScope() {
+  if (!e0) return;
+  cudaEvent_t e1 = get_event();
+  if (!e1) return;
+  cudaEventRecord(e1, st);
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_prof_pending.push_back({name, e0, e1});
+}
 
 void set_error(const std::string& s) { g_last_error = s; }
 
@@ -143,6 +184,45 @@ extern "C" {
 const char* hm_version(void) { return "hm 0.1 (sm_100a, spec v1)"; }
 
 uint64_t hm_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
+
+void hm_profile_enable(int on) { g_profile.store(on ? 1 : 0); }
+
+int hm_profile_read(hm_kernel_stat* out, int max) {
+  std::vector<ProfRec> recs;
+  {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    recs.swap(g_prof_pending);
+  }
+  std::vector<hm_kernel_stat> agg;
+  for (const ProfRec& r : recs) {
+    float ms = 0.f;
+    cudaEventSynchronize(r.e1);
+    if (cudaEventElapsedTime(&ms, r.e0, r.e1) != cudaSuccess) {
+      cudaGetLastError();
+      ms = 0.f;
+    }
+    size_t k = 0;
+    for (; k < agg.size(); k++)
+      if (std::strncmp(agg[k].name, r.name, sizeof(agg[k].name)) == 0) break;
+    if (k == agg.size()) {
+      hm_kernel_stat z{};
+      std::strncpy(z.name, r.name, sizeof(z.name) - 1);
+      agg.push_back(z);
+    }
+    agg[k].launches += 1;
+    agg[k].ms += ms;
+  }
+  {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    for (const ProfRec& r : recs) {
+      g_event_pool.push_back(r.e0);
+      g_event_pool.push_back(r.e1);
+    }
+  }
+  const int n = int(std::min<size_t>(agg.size(), size_t(max > 0 ? max : 0)));
+  for (int i = 0; i < n; i++) out[i] = agg[i];
+  return int(agg.size());
+}
 
 const char* hm_last_error(void) { return g_last_error.c_str(); }
 

@@ -89,7 +89,16 @@ void set_error(const std::string& s);
 hm_status cuda_fail(cudaError_t e, const char* where);
 L1Params make_l1(uint64_t smix, uint32_t t1, uint64_t n_global);
 int num_sms();
-void count_launch();  // one of our kernels was launched (hm_kernel_launches)
+// Scope around every kernel launch of this library: counts it
+// (hm_kernel_launches) and, when hm_profile_enable(1) is on, brackets it with
+// CUDA events recorded on the launching stream (hm_profile_read).
+struct LaunchScope {
+  const char* name;
+  cudaStream_t st;
+  cudaEvent_t e0 = nullptr;
+  LaunchScope(const char* n, cudaStream_t s);
+  ~LaunchScope();
+};
 
 // build.cu
 struct BuildOut {

@@ -122,8 +122,10 @@ hm_status lookup_u64_launch(const hm_map* m, const uint64_t* q, uint64_t nq, uin
   const uint64_t per = uint64_t(kLThreads) * QPT;
   const uint64_t blocks = (nq + per - 1) / per;
   const unsigned grid = unsigned(std::min<uint64_t>(blocks, uint64_t(num_sms()) * 8));
-  count_launch();
-  k_lookup_u64<QPT><<<grid, kLThreads, 0, st>>>(lp, q, nq, out_vals, out_found);
+  {
+    LaunchScope ls_("k_lookup_u64", st);
+    k_lookup_u64<QPT><<<grid, kLThreads, 0, st>>>(lp, q, nq, out_vals, out_found);
+  }
   HM_CUDA_TRY(cudaGetLastError());
   return HM_OK;
 }
@@ -201,8 +203,10 @@ hm_status lookup_bytes_launch(const hm_map* m, const uint8_t* qb, const uint64_t
   const uint64_t per = uint64_t(kLThreads) * QPT;
   const uint64_t blocks = (nq + per - 1) / per;
   const unsigned grid = unsigned(std::min<uint64_t>(blocks, uint64_t(num_sms()) * 8));
-  count_launch();
-  k_lookup_bytes<QPT><<<grid, kLThreads, 0, st>>>(lp, qb, qo, nq, out_vals, out_found);
+  {
+    LaunchScope ls_("k_lookup_bytes", st);
+    k_lookup_bytes<QPT><<<grid, kLThreads, 0, st>>>(lp, qb, qo, nq, out_vals, out_found);
+  }
   HM_CUDA_TRY(cudaGetLastError());
   return HM_OK;
 }
@@ -268,12 +272,18 @@ static hm_status route_common(const uint64_t* keys, const uint64_t* vals, uint64
   cudaError_t e = cudaMemsetAsync(counts, 0, size_t(world) * 8, st);
   const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, uint64_t(num_sms()) * 8)));
   if (e == cudaSuccess && n) {
-    count_launch();
-    k_route_count<<<grid, 256, 0, st>>>(keys, n, l1, world, reinterpret_cast<unsigned long long*>(counts));
-    count_launch();
-    k_route_prefix<<<1, 32, 0, st>>>(reinterpret_cast<unsigned long long*>(counts), world, cur);
-    count_launch();
-    k_route_scatter<<<grid, 256, 0, st>>>(keys, vals, n, l1, world, cur, sk, sv, perm);
+    {
+      LaunchScope ls_("k_route_count", st);
+      k_route_count<<<grid, 256, 0, st>>>(keys, n, l1, world, reinterpret_cast<unsigned long long*>(counts));
+    }
+    {
+      LaunchScope ls_("k_route_prefix", st);
+      k_route_prefix<<<1, 32, 0, st>>>(reinterpret_cast<unsigned long long*>(counts), world, cur);
+    }
+    {
+      LaunchScope ls_("k_route_scatter", st);
+      k_route_scatter<<<grid, 256, 0, st>>>(keys, vals, n, l1, world, cur, sk, sv, perm);
+    }
     e = cudaGetLastError();
   }
   cudaFreeAsync(cur, st);
@@ -305,8 +315,10 @@ hm_status unroute_launch(const uint64_t* vr, const uint8_t* fr, const uint64_t* 
                          uint8_t* of, cudaStream_t st) {
   if (!nq) return HM_OK;
   const unsigned grid = unsigned(std::min<uint64_t>((nq + 255) / 256, uint64_t(num_sms()) * 8));
-  count_launch();
-  k_unroute<<<grid, 256, 0, st>>>(vr, fr, perm, nq, ov, of);
+  {
+    LaunchScope ls_("k_unroute", st);
+    k_unroute<<<grid, 256, 0, st>>>(vr, fr, perm, nq, ov, of);
+  }
   HM_CUDA_TRY(cudaGetLastError());
   return HM_OK;
 }

@@ -77,6 +77,10 @@ def lib():
         L.hm_last_error.restype = C.c_char_p
         L.hm_version.restype = C.c_char_p
         L.hm_kernel_launches.restype = C.c_uint64
+        L.hm_profile_enable.argtypes = [C.c_int]
+        L.hm_profile_enable.restype = None
+        L.hm_profile_read.argtypes = [C.c_void_p, C.c_int]
+        L.hm_profile_read.restype = C.c_int
         L.hm_route_u64.argtypes = [p, p, u64, u64, u64, u32, i32, p, p, p, p]
         L.hm_build_u64_shard.argtypes = [p, p, u64, u64, u64, u64, u32, C.POINTER(_Opts), p, C.POINTER(p),
                                          C.POINTER(u64)]
@@ -309,6 +313,22 @@ def unroute_u64(vals_routed, found_routed, perm, out_vals, out_found, stream=Non
     v, vk = _ptr(out_vals)
     f, fk = _ptr(out_found)
     _check(lib().hm_unroute_u64(a, b, p, _numel(perm), v, f, _stream(stream)))
+
+
+class _KStat(C.Structure):
+    _fields_ = [("name", C.c_char * 32), ("launches", C.c_uint64), ("ms", C.c_double)]
+
+
+def profile_enable(on: bool = True):
+    """Bracket every libhm kernel launch with CUDA events on its stream."""
+    lib().hm_profile_enable(1 if on else 0)
+
+
+def profile_read() -> dict:
+    """{kernel name: (launches, device ms)} since the last read (synchronises the events)."""
+    buf = (_KStat * 64)()
+    n = lib().hm_profile_read(buf, 64)
+    return {buf[i].name.decode(): (int(buf[i].launches), float(buf[i].ms)) for i in range(min(n, 64))}
 
 
 def kernel_launches() -> int:
