@@ -61,8 +61,13 @@ typedef struct hm_map hm_map; /* opaque; immutable after build; bound to its dev
 typedef struct {
   uint64_t seed;       /* table seed: selects the constant schedule (R6). default 0  */
   uint32_t log2_bp;    /* 0 = auto. log2 of the level-1 buckets per build partition   */
-  uint32_t flags;      /* reserved, must be 0                                         */
+  uint32_t flags;      /* 0, or HM_FLAG_* below; other bits -> HM_ERR_INVALID_ARG     */
 } hm_opts;
+
+/* Lookups of this map bypass the L2-resident compact directory and read the
+ * full directory entry for every query (a testing/diagnostic knob: the
+ * results are identical, only slower).  The table itself is unchanged. */
+#define HM_FLAG_FULL_DIRECTORY 1u
 
 /* Table header, 56 bytes, little-endian (DESIGN.md §4 "Table layout"). */
 typedef struct {

@@ -243,8 +243,8 @@ __host__ __device__ __forceinline__ BucketSmem bucket_smem_layout(uint32_t cap, 
 template <class E, class Same>
 __global__ void __launch_bounds__(kBThreads, 2)
     k_bucket(BuildParams bp, const E* __restrict__ pbuf, const unsigned int* __restrict__ pcount,
-             unsigned long long* __restrict__ lbstate, uint64_t* __restrict__ dir, E* __restrict__ slots,
-             DevStatus* __restrict__ stt, Same same) {
+             unsigned long long* __restrict__ lbstate, uint64_t* __restrict__ dir, CDir* __restrict__ cdir,
+             E* __restrict__ slots, DevStatus* __restrict__ stt, Same same) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint64_t s_m2[33];
   __shared__ uint32_t s_p;
@@ -486,12 +486,38 @@ __global__ void __launch_bounds__(kBThreads, 2)
     return;
   }
 
-  // directory (coalesced) and singleton slots (R12: a singleton sits at soff)
-  for (uint32_t lb = tid; lb < nbp; lb += kBThreads) {
-    const uint32_t st0 = lb ? cur_get(scur, lb - 1) : 0u, s = cur_get(scur, lb) - st0;
-    const uint64_t soff = base + ssoff[lb];
-    dir[lb0 + lb] = dir_entry(soff, s, s_t[lb]);
-    if (s == 1) slots[soff] = part[sidx[st0]];
+  // directory (coalesced), compact directory record per 32 buckets (one per
+  // warp iteration), and singleton slots (R12: a singleton sits at soff)
+  for (uint32_t cb = 0; cb < nbp; cb += kBThreads) {
+    const uint32_t lb = cb + tid;
+    uint32_t s = 0, t = 0, st0 = 0;
+    uint64_t soff = 0;
+    if (lb < nbp) {
+      st0 = lb ? cur_get(scur, lb - 1) : 0u;
+      s = cur_get(scur, lb) - st0;
+      t = s_t[lb];
+      soff = base + ssoff[lb];
+      dir[lb0 + lb] = dir_entry(soff, s, t);
+      if (s == 1) slots[soff] = part[sidx[st0]];
+    }
+    uint32_t pa = __ballot_sync(0xffffffffu, s & 4), pb = __ballot_sync(0xffffffffu, s & 2),
+             pc = __ballot_sync(0xffffffffu, s & 1);
+    const uint32_t t0 = __ballot_sync(0xffffffffu, t & 1), t1 = __ballot_sync(0xffffffffu, t & 2),
+                   t2 = __ballot_sync(0xffffffffu, t & 4), t3 = __ballot_sync(0xffffffffu, t & 8);
+    if (__any_sync(0xffffffffu, s >= kCdirEscS || t >= kCdirEscT) || (bp.flags & HM_FLAG_FULL_DIRECTORY))
+      pa = pb = pc = 0xffffffffu;
+    if (lane == 0 && lb < nbp) {
+      CDir r;
+      r.w[0] = uint32_t(soff);
+      r.w[1] = pa;
+      r.w[2] = pb;
+      r.w[3] = pc;
+      r.w[4] = t0;
+      r.w[5] = t1;
+      r.w[6] = t2;
+      r.w[7] = t3;
+      cdir[(lb0 + lb) >> 5] = r;
+    }
   }
   // multi-key buckets: members at soff + h, every unused slot gets the
   // lowest-slot member with value 0 (R10)
@@ -631,6 +657,8 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
   int smem_optin = 0;
   HM_CUDA_TRY(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   const size_t static_smem_B = 4096;  // upper bound for k_bucket's static shared memory
+  const uint32_t knob_flags = log2_req >> 16;
+  log2_req &= 0xFFFFu;
   const Plan pl = make_plan(n_in, nb, log2_req, size_t(smem_optin) - static_smem_B);
   if (pl.smemB + static_smem_B > size_t(smem_optin)) {
     set_error("build plan does not fit in shared memory");
@@ -652,16 +680,23 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
 
   uint64_t* dir = nullptr;
   E* slots = nullptr;
+  CDir* cdir = nullptr;
   if ((s = dmalloc(&dir, nb * 8, st)) != HM_OK) return s;
+  if ((s = dmalloc(&cdir, ((nb + 31) / 32) * sizeof(CDir), st)) != HM_OK) {
+    cudaFreeAsync(dir, st);
+    return s;
+  }
   const double sn = double(n_in);
   uint64_t slot_cap = uint64_t(2.0 * sn + 8.0 * std::sqrt(2.0 * sn + 1.0) + 1024.0);
   if (n_in <= 4096) slot_cap = std::max<uint64_t>(slot_cap, 4 * std::max<uint64_t>(n_in, 1));
   if ((s = dmalloc(&slots, slot_cap * sizeof(E), st)) != HM_OK) {
     cudaFreeAsync(dir, st);
+    cudaFreeAsync(cdir, st);
     return s;
   }
   auto fail = [&](hm_status code) {
     cudaFreeAsync(dir, st);
+    cudaFreeAsync(cdir, st);
     cudaFreeAsync(slots, st);
     return code;
   };
@@ -692,6 +727,7 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
   bp.log2_bp = pl.log2_bp;
   bp.np = pl.np;
   bp.cap = pl.cap;
+  bp.flags = knob_flags;
 
   DevStatus hs{};
   const uint32_t t1_lo = t1_fixed >= 0 ? uint32_t(t1_fixed) : 0u;
@@ -715,7 +751,7 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
       run_a = false;
       {
         LaunchScope ls_("k_bucket", st);
-        kB<<<pl.np, kBThreads, pl.smemB, st>>>(bp, pbuf, pcount, lbstate, dir, slots, dstat, same);
+        kB<<<pl.np, kBThreads, pl.smemB, st>>>(bp, pbuf, pcount, lbstate, dir, cdir, slots, dstat, same);
       }
       HM_CUDA_TRY(cudaGetLastError());
       HM_CUDA_TRY(cudaMemcpyAsync(&hs, dstat, sizeof(hs), cudaMemcpyDeviceToHost, st));
@@ -737,6 +773,7 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
         bp.slot_cap = slot_cap;
         if ((s = dmalloc(&slots, slot_cap * sizeof(E), st)) != HM_OK) {
           cudaFreeAsync(dir, st);
+          cudaFreeAsync(cdir, st);
           return s;
         }
         continue;
@@ -747,6 +784,7 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
       if (t1_fixed < 0) continue;
       // a shard with a fixed t1: report the failed bound, the caller redraws
       out->dir = dir;
+    out->cdir = cdir;
       out->slots = slots;
       out->S = std::max<uint64_t>(hs.S, 4 * n_global + 1);
       out->t1 = t1;
@@ -774,6 +812,7 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
       return fail(HM_ERR_CUDA);
     }
     out->dir = dir;
+    out->cdir = cdir;
     out->slots = slots;
     out->S = hs.S;
     out->t1 = t1;

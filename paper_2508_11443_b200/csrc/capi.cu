@@ -251,7 +251,7 @@ hm_status hm_build_u64(const uint64_t* keys, const uint64_t* vals, uint64_t n, c
   if (n == 0) return HM_ERR_EMPTY;
   if (!keys || !vals) return HM_ERR_INVALID_ARG;
   if (n > (1ull << 30)) return HM_ERR_TOO_LARGE;
-  if (opts && opts->flags) return HM_ERR_INVALID_ARG;
+  if (opts && (opts->flags & ~uint32_t(HM_FLAG_FULL_DIRECTORY))) return HM_ERR_INVALID_ARG;
   hm_status s = check_device();
   if (s != HM_OK) return s;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -261,7 +261,7 @@ hm_status hm_build_u64(const uint64_t* keys, const uint64_t* vals, uint64_t n, c
   if ((s = sg.in(vals, n, &dv)) != HM_OK) return s;
   const uint64_t seed = opts ? opts->seed : 0;
   BuildOut bo;
-  s = build_u64_core(dk, dv, n, n, 0, n, -1, seed, opts ? opts->log2_bp : 0, st, &bo);
+  s = build_u64_core(dk, dv, n, n, 0, n, -1, seed, opts ? (opts->log2_bp | (opts->flags << 16)) : 0, st, &bo);
   if (s != HM_OK) return s;
   hm_map* m = new_map();
   m->key_kind = 0;
@@ -274,6 +274,7 @@ hm_status hm_build_u64(const uint64_t* keys, const uint64_t* vals, uint64_t n, c
   m->smix = seed_mix(seed);
   m->l1 = make_l1(m->smix, bo.t1, n);
   m->dir = bo.dir;
+  m->cdir = bo.cdir;
   m->slots = bo.slots;
   *out = m;
   return HM_OK;
@@ -287,7 +288,7 @@ hm_status hm_build_bytes(const uint8_t* bytes, const uint64_t* offsets, const ui
   if (n == 0) return HM_ERR_EMPTY;
   if (!offsets || !vals) return HM_ERR_INVALID_ARG;
   if (n > (1ull << 30)) return HM_ERR_TOO_LARGE;
-  if (opts && opts->flags) return HM_ERR_INVALID_ARG;
+  if (opts && (opts->flags & ~uint32_t(HM_FLAG_FULL_DIRECTORY))) return HM_ERR_INVALID_ARG;
   hm_status s = check_device();
   if (s != HM_OK) return s;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -316,7 +317,7 @@ hm_status hm_build_bytes(const uint8_t* bytes, const uint64_t* offsets, const ui
   BuildOut bo;
   uint32_t t0 = 0;
   uint64_t r = 0;
-  s = build_bytes_core(db, doff, dv, n, seed, opts ? opts->log2_bp : 0, st, &bo, &t0, &r);
+  s = build_bytes_core(db, doff, dv, n, seed, opts ? (opts->log2_bp | (opts->flags << 16)) : 0, st, &bo, &t0, &r);
   if (s != HM_OK) return s;
   hm_map* m = new_map();
   m->key_kind = 1;
@@ -330,6 +331,7 @@ hm_status hm_build_bytes(const uint8_t* bytes, const uint64_t* offsets, const ui
   m->smix = seed_mix(seed);
   m->l1 = make_l1(m->smix, bo.t1, n);
   m->dir = bo.dir;
+  m->cdir = bo.cdir;
   m->slots = bo.slots;
   m->ctx_bytes = on - o0;
   void* c = nullptr;
@@ -427,6 +429,7 @@ void hm_free(hm_map* map) {
   if (cur != map->device) cudaSetDevice(map->device);
   cudaDeviceSynchronize();
   if (map->dir) cudaFree(map->dir);
+  if (map->cdir) cudaFree(map->cdir);
   if (map->slots) cudaFree(map->slots);
   if (map->ctx) cudaFree(map->ctx);
   if (cur != map->device) cudaSetDevice(cur);
@@ -504,12 +507,13 @@ hm_status hm_build_u64_shard(const uint64_t* keys, const uint64_t* vals, uint64_
     m->smix = seed_mix(seed);
     m->l1 = make_l1(m->smix, t1, n_global);
     HM_CUDA_TRY(cudaMalloc(&m->dir, 16));
+    HM_CUDA_TRY(cudaMalloc(&m->cdir, sizeof(CDir)));
     HM_CUDA_TRY(cudaMalloc(&m->slots, 16));
     *S_local = 0;
     *out = m;
     return HM_OK;
   }
-  s = build_u64_core(keys, vals, n_recv, n_global, b_lo, nb, int(t1), seed, opts ? opts->log2_bp : 0, st, &bo);
+  s = build_u64_core(keys, vals, n_recv, n_global, b_lo, nb, int(t1), seed, opts ? (opts->log2_bp | (opts->flags << 16)) : 0, st, &bo);
   if (s != HM_OK) return s;
   hm_map* m = new_map();
   m->is_shard = true;
@@ -523,6 +527,7 @@ hm_status hm_build_u64_shard(const uint64_t* keys, const uint64_t* vals, uint64_
   m->smix = seed_mix(seed);
   m->l1 = make_l1(m->smix, t1, n_global);
   m->dir = bo.dir;
+  m->cdir = bo.cdir;
   m->slots = bo.slots;
   *S_local = bo.S;
   *out = m;

@@ -49,7 +49,7 @@ struct BuildParams {
   uint32_t log2_bp;   // buckets per partition = 1 << log2_bp
   uint32_t np;        // partitions
   uint32_t cap;       // partition capacity (elements)
-  uint32_t pad;
+  uint32_t flags;     // HM_FLAG_* (hm.h)
 };
 
 struct LookupParams {
@@ -57,6 +57,7 @@ struct LookupParams {
   uint64_t smix;
   uint64_t b_lo, nb;
   const uint64_t* dir;
+  const CDir* cdir;
   const void* slots;
   // byte keys
   const uint8_t* ctx;
@@ -79,6 +80,7 @@ struct hm_map {
   uint64_t smix;
   uint64_t r_fp;         // byte keys: fingerprint point (a1 of derive(seed,0,0,t0))
   uint64_t* dir;         // nb entries, local soff
+  hm::CDir* cdir;        // compact lookup directory, ceil(nb/32) records
   void* slots;           // S records
   uint8_t* ctx;          // byte keys: context copy
   uint64_t ctx_bytes;
@@ -103,6 +105,7 @@ struct LaunchScope {
 // build.cu
 struct BuildOut {
   uint64_t* dir = nullptr;
+  CDir* cdir = nullptr;
   void* slots = nullptr;
   uint64_t S = 0;
   uint32_t t1 = 0;

@@ -136,6 +136,31 @@ __host__ __device__ __forceinline__ uint64_t dir_entry(uint64_t soff, uint64_t s
   return soff | (s << 40) | (t << 56);
 }
 
+// Compact lookup directory: one 32-byte record per 32
+// consecutive buckets, small enough (1 B/bucket) to stay resident in L2 so
+// that probe 1 of a lookup does not touch DRAM:
+//   w[0] = soff of the record's first bucket (u32)
+//   w[1..3] = bit-planes of s (bit 2, bit 1, bit 0): bit j = that bit of s_j
+//   w[4..7] = bit-planes of t (bit 0..3)
+// s_j = 7 or t_j = 15 means "read the full directory entry"; a record with any
+// s >= 7 or t >= 15 stores all-ones s planes (every bucket escapes).
+// soff_j = w[0] + sum_{i<j} s_i^2, where with s = 4a+2b+c (bits):
+//   s^2 = 16a + 4b + c + 16ab + 8ac + 4bc  -> six popcounts over masked planes.
+struct CDir {
+  uint32_t w[8];
+};
+constexpr uint32_t kCdirEscS = 7, kCdirEscT = 15;
+
+__host__ __device__ __forceinline__ uint32_t cdir_prefix_sq(uint32_t a, uint32_t b, uint32_t c) {
+#if defined(__CUDA_ARCH__)
+  return 16u * __popc(a) + 4u * __popc(b) + __popc(c) + 16u * __popc(a & b) + 8u * __popc(a & c) +
+         4u * __popc(b & c);
+#else
+  return 16u * __builtin_popcount(a) + 4u * __builtin_popcount(b) + __builtin_popcount(c) +
+         16u * __builtin_popcount(a & b) + 8u * __builtin_popcount(a & c) + 4u * __builtin_popcount(b & c);
+#endif
+}
+
 #if defined(__CUDACC__)
 // Fingerprint (R5): acc = (acc + w_i) * r mod P over little-endian u32 words
 // (zero padded), fp = acc + len mod P.  Thread per key; the words are

@@ -64,6 +64,64 @@ __device__ __forceinline__ uint64_t slot_index(uint64_t smix, uint64_t b, uint64
   return soff + mod_s2(hash64(c, k), s, s_m2);
 }
 
+// L2 cache policies: the compact directory should stay resident (evict_last);
+// query streams, slot probes and outputs pass through (evict_first).
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t ld_q(const uint64_t* p, uint64_t pol) {
+  uint64_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ CDir ld_cdir(const CDir* p, uint64_t pol) {
+  CDir r;
+  uint64_t a, b, c, d;
+  asm volatile("ld.global.cg.L2::cache_hint.v4.u64 {%0, %1, %2, %3}, [%4], %5;"
+               : "=l"(a), "=l"(b), "=l"(c), "=l"(d)
+               : "l"(p), "l"(pol));
+  r.w[0] = uint32_t(a);
+  r.w[1] = uint32_t(a >> 32);
+  r.w[2] = uint32_t(b);
+  r.w[3] = uint32_t(b >> 32);
+  r.w[4] = uint32_t(c);
+  r.w[5] = uint32_t(c >> 32);
+  r.w[6] = uint32_t(d);
+  r.w[7] = uint32_t(d >> 32);
+  return r;
+}
+__device__ __forceinline__ KV16 ld_slot16_ef(const KV16* p, uint64_t pol) {
+  KV16 e;
+  asm volatile("ld.global.cg.L2::cache_hint.v2.u64 {%0, %1}, [%2], %3;"
+               : "=l"(e.key), "=l"(e.value)
+               : "l"(p), "l"(pol));
+  return e;
+}
+__device__ __forceinline__ void st_ef_u64(uint64_t* p, uint64_t v, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(pol) : "memory");
+}
+
+// Decode bucket lb from its compact-directory record into a full directory
+// entry (soff | s<<40 | t<<56); escapes read the full directory (DRAM).
+__device__ __forceinline__ uint64_t cdir_entry(const CDir& r, uint64_t lb, const uint64_t* dir, bool* escaped) {
+  const uint32_t j = uint32_t(lb & 31), bit = 1u << j, below = bit - 1u;
+  const uint32_t s = ((r.w[1] & bit) ? 4u : 0u) | ((r.w[2] & bit) ? 2u : 0u) | ((r.w[3] & bit) ? 1u : 0u);
+  const uint32_t t = ((r.w[4] & bit) ? 1u : 0u) | ((r.w[5] & bit) ? 2u : 0u) | ((r.w[6] & bit) ? 4u : 0u) |
+                     ((r.w[7] & bit) ? 8u : 0u);
+  *escaped = s == kCdirEscS || t == kCdirEscT;
+  const uint64_t soff = uint64_t(r.w[0]) + cdir_prefix_sq(r.w[1] & below, r.w[2] & below, r.w[3] & below);
+  return dir_entry(soff, s, t);
+}
+
+// u64 lookup: probe 1 reads the L2-resident compact directory, probe 2 the
+// slot (the one DRAM line a query needs); 4 queries in flight per thread.
 template <int QPT>
 __global__ void __launch_bounds__(kLThreads) k_lookup_u64(LookupParams lp, const uint64_t* __restrict__ q,
                                                           uint64_t nq, uint64_t* __restrict__ ov,
@@ -71,21 +129,32 @@ __global__ void __launch_bounds__(kLThreads) k_lookup_u64(LookupParams lp, const
   __shared__ uint64_t s_m2[33];
   if (threadIdx.x < 33) s_m2[threadIdx.x] = threadIdx.x ? ~0ull / (uint64_t(threadIdx.x) * threadIdx.x) : 0ull;
   __syncthreads();
+  const uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_first();
   const KV16* __restrict__ slots = reinterpret_cast<const KV16*>(lp.slots);
   const uint64_t per = uint64_t(kLThreads) * QPT;
   for (uint64_t base = blockIdx.x * per; base < nq; base += uint64_t(gridDim.x) * per) {
     uint64_t key[QPT], b[QPT], d[QPT];
+    CDir rec[QPT];
 #pragma unroll
     for (int j = 0; j < QPT; j++) {
       const uint64_t idx = base + uint64_t(j) * kLThreads + threadIdx.x;
-      key[j] = idx < nq ? ld_stream_u64(q + idx) : 0ull;
+      key[j] = idx < nq ? ld_q(q + idx, pol_stream) : 0ull;
     }
-    // L1 + L2: g q and the directory probe
+    // L1 + L2: g q and the (compact) directory probe
 #pragma unroll
     for (int j = 0; j < QPT; j++) {
       const uint64_t idx = base + uint64_t(j) * kLThreads + threadIdx.x;
       b[j] = level1_bucket(lp.l1, key[j]) - lp.b_lo;
-      d[j] = (idx < nq && b[j] < lp.nb) ? ld_dir(lp.dir + b[j]) : 0ull;
+      const bool ok = idx < nq && b[j] < lp.nb;
+      if (!ok) b[j] = 0;
+      rec[j] = ld_cdir(lp.cdir + (b[j] >> 5), pol_keep);
+      if (!ok) rec[j].w[1] = rec[j].w[2] = rec[j].w[3] = 0;  // s = 0: no probe
+    }
+#pragma unroll
+    for (int j = 0; j < QPT; j++) {
+      bool esc;
+      d[j] = cdir_entry(rec[j], b[j], lp.dir, &esc);
+      if (esc) d[j] = ld_dir(lp.dir + b[j]);
     }
     // L3 + L4: slot index and the slot probe
     KV16 e[QPT];
@@ -94,14 +163,14 @@ __global__ void __launch_bounds__(kLThreads) k_lookup_u64(LookupParams lp, const
       const bool live = ((d[j] >> 40) & 0xFFFF) != 0;
       e[j].key = ~key[j];
       e[j].value = 0;
-      if (live) e[j] = ld_slot16(slots + slot_index(lp.smix, b[j] + lp.b_lo, d[j], key[j], s_m2));
+      if (live) e[j] = ld_slot16_ef(slots + slot_index(lp.smix, b[j] + lp.b_lo, d[j], key[j], s_m2), pol_stream);
     }
 #pragma unroll
     for (int j = 0; j < QPT; j++) {
       const uint64_t idx = base + uint64_t(j) * kLThreads + threadIdx.x;
       if (idx < nq) {
         const bool hit = e[j].key == key[j];
-        if (ov) st_stream_u64(ov + idx, hit ? e[j].value : 0ull);
+        if (ov) st_ef_u64(ov + idx, hit ? e[j].value : 0ull, pol_stream);
         if (of) of[idx] = hit ? 1 : 0;
       }
     }
@@ -117,6 +186,7 @@ hm_status lookup_u64_launch(const hm_map* m, const uint64_t* q, uint64_t nq, uin
   lp.b_lo = m->b_lo;
   lp.nb = m->nb;
   lp.dir = m->dir;
+  lp.cdir = m->cdir;
   lp.slots = m->slots;
   constexpr int QPT = 4;
   const uint64_t per = uint64_t(kLThreads) * QPT;
@@ -196,6 +266,7 @@ hm_status lookup_bytes_launch(const hm_map* m, const uint8_t* qb, const uint64_t
   lp.b_lo = m->b_lo;
   lp.nb = m->nb;
   lp.dir = m->dir;
+  lp.cdir = m->cdir;
   lp.slots = m->slots;
   lp.ctx = m->ctx;
   lp.r_fp = m->r_fp;

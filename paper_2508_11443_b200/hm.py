@@ -134,8 +134,11 @@ def _stream(stream=None):
     return C.c_void_p(0)
 
 
-def _opts(seed: int, log2_bp: int = 0):
-    return _Opts(seed & ((1 << 64) - 1), log2_bp, 0)
+FLAG_FULL_DIRECTORY = 1  # HM_FLAG_FULL_DIRECTORY
+
+
+def _opts(seed: int, log2_bp: int = 0, flags: int = 0):
+    return _Opts(seed & ((1 << 64) - 1), log2_bp, flags)
 
 
 @dataclass
@@ -158,19 +161,19 @@ class HashMap:
 
     # -- build
     @classmethod
-    def build_u64(cls, keys, vals, seed: int = 0, stream=None, log2_bp: int = 0) -> "HashMap":
+    def build_u64(cls, keys, vals, seed: int = 0, stream=None, log2_bp: int = 0, flags: int = 0) -> "HashMap":
         kp, kk = _ptr(keys)
         vp, vk = _ptr(vals)
         n = _numel(keys)
         if _numel(vals) != n:
             raise ValueError("keys and vals differ in length")
         h = C.c_void_p()
-        o = _opts(seed, log2_bp)
+        o = _opts(seed, log2_bp, flags)
         _check(lib().hm_build_u64(kp, vp, n, C.byref(o), _stream(stream), C.byref(h)))
         return cls(h.value, 0)
 
     @classmethod
-    def build_bytes(cls, ctx, offsets, vals, seed: int = 0, stream=None, log2_bp: int = 0) -> "HashMap":
+    def build_bytes(cls, ctx, offsets, vals, seed: int = 0, stream=None, log2_bp: int = 0, flags: int = 0) -> "HashMap":
         cp, ck = _ptr(ctx)
         op, ok = _ptr(offsets)
         vp, vk = _ptr(vals)
@@ -178,7 +181,7 @@ class HashMap:
         if _numel(vals) != n:
             raise ValueError("offsets and vals disagree on n")
         h = C.c_void_p()
-        o = _opts(seed, log2_bp)
+        o = _opts(seed, log2_bp, flags)
         _check(lib().hm_build_bytes(cp, op, vp, n, C.byref(o), _stream(stream), C.byref(h)))
         return cls(h.value, 1)
 

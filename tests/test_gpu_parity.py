@@ -82,6 +82,40 @@ def test_u64_many_seeds_small():
             m.free()
 
 
+def test_u64_compact_directory_escapes():
+    """Lookups read a compact directory whose records escape to
+    the full directory when a bucket has s >= 7 or t >= 15: exercise both."""
+    hm = _hm()
+    escapes = 0
+    for n in (20, 24):
+        keys, vals = gen.u64_keys(n, lo=7 * n), gen.u64_values(n)
+        q = np.concatenate([keys, gen.u64_keys(3 * n, lo=100 * n)])
+        for seed in range(300):
+            ot = O.build_u64(keys, vals, seed)
+            _, s, t = O.decode_dir(ot.dir)
+            esc = bool(((s >= 7) | (t >= 15)).any())
+            if not esc and seed % 10:
+                continue
+            escapes += esc
+            m = hm.HashMap.build_u64(dev(keys), dev(vals), seed=seed)
+            assert_table_equal(m, ot)
+            ov, of = O.lookup_u64(ot, q)
+            gv, gf = m.lookup(dev(q))
+            assert np.array_equal(host(gv), ov) and np.array_equal(host(gf), of)
+            m.free()
+    assert escapes > 0
+    # every record escaping (HM_FLAG_FULL_DIRECTORY) must give the same answers
+    n = 70_001
+    keys, vals = gen.u64_keys(n), gen.u64_values(n)
+    q, _, _ = gen.u64_queries(n, 3 * n)
+    ot = O.build_u64(keys, vals, 4)
+    m = hm.HashMap.build_u64(dev(keys), dev(vals), seed=4, flags=hm.FLAG_FULL_DIRECTORY)
+    assert_table_equal(m, ot)
+    ov, of = O.lookup_u64(ot, q)
+    gv, gf = m.lookup(dev(q))
+    assert np.array_equal(host(gv), ov) and np.array_equal(host(gf), of)
+
+
 def test_u64_order_invariance_and_host_path():
     hm = _hm()
     n = 123_457
