@@ -32,7 +32,13 @@
 namespace hm {
 
 constexpr int kAThreads = 512;
-constexpr int kBThreads = 512;
+#ifndef HM_KB_THREADS
+#define HM_KB_THREADS 512
+#endif
+#ifndef HM_KB_LOG2BP
+#define HM_KB_LOG2BP 12
+#endif
+constexpr int kBThreads = HM_KB_THREADS;
 constexpr int kBWarps = kBThreads / 32;
 constexpr unsigned long long kFlagAgg = 1ull << 62, kFlagInc = 2ull << 62, kValMask = (1ull << 62) - 1;
 
@@ -118,10 +124,48 @@ __device__ __forceinline__ unsigned long long block_excl_scan(unsigned long long
   return before + x - v;
 }
 
-__device__ __forceinline__ uint32_t cur_get(const uint32_t* scur, uint32_t lb) {
-  const uint32_t w = scur[lb >> 1];
-  return (lb & 1) ? (w >> 16) : (w & 0xFFFFu);
+// Debug-only phase timestamps (compile with -DHM_PHASE_TIMING).
+#ifdef HM_PHASE_TIMING
+__device__ unsigned long long g_hm_phase[65536 * 12];
+__device__ unsigned long long g_hm_ka[4096 * 2];
+#define HM_TMARK(k)                                                     \
+  do {                                                                  \
+    if (threadIdx.x == 0) {                                             \
+      unsigned long long t_;                                            \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));            \
+      g_hm_phase[(s_p & 65535u) * 12 + (k)] = t_;                       \
+    }                                                                   \
+  } while (0)
+extern "C" int hm_debug_phase_times(unsigned long long* host, unsigned long long n) {
+  int e = int(cudaMemcpyFromSymbol(host, g_hm_phase, n * 8));
+  if (!e) e = int(cudaMemcpyFromSymbol(host + n, g_hm_ka, 4096 * 2 * 8));
+  return e;
 }
+#define HM_TKA(k)                                                       \
+  do {                                                                  \
+    if (threadIdx.x == 0 && blockIdx.x < 4096) {                        \
+      unsigned long long t_;                                            \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));            \
+      g_hm_ka[blockIdx.x * 2 + (k)] = t_;                               \
+    }                                                                   \
+  } while (0)
+#elif defined(HM_STOP_AFTER)
+// debug: cut the kernel after phase mark HM_STOP_AFTER (marginal phase costs)
+#define HM_TMARK(k)                   \
+  do {                                \
+    if ((k) == HM_STOP_AFTER) return; \
+  } while (0)
+#define HM_TKA(k) \
+  do {            \
+  } while (0)
+#else
+#define HM_TKA(k) \
+  do {            \
+  } while (0)
+#define HM_TMARK(k) \
+  do {              \
+  } while (0)
+#endif
 
 // ------------------------------------------------------------------ K_A
 template <class Src, class E, int KPT, bool kSmemHist>
@@ -135,6 +179,7 @@ __global__ void __launch_bounds__(kAThreads) k_partition(Src src, BuildParams bp
     for (uint32_t i = tid; i < bp.np; i += kAThreads) s_hist[i] = 0;
     __syncthreads();
   }
+  HM_TKA(0);
   const uint64_t T = uint64_t(kAThreads) * KPT;
   const uint64_t ntiles = (bp.n_in + T - 1) / T;
   bool ovf = false, bad = false;
@@ -203,6 +248,7 @@ __global__ void __launch_bounds__(kAThreads) k_partition(Src src, BuildParams bp
   }
   if (ovf) atomicOr(&stt->part_overflow, 1u);
   if (bad) atomicOr(&stt->pad, 1u);
+  HM_TKA(1);
 }
 
 // ------------------------------------------------------------------ K_B
@@ -223,25 +269,250 @@ __device__ __forceinline__ E shfl_elem(const E& e, int src) {
   return out;
 }
 
-// Dynamic shared memory of k_bucket (all offsets 16-byte aligned).
+// make2 for one size class, K key registers per thread.
+// Every thread owns one bucket at a time and makes one attempt per loop
+// iteration: derive(seed,2,b,t), the s level-2 slots hash mod s^2, and an
+// occupancy bitmap as `collision`.  Threads that finish take
+// the next bucket of the class from a shared counter (one warp-aggregated
+// atomic per refill), so the spread of attempt counts does not idle the warp.
+template <int K, class E, class Same>
+__device__ __forceinline__ void search_threads(const BuildParams& bp, const E* part, const uint64_t* skey,
+                                               const uint16_t* list, uint32_t L,
+                                               uint32_t* next, const uint16_t* sstart, const uint16_t* sidx,
+                                               uint16_t* sA, uint8_t* s_t, const uint64_t* s_m2, uint64_t bbase,
+                                               DevStatus* stt, const Same& same) {
+  const uint32_t lane = threadIdx.x & 31, lt = (1u << lane) - 1u;
+  bool have = false, drained = false;
+  uint32_t lb = 0, st0 = 0, s = 2, t = 0;
+  uint64_t k[K];
+  FastMod fm{4, s_m2[2]};
+#pragma unroll
+  for (int j = 0; j < K; j++) k[j] = 0;
+  while (true) {
+    const bool need = !have && !drained;
+    const uint32_t nm = __ballot_sync(0xffffffffu, need);
+    if (nm) {
+      const uint32_t leader = __ffs(nm) - 1;
+      uint32_t b0 = 0;
+      if (lane == leader) b0 = atomicAdd(next, uint32_t(__popc(nm)));
+      b0 = __shfl_sync(0xffffffffu, b0, leader);
+      if (need) {
+        const uint32_t idx = b0 + __popc(nm & lt);
+        if (idx < L) {
+          lb = list[idx];
+          st0 = sstart[lb];
+          s = uint32_t(sstart[lb + 1]) - st0;
+          t = 0;
+          have = true;
+          fm = FastMod{uint64_t(s) * s, s_m2[s]};
+#pragma unroll
+          for (int j = 0; j < K; j++) k[j] = uint32_t(j) < s ? skey[sidx[st0 + j]] : 0ull;
+        } else {
+          drained = true;
+        }
+      }
+    }
+    if (!__any_sync(0xffffffffu, have)) break;
+    if (have) {
+      const Consts c = derive(bp.smix, 2, bbase + lb, t);
+      uint64_t bits = 0;
+      bool coll = false;
+      uint32_t h[K];
+#pragma unroll
+      for (int j = 0; j < K; j++) {
+        h[j] = 0;
+        if (uint32_t(j) < s) {
+          const uint64_t hv = hash64(c, k[j]);
+          // mod s^2: a mask when s is a power of two (always for the s = 2 class)
+          h[j] = (K == 2 || (s & (s - 1)) == 0) ? uint32_t(hv) & (s * s - 1) : uint32_t(fastmod(hv, fm));
+          const uint64_t bit = 1ull << h[j];
+          coll |= (bits & bit) != 0;
+          bits |= bit;
+        }
+      }
+      bool done = false;
+      if (!coll) {
+#pragma unroll
+        for (int j = 0; j < K; j++)
+          if (uint32_t(j) < s) sA[st0 + j] = uint16_t(h[j]);
+        done = true;
+      } else {
+        if (t == 0) {  // equal keys collide under every t: check the bucket once
+          int di = -1, dj = -1;
+#pragma unroll
+          for (int i = 0; i < K; i++)
+#pragma unroll
+            for (int j = i + 1; j < K; j++)
+              if (uint32_t(j) < s && k[i] == k[j] && di < 0) {
+                di = i;
+                dj = j;
+              }
+          if (di >= 0) {
+            const bool d = same.same(part[sidx[st0 + di]], part[sidx[st0 + dj]]);
+            atomicOr(d ? &stt->dup : &stt->fpcoll, 1u);
+            done = true;
+          }
+        }
+        if (!done) {
+          if (t + 1 >= kT2Cap) {
+            atomicOr(&stt->exhausted, 1u);
+            t = 0;
+            done = true;
+          } else {
+            t++;
+          }
+        }
+      }
+      if (done) {
+        s_t[lb] = uint8_t(t);
+        have = false;
+      }
+    }
+  }
+}
+
+// make2 for the rare 9 <= s <= 32 buckets: a warp per bucket, a lane per key,
+// __match_any_sync on the level-2 slots as the injectivity test.
+template <class E, class Same>
+__device__ __forceinline__ void search_warp(const BuildParams& bp, const E* part, const uint64_t* skey,
+                                            const uint16_t* list, uint32_t L,
+                                            const uint16_t* sstart, const uint16_t* sidx, uint16_t* sA, uint8_t* s_t,
+                                            const uint64_t* s_m2, uint64_t bbase, DevStatus* stt, const Same& same) {
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (uint32_t idx = warp; idx < L; idx += kBWarps) {
+    const uint32_t lb = list[idx], st0 = sstart[lb], s = uint32_t(sstart[lb + 1]) - st0;
+    const bool mine = lane < s;
+    const uint64_t key = mine ? skey[sidx[st0 + lane]] : 0ull;
+    const uint32_t valid = __ballot_sync(0xffffffffu, mine);
+    const uint32_t dm = __match_any_sync(0xffffffffu, key) & valid & ~(1u << lane);
+    uint32_t t = 0;
+    if (__any_sync(0xffffffffu, mine && dm != 0)) {
+      if (mine && dm != 0) {
+        const bool d = same.same(part[sidx[st0 + lane]], part[sidx[st0 + __ffs(dm) - 1]]);
+        atomicOr(d ? &stt->dup : &stt->fpcoll, 1u);
+      }
+    } else {
+      const FastMod fm{uint64_t(s) * s, s_m2[s]};
+      uint32_t h = 0;
+      for (t = 0; t < kT2Cap; t++) {
+        const Consts c = derive(bp.smix, 2, bbase + lb, t);
+        h = uint32_t(fastmod(hash64(c, key), fm));
+        const uint32_t mh = __match_any_sync(0xffffffffu, mine ? h : (0x80000000u | lane));
+        if (!__any_sync(0xffffffffu, mine && __popc(mh) > 1)) break;
+      }
+      if (t >= kT2Cap) {
+        if (lane == 0) atomicOr(&stt->exhausted, 1u);
+        t = 0;
+      } else if (mine) {
+        sA[st0 + lane] = uint16_t(h);
+      }
+    }
+    if (lane == 0) s_t[lb] = uint8_t(t);
+  }
+}
+
+// Table write of one class, thread per bucket: members at soff + h, unused
+// slots get the lowest-slot member with value 0 (R10).
+template <int K, class E>
+__device__ __forceinline__ void write_threads(const uint16_t* list, uint32_t L, const uint16_t* sstart,
+                                              const uint16_t* sidx, const uint16_t* sA, const E* part, E* slots,
+                                              unsigned long long base, const uint32_t* s_cbase, const uint16_t* srel,
+                                              uint32_t lgch) {
+  for (uint32_t idx = threadIdx.x; idx < L; idx += kBThreads) {
+    const uint32_t lb = list[idx], st0 = sstart[lb], s = uint32_t(sstart[lb + 1]) - st0;
+    const uint64_t soff = base + s_cbase[lb >> lgch] + srel[lb];
+    E e[K];
+    uint32_t h[K];
+#pragma unroll
+    for (int j = 0; j < K; j++)  // all member loads in flight before any store
+      if (uint32_t(j) < s) {
+        h[j] = sA[st0 + j];
+        e[j] = part[sidx[st0 + j]];
+      }
+    uint64_t bits = 0;
+    uint32_t hmin = 0xFFFFu;
+    int jmin = 0;
+#pragma unroll
+    for (int j = 0; j < K; j++) {
+      if (uint32_t(j) < s) {
+        slots[soff + h[j]] = e[j];
+        bits |= 1ull << h[j];
+        if (h[j] < hmin) {
+          hmin = h[j];
+          jmin = j;
+        }
+      }
+    }
+    E f = e[0];
+#pragma unroll
+    for (int j = 1; j < K; j++)
+      if (j == jmin) f = e[j];
+    f.value = 0;
+    const uint32_t s2 = s * s;
+    for (uint32_t x = 0; x < s2; x++)
+      if (!((bits >> x) & 1)) slots[soff + x] = f;
+  }
+}
+
+template <class E>
+__device__ __forceinline__ void write_warp(const uint16_t* list, uint32_t L, const uint16_t* sstart,
+                                           const uint16_t* sidx, const uint16_t* sA, const E* part, E* slots,
+                                           unsigned long long base, const uint32_t* s_cbase, const uint16_t* srel,
+                                           uint32_t lgch, uint32_t* bitsw) {
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (uint32_t idx = warp; idx < L; idx += kBWarps) {
+    const uint32_t lb = list[idx], st0 = sstart[lb], s = uint32_t(sstart[lb + 1]) - st0;
+    const uint64_t soff = base + s_cbase[lb >> lgch] + srel[lb];
+    const bool mine = lane < s;
+    uint32_t h = 0xFFFFu;
+    E e;
+    bitsw[lane] = 0;
+    __syncwarp();
+    if (mine) {
+      h = sA[st0 + lane];
+      e = part[sidx[st0 + lane]];
+      slots[soff + h] = e;
+      atomicOr(&bitsw[h >> 5], 1u << (h & 31));
+    }
+    const uint32_t hmin = __reduce_min_sync(0xffffffffu, h);
+    const uint32_t who = __ffs(__ballot_sync(0xffffffffu, mine && h == hmin)) - 1;
+    E f = shfl_elem(e, who);
+    f.value = 0;
+    __syncwarp();
+    for (uint32_t x = lane; x < s * s; x += 32)
+      if (!((bitsw[x >> 5] >> (x & 31)) & 1)) slots[soff + x] = f;
+    __syncwarp();
+  }
+}
+
+// Dynamic shared memory of k_bucket (all offsets 16-byte aligned).  Regions
+// are reused once their first use is over (see the phase comments).
 struct BucketSmem {
-  size_t sA, sidx, scur, ssoff, st, slist, total;
+  size_t skey, sA, sidx, tmp, whist, sstart, st, total;
 };
 __host__ __device__ __forceinline__ size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
+__host__ __device__ __forceinline__ uint32_t bucket_chunk(uint32_t BP) {  // buckets per owner thread
+  return BP / kBThreads > 2 ? BP / kBThreads : 2;
+}
 __host__ __device__ __forceinline__ BucketSmem bucket_smem_layout(uint32_t cap, uint32_t BP) {
+  const uint32_t CH = bucket_chunk(BP), nown = BP / CH;
+  size_t wh = size_t(kBWarps) * nown * 2;                      // P1-P3: per-warp owner counters
+  wh = wh > size_t(CH) * kBThreads * 2 ? wh : size_t(CH) * kBThreads * 2;  // P4: per-thread bucket counters
+  wh = wh > (size_t(cap) / 2 + 8) * 2 ? wh : (size_t(cap) / 2 + 8) * 2;   // then: class lists
   BucketSmem L;
-  L.sA = 0;                                            // u16[cap]: bucket of element i, later h of position
-  L.sidx = L.sA + al16(size_t(cap) * 2);               // u16[cap]: grouped position -> element index
-  L.scur = L.sidx + al16(size_t(cap) * 2);             // u32[BP/2+1]: packed u16 counts -> starts -> ends
-  L.ssoff = L.scur + al16((size_t(BP) / 2 + 1) * 4);   // u32[BP]: slot offset of the bucket within the partition
-  L.st = L.ssoff + al16(size_t(BP) * 4);               // u8[BP]: attempt t of the bucket
-  L.slist = L.st + al16(BP);                           // u16[cap/2+8]: multi-key buckets grouped by class
-  L.total = L.slist + al16((size_t(cap) / 2 + 8) * 2);
+  L.skey = 0;                                           // u64[cap]: the partition's keys (item order)
+  L.sA = L.skey + al16(size_t(cap) * 8);                // u16[cap]: bucket of item i; later level-2 slot of position
+  L.sidx = L.sA + al16(size_t(cap) * 2);                // u16[cap]: P1-P3 warp rank of item; P4+ position -> item
+  L.tmp = L.sidx + al16(size_t(cap) * 2);               // u16[max(cap,BP)]: owner-grouped items; P4c+ slot offset in chunk
+  L.whist = L.tmp + al16(size_t(cap > BP ? cap : BP) * 2);
+  L.sstart = L.whist + al16(wh);                        // u16[BP+1]: first position of each bucket
+  L.st = L.sstart + al16((size_t(BP) + 1) * 2);         // u8[BP]: attempt t of each bucket
+  L.total = L.st + al16(BP);
   return L;
 }
 
 template <class E, class Same>
-__global__ void __launch_bounds__(kBThreads, 2)
+__global__ void __launch_bounds__(kBThreads, 1024 / kBThreads)
     k_bucket(BuildParams bp, const E* __restrict__ pbuf, const unsigned int* __restrict__ pcount,
              unsigned long long* __restrict__ lbstate, uint64_t* __restrict__ dir, CDir* __restrict__ cdir,
              E* __restrict__ slots, DevStatus* __restrict__ stt, Same same) {
@@ -252,50 +523,143 @@ __global__ void __launch_bounds__(kBThreads, 2)
   __shared__ unsigned long long s_base;
   __shared__ uint32_t s_cls_off[kNCls + 1];
   __shared__ uint32_t s_bits[kBWarps][32];
+  __shared__ uint32_t s_cbase[kBThreads];  // slot offset of each thread's bucket chunk in the partition
+  __shared__ uint32_t s_next[kNCls];        // work counters of the search classes
 
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) s_p = atomicAdd(&stt->ticket, 1u);
   if (tid < 33) s_m2[tid] = tid ? ~0ull / (uint64_t(tid) * tid) : 0ull;
   __syncthreads();
   const uint32_t p = s_p;
+  HM_TMARK(0);
   const uint32_t cap = bp.cap;
   const uint32_t BP = 1u << bp.log2_bp;
+  const uint32_t CH = bucket_chunk(BP), lgch = 31 - __clz(CH), nown = BP / CH, obits = 31 - __clz(nown);
   const uint64_t lb0 = uint64_t(p) << bp.log2_bp;
   const uint32_t nbp = uint32_t(bp.nb - lb0 < uint64_t(BP) ? bp.nb - lb0 : uint64_t(BP));
   const uint32_t cnt_raw = pcount[p];
   const bool ovf = cnt_raw > cap;
   const uint32_t cnt = ovf ? 0u : cnt_raw;
   const BucketSmem SL = bucket_smem_layout(cap, BP);
+  uint64_t* skey = reinterpret_cast<uint64_t*>(smem + SL.skey);
   uint16_t* sA = reinterpret_cast<uint16_t*>(smem + SL.sA);
-  uint16_t* sidx = reinterpret_cast<uint16_t*>(smem + SL.sidx);
-  uint32_t* scur = reinterpret_cast<uint32_t*>(smem + SL.scur);
-  uint32_t* ssoff = reinterpret_cast<uint32_t*>(smem + SL.ssoff);
+  uint16_t* srk = reinterpret_cast<uint16_t*>(smem + SL.sidx);   // P1-P3
+  uint16_t* sidx = srk;                                           // P4+
+  uint16_t* tmp = reinterpret_cast<uint16_t*>(smem + SL.tmp);    // P3-P4b
+  uint16_t* srel = tmp;                                           // P4c+
+  uint16_t* whist = reinterpret_cast<uint16_t*>(smem + SL.whist); // P1-P3
+  uint16_t* scnt = whist;                                         // P4a-P4b
+  uint16_t* slist = whist;                                        // P4c+
+  uint16_t* sstart = reinterpret_cast<uint16_t*>(smem + SL.sstart);
   uint8_t* s_t = smem + SL.st;
-  uint16_t* slist = reinterpret_cast<uint16_t*>(smem + SL.slist);
-  const uint32_t ncw = BP / 2 + 1;
-  for (uint32_t w = tid; w < ncw; w += kBThreads) scur[w] = 0;
+  for (uint32_t w = tid; w < kBWarps * nown / 2; w += kBThreads) reinterpret_cast<uint32_t*>(whist)[w] = 0;
   __syncthreads();
   const E* part = pbuf + size_t(p) * cap;
   const uint64_t bbase = bp.b_lo + lb0;  // global id of the partition's first bucket
 
-  // pass 1 — hist n hashes (rep n 1) on this partition's buckets
-  for (uint32_t i = tid; i < cnt; i += kBThreads) {
-    const uint32_t lb = uint32_t(level1_bucket(bp.l1, part[i].key) - bbase);
-    sA[i] = uint16_t(lb);
-    atomicAdd(&scur[lb >> 1], 1u << ((lb & 1) * 16));
+  // groupby of the partition's items by bucket without shared
+  // atomics: P1 ranks every item among the items of its owner thread (the
+  // thread owning CH consecutive buckets) with `obits` warp ballots and
+  // per-warp counters; P2 scans the counters; P3 scatters into owner order;
+  // P4 groups each owner's ~CH items by bucket with thread-private counters.
+  HM_TMARK(1);
+  // ---- P1: level-1 bucket g k, warp-level owner rank
+  const uint32_t lt = (1u << lane) - 1u;
+  uint16_t* wh = whist + warp * nown;
+  for (uint32_t i0 = warp * 32; i0 < cnt; i0 += 8 * kBThreads) {
+    uint64_t ks[8];
+    uint32_t lbs[8];
+#pragma unroll
+    for (int j = 0; j < 8; j++) {  // the partition's keys are read from HBM once, 8 loads in flight
+      const uint32_t i = i0 + j * kBThreads + lane;
+      ks[j] = i < cnt ? part[i].key : 0ull;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+      const uint32_t i = i0 + j * kBThreads + lane;
+      lbs[j] = 0;
+      if (i < cnt) {
+        skey[i] = ks[j];
+        lbs[j] = uint32_t(level1_bucket(bp.l1, ks[j]) - bbase);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+      const uint32_t i = i0 + j * kBThreads + lane;
+      const bool valid = i < cnt;
+      const uint32_t o = lbs[j] >> lgch;
+      uint32_t m = __ballot_sync(0xffffffffu, valid);
+      for (uint32_t bit = 0; bit < obits; bit++) {
+        const uint32_t bl = __ballot_sync(0xffffffffu, (o >> bit) & 1u);
+        m &= ((o >> bit) & 1u) ? bl : ~bl;
+      }
+      const uint32_t below = m & lt;
+      const uint32_t wc = valid ? wh[o] : 0u;
+      __syncwarp();
+      if (valid && below == 0) wh[o] = uint16_t(wc + __popc(m));
+      __syncwarp();
+      if (valid) {
+        sA[i] = uint16_t(lbs[j]);
+        srk[i] = uint16_t(wc + __popc(below));
+      }
+    }
   }
   __syncthreads();
-
-  // scans over a contiguous chunk of CH buckets per thread: group starts
-  // (presum of s), slot offsets (presum of s^2, R1/R2),
-  // and the class lists of multi-key buckets in bucket order.
-  const uint32_t CH = max(2u, BP / kBThreads);
+  HM_TMARK(2);
+  // ---- P2: owner totals and offsets (owner-major, warp-minor)
+  uint32_t ostart = 0, otot = 0;
+  {
+    uint32_t pre[kBWarps];
+    if (tid < nown) {
+#pragma unroll
+      for (int w = 0; w < kBWarps; w++) {
+        pre[w] = otot;
+        otot += whist[w * nown + tid];
+      }
+    }
+    unsigned long long tot;
+    ostart = uint32_t(block_excl_scan(otot, &tot, s_red));
+    if (tid < nown) {
+#pragma unroll
+      for (int w = 0; w < kBWarps; w++) whist[w * nown + tid] = uint16_t(ostart + pre[w]);
+    }
+  }
+  __syncthreads();
+  HM_TMARK(3);
+  // ---- P3: scatter items into owner order
+  for (uint32_t i0 = warp * 32; i0 < cnt; i0 += kBThreads) {
+    const uint32_t i = i0 + lane;
+    if (i < cnt) tmp[wh[sA[i] >> lgch] + srk[i]] = uint16_t(i);
+  }
+  __syncthreads();
+  HM_TMARK(4);
+  // ---- P4a/b: each owner groups its items by bucket (thread-private counters)
+  if (tid < nown) {
+    for (uint32_t k = 0; k < CH; k++) scnt[k * kBThreads + tid] = 0;
+    for (uint32_t q = ostart; q < ostart + otot; q++) scnt[(sA[tmp[q]] & (CH - 1)) * kBThreads + tid]++;
+    uint32_t run = ostart;
+    for (uint32_t k = 0; k < CH; k++) {
+      const uint32_t c = scnt[k * kBThreads + tid];
+      scnt[k * kBThreads + tid] = uint16_t(run);
+      sstart[tid * CH + k] = uint16_t(run);
+      run += c;
+    }
+    for (uint32_t q = ostart; q < ostart + otot; q++) {
+      const uint32_t i = tmp[q];
+      uint16_t* c = &scnt[(sA[i] & (CH - 1)) * kBThreads + tid];
+      sidx[*c] = uint16_t(i);
+      *c = uint16_t(*c + 1);
+    }
+  }
+  if (tid == 0) sstart[BP] = uint16_t(cnt);
+  __syncthreads();
+  HM_TMARK(5);
+  // ---- P4c: sizes, s^2 offsets (presum, R1/R2), class lists
   const uint32_t c0 = tid * CH, c1 = min(c0 + CH, nbp);
-  uint32_t lcnt = 0, lsq = 0, maxs = 0;
+  uint32_t lsq = 0, maxs = 0;
   unsigned long long lcls = 0;
   for (uint32_t j = c0; j < c1; j++) {
-    const uint32_t v = cur_get(scur, j);
-    lcnt += v;
+    const uint32_t v = uint32_t(sstart[j + 1]) - sstart[j];
     lsq += v * v;
     maxs = max(maxs, v);
     if (v >= 2) {
@@ -303,178 +667,71 @@ __global__ void __launch_bounds__(kBThreads, 2)
       if (c < kNCls && uint64_t(v) * v <= bp.bound4n) lcls += 1ull << (16 * c);
     }
   }
-  unsigned long long totA, totB;
-  const unsigned long long exA = block_excl_scan(uint64_t(lcnt) | (uint64_t(lsq) << 32), &totA, s_red);
+  unsigned long long S_p, totB;
+  const uint32_t exsq = uint32_t(block_excl_scan(lsq, &S_p, s_red));
   const unsigned long long exB = block_excl_scan(lcls, &totB, s_red);
-  const unsigned long long S_p = totA >> 32;
   if (tid == 0) {
     s_cls_off[0] = 0;
     for (int c = 0; c < kNCls; c++) s_cls_off[c + 1] = s_cls_off[c] + uint32_t((totB >> (16 * c)) & 0xFFFF);
   }
+  s_cbase[tid] = exsq;
   __syncthreads();
   {
-    uint32_t run = uint32_t(exA & 0xFFFFFFFFu), fsq = uint32_t(exA >> 32);
     uint32_t ccur[kNCls];
 #pragma unroll
     for (int c = 0; c < kNCls; c++) ccur[c] = s_cls_off[c] + uint32_t((exB >> (16 * c)) & 0xFFFF);
     bool huge = false, bfail = false;
-    for (uint32_t j = c0; j < c1; j += 2) {
-      const uint32_t w = scur[j >> 1], a = w & 0xFFFFu, b2 = w >> 16;
-      scur[j >> 1] = run | ((run + a) << 16);  // starts of buckets j, j+1
-      run += a + b2;
-#pragma unroll
-      for (int k = 0; k < 2; k++) {
-        const uint32_t jj = j + k, v = k ? b2 : a;
-        if (jj >= c1) break;
-        ssoff[jj] = fsq;
-        fsq += v * v;
-        s_t[jj] = 0;
-        if (v >= 2) {
-          const int c = size_class(v);
-          if (uint64_t(v) * v > bp.bound4n) bfail = true;  // S > 4n: level one redraws
-          else if (c >= kNCls) huge = true;
-          else slist[ccur[c]++] = uint16_t(jj);
-        }
+    uint32_t fsq = 0;
+    for (uint32_t j = c0; j < c1; j++) {
+      const uint32_t v = uint32_t(sstart[j + 1]) - sstart[j];
+      srel[j] = uint16_t(fsq);
+      fsq += v * v;
+      s_t[j] = 0;
+      if (v >= 2) {
+        const int c = size_class(v);
+        if (uint64_t(v) * v > bp.bound4n) bfail = true;  // S > 4n: level one redraws
+        else if (c >= kNCls) huge = true;
+        else slist[ccur[c]++] = uint16_t(j);
       }
     }
+    if (fsq > 0xFFFFu) huge = true;
     if (huge) atomicOr(&stt->huge, 1u);
     if (bfail || uint64_t(maxs) * maxs > bp.bound4n) atomicOr(&stt->bound_fail, 1u);
   }
-  // publish the partition's aggregate early (decoupled look-back)
-  if (tid == 0) st_release(&lbstate[p], (p == 0 ? kFlagInc : kFlagAgg) | (S_p & kValMask));
-  __syncthreads();
-
-  // pass 2 — groupby: counting scatter of element indices into bucket order
-  for (uint32_t i = tid; i < cnt; i += kBThreads) {
-    const uint32_t lb = sA[i];
-    const uint32_t sh = (lb & 1) * 16;
-    const uint32_t old = atomicAdd(&scur[lb >> 1], 1u << sh);
-    sidx[(old >> sh) & 0xFFFFu] = uint16_t(i);
-  }
-  __syncthreads();
-  // from here: end(lb) = cur_get(lb), start(lb) = end(lb-1); sA[pos] holds level-2 slots
-
-  // level-2 seed search, map make2 over the multi-key buckets.
-  // A group of G lanes owns one bucket; each loop iteration is one attempt t
-  // for every group: derive(seed,2,b,t), hash every member mod s^2, and
-  // __match_any_sync on (group, slot) finds collisions (`collision`,
-  // PAPER.md:280-282).  A group that succeeds takes the next bucket of its
-  // class, so lanes stay busy whatever the attempt counts are.
-  for (int c = 0; c < kNCls; c++) {
-    const int lg = class_log2g(c);
-    const uint32_t G = 1u << lg;
-    const uint32_t L = s_cls_off[c + 1] - s_cls_off[c];
-    const uint16_t* list = slist + s_cls_off[c];
-    const uint32_t gpw = 32u >> lg, NG = kBWarps * gpw;
-    const uint32_t gbase = lane & ~(G - 1), r = lane & (G - 1);
-    const uint32_t gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << gbase;
-    uint32_t idx = warp * gpw + (lane >> lg);
-    bool have = false;
-    uint32_t lb = 0, st0 = 0, s = 2, t = 0;
-    uint64_t key = 0, b = 0;
-    auto load = [&]() {
-      have = idx < L;
-      t = 0;
-      if (have) {
-        lb = list[idx];
-        st0 = lb ? cur_get(scur, lb - 1) : 0u;
-        s = cur_get(scur, lb) - st0;
-        b = bbase + lb;
-        key = r < s ? part[sidx[st0 + r]].key : 0ull;
-      }
-    };
-    load();
-    while (__any_sync(0xffffffffu, have)) {
-      const bool mine = have && r < s;
-      const Consts cc = derive(bp.smix, 2, b, t);
-      const uint32_t s2 = have ? s * s : 4u;
-      const FastMod fm{s2, s_m2[have ? s : 2u]};
-      const uint32_t h = uint32_t(fastmod(hash64(cc, key), fm));
-      // injectivity of the group's slots: an OR-reduced occupancy bitmap
-      // (s^2 <= 64) for G <= 8, __match_any_sync for the rare G = 32 class
-      bool gcoll;
-      if (G < 32) {
-        uint64_t bits = mine ? (1ull << h) : 0ull;
-#pragma unroll
-        for (uint32_t o = 1; o < 8; o <<= 1)
-          if (o < G) bits |= __shfl_xor_sync(0xffffffffu, bits, o);
-        gcoll = have && uint32_t(__popcll(bits)) < s;
-      } else {
-        const uint32_t mh = __match_any_sync(0xffffffffu, mine ? h : (0x80000000u | lane));
-        gcoll = __any_sync(0xffffffffu, mine && __popc(mh) > 1);
-      }
-      // equal keys collide under every t, so only a bucket whose first
-      // attempt collides can hold duplicates: check those pairwise, once
-      const bool suspect = have && gcoll && t == 0;
-      bool gdup = false;
-      if (__any_sync(0xffffffffu, suspect)) {
-        bool dupl = false;
-        uint32_t other = 0;
-        if (G < 32) {
-          for (uint32_t d = 1; d < G; d++) {
-            const uint32_t rp = (r + d) & (G - 1);
-            const uint64_t pk = __shfl_sync(0xffffffffu, key, gbase + rp);
-            if (mine && rp < s && pk == key && !dupl) {
-              dupl = true;
-              other = rp;
-            }
-          }
-        } else {
-          const uint32_t valid = __ballot_sync(0xffffffffu, mine);
-          const uint32_t dm = __match_any_sync(0xffffffffu, key) & valid & ~(1u << lane);
-          dupl = mine && dm != 0;
-          other = dm ? __ffs(dm) - 1 : 0;
-        }
-        const uint32_t dball = __ballot_sync(0xffffffffu, dupl);  // all lanes: no short-circuit
-        gdup = suspect && (dball & gmask) != 0;
-        if (gdup && dupl) {
-          const bool d = same.same(part[sidx[st0 + r]], part[sidx[st0 + other]]);
-          atomicOr(d ? &stt->dup : &stt->fpcoll, 1u);
-        }
-      }
-      bool done = false;
-      if (have) {
-        if (gdup) {
-          t = 0;
-          done = true;
-        } else if (!gcoll) {
-          if (mine) sA[st0 + r] = uint16_t(h);
-          done = true;
-        } else if (t + 1 >= kT2Cap) {
-          if (r == 0) atomicOr(&stt->exhausted, 1u);
-          t = 0;
-          done = true;
-        } else {
-          t++;
-        }
-        if (done && r == 0) s_t[lb] = uint8_t(t);
-      }
-      if (done) {
-        idx += NG;
-        load();
-      }
-    }
-  }
-  __syncthreads();
-
-  // look-back: exclusive prefix of S over the partitions before p
-  if (tid == 0) {
+  // publish the partition's aggregate, then look back for the exclusive prefix
+  // of S over the partitions before p (decoupled look-back; the predecessors
+  // started earlier and publish at this same point, so the wait is short)
+  if (warp == 0) {
+    // warp-parallel look-back: lane i inspects partition q0 - i; the closest
+    // inclusive prefix plus the aggregates in front of it give the base
+    if (lane == 0) st_release(&lbstate[p], (p == 0 ? kFlagInc : kFlagAgg) | (S_p & kValMask));
     unsigned long long base = 0;
     if (p > 0) {
-      int64_t q = int64_t(p) - 1;
+      int64_t q0 = int64_t(p) - 1;
       while (true) {
-        const unsigned long long v = ld_acquire(&lbstate[q]);
+        const int64_t q = q0 - int64_t(lane);
+        const unsigned long long v = q >= 0 ? ld_acquire(&lbstate[q]) : kFlagInc;
         const unsigned long long f = v & ~kValMask;
-        if (f == 0) continue;
-        base += v & kValMask;
-        if (f == kFlagInc) break;
-        q--;
+        const uint32_t notready = __ballot_sync(0xffffffffu, f == 0);
+        const uint32_t incs = __ballot_sync(0xffffffffu, f == kFlagInc);
+        const uint32_t upto = incs ? (__ffs(incs) - 1) : 31u;  // lanes 0..upto are needed
+        const uint32_t need = upto == 31u ? 0xffffffffu : ((2u << upto) - 1u);
+        if (notready & need) continue;  // a closer partition has not published yet
+        unsigned long long x = lane <= upto ? (v & kValMask) : 0ull;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        base += x;
+        if (incs) break;
+        q0 -= 32;
       }
-      st_release(&lbstate[p], kFlagInc | ((base + S_p) & kValMask));
+      if (lane == 0) st_release(&lbstate[p], kFlagInc | ((base + S_p) & kValMask));
     }
-    if (p == bp.np - 1) stt->S = base + S_p;
-    s_base = base;
+    if (lane == 0) {
+      if (p == bp.np - 1) stt->S = base + S_p;
+      s_base = base;
+    }
   }
+  if (tid < kNCls) s_next[tid] = 0;
   __syncthreads();
   const unsigned long long base = s_base;
   if (ovf) {
@@ -486,19 +743,60 @@ __global__ void __launch_bounds__(kBThreads, 2)
     return;
   }
 
-  // directory (coalesced), compact directory record per 32 buckets (one per
-  // warp iteration), and singleton slots (R12: a singleton sits at soff)
+
+  // from here: bucket lb holds positions [sstart[lb], sstart[lb+1]); sidx[pos] = item;
+  // slot offset within the partition = s_cbase[lb / CH] + srel[lb]
+
+  HM_TMARK(6);
+  // level-2 seed search, map make2 over the multi-key buckets:
+  // warp-per-bucket for 9 <= s <= 32, then thread-per-bucket classes from the
+  // rarest (longest chains) to the most common, so the tail of the last class
+  // is short and early warps go on to the singleton slots
+  search_warp(bp, part, skey, slist + s_cls_off[3], s_cls_off[4] - s_cls_off[3], sstart, sidx, sA, s_t, s_m2, bbase, stt,
+              same);
+  search_threads<8>(bp, part, skey, slist + s_cls_off[2], s_cls_off[3] - s_cls_off[2], &s_next[2], sstart, sidx, sA, s_t,
+                    s_m2, bbase, stt, same);
+  search_threads<4>(bp, part, skey, slist + s_cls_off[1], s_cls_off[2] - s_cls_off[1], &s_next[1], sstart, sidx, sA, s_t,
+                    s_m2, bbase, stt, same);
+  search_threads<2>(bp, part, skey, slist + s_cls_off[0], s_cls_off[1] - s_cls_off[0], &s_next[0], sstart, sidx, sA, s_t,
+                    s_m2, bbase, stt, same);
+  HM_TMARK(7);
+  // singleton slots (R12: a singleton sits at soff) need no search result;
+  // 8 element loads in flight per thread, then the stores
+  for (uint32_t lb0s = 0; lb0s < nbp; lb0s += 8 * kBThreads) {
+    E ev[8];
+    uint64_t so[8];
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+      const uint32_t lb = lb0s + j * kBThreads + tid;
+      so[j] = ~0ull;
+      if (lb < nbp) {
+        const uint32_t st0 = sstart[lb];
+        if (uint32_t(sstart[lb + 1]) - st0 == 1) {
+          so[j] = base + s_cbase[lb >> lgch] + srel[lb];
+          ev[j] = part[sidx[st0]];
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; j++)
+      if (so[j] != ~0ull) slots[so[j]] = ev[j];
+  }
+  __syncthreads();
+
+  HM_TMARK(8);
+  // directory (coalesced) and compact directory record per 32 buckets (one per
+  // warp iteration)
   for (uint32_t cb = 0; cb < nbp; cb += kBThreads) {
     const uint32_t lb = cb + tid;
     uint32_t s = 0, t = 0, st0 = 0;
     uint64_t soff = 0;
     if (lb < nbp) {
-      st0 = lb ? cur_get(scur, lb - 1) : 0u;
-      s = cur_get(scur, lb) - st0;
+      st0 = sstart[lb];
+      s = uint32_t(sstart[lb + 1]) - st0;
       t = s_t[lb];
-      soff = base + ssoff[lb];
+      soff = base + s_cbase[lb >> lgch] + srel[lb];
       dir[lb0 + lb] = dir_entry(soff, s, t);
-      if (s == 1) slots[soff] = part[sidx[st0]];
     }
     uint32_t pa = __ballot_sync(0xffffffffu, s & 4), pb = __ballot_sync(0xffffffffu, s & 2),
              pc = __ballot_sync(0xffffffffu, s & 1);
@@ -519,66 +817,18 @@ __global__ void __launch_bounds__(kBThreads, 2)
       cdir[(lb0 + lb) >> 5] = r;
     }
   }
+  HM_TMARK(9);
   // multi-key buckets: members at soff + h, every unused slot gets the
   // lowest-slot member with value 0 (R10)
-  for (int c = 0; c < kNCls; c++) {
-    const int lg = class_log2g(c);
-    const uint32_t G = 1u << lg;
-    const uint32_t L = s_cls_off[c + 1] - s_cls_off[c];
-    const uint16_t* list = slist + s_cls_off[c];
-    const uint32_t gpw = 32u >> lg, NG = kBWarps * gpw;
-    const uint32_t gbase = lane & ~(G - 1), r = lane & (G - 1);
-    const uint32_t gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << gbase;
-    for (uint32_t i0 = 0; i0 < L; i0 += NG) {
-      const uint32_t idx = i0 + warp * gpw + (lane >> lg);
-      const bool have = idx < L;
-      uint32_t st0 = 0, s = 0, h = 0xFFFFu;
-      uint64_t soff = 0;
-      E e;
-      if (have) {
-        const uint32_t lb = list[idx];
-        st0 = lb ? cur_get(scur, lb - 1) : 0u;
-        s = cur_get(scur, lb) - st0;
-        soff = base + ssoff[lb];
-      }
-      const bool mine = have && r < s;
-      if (mine) {
-        h = sA[st0 + r];
-        e = part[sidx[st0 + r]];
-        slots[soff + h] = e;
-      }
-      uint32_t hmin = h;
-      if (G < 32) {
-        uint64_t bits = mine ? (1ull << h) : 0ull;
-#pragma unroll
-        for (uint32_t o = 1; o < 8; o <<= 1) {
-          if (o < G) {
-            bits |= __shfl_xor_sync(0xffffffffu, bits, o);
-            hmin = min(hmin, __shfl_xor_sync(0xffffffffu, hmin, o));
-          }
-        }
-        const uint32_t who = __ffs(__ballot_sync(0xffffffffu, mine && h == hmin) & gmask);
-        E f = shfl_elem(e, who ? who - 1 : lane);
-        f.value = 0;
-        if (have)
-          for (uint32_t x = r; x < s * s; x += G)
-            if (!((bits >> x) & 1)) slots[soff + x] = f;
-      } else {
-        s_bits[warp][lane] = 0;
-        __syncwarp();
-        if (mine) atomicOr(&s_bits[warp][h >> 5], 1u << (h & 31));
-        hmin = __reduce_min_sync(0xffffffffu, h);
-        const uint32_t who = __ffs(__ballot_sync(0xffffffffu, mine && h == hmin));
-        E f = shfl_elem(e, who ? who - 1 : lane);
-        f.value = 0;
-        __syncwarp();
-        if (have)
-          for (uint32_t x = lane; x < s * s; x += 32)
-            if (!((s_bits[warp][x >> 5] >> (x & 31)) & 1)) slots[soff + x] = f;
-        __syncwarp();
-      }
-    }
-  }
+  write_threads<2>(slist + s_cls_off[0], s_cls_off[1] - s_cls_off[0], sstart, sidx, sA, part, slots, base, s_cbase,
+                   srel, lgch);
+  write_threads<4>(slist + s_cls_off[1], s_cls_off[2] - s_cls_off[1], sstart, sidx, sA, part, slots, base, s_cbase,
+                   srel, lgch);
+  write_threads<8>(slist + s_cls_off[2], s_cls_off[3] - s_cls_off[2], sstart, sidx, sA, part, slots, base, s_cbase,
+                   srel, lgch);
+  write_warp(slist + s_cls_off[3], s_cls_off[4] - s_cls_off[3], sstart, sidx, sA, part, slots, base, s_cbase, srel,
+             lgch, s_bits[warp]);
+  HM_TMARK(10);
 }
 
 // ------------------------------------------------------------- host side
@@ -596,7 +846,7 @@ static Plan make_plan(uint64_t n_in, uint64_t nb, uint32_t log2_req, size_t smem
   const int sms = num_sms();
   // 8K buckets per partition (two CTAs of k_bucket per SM); 16K when that
   // would make more than 32K partitions (k_partition's shared histogram)
-  uint32_t lg = log2_req ? log2_req : ((nb >> 13) > 32768 ? 14 : 13);
+  uint32_t lg = log2_req ? log2_req : ((nb >> HM_KB_LOG2BP) > 32768 ? 14 : HM_KB_LOG2BP);
   if (!log2_req) {
     while (lg > 6 && (nb >> lg) < uint64_t(4 * sms)) lg--;
   }
@@ -656,7 +906,7 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
   HM_CUDA_TRY(cudaGetDevice(&dev));
   int smem_optin = 0;
   HM_CUDA_TRY(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-  const size_t static_smem_B = 4096;  // upper bound for k_bucket's static shared memory
+  const size_t static_smem_B = 6144;  // upper bound for k_bucket static shared memory (4.5 KB)
   const uint32_t knob_flags = log2_req >> 16;
   log2_req &= 0xFFFFu;
   const Plan pl = make_plan(n_in, nb, log2_req, size_t(smem_optin) - static_smem_B);

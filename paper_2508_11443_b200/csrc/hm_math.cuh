@@ -69,17 +69,23 @@ __host__ __device__ __forceinline__ uint64_t mod_p128(uint64_t hi, uint64_t lo) 
   return x >= kP ? x - kP : x;
 }
 
-// The universal family (R4).  a1, a2 < 2^61, limbs < 2^32: the sum of the two
-// products and b is < 2^95, so hi < 2^31.
+// The universal family (R4):  (a1*xl + a2*xh + b) mod P with xl, xh the 32-bit
+// limbs of x and a1, a2, b < P.  Computed on 32-bit pieces of the constants:
+//   a*x = al*x + (ah*x)*2^32  (al < 2^32, ah < 2^29),
+// with (ah1*xl + ah2*xh) = R < 2^62 folded as R*2^32 = (R >> 29) + (R mod 2^29)*2^32
+// (mod P, since 2^61 = 1), and the two 64-bit products al*x folded to < 2^61+8
+// before the sum, so every intermediate fits in 64 bits.
 __host__ __device__ __forceinline__ uint64_t hash64(const Consts& c, uint64_t x) {
-  const uint64_t xl = x & 0xFFFFFFFFull, xh = x >> 32;
-  const uint64_t l1 = c.a1 * xl, h1 = umulhi(c.a1, xl);
-  const uint64_t l2 = c.a2 * xh, h2 = umulhi(c.a2, xh);
-  uint64_t lo = l1 + l2;
-  uint64_t hi = h1 + h2 + (lo < l1);
-  const uint64_t lo2 = lo + c.b;
-  hi += (lo2 < lo);
-  return mod_p128(hi, lo2);
+  const uint32_t xl = uint32_t(x), xh = uint32_t(x >> 32);
+  const uint64_t p = uint64_t(uint32_t(c.a1)) * xl;          // < 2^64
+  const uint64_t q = uint64_t(uint32_t(c.a2)) * xh;          // < 2^64
+  const uint64_t r = uint64_t(uint32_t(c.a1 >> 32)) * xl + uint64_t(uint32_t(c.a2 >> 32)) * xh;  // < 2^62
+  const uint64_t fp_ = (p & kP) + (p >> 61);
+  const uint64_t fq = (q & kP) + (q >> 61);
+  const uint64_t fr = (r >> 29) + ((r & ((1ull << 29) - 1)) << 32);
+  uint64_t s = fp_ + fq + fr + c.b;                          // < 4*2^61 + 16
+  s = (s & kP) + (s >> 61);
+  return s >= kP ? s - kP : s;
 }
 
 // (a*b) mod P for a, b < 2^62.
@@ -97,7 +103,7 @@ __host__ __device__ __forceinline__ uint64_t mulmod_p(uint64_t a, uint64_t b) {
 
 // Exact x mod d for x < 2^62 and 1 <= d < 2^32, with m = floor((2^64-1)/d):
 // q = umulhi(x, m) underestimates floor(x/d) by at most 1 (x/2^64 < 1/4), so
-// one or two corrections give the exact remainder (R22).
+// one correction gives the exact remainder (R22).
 struct FastMod {
   uint64_t d, m;
 };
@@ -108,11 +114,11 @@ __host__ __device__ __forceinline__ FastMod make_fastmod(uint64_t d) {
   return f;
 }
 __host__ __device__ __forceinline__ uint64_t fastmod(uint64_t x, const FastMod& f) {
+  // x < 2^62: x*m/2^64 >= x/d - 2x/2^64 > x/d - 1/2, so q >= floor(x/d) - 1
+  // and a single correction suffices
   const uint64_t q = umulhi(x, f.m);
-  uint64_t r = x - q * f.d;
-  if (r >= f.d) r -= f.d;
-  if (r >= f.d) r -= f.d;
-  return r;
+  const uint64_t r = x - q * f.d;
+  return r >= f.d ? r - f.d : r;
 }
 
 // Level-one range reduction `mod n`: mask when n is a power of

@@ -17,7 +17,7 @@ from dataclasses import dataclass
 import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libhm.so")
+LIB_PATH = os.environ.get("HM_LIB_PATH") or os.path.join(PKG, "libhm.so")  # override: debug builds only
 
 STATUS = {
     0: "OK", 1: "INVALID_ARG", 2: "EMPTY", 3: "DUPLICATE_KEY", 4: "SEED_EXHAUSTED",
