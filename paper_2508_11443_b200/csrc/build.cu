@@ -25,6 +25,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <type_traits>
 #include <vector>
 
 #include "hm_internal.cuh"
@@ -249,6 +250,141 @@ __global__ void __launch_bounds__(kAThreads) k_partition(Src src, BuildParams bp
   if (ovf) atomicOr(&stt->part_overflow, 1u);
   if (bad) atomicOr(&stt->pad, 1u);
   HM_TKA(1);
+}
+
+// ------------------------------------------------------------ K_A, two passes
+// For large tables the partition step runs as two 128-way radix-partition
+// passes over the partition id (high 7 bits, then low 7 bits): a 16K-way
+// single pass writes ~one 16-byte element per partition per tile (scattered
+// partial-sector stores), a 128-way pass writes runs of ~32 elements from a
+// shared-memory staging tile, fully coalesced.  Ranking inside the tile uses
+// warp ballots over the 7 digit bits and per-warp counters (no atomics).
+constexpr int kSThreads = 512, kSPT = 4, kSTile = kSThreads * kSPT;
+constexpr int kSWarps = kSThreads / 32, kSDigits = 128;
+
+struct SplitArgs {
+  // pass 2 source: the coarse buffer
+  const void* cbuf;
+  const unsigned int* ccount;
+  uint32_t ccap;
+  uint32_t tpc;  // tiles per coarse partition
+  // destination
+  void* dst;
+  unsigned int* dcount;
+  uint32_t dcap;
+  uint32_t nreg;      // destination regions
+  uint32_t nreg_src;  // pass 2: source (coarse) regions
+};
+
+template <class Src, class E, int PASS>
+__global__ void __launch_bounds__(kSThreads, 2) k_split(Src src, BuildParams bp, SplitArgs a,
+                                                        DevStatus* __restrict__ stt) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  E* stage = reinterpret_cast<E*>(smem);
+  uint8_t* sdig = smem + size_t(kSTile) * sizeof(E);
+  __shared__ uint16_t s_wh[kSWarps][kSDigits];
+  __shared__ uint32_t s_dstart[kSDigits], s_gbase[kSDigits];
+  __shared__ unsigned long long s_red[kSWarps];
+
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, lt = (1u << lane) - 1u;
+  for (uint32_t i = tid; i < kSWarps * kSDigits / 2; i += kSThreads) reinterpret_cast<uint32_t*>(&s_wh[0][0])[i] = 0;
+  // this CTA's elements
+  uint64_t base;
+  uint32_t nvalid, coarse = 0;
+  const E* cb = reinterpret_cast<const E*>(a.cbuf);
+  if (PASS == 1) {
+    base = uint64_t(blockIdx.x) * kSTile;
+    nvalid = bp.n_in - base < uint64_t(kSTile) ? uint32_t(bp.n_in - base) : uint32_t(kSTile);
+  } else {
+    coarse = blockIdx.x / a.tpc;
+    const uint32_t k = blockIdx.x % a.tpc;
+    const uint32_t cc = min(a.ccount[coarse], a.ccap);
+    base = uint64_t(k) * kSTile;
+    nvalid = cc > base ? (cc - base < uint64_t(kSTile) ? uint32_t(cc - base) : uint32_t(kSTile)) : 0u;
+  }
+  __syncthreads();
+  if (nvalid == 0) return;
+  E e[kSPT];
+  uint32_t dg[kSPT], rk[kSPT];
+  bool bad = false;
+#pragma unroll
+  for (int j = 0; j < kSPT; j++) {
+    const uint32_t i = j * kSThreads + tid;
+    if (i < nvalid) e[j] = PASS == 1 ? src.load(base + i) : cb[size_t(coarse) * a.ccap + base + i];
+  }
+#pragma unroll
+  for (int j = 0; j < kSPT; j++) {
+    const uint32_t i = j * kSThreads + tid;
+    dg[j] = 0;
+    if (i < nvalid) {
+      const uint64_t lb = level1_bucket(bp.l1, e[j].key) - bp.b_lo;
+      if (lb >= bp.nb) bad = true;
+      const uint32_t p = uint32_t(lb >> bp.log2_bp);
+      dg[j] = PASS == 1 ? ((p >> 7) & (kSDigits - 1)) : (p & (kSDigits - 1));
+    }
+  }
+  // warp-ballot rank of every element among the warp's elements with its digit
+#pragma unroll
+  for (int j = 0; j < kSPT; j++) {
+    const bool valid = j * kSThreads + tid < nvalid;
+    uint32_t m = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+    for (int bit = 0; bit < 7; bit++) {
+      const uint32_t bl = __ballot_sync(0xffffffffu, (dg[j] >> bit) & 1u);
+      m &= ((dg[j] >> bit) & 1u) ? bl : ~bl;
+    }
+    const uint32_t below = m & lt;
+    const uint32_t c = valid ? s_wh[warp][dg[j]] : 0u;
+    __syncwarp();
+    if (valid && below == 0) s_wh[warp][dg[j]] = uint16_t(c + __popc(m));
+    __syncwarp();
+    rk[j] = c + __popc(below);
+  }
+  __syncthreads();
+  // digit-major offsets inside the tile; one global reservation per digit
+  {
+    uint32_t pre[kSWarps], tot = 0;
+    if (tid < kSDigits) {
+#pragma unroll
+      for (int w = 0; w < kSWarps; w++) {
+        pre[w] = tot;
+        tot += s_wh[w][tid];
+      }
+    }
+    unsigned long long t_all;
+    const uint32_t ds = uint32_t(block_excl_scan(tot, &t_all, s_red));
+    if (tid < kSDigits) {
+#pragma unroll
+      for (int w = 0; w < kSWarps; w++) s_wh[w][tid] = uint16_t(ds + pre[w]);
+      s_dstart[tid] = ds;
+      if (tot) {
+        const uint32_t reg = PASS == 1 ? tid : coarse * kSDigits + tid;
+        s_gbase[tid] = reg < a.nreg ? atomicAdd(&a.dcount[reg], tot) : 0xFFFFFFFFu;
+      }
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kSPT; j++) {
+    if (j * kSThreads + tid < nvalid) {
+      const uint32_t pos = s_wh[warp][dg[j]] + rk[j];
+      stage[pos] = e[j];
+      sdig[pos] = uint8_t(dg[j]);
+    }
+  }
+  __syncthreads();
+  // runs of equal digit are contiguous: consecutive threads write consecutive addresses
+  E* dst = reinterpret_cast<E*>(a.dst);
+  bool ovf = false;
+  for (uint32_t i = tid; i < nvalid; i += kSThreads) {
+    const uint32_t d = sdig[i];
+    const uint32_t reg = PASS == 1 ? d : coarse * kSDigits + d;
+    const uint32_t pos = s_gbase[d] + (i - s_dstart[d]);
+    if (reg < a.nreg && pos < a.dcap) dst[size_t(reg) * a.dcap + pos] = stage[i];
+    else ovf = true;
+  }
+  if (ovf) atomicOr(&stt->part_overflow, 1u);
+  if (bad) atomicOr(&stt->pad, 1u);
 }
 
 // ------------------------------------------------------------------ K_B
@@ -967,6 +1103,24 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
   const uint64_t T = uint64_t(kAThreads) * KPT;
   const uint64_t ntiles = (n_in + T - 1) / T;
   const unsigned gridA = unsigned(std::max<uint64_t>(1, std::min<uint64_t>(ntiles, uint64_t(sms) * occA)));
+  // large tables: two coalesced 128-way passes instead of one 16K-way scatter
+  const bool two_pass = sizeof(E) == 16 && pl.np > 1024 && !getenv("HM_ONE_PASS");
+  uint32_t ncoarse = 0, ccap = 0, tpc = 0;
+  E* cbuf = nullptr;
+  unsigned int* ccount = nullptr;
+  const size_t smemS = size_t(kSTile) * (sizeof(E) + 1);
+  auto kS1 = k_split<Src, E, 1>;
+  auto kS2 = k_split<Src, E, 2>;
+  if (two_pass) {
+    ncoarse = (pl.np + kSDigits - 1) / kSDigits;
+    const double mc = double(n_in) * double(kSDigits) * double(uint64_t(1) << pl.log2_bp) / double(nb);
+    ccap = uint32_t(mc + 8.0 * std::sqrt(mc + 1.0) + 1024.0);
+    tpc = (ccap + kSTile - 1) / kSTile;
+    if ((s = sc.alloc(&cbuf, size_t(ncoarse) * ccap * sizeof(E))) != HM_OK) return fail(s);
+    if ((s = sc.alloc(&ccount, size_t(ncoarse) * 4)) != HM_OK) return fail(s);
+    HM_CUDA_TRY(cudaFuncSetAttribute(kS1, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smemS)));
+    HM_CUDA_TRY(cudaFuncSetAttribute(kS2, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smemS)));
+  }
 
   BuildParams bp{};
   bp.smix = smix;
@@ -990,7 +1144,21 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
     for (int pass = 0; pass < 3; pass++) {
       HM_CUDA_TRY(cudaMemsetAsync(lbstate, 0, size_t(pl.np) * 8, st));
       HM_CUDA_TRY(cudaMemsetAsync(dstat, 0, sizeof(DevStatus), st));
-      if (run_a && ntiles > 0) {
+      if (run_a && ntiles > 0 && two_pass) {
+        HM_CUDA_TRY(cudaMemsetAsync(ccount, 0, size_t(ncoarse) * 4, st));
+        const SplitArgs a1{nullptr, nullptr, 0, 0, cbuf, ccount, ccap, ncoarse, 0};
+        {
+          LaunchScope ls_("k_split1", st);
+          kS1<<<unsigned((n_in + kSTile - 1) / kSTile), kSThreads, smemS, st>>>(src, bp, a1, dstat);
+        }
+        HM_CUDA_TRY(cudaGetLastError());
+        const SplitArgs a2{cbuf, ccount, ccap, tpc, pbuf, pcount, pl.cap, pl.np, ncoarse};
+        {
+          LaunchScope ls_("k_split2", st);
+          kS2<<<ncoarse * tpc, kSThreads, smemS, st>>>(src, bp, a2, dstat);
+        }
+        HM_CUDA_TRY(cudaGetLastError());
+      } else if (run_a && ntiles > 0) {
         {
           LaunchScope ls_("k_partition", st);
           if (smemHist) kA_s<<<gridA, kAThreads, smemA, st>>>(src, bp, pbuf, pcount, dstat);
