@@ -834,13 +834,34 @@ __global__ void __launch_bounds__(kBThreads, 1024 / kBThreads)
     if (huge) atomicOr(&stt->huge, 1u);
     if (bfail || uint64_t(maxs) * maxs > bp.bound4n) atomicOr(&stt->bound_fail, 1u);
   }
-  // publish the partition's aggregate, then look back for the exclusive prefix
-  // of S over the partitions before p (decoupled look-back; the predecessors
-  // started earlier and publish at this same point, so the wait is short)
+  // publish the partition's aggregate S_p now (decoupled look-back); the
+  // exclusive prefix is looked up after the search, when the predecessors
+  // have long published theirs
+  if (tid == 0) st_release(&lbstate[p], (p == 0 ? kFlagInc : kFlagAgg) | (S_p & kValMask));
+  if (tid < kNCls) s_next[tid] = 0;
+  __syncthreads();
+
+  // from here: bucket lb holds positions [sstart[lb], sstart[lb+1]); sidx[pos] = item;
+  // slot offset within the partition = s_cbase[lb / CH] + srel[lb]
+
+  HM_TMARK(6);
+  // level-2 seed search, map make2 over the multi-key buckets (PAPER.md:286-292):
+  // warp-per-bucket for 9 <= s <= 32, then thread-per-bucket classes from the
+  // rarest (longest chains) to the most common, so the tail of the last class
+  // is short and early warps go on to the singleton slots
+  search_warp(bp, part, skey, slist + s_cls_off[3], s_cls_off[4] - s_cls_off[3], sstart, sidx, sA, s_t, s_m2, bbase, stt,
+              same);
+  search_threads<8>(bp, part, skey, slist + s_cls_off[2], s_cls_off[3] - s_cls_off[2], &s_next[2], sstart, sidx, sA, s_t,
+                    s_m2, bbase, stt, same);
+  search_threads<4>(bp, part, skey, slist + s_cls_off[1], s_cls_off[2] - s_cls_off[1], &s_next[1], sstart, sidx, sA, s_t,
+                    s_m2, bbase, stt, same);
+  search_threads<2>(bp, part, skey, slist + s_cls_off[0], s_cls_off[1] - s_cls_off[0], &s_next[0], sstart, sidx, sA, s_t,
+                    s_m2, bbase, stt, same);
+  HM_TMARK(7);
+  // look-back: exclusive prefix of S over the partitions before p (warp 0,
+  // lane i inspects partition q0 - i: the closest inclusive prefix plus the
+  // aggregates in front of it give the base)
   if (warp == 0) {
-    // warp-parallel look-back: lane i inspects partition q0 - i; the closest
-    // inclusive prefix plus the aggregates in front of it give the base
-    if (lane == 0) st_release(&lbstate[p], (p == 0 ? kFlagInc : kFlagAgg) | (S_p & kValMask));
     unsigned long long base = 0;
     if (p > 0) {
       int64_t q0 = int64_t(p) - 1;
@@ -867,7 +888,6 @@ __global__ void __launch_bounds__(kBThreads, 1024 / kBThreads)
       s_base = base;
     }
   }
-  if (tid < kNCls) s_next[tid] = 0;
   __syncthreads();
   const unsigned long long base = s_base;
   if (ovf) {
@@ -880,23 +900,6 @@ __global__ void __launch_bounds__(kBThreads, 1024 / kBThreads)
   }
 
 
-  // from here: bucket lb holds positions [sstart[lb], sstart[lb+1]); sidx[pos] = item;
-  // slot offset within the partition = s_cbase[lb / CH] + srel[lb]
-
-  HM_TMARK(6);
-  // level-2 seed search, map make2 over the multi-key buckets (PAPER.md:286-292):
-  // warp-per-bucket for 9 <= s <= 32, then thread-per-bucket classes from the
-  // rarest (longest chains) to the most common, so the tail of the last class
-  // is short and early warps go on to the singleton slots
-  search_warp(bp, part, skey, slist + s_cls_off[3], s_cls_off[4] - s_cls_off[3], sstart, sidx, sA, s_t, s_m2, bbase, stt,
-              same);
-  search_threads<8>(bp, part, skey, slist + s_cls_off[2], s_cls_off[3] - s_cls_off[2], &s_next[2], sstart, sidx, sA, s_t,
-                    s_m2, bbase, stt, same);
-  search_threads<4>(bp, part, skey, slist + s_cls_off[1], s_cls_off[2] - s_cls_off[1], &s_next[1], sstart, sidx, sA, s_t,
-                    s_m2, bbase, stt, same);
-  search_threads<2>(bp, part, skey, slist + s_cls_off[0], s_cls_off[1] - s_cls_off[0], &s_next[0], sstart, sidx, sA, s_t,
-                    s_m2, bbase, stt, same);
-  HM_TMARK(7);
   // singleton slots (R12: a singleton sits at soff) need no search result;
   // 8 element loads in flight per thread, then the stores
   for (uint32_t lb0s = 0; lb0s < nbp; lb0s += 8 * kBThreads) {
@@ -918,7 +921,6 @@ __global__ void __launch_bounds__(kBThreads, 1024 / kBThreads)
     for (int j = 0; j < 8; j++)
       if (so[j] != ~0ull) slots[so[j]] = ev[j];
   }
-  __syncthreads();
 
   HM_TMARK(8);
   // directory (coalesced) and compact directory record per 32 buckets (one per
