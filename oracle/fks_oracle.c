@@ -643,3 +643,11 @@ int or_build_u64_shard(const uint64_t* keys, const uint64_t* vals, uint64_t n_re
   if (exhausted) return OR_ERR_SEED_EXHAUSTED;
   return OR_OK;
 }
+
+/* g k = hash(derive(seed,1,0,t1), k) mod n for every key: used
+ * by the full-size tests to select the keys of sampled bucket ranges. */
+void or_level1_buckets(const uint64_t* keys, uint64_t m, uint64_t n, uint64_t seed, uint32_t t1, uint64_t* out) {
+  uint64_t c1[3];
+  or_derive(seed, 1, 0, t1, c1);
+  for (uint64_t i = 0; i < m; i++) out[i] = or_hash(c1, keys[i]) % n;
+}

@@ -96,6 +96,7 @@ def lib():
         L.or_table_ctx.restype = p
         L.or_table_ctx.argtypes = [p]
         L.or_sizeof_header.restype = u64
+        L.or_level1_buckets.argtypes = [p, u64, u64, u64, u32, p]
         L.or_level1_S.restype = u64
         L.or_level1_S.argtypes = [p, u64, u64, u32, p]
         assert L.or_sizeof_header() == HEADER_DTYPE.itemsize
@@ -157,6 +158,15 @@ def groupby(m: int, is_, vs):
     items = np.zeros(max(1, len(is_)), np.uint64)
     lib().or_groupby(m, _ptr(is_), len(is_), _ptr(start), _ptr(items))
     return [[vs[int(i)] for i in items[int(start[g]):int(start[g + 1])]] for g in range(m)]
+
+
+def level1_buckets(keys, n: int, seed: int, t1: int) -> np.ndarray:
+    """g k for every key (mod n, the global key count)."""
+    keys = _u64(keys)
+    out = np.empty(len(keys), np.uint64)
+    if len(keys):
+        lib().or_level1_buckets(_ptr(keys), len(keys), n, seed, t1, _ptr(out))
+    return out
 
 
 def level1_S(keys, seed: int, t1: int):

@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(kAThreads) k_partition(Src src, BuildParams bp
 // shared-memory staging tile, fully coalesced.  Ranking inside the tile uses
 // warp ballots over the 7 digit bits and per-warp counters (no atomics).
 constexpr int kSThreads = 512, kSPT = 4, kSTile = kSThreads * kSPT;
-constexpr int kSWarps = kSThreads / 32, kSDigits = 128;
+constexpr int kSWarps = kSThreads / 32, kSDigits = 256, kSBits = 8;  // 8-bit digits: up to 64K partitions in two passes
 
 struct SplitArgs {
   // pass 2 source: the coarse buffer
@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(kSThreads, 2) k_split(Src src, BuildParams bp,
       const uint64_t lb = level1_bucket(bp.l1, e[j].key) - bp.b_lo;
       if (lb >= bp.nb) bad = true;
       const uint32_t p = uint32_t(lb >> bp.log2_bp);
-      dg[j] = PASS == 1 ? ((p >> 7) & (kSDigits - 1)) : (p & (kSDigits - 1));
+      dg[j] = PASS == 1 ? ((p >> kSBits) & (kSDigits - 1)) : (p & (kSDigits - 1));
     }
   }
   // warp-ballot rank of every element among the warp's elements with its digit
@@ -329,7 +329,7 @@ __global__ void __launch_bounds__(kSThreads, 2) k_split(Src src, BuildParams bp,
     const bool valid = j * kSThreads + tid < nvalid;
     uint32_t m = __ballot_sync(0xffffffffu, valid);
 #pragma unroll
-    for (int bit = 0; bit < 7; bit++) {
+    for (int bit = 0; bit < kSBits; bit++) {
       const uint32_t bl = __ballot_sync(0xffffffffu, (dg[j] >> bit) & 1u);
       m &= ((dg[j] >> bit) & 1u) ? bl : ~bl;
     }
@@ -717,6 +717,10 @@ __global__ void __launch_bounds__(kBThreads, 1024 / kBThreads)
       if (i < cnt) {
         skey[i] = ks[j];
         lbs[j] = uint32_t(level1_bucket(bp.l1, ks[j]) - bbase);
+        if (lbs[j] >= nbp) {  // cannot happen for a well-routed partition; never index out of range
+          atomicOr(&stt->pad, 1u);
+          lbs[j] = 0;
+        }
       }
     }
 #pragma unroll
@@ -1106,7 +1110,7 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
   const uint64_t ntiles = (n_in + T - 1) / T;
   const unsigned gridA = unsigned(std::max<uint64_t>(1, std::min<uint64_t>(ntiles, uint64_t(sms) * occA)));
   // large tables: two coalesced 128-way passes instead of one 16K-way scatter
-  const bool two_pass = sizeof(E) == 16 && pl.np > 1024 && !getenv("HM_ONE_PASS");
+  const bool two_pass = sizeof(E) == 16 && pl.np > 1024 && pl.np <= 65536 && !getenv("HM_ONE_PASS");
   uint32_t ncoarse = 0, ccap = 0, tpc = 0;
   E* cbuf = nullptr;
   unsigned int* ccount = nullptr;
