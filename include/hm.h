@@ -163,6 +163,12 @@ const char* hm_version(void);
  * devices, all threads): the evidence bench.py reports as gpu_launches. */
 uint64_t hm_kernel_launches(void);
 
+/* hm_release_workspace — free the build scratch this library caches between
+ * builds (per device and stream: partition buffers, fingerprints; about
+ * 40 B per key for u64 builds, 48 B per key for byte-key builds) on the
+ * current device.  Maps are not affected.  Synchronises the device. */
+hm_status hm_release_workspace(void);
+
 /* Per-kernel device timing (diagnostics, used by bench.py for the roofline).
  * While enabled, every kernel launch of this library is bracketed by two CUDA
  * events recorded on the stream it is launched on.  hm_profile_read

@@ -25,6 +25,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <map>
+#include <mutex>
 #include <type_traits>
 #include <vector>
 
@@ -1023,19 +1025,63 @@ static hm_status dmalloc(T** p, size_t bytes, cudaStream_t st) {
   return HM_OK;
 }
 
+// Build scratch, cached per (device, stream) between builds.  The partition
+// buffers have the same sizes build after build; taking them from the
+// stream-ordered pool each time cost up to 5.4 ms of page mapping per build
+// (measured on the 2^24-string config, when the pool was fragmented by the
+// maps' own arrays), so they stay allocated until hm_release_workspace().
+// Reuse is safe because everything that touches a stream's workspace is
+// ordered on that stream.
+enum WsRole { WS_FP, WS_BAD, WS_PBUF, WS_PCOUNT, WS_LBSTATE, WS_DSTAT, WS_CBUF, WS_CCOUNT, WS_NROLES };
+struct Workspace {
+  void* p[WS_NROLES] = {};
+  size_t bytes[WS_NROLES] = {};
+};
+static std::mutex g_ws_mu;
+static std::map<std::pair<int, cudaStream_t>, Workspace> g_ws;
+
 struct Scratch {
   cudaStream_t st;
-  std::vector<void*> ptrs;
-  ~Scratch() {
-    for (void* p : ptrs) cudaFreeAsync(p, st);
-  }
   template <class T>
-  hm_status alloc(T** p, size_t bytes) {
-    hm_status s = dmalloc(p, bytes, st);
-    if (s == HM_OK) ptrs.push_back(*p);
-    return s;
+  hm_status alloc(WsRole role, T** out, size_t bytes) {
+    int dev = 0;
+    HM_CUDA_TRY(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    Workspace& w = g_ws[{dev, st}];
+    bytes = std::max<size_t>(bytes, 16);
+    if (w.bytes[role] < bytes) {
+      if (w.p[role]) cudaFreeAsync(w.p[role], st);
+      w.p[role] = nullptr;
+      w.bytes[role] = 0;
+      void* v = nullptr;
+      hm_status s = dmalloc(&v, bytes, st);
+      if (s != HM_OK) return s;
+      w.p[role] = v;
+      w.bytes[role] = bytes;
+    }
+    *out = reinterpret_cast<T*>(w.p[role]);
+    return HM_OK;
   }
 };
+
+// Frees every cached workspace of the current device (stream-ordered on the
+// stream that owns it).
+hm_status release_workspace() {
+  int dev = 0;
+  HM_CUDA_TRY(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_ws_mu);
+  for (auto it = g_ws.begin(); it != g_ws.end();) {
+    if (it->first.first == dev) {
+      for (int r = 0; r < WS_NROLES; r++)
+        if (it->second.p[r]) cudaFreeAsync(it->second.p[r], it->first.second);
+      it = g_ws.erase(it);
+    } else {
+      ++it;
+    }
+  }
+  HM_CUDA_TRY(cudaDeviceSynchronize());
+  return HM_OK;
+}
 
 // Builds one table for buckets [b_lo, b_lo+nb) of a level-1 function mod
 // n_global from the n_in elements produced by `src`.
@@ -1059,16 +1105,16 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
   const int sms = num_sms();
   const uint64_t smix = seed_mix(seed);
 
-  Scratch sc{st, {}};
+  Scratch sc{st};
   E* pbuf = nullptr;
   unsigned int* pcount = nullptr;
   unsigned long long* lbstate = nullptr;
   DevStatus* dstat = nullptr;
   hm_status s;
-  if ((s = sc.alloc(&pbuf, size_t(pl.np) * pl.cap * sizeof(E))) != HM_OK) return s;
-  if ((s = sc.alloc(&pcount, size_t(pl.np) * 4)) != HM_OK) return s;
-  if ((s = sc.alloc(&lbstate, size_t(pl.np) * 8)) != HM_OK) return s;
-  if ((s = sc.alloc(&dstat, sizeof(DevStatus))) != HM_OK) return s;
+  if ((s = sc.alloc(WS_PBUF, &pbuf, size_t(pl.np) * pl.cap * sizeof(E))) != HM_OK) return s;
+  if ((s = sc.alloc(WS_PCOUNT, &pcount, size_t(pl.np) * 4)) != HM_OK) return s;
+  if ((s = sc.alloc(WS_LBSTATE, &lbstate, size_t(pl.np) * 8)) != HM_OK) return s;
+  if ((s = sc.alloc(WS_DSTAT, &dstat, sizeof(DevStatus))) != HM_OK) return s;
 
   uint64_t* dir = nullptr;
   E* slots = nullptr;
@@ -1122,8 +1168,8 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
     const double mc = double(n_in) * double(kSDigits) * double(uint64_t(1) << pl.log2_bp) / double(nb);
     ccap = uint32_t(mc + 8.0 * std::sqrt(mc + 1.0) + 1024.0);
     tpc = (ccap + kSTile - 1) / kSTile;
-    if ((s = sc.alloc(&cbuf, size_t(ncoarse) * ccap * sizeof(E))) != HM_OK) return fail(s);
-    if ((s = sc.alloc(&ccount, size_t(ncoarse) * 4)) != HM_OK) return fail(s);
+    if ((s = sc.alloc(WS_CBUF, &cbuf, size_t(ncoarse) * ccap * sizeof(E))) != HM_OK) return fail(s);
+    if ((s = sc.alloc(WS_CCOUNT, &ccount, size_t(ncoarse) * 4)) != HM_OK) return fail(s);
     HM_CUDA_TRY(cudaFuncSetAttribute(kS1, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smemS)));
     HM_CUDA_TRY(cudaFuncSetAttribute(kS2, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smemS)));
   }
@@ -1255,11 +1301,16 @@ hm_status build_u64_core(const uint64_t* keys, const uint64_t* vals, uint64_t n_
 }
 
 // ------------------------------------------------------------ byte keys
-__global__ void k_fingerprint(const uint8_t* __restrict__ bytes, const uint64_t* __restrict__ offs, uint64_t n,
-                              uint64_t r, uint64_t* __restrict__ fp) {
+// Fingerprints (R5) of all keys, thread per key, expanded form (fingerprint_pw).
+__global__ void __launch_bounds__(256) k_fingerprint(const uint8_t* __restrict__ bytes,
+                                                     const uint64_t* __restrict__ offs, uint64_t n, uint64_t r,
+                                                     uint64_t* __restrict__ fp) {
+  __shared__ FpPow s_pw;
+  if (threadIdx.x == 0) fp_pow_fill(&s_pw, r);
+  __syncthreads();
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
     const uint64_t o = offs[i], o1 = offs[i + 1];
-    fp[i] = fingerprint_dev(bytes, o, o1 - o, r);
+    fp[i] = fingerprint_pw(bytes, o, o1 - o, r, &s_pw);
   }
 }
 
@@ -1273,7 +1324,7 @@ __global__ void k_check_offsets(const uint64_t* __restrict__ offs, uint64_t n, u
 
 void launch_fingerprint(const uint8_t* bytes, const uint64_t* offs, uint64_t n, uint64_t r, uint64_t* fp,
                         cudaStream_t st) {
-  const unsigned grid = unsigned(std::min<uint64_t>((n + 255) / 256, uint64_t(num_sms()) * 16));
+  const unsigned grid = unsigned(std::min<uint64_t>((n + 255) / 256, uint64_t(num_sms()) * 8));
   {
     LaunchScope ls_("k_fingerprint", st);
     k_fingerprint<<<std::max(grid, 1u), 256, 0, st>>>(bytes, offs, n, r, fp);
@@ -1283,12 +1334,12 @@ void launch_fingerprint(const uint8_t* bytes, const uint64_t* offs, uint64_t n, 
 hm_status build_bytes_core(const uint8_t* bytes, const uint64_t* offsets, const uint64_t* vals, uint64_t n,
                            uint64_t seed, uint32_t log2_bp, cudaStream_t st, BuildOut* out, uint32_t* t0_out,
                            uint64_t* r_out) {
-  Scratch sc{st, {}};
+  Scratch sc{st};
   uint64_t* fp = nullptr;
   unsigned int* bad = nullptr;
   hm_status s;
-  if ((s = sc.alloc(&fp, n * 8)) != HM_OK) return s;
-  if ((s = sc.alloc(&bad, 4)) != HM_OK) return s;
+  if ((s = sc.alloc(WS_FP, &fp, n * 8)) != HM_OK) return s;
+  if ((s = sc.alloc(WS_BAD, &bad, 4)) != HM_OK) return s;
   HM_CUDA_TRY(cudaMemsetAsync(bad, 0, 4, st));
   {
     const unsigned grid = unsigned(std::min<uint64_t>((n + 255) / 256, uint64_t(num_sms()) * 16));

@@ -185,6 +185,13 @@ const char* hm_version(void) { return "hm 0.1 (sm_100a, spec v1)"; }
 
 uint64_t hm_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
 
+hm_status hm_release_workspace(void) {
+  g_last_error.clear();
+  hm_status s = check_device();
+  if (s != HM_OK) return s;
+  return release_workspace();
+}
+
 void hm_profile_enable(int on) { g_profile.store(on ? 1 : 0); }
 
 int hm_profile_read(hm_kernel_stat* out, int max) {

@@ -111,6 +111,7 @@ struct BuildOut {
   uint32_t t1 = 0;
 };
 // t1_fixed < 0: search t1 = 0..15 with the space bound of this table.
+hm_status release_workspace();
 hm_status build_u64_core(const uint64_t* keys, const uint64_t* vals, uint64_t n_in, uint64_t n_global,
                          uint64_t b_lo, uint64_t nb, int t1_fixed, uint64_t seed, uint32_t log2_bp,
                          cudaStream_t st, BuildOut* out);

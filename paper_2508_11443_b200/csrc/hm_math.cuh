@@ -195,6 +195,65 @@ __device__ __forceinline__ uint64_t fingerprint_dev(const uint8_t* bytes, uint64
   return f >= kP ? f - kP : f;
 }
 
+// The same fingerprint in expanded form.  Unrolling the Horner recurrence
+// acc_{i+1} = (acc_i + w_i) * r gives, exactly (mod P),
+//   acc_nw = sum_{i < nw} w_i * r^(nw - i),
+// so with the powers r^1 .. r^kFpPowMax tabulated once per block every word
+// costs one 32 x 61-bit product (two 32x32->64 multiplies and a fold) instead
+// of a dependent 61 x 61-bit modular multiply, and the words are independent.
+// Keys longer than 4*kFpPowMax bytes take the Horner loop above.
+constexpr int kFpPowMax = 16;
+struct FpPow {
+  uint32_t lo[kFpPowMax + 1];
+  uint32_t hi[kFpPowMax + 1];
+};
+// One thread of the block fills the table; the caller synchronises.
+__device__ inline void fp_pow_fill(FpPow* pw, uint64_t r) {
+  uint64_t p = 1;
+  pw->lo[0] = 1;
+  pw->hi[0] = 0;
+  for (int e = 1; e <= kFpPowMax; e++) {
+    p = mulmod_p(p, r);
+    pw->lo[e] = uint32_t(p);
+    pw->hi[e] = uint32_t(p >> 32);
+  }
+}
+
+// w * R (mod P), partially reduced (< 2^62 + 2^33), for w < 2^32 and R < P
+// given as 32-bit halves R = rh*2^32 + rl (rh < 2^29):  w*rl < 2^64 is folded
+// with 2^61 == 1; t = w*rh < 2^61 and t*2^32 = (t >> 29)*2^61 + (t mod 2^29)*2^32
+// == (t >> 29) + (t mod 2^29)*2^32.
+__device__ __forceinline__ uint64_t mul32_p(uint32_t w, uint32_t rl, uint32_t rh) {
+  const uint64_t x = uint64_t(w) * rl;
+  const uint64_t t = uint64_t(w) * rh;
+  return (x & kP) + (x >> 61) + (t >> 29) + ((t & 0x1FFFFFFFull) << 32);
+}
+
+__device__ __forceinline__ uint64_t fingerprint_pw(const uint8_t* bytes, uint64_t off, uint64_t len, uint64_t r,
+                                                   const FpPow* pw) {
+  if (len == 0) return 0;
+  if (len > 4 * kFpPowMax) return fingerprint_dev(bytes, off, len, r);
+  const uint64_t abase = off & ~uint64_t(3);
+  const uint32_t sh = uint32_t(off & 3) * 8;
+  const uint64_t last_aligned = (off + len - 1) & ~uint64_t(3);
+  const uint32_t nw = uint32_t(len + 3) >> 2;
+  uint64_t acc = 0;  // < 2^61 + 4 after every fold
+  uint32_t cur = ld_u32(bytes + abase);
+  for (uint32_t i = 0; i < nw; i++) {
+    const uint64_t na = abase + 4 * (uint64_t(i) + 1);
+    const uint32_t nxt = na <= last_aligned ? ld_u32(bytes + na) : 0u;
+    uint32_t w = sh ? __funnelshift_r(cur, nxt, sh) : cur;
+    const uint32_t rem = uint32_t(len) - 4 * i;
+    if (rem < 4) w &= (1u << (8 * rem)) - 1u;
+    acc += mul32_p(w, pw->lo[nw - i], pw->hi[nw - i]);
+    acc = (acc & kP) + (acc >> 61);
+    cur = nxt;
+  }
+  uint64_t f = acc + len;
+  f = (f & kP) + (f >> 61);
+  return f >= kP ? f - kP : f;
+}
+
 #endif
 
 }  // namespace hm

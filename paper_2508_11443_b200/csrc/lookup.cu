@@ -202,17 +202,24 @@ hm_status lookup_u64_launch(const hm_map* m, const uint64_t* q, uint64_t nq, uin
 
 // ------------------------------------------------------------ byte keys
 
+// Byte-key lookup: fingerprint the needle (R5,
+// expanded form), probe the compact directory and the 32-byte slot, and on a
+// fingerprint + length match compare the bytes with the map's context copy.
 template <int QPT>
 __global__ void __launch_bounds__(kLThreads) k_lookup_bytes(LookupParams lp, const uint8_t* __restrict__ qb,
                                                             const uint64_t* __restrict__ qo, uint64_t nq,
                                                             uint64_t* __restrict__ ov, uint8_t* __restrict__ of) {
   __shared__ uint64_t s_m2[33];
+  __shared__ FpPow s_pw;
   if (threadIdx.x < 33) s_m2[threadIdx.x] = threadIdx.x ? ~0ull / (uint64_t(threadIdx.x) * threadIdx.x) : 0ull;
+  if (threadIdx.x == 64) fp_pow_fill(&s_pw, lp.r_fp);
   __syncthreads();
+  const uint64_t pol_keep = policy_evict_last();
   const KV32* __restrict__ slots = reinterpret_cast<const KV32*>(lp.slots);
   const uint64_t per = uint64_t(kLThreads) * QPT;
   for (uint64_t base = blockIdx.x * per; base < nq; base += uint64_t(gridDim.x) * per) {
     uint64_t fp[QPT], b[QPT], d[QPT], off[QPT], len[QPT];
+    CDir rec[QPT];
 #pragma unroll
     for (int j = 0; j < QPT; j++) {
       const uint64_t idx = base + uint64_t(j) * kLThreads + threadIdx.x;
@@ -222,14 +229,23 @@ __global__ void __launch_bounds__(kLThreads) k_lookup_bytes(LookupParams lp, con
       if (idx < nq) {
         off[j] = qo[idx];
         len[j] = qo[idx + 1] - off[j];
-        fp[j] = fingerprint_dev(qb, off[j], len[j], lp.r_fp);
+        fp[j] = fingerprint_pw(qb, off[j], len[j], lp.r_fp, &s_pw);
       }
     }
 #pragma unroll
     for (int j = 0; j < QPT; j++) {
       const uint64_t idx = base + uint64_t(j) * kLThreads + threadIdx.x;
       b[j] = level1_bucket(lp.l1, fp[j]) - lp.b_lo;
-      d[j] = (idx < nq && b[j] < lp.nb) ? ld_dir(lp.dir + b[j]) : 0ull;
+      const bool ok = idx < nq && b[j] < lp.nb;
+      if (!ok) b[j] = 0;
+      rec[j] = ld_cdir(lp.cdir + (b[j] >> 5), pol_keep);
+      if (!ok) rec[j].w[1] = rec[j].w[2] = rec[j].w[3] = 0;
+    }
+#pragma unroll
+    for (int j = 0; j < QPT; j++) {
+      bool esc;
+      d[j] = cdir_entry(rec[j], b[j], lp.dir, &esc);
+      if (esc) d[j] = ld_dir(lp.dir + b[j]);
     }
 #pragma unroll
     for (int j = 0; j < QPT; j++) {
@@ -270,13 +286,11 @@ hm_status lookup_bytes_launch(const hm_map* m, const uint8_t* qb, const uint64_t
   lp.slots = m->slots;
   lp.ctx = m->ctx;
   lp.r_fp = m->r_fp;
-  constexpr int QPT = 2;
-  const uint64_t per = uint64_t(kLThreads) * QPT;
-  const uint64_t blocks = (nq + per - 1) / per;
+  const uint64_t blocks = (nq + kLThreads * 2 - 1) / (kLThreads * 2);
   const unsigned grid = unsigned(std::min<uint64_t>(blocks, uint64_t(num_sms()) * 8));
   {
     LaunchScope ls_("k_lookup_bytes", st);
-    k_lookup_bytes<QPT><<<grid, kLThreads, 0, st>>>(lp, qb, qo, nq, out_vals, out_found);
+    k_lookup_bytes<2><<<grid, kLThreads, 0, st>>>(lp, qb, qo, nq, out_vals, out_found);
   }
   HM_CUDA_TRY(cudaGetLastError());
   return HM_OK;

@@ -77,6 +77,7 @@ def lib():
         L.hm_last_error.restype = C.c_char_p
         L.hm_version.restype = C.c_char_p
         L.hm_kernel_launches.restype = C.c_uint64
+        L.hm_release_workspace.restype = C.c_int
         L.hm_profile_enable.argtypes = [C.c_int]
         L.hm_profile_enable.restype = None
         L.hm_profile_read.argtypes = [C.c_void_p, C.c_int]
@@ -337,6 +338,11 @@ def profile_read() -> dict:
 def kernel_launches() -> int:
     """Kernels launched by libhm so far in this process."""
     return int(lib().hm_kernel_launches())
+
+
+def release_workspace() -> None:
+    """Free the build scratch cached between builds on the current device."""
+    _check(lib().hm_release_workspace())
 
 
 def version() -> str:

@@ -113,13 +113,15 @@ def str_config(name, log2n, reps=5):
 
 
 def main():
-    res = [
-        u64_config("C1 2^16 u64 + 2^16 lookups", 16, 16, reps=20),
-        u64_config("C2 2^26 u64 + 2^26 lookups", 26, 26),
-        str_config("C3 2^24 strings + 2^24 lookups", 24),
-        u64_config("C4 2^29 u64 build (1 GPU)", 29, 26, reps=3),
-        u64_config("C5 2^30 lookups on a 2^27 table (1 GPU)", 27, 30, reps=3),
+    only = os.environ.get("ONLY", "C1,C2,C3,C4,C5").split(",")
+    todo = [
+        ("C1", lambda: u64_config("C1 2^16 u64 + 2^16 lookups", 16, 16, reps=20)),
+        ("C2", lambda: u64_config("C2 2^26 u64 + 2^26 lookups", 26, 26)),
+        ("C3", lambda: str_config("C3 2^24 strings + 2^24 lookups", 24)),
+        ("C4", lambda: u64_config("C4 2^29 u64 build (1 GPU)", 29, 26, reps=3)),
+        ("C5", lambda: u64_config("C5 2^30 lookups on a 2^27 table (1 GPU)", 27, 30, reps=3)),
     ]
+    res = [fn() for tag, fn in todo if tag in only]
     meta = {"gpu": torch.cuda.get_device_name(0), "peak_gbs": PEAK, "when": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime())}
     for r in res:
         print(json.dumps(r))

@@ -154,6 +154,30 @@ def test_u64_error_cases():
     assert e.value.name == "EMPTY"
 
 
+def test_build_workspace_reuse_release_and_streams():
+    """The cached build scratch (hm_release_workspace): shrinking and growing
+    sizes, a second stream, and a release between builds all give the
+    oracle's table."""
+    hm = _hm()
+    side = torch.cuda.Stream()
+    for i, n in enumerate([300_000, 1000, 70_001, 300_000, 5]):
+        keys, vals = gen.u64_keys(n), gen.u64_values(n)
+        ot = O.build_u64(keys, vals, i)
+        if i == 3:
+            hm.release_workspace()
+        k, v = dev(keys), dev(vals)
+        if i % 2:
+            torch.cuda.synchronize()
+            with torch.cuda.stream(side):
+                m = hm.HashMap.build_u64(k, v, seed=i)
+            side.synchronize()
+        else:
+            m = hm.HashMap.build_u64(k, v, seed=i)
+        assert_table_equal(m, ot)
+        m.free()
+    hm.release_workspace()
+
+
 def test_u64_adversarial_values_and_keys():
     """Keys at the edges of u64 (0, 2^64-1, P, P+5, 2^32 boundaries)."""
     hm = _hm()
