@@ -47,3 +47,16 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose=True)
+
+
+def build_variant(tag: str, defines: list[str]) -> str:
+    """Debug/experiment builds (libhm_<tag>.so with extra -D flags); never loaded
+    by the product path unless HM_LIB_PATH points at one."""
+    out = os.path.join(PKG, f"libhm_{tag}.so")
+    cmd = [NVCC, *[f for f in FLAGS if f != "-v" and f != "-Xptxas"], *[f"-D{d}" for d in defines], "-o", out] + \
+        [os.path.join(CSRC, f) for f in SOURCES]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError(f"nvcc failed building {out}")
+    return out

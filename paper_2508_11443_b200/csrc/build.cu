@@ -38,9 +38,6 @@ constexpr int kAThreads = 512;
 #ifndef HM_KB_THREADS
 #define HM_KB_THREADS 512
 #endif
-#ifndef HM_KB_LOG2BP
-#define HM_KB_LOG2BP 12
-#endif
 constexpr int kBThreads = HM_KB_THREADS;
 constexpr int kBWarps = kBThreads / 32;
 constexpr unsigned long long kFlagAgg = 1ull << 62, kFlagInc = 2ull << 62, kValMask = (1ull << 62) - 1;
@@ -99,7 +96,8 @@ __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long lon
   return v;
 }
 
-// Block-wide exclusive scan of u64 (kBThreads threads); also returns the total.
+// Block-wide exclusive scan of u64 (NT threads); also returns the total.
+template <int NT>
 __device__ __forceinline__ unsigned long long block_excl_scan(unsigned long long v, unsigned long long* total,
                                                               unsigned long long* s_red) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -112,17 +110,17 @@ __device__ __forceinline__ unsigned long long block_excl_scan(unsigned long long
   if (lane == 31) s_red[warp] = x;
   __syncthreads();
   if (warp == 0) {
-    unsigned long long w = lane < kBWarps ? s_red[lane] : 0ull;
+    unsigned long long w = lane < (NT / 32) ? s_red[lane] : 0ull;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       unsigned long long y = __shfl_up_sync(0xffffffffu, w, o);
       if (lane >= o) w += y;
     }
-    if (lane < kBWarps) s_red[lane] = w;
+    if (lane < (NT / 32)) s_red[lane] = w;
   }
   __syncthreads();
   const unsigned long long before = warp ? s_red[warp - 1] : 0ull;
-  *total = s_red[kBWarps - 1];
+  *total = s_red[(NT / 32) - 1];
   __syncthreads();
   return before + x - v;
 }
@@ -262,7 +260,7 @@ __global__ void __launch_bounds__(kAThreads) k_partition(Src src, BuildParams bp
 // shared-memory staging tile, fully coalesced.  Ranking inside the tile uses
 // warp ballots over the 7 digit bits and per-warp counters (no atomics).
 constexpr int kSThreads = 512, kSPT = 4, kSTile = kSThreads * kSPT;
-constexpr int kSWarps = kSThreads / 32, kSDigits = 256, kSBits = 8;  // 8-bit digits: up to 64K partitions in two passes
+constexpr int kSWarps = kSThreads / 32;  // BITS-bit digits: up to 2^(2 BITS) partitions in two passes
 
 struct SplitArgs {
   // pass 2 source: the coarse buffer
@@ -278,12 +276,13 @@ struct SplitArgs {
   uint32_t nreg_src;  // pass 2: source (coarse) regions
 };
 
-template <class Src, class E, int PASS>
+template <class Src, class E, int PASS, int BITS>
 __global__ void __launch_bounds__(kSThreads, 2) k_split(Src src, BuildParams bp, SplitArgs a,
                                                         DevStatus* __restrict__ stt) {
   extern __shared__ __align__(16) uint8_t smem[];
+  constexpr int kSDigits = 1 << BITS, kSBits = BITS;
   E* stage = reinterpret_cast<E*>(smem);
-  uint8_t* sdig = smem + size_t(kSTile) * sizeof(E);
+  uint16_t* sdig = reinterpret_cast<uint16_t*>(smem + size_t(kSTile) * sizeof(E));
   __shared__ uint16_t s_wh[kSWarps][kSDigits];
   __shared__ uint32_t s_dstart[kSDigits], s_gbase[kSDigits];
   __shared__ unsigned long long s_red[kSWarps];
@@ -354,7 +353,7 @@ __global__ void __launch_bounds__(kSThreads, 2) k_split(Src src, BuildParams bp,
       }
     }
     unsigned long long t_all;
-    const uint32_t ds = uint32_t(block_excl_scan(tot, &t_all, s_red));
+    const uint32_t ds = uint32_t(block_excl_scan<kSThreads>(tot, &t_all, s_red));
     if (tid < kSDigits) {
 #pragma unroll
       for (int w = 0; w < kSWarps; w++) s_wh[w][tid] = uint16_t(ds + pre[w]);
@@ -371,7 +370,7 @@ __global__ void __launch_bounds__(kSThreads, 2) k_split(Src src, BuildParams bp,
     if (j * kSThreads + tid < nvalid) {
       const uint32_t pos = s_wh[warp][dg[j]] + rk[j];
       stage[pos] = e[j];
-      sdig[pos] = uint8_t(dg[j]);
+      sdig[pos] = uint16_t(dg[j]);
     }
   }
   __syncthreads();
@@ -390,143 +389,323 @@ __global__ void __launch_bounds__(kSThreads, 2) k_split(Src src, BuildParams bp,
 }
 
 // ------------------------------------------------------------------ K_B
-// Size classes of multi-key buckets and the lane-group width G that searches
-// one bucket: s=2 -> 2 lanes, s=3..4 -> 4, s=5..8 -> 8, s=9..32 -> 32.
-constexpr int kNCls = 4;
-__device__ __forceinline__ int size_class(uint32_t s) { return s == 2 ? 0 : s <= 4 ? 1 : s <= 8 ? 2 : s <= 32 ? 3 : 4; }
-__device__ __forceinline__ int class_log2g(int c) { return c == 0 ? 1 : c == 1 ? 2 : c == 2 ? 3 : 5; }
+// One CTA per build partition of BP = 2^log2_bp level-1 buckets; everything
+// between reading the partition and writing its table slice happens in shared
+// memory, so that global memory sees one bulk read of the partition and fully
+// coalesced writes of the directory and the slots:
+//   load   the partition's elements, one cp.async.bulk (TMA) into shared memory
+//   hist   g k of every item and its rank in its bucket from a
+//          shared-memory atomicAdd (hist) — measured on B200 at
+//          ~4.6 SM-cycles per warp-wide spread-address atomic, 9x cheaper than
+//          a warp-ballot rank over 11 bucket bits (scripts/micro/smem_atomics.cu)
+//   scan   exclusive scans of s and s^2 (presum, R1/R2) and of
+//          the size-class counts; groupby as a counting scatter
+//   search make2 per multi-key bucket (search_* above); a
+//          finished bucket maps its s^2 slots to their source items: members,
+//          and the lowest-slot member as value-0 filler elsewhere (R10)
+//   out    decoupled look-back for the global slot base, then the slots
+//          (consecutive lanes -> consecutive 16/32-byte records), the directory
+//          and the compact directory.
+// Size classes of multi-key buckets for the search: s=2, 3..8 (a thread per
+// bucket and attempt, K = 2/8 key registers) and 9..32 (a warp per bucket).
+constexpr int kNCls = 3;
+__device__ __forceinline__ int size_class(uint32_t s) { return s == 2 ? 0 : s <= 8 ? 1 : s <= 32 ? 2 : 3; }
 
-template <class E>
-__device__ __forceinline__ E shfl_elem(const E& e, int src) {
-  constexpr int W = sizeof(E) / 8;
-  const uint64_t* p = reinterpret_cast<const uint64_t*>(&e);
-  E out;
-  uint64_t* q = reinterpret_cast<uint64_t*>(&out);
-#pragma unroll
-  for (int w = 0; w < W; w++) q[w] = __shfl_sync(0xffffffffu, p[w], src);
-  return out;
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-// make2 for one size class, K key registers per thread.
-// Every thread owns one bucket at a time and makes one attempt per loop
-// iteration: derive(seed,2,b,t), the s level-2 slots hash mod s^2, and an
-// occupancy bitmap as `collision`.  Threads that finish take
-// the next bucket of the class from a shared counter (one warp-aggregated
-// atomic per refill), so the spread of attempt counts does not idle the warp.
-template <int K, class E, class Same>
-__device__ __forceinline__ void search_threads(const BuildParams& bp, const E* part, const uint64_t* skey,
-                                               const uint16_t* list, uint32_t L,
-                                               uint32_t* next, const uint16_t* sstart, const uint16_t* sidx,
-                                               uint16_t* sA, uint8_t* s_t, const uint64_t* s_m2, uint64_t bbase,
-                                               DevStatus* stt, const Same& same) {
-  const uint32_t lane = threadIdx.x & 31, lt = (1u << lane) - 1u;
-  bool have = false, drained = false;
-  uint32_t lb = 0, st0 = 0, s = 2, t = 0;
-  uint64_t k[K];
-  FastMod fm{4, s_m2[2]};
+// make2 for buckets with 2 <= s <= 8, in CTA-wide rounds.
+// One attempt = derive(seed,2,b,t), the s level-2 slots hash mod s^2 and the
+// occupancy bitmap as `collision`.  Round 0 tries t = 0 for
+// every multi-key bucket (a thread per bucket); the buckets that collide are
+// queued, and every later round tries A consecutive attempts of each queued
+// bucket on A adjacent lanes (A = 512 / queue length, up to 8), the lowest
+// successful attempt winning — the same t as trying them one by one (R13),
+// without the long per-bucket chains that leave most lanes idle.
+
+// Search state shared by the rounds (shared memory).
+struct SearchCtx {
+  const uint16_t* sstart;
+  const uint8_t* ss;
+  const uint16_t* sidx;
+  const uint32_t* soff;  // slot offset of each bucket inside the partition
+  uint16_t* sA;
+  uint8_t* s_t;
+  uint16_t* src;  // slot -> item map (nullptr: not staged)
+};
+
+__device__ __forceinline__ uint32_t l2_slot(const Consts& c, uint64_t key, uint32_t s, const FastMod& fm) {
+  const uint64_t hv = hash64(c, key);
+  // mod s^2: a mask when s is a power of two
+  return (s & (s - 1)) == 0 ? uint32_t(hv) & (s * s - 1) : uint32_t(fastmod(hv, fm));
+}
+
+// Is attempt t injective on the bucket?  Keys are read from shared memory, s
+// is a runtime bound (no predicated-off work for small buckets).
+template <class E>
+__device__ __forceinline__ bool attempt_ok(uint64_t smix, uint64_t b, uint32_t t, const E* skv, const uint16_t* sidx,
+                                           uint32_t st0, uint32_t s, const FastMod& fm) {
+  const Consts c = derive(smix, 2, b, t);
+  uint64_t bits = 0;
+  for (uint32_t j = 0; j < s; j++) {
+    const uint64_t bit = 1ull << l2_slot(c, skv[sidx[st0 + j]].key, s, fm);
+    if (bits & bit) return false;
+    bits |= bit;
+  }
+  return true;
+}
+
+// The bucket is done with attempt t: record t and the level-2 slot of every
+// member, and map its s^2 slots to their source items — the members, and the
+// lowest-slot member as value-0 filler everywhere else (R10).
+template <class E>
+__device__ __forceinline__ void bucket_done(const SearchCtx& X, uint64_t smix, uint64_t b, uint32_t lb, uint32_t st0,
+                                            uint32_t s, uint32_t t, const E* skv, const FastMod& fm) {
+  X.s_t[lb] = uint8_t(t);
+  const Consts c = derive(smix, 2, b, t);
+  uint64_t bits = 0;
+  uint32_t hmin = 0xFFFFu, fill = 0;
+  for (uint32_t j = 0; j < s; j++) {
+    const uint32_t it = X.sidx[st0 + j];
+    const uint32_t h = l2_slot(c, skv[it].key, s, fm);
+    X.sA[st0 + j] = uint16_t(h);
+    bits |= 1ull << h;
+    if (h < hmin) {
+      hmin = h;
+      fill = it;
+    }
+  }
+  if (X.src) {
+    uint16_t* o = X.src + X.soff[lb];
+    const uint32_t s2 = s * s;
+    uint64_t fr = ~bits & (s2 == 64 ? ~0ull : ((1ull << s2) - 1));  // the unused slots
+    while (fr) {
+      o[__ffsll(fr) - 1] = uint16_t(fill | 0x8000u);
+      fr &= fr - 1;
+    }
+    for (uint32_t j = 0; j < s; j++) o[X.sA[st0 + j]] = X.sidx[st0 + j];
+  }
+}
+
+// Slots h[] of bucket lb under constants c (K keys in registers); returns the
+// occupancy bitmap, or 0 on a collision (s >= 2, so a valid map is never 0).
+template <int K>
+__device__ __forceinline__ uint64_t slots_of(const Consts& c, const uint64_t* k, uint32_t s, const FastMod& fm,
+                                             uint32_t* h) {
+  uint64_t bits = 0;
+  bool coll = false;
 #pragma unroll
-  for (int j = 0; j < K; j++) k[j] = 0;
-  while (true) {
-    const bool need = !have && !drained;
-    const uint32_t nm = __ballot_sync(0xffffffffu, need);
-    if (nm) {
-      const uint32_t leader = __ffs(nm) - 1;
-      uint32_t b0 = 0;
-      if (lane == leader) b0 = atomicAdd(next, uint32_t(__popc(nm)));
-      b0 = __shfl_sync(0xffffffffu, b0, leader);
-      if (need) {
-        const uint32_t idx = b0 + __popc(nm & lt);
-        if (idx < L) {
-          lb = list[idx];
-          st0 = sstart[lb];
-          s = uint32_t(sstart[lb + 1]) - st0;
-          t = 0;
-          have = true;
-          fm = FastMod{uint64_t(s) * s, s_m2[s]};
+  for (int j = 0; j < K; j++) {
+    h[j] = 0;
+    if (uint32_t(j) < s) {
+      const uint64_t hv = hash64(c, k[j]);
+      h[j] = (K == 2 || (s & (s - 1)) == 0) ? uint32_t(hv) & (s * s - 1) : uint32_t(fastmod(hv, fm));
+      const uint64_t bit = 1ull << h[j];
+      coll |= (bits & bit) != 0;
+      bits |= bit;
+    }
+  }
+  return coll ? 0ull : bits;
+}
+
+// bucket_done with the slots already in registers.
+template <int K>
+__device__ __forceinline__ void bucket_done_regs(const SearchCtx& X, uint32_t lb, uint32_t st0, uint32_t s,
+                                                 uint32_t t, const uint32_t* h, uint64_t bits) {
+  X.s_t[lb] = uint8_t(t);
+  uint32_t hmin = 0xFFFFu, fill = 0;
+  uint32_t it[K];
 #pragma unroll
-          for (int j = 0; j < K; j++) k[j] = uint32_t(j) < s ? skey[sidx[st0 + j]] : 0ull;
-        } else {
-          drained = true;
-        }
+  for (int j = 0; j < K; j++)
+    if (uint32_t(j) < s) {
+      it[j] = X.sidx[st0 + j];
+      X.sA[st0 + j] = uint16_t(h[j]);
+      if (h[j] < hmin) {
+        hmin = h[j];
+        fill = it[j];
       }
     }
-    if (!__any_sync(0xffffffffu, have)) break;
-    if (have) {
-      const Consts c = derive(bp.smix, 2, bbase + lb, t);
-      uint64_t bits = 0;
-      bool coll = false;
-      uint32_t h[K];
+  if (X.src) {
+    uint16_t* o = X.src + X.soff[lb];
+    const uint32_t s2 = s * s;
+    uint64_t fr = ~bits & (s2 == 64 ? ~0ull : ((1ull << s2) - 1));  // the unused slots
+    while (fr) {
+      o[__ffsll(fr) - 1] = uint16_t(fill | 0x8000u);
+      fr &= fr - 1;
+    }
 #pragma unroll
-      for (int j = 0; j < K; j++) {
-        h[j] = 0;
-        if (uint32_t(j) < s) {
-          const uint64_t hv = hash64(c, k[j]);
-          // mod s^2: a mask when s is a power of two (always for the s = 2 class)
-          h[j] = (K == 2 || (s & (s - 1)) == 0) ? uint32_t(hv) & (s * s - 1) : uint32_t(fastmod(hv, fm));
-          const uint64_t bit = 1ull << h[j];
-          coll |= (bits & bit) != 0;
-          bits |= bit;
+    for (int j = 0; j < K; j++)
+      if (uint32_t(j) < s) o[h[j]] = uint16_t(it[j]);
+  }
+}
+
+// Round 0 for one bucket with K key registers: attempts t = 0 and t = 1 are
+// evaluated together (two independent derive/hash chains: the second one
+// hides the first one's latency), the lower successful one wins.  Equal keys
+// -> duplicate / fingerprint collision (checked once: equal keys collide under
+// every t).  Returns the first attempt still to try (0: the bucket is done).
+template <int K, class E, class Same>
+__device__ __forceinline__ uint32_t round0_bucket(const BuildParams& bp, const E* skv, const SearchCtx& X, uint32_t lb,
+                                              const uint64_t* s_m2, uint64_t bbase, DevStatus* stt,
+                                              const Same& same) {
+  const uint32_t st0 = X.sstart[lb], s = X.ss[lb];
+  uint64_t k[K];
+#pragma unroll
+  for (int j = 0; j < K; j++) k[j] = uint32_t(j) < s ? skv[X.sidx[st0 + j]].key : 0ull;
+  const FastMod fm{uint64_t(s) * s, s_m2[s]};
+  constexpr bool kTwo = K <= 4;  // (two attempts in flight; the rare s = 5..8 buckets try one)
+  uint32_t h0[K], h1[kTwo ? K : 1];
+  uint64_t b0, b1 = 0;
+  if (kTwo) {
+    const Consts c0 = derive(bp.smix, 2, bbase + lb, 0), c1 = derive(bp.smix, 2, bbase + lb, 1);
+    b0 = slots_of<K>(c0, k, s, fm, h0);
+    b1 = slots_of<K>(c1, k, s, fm, h1);
+  } else {
+    b0 = slots_of<K>(derive(bp.smix, 2, bbase + lb, 0), k, s, fm, h0);
+  }
+  if (b0) {
+    bucket_done_regs<K>(X, lb, st0, s, 0, h0, b0);
+    return 0;
+  }
+  int di = -1, dj = -1;
+#pragma unroll
+  for (int i = 0; i < K; i++)
+#pragma unroll
+    for (int j = i + 1; j < K; j++)
+      if (uint32_t(j) < s && k[i] == k[j] && di < 0) {
+        di = i;
+        dj = j;
+      }
+  if (di >= 0) {
+    const bool d = same.same(skv[X.sidx[st0 + di]], skv[X.sidx[st0 + dj]]);
+    atomicOr(d ? &stt->dup : &stt->fpcoll, 1u);
+    X.s_t[lb] = 0;
+    return 0;
+  }
+  if (kTwo && b1) {
+    bucket_done_regs<K>(X, lb, st0, s, 1, h1, b1);
+    return 0;
+  }
+  return kTwo ? 2 : 1;
+}
+
+// Round 0 over the multi-key list ([s = 2 | s = 3..4 | s = 5..8] regions, so
+// almost every warp runs one key-register width): the buckets that need t >= 2
+// are queued.
+template <class E, class Same>
+__device__ __forceinline__ void search_round0(const BuildParams& bp, const E* skv, const SearchCtx& X,
+                                              const uint16_t* list, uint32_t n2, uint32_t n4, uint32_t L,
+                                              uint32_t* queue, uint32_t* qn, const uint64_t* s_m2, uint64_t bbase,
+                                              DevStatus* stt, const Same& same) {
+  const uint32_t lane = threadIdx.x & 31, lt = (1u << lane) - 1u;
+  // one entry per thread, warps in reverse order (warp 0, which did the
+  // look-back, gets the fewest); entries beyond kBThreads go to the queue with
+  // t = 0 — every warp runs one round-0 iteration
+  const uint32_t e = (kBWarps - 1 - (threadIdx.x >> 5)) * 32 + lane;
+  for (uint32_t x = kBThreads + threadIdx.x; x < L; x += kBThreads) queue[atomicAdd(qn, 1u)] = list[x];
+  if (e - lane < L) {
+    uint32_t lb = 0, tn = 0;
+    if (e < L) {
+      lb = list[e];
+      if (e < n2) tn = round0_bucket<2>(bp, skv, X, lb, s_m2, bbase, stt, same);
+      else if (e < n4) tn = round0_bucket<4>(bp, skv, X, lb, s_m2, bbase, stt, same);
+      else tn = round0_bucket<8>(bp, skv, X, lb, s_m2, bbase, stt, same);
+    }
+    const bool retry = tn != 0;
+    const uint32_t m = __ballot_sync(0xffffffffu, retry);
+    if (m) {
+      const uint32_t leader = __ffs(m) - 1;
+      uint32_t q0 = 0;
+      if (lane == leader) q0 = atomicAdd(qn, uint32_t(__popc(m)));
+      q0 = __shfl_sync(0xffffffffu, q0, leader);
+      if (retry) queue[q0 + __popc(m & lt)] = lb | (tn << 16);
+    }
+  }
+}
+
+// Round r >= 1: A = 2^logA adjacent lanes per queued bucket, attempt tb + j on lane j.
+template <class E, class Same>
+__device__ __forceinline__ void search_round(const BuildParams& bp, const E* skv, const SearchCtx& X,
+                                             const uint32_t* queue, uint32_t L, uint32_t logA, uint32_t* nqueue,
+                                             uint32_t* nqn, const uint64_t* s_m2, uint64_t bbase, DevStatus* stt,
+                                             const Same& same) {
+  const uint32_t lane = threadIdx.x & 31, lt = (1u << lane) - 1u;
+  const uint32_t A = 1u << logA, W = L << logA;
+  const uint32_t gmask = A == 32 ? 0xffffffffu : (((1u << A) - 1u) << (lane & ~(A - 1u)));
+  for (uint32_t w0 = threadIdx.x & ~31u; w0 < W; w0 += kBThreads) {
+    const uint32_t w = w0 + lane;
+    bool ok = false, lead = false;
+    uint32_t lb = 0, st0 = 0, s = 2, t = 0, tb = 0;
+    FastMod fm{4, 0};
+    if (w < W) {
+      const uint32_t q = queue[w >> logA];
+      lb = q & 0xFFFFu;
+      tb = q >> 16;
+      t = tb + (w & (A - 1u));
+      lead = (w & (A - 1u)) == 0;
+      st0 = X.sstart[lb];
+      s = X.ss[lb];
+      fm = FastMod{uint64_t(s) * s, s_m2[s]};
+      if (t < kT2Cap) ok = attempt_ok(bp.smix, bbase + lb, t, skv, X.sidx, st0, s, fm);
+    }
+    const uint32_t om = __ballot_sync(0xffffffffu, ok) & gmask;
+    if (ok && lane == uint32_t(__ffs(om) - 1)) bucket_done(X, bp.smix, bbase + lb, lb, st0, s, t, skv, fm);
+    bool retry = false;
+    if (lead && om == 0 && tb == 0) {  // equal keys collide under every t: check once
+      for (uint32_t i = 0; i < s && !retry; i++) {
+        const uint32_t ii = X.sidx[st0 + i];
+        for (uint32_t j = i + 1; j < s; j++) {
+          const uint32_t jj = X.sidx[st0 + j];
+          if (skv[jj].key == skv[ii].key) {
+            atomicOr(same.same(skv[ii], skv[jj]) ? &stt->dup : &stt->fpcoll, 1u);
+            X.s_t[lb] = 0;
+            retry = true;  // (marks "handled")
+            break;
+          }
         }
       }
-      bool done = false;
-      if (!coll) {
-#pragma unroll
-        for (int j = 0; j < K; j++)
-          if (uint32_t(j) < s) sA[st0 + j] = uint16_t(h[j]);
-        done = true;
+      lead = !retry;
+      retry = false;
+    }
+    if (lead && om == 0) {
+      if (tb + A >= kT2Cap) {
+        atomicOr(&stt->exhausted, 1u);
+        X.s_t[lb] = 0;
       } else {
-        if (t == 0) {  // equal keys collide under every t: check the bucket once
-          int di = -1, dj = -1;
-#pragma unroll
-          for (int i = 0; i < K; i++)
-#pragma unroll
-            for (int j = i + 1; j < K; j++)
-              if (uint32_t(j) < s && k[i] == k[j] && di < 0) {
-                di = i;
-                dj = j;
-              }
-          if (di >= 0) {
-            const bool d = same.same(part[sidx[st0 + di]], part[sidx[st0 + dj]]);
-            atomicOr(d ? &stt->dup : &stt->fpcoll, 1u);
-            done = true;
-          }
-        }
-        if (!done) {
-          if (t + 1 >= kT2Cap) {
-            atomicOr(&stt->exhausted, 1u);
-            t = 0;
-            done = true;
-          } else {
-            t++;
-          }
-        }
+        retry = true;
       }
-      if (done) {
-        s_t[lb] = uint8_t(t);
-        have = false;
-      }
+    }
+    const uint32_t m = __ballot_sync(0xffffffffu, retry);
+    if (m) {
+      const uint32_t leader = __ffs(m) - 1;
+      uint32_t q0 = 0;
+      if (lane == leader) q0 = atomicAdd(nqn, uint32_t(__popc(m)));
+      q0 = __shfl_sync(0xffffffffu, q0, leader);
+      if (retry) nqueue[q0 + __popc(m & lt)] = lb | ((tb + A) << 16);
     }
   }
 }
 
 // make2 for the rare 9 <= s <= 32 buckets: a warp per bucket, a lane per key,
-// __match_any_sync on the level-2 slots as the injectivity test.
+// __match_any_sync on the level-2 slots as the injectivity test; then the
+// bucket's s^2 slots are mapped as in bucket_done (bitsw: a per-warp bitmap).
 template <class E, class Same>
-__device__ __forceinline__ void search_warp(const BuildParams& bp, const E* part, const uint64_t* skey,
-                                            const uint16_t* list, uint32_t L,
-                                            const uint16_t* sstart, const uint16_t* sidx, uint16_t* sA, uint8_t* s_t,
-                                            const uint64_t* s_m2, uint64_t bbase, DevStatus* stt, const Same& same) {
+__device__ __forceinline__ void search_warp(const BuildParams& bp, const E* skv, const SearchCtx& X,
+                                            const uint16_t* list, uint32_t L, const uint64_t* s_m2, uint64_t bbase,
+                                            DevStatus* stt, const Same& same, uint32_t* bitsw) {
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (uint32_t idx = warp; idx < L; idx += kBWarps) {
-    const uint32_t lb = list[idx], st0 = sstart[lb], s = uint32_t(sstart[lb + 1]) - st0;
+    const uint32_t lb = list[idx], st0 = X.sstart[lb], s = X.ss[lb];
     const bool mine = lane < s;
-    const uint64_t key = mine ? skey[sidx[st0 + lane]] : 0ull;
+    const uint32_t item = mine ? X.sidx[st0 + lane] : 0u;
+    const uint64_t key = mine ? skv[item].key : 0ull;
     const uint32_t valid = __ballot_sync(0xffffffffu, mine);
     const uint32_t dm = __match_any_sync(0xffffffffu, key) & valid & ~(1u << lane);
     uint32_t t = 0;
     if (__any_sync(0xffffffffu, mine && dm != 0)) {
       if (mine && dm != 0) {
-        const bool d = same.same(part[sidx[st0 + lane]], part[sidx[st0 + __ffs(dm) - 1]]);
+        const bool d = same.same(skv[item], skv[X.sidx[st0 + __ffs(dm) - 1]]);
         atomicOr(d ? &stt->dup : &stt->fpcoll, 1u);
       }
     } else {
@@ -541,112 +720,97 @@ __device__ __forceinline__ void search_warp(const BuildParams& bp, const E* part
       if (t >= kT2Cap) {
         if (lane == 0) atomicOr(&stt->exhausted, 1u);
         t = 0;
-      } else if (mine) {
-        sA[st0 + lane] = uint16_t(h);
-      }
-    }
-    if (lane == 0) s_t[lb] = uint8_t(t);
-  }
-}
-
-// Table write of one class, thread per bucket: members at soff + h, unused
-// slots get the lowest-slot member with value 0 (R10).
-template <int K, class E>
-__device__ __forceinline__ void write_threads(const uint16_t* list, uint32_t L, const uint16_t* sstart,
-                                              const uint16_t* sidx, const uint16_t* sA, const E* part, E* slots,
-                                              unsigned long long base, const uint32_t* s_cbase, const uint16_t* srel,
-                                              uint32_t lgch) {
-  for (uint32_t idx = threadIdx.x; idx < L; idx += kBThreads) {
-    const uint32_t lb = list[idx], st0 = sstart[lb], s = uint32_t(sstart[lb + 1]) - st0;
-    const uint64_t soff = base + s_cbase[lb >> lgch] + srel[lb];
-    E e[K];
-    uint32_t h[K];
-#pragma unroll
-    for (int j = 0; j < K; j++)  // all member loads in flight before any store
-      if (uint32_t(j) < s) {
-        h[j] = sA[st0 + j];
-        e[j] = part[sidx[st0 + j]];
-      }
-    uint64_t bits = 0;
-    uint32_t hmin = 0xFFFFu;
-    int jmin = 0;
-#pragma unroll
-    for (int j = 0; j < K; j++) {
-      if (uint32_t(j) < s) {
-        slots[soff + h[j]] = e[j];
-        bits |= 1ull << h[j];
-        if (h[j] < hmin) {
-          hmin = h[j];
-          jmin = j;
+      } else {
+        if (mine) X.sA[st0 + lane] = uint16_t(h);
+        if (X.src) {
+          uint16_t* o = X.src + X.soff[lb];
+          bitsw[lane] = 0;
+          __syncwarp();
+          if (mine) atomicOr(&bitsw[h >> 5], 1u << (h & 31));
+          const uint32_t hmin = __reduce_min_sync(0xffffffffu, mine ? h : 0xFFFFu);
+          const uint32_t who = __ffs(__ballot_sync(0xffffffffu, mine && h == hmin)) - 1;
+          const uint32_t fill = __shfl_sync(0xffffffffu, item, who);
+          __syncwarp();
+          for (uint32_t x = lane; x < s * s; x += 32)
+            if (!((bitsw[x >> 5] >> (x & 31)) & 1)) o[x] = uint16_t(fill | 0x8000u);
+          __syncwarp();
+          if (mine) o[h] = uint16_t(item);
         }
       }
     }
-    E f = e[0];
-#pragma unroll
-    for (int j = 1; j < K; j++)
-      if (j == jmin) f = e[j];
-    f.value = 0;
-    const uint32_t s2 = s * s;
-    for (uint32_t x = 0; x < s2; x++)
-      if (!((bits >> x) & 1)) slots[soff + x] = f;
+    if (lane == 0) X.s_t[lb] = uint8_t(t);
   }
 }
 
-template <class E>
-__device__ __forceinline__ void write_warp(const uint16_t* list, uint32_t L, const uint16_t* sstart,
-                                           const uint16_t* sidx, const uint16_t* sA, const E* part, E* slots,
-                                           unsigned long long base, const uint32_t* s_cbase, const uint16_t* srel,
-                                           uint32_t lgch, uint32_t* bitsw) {
-  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (uint32_t idx = warp; idx < L; idx += kBWarps) {
-    const uint32_t lb = list[idx], st0 = sstart[lb], s = uint32_t(sstart[lb + 1]) - st0;
-    const uint64_t soff = base + s_cbase[lb >> lgch] + srel[lb];
-    const bool mine = lane < s;
-    uint32_t h = 0xFFFFu;
-    E e;
-    bitsw[lane] = 0;
-    __syncwarp();
-    if (mine) {
-      h = sA[st0 + lane];
-      e = part[sidx[st0 + lane]];
-      slots[soff + h] = e;
-      atomicOr(&bitsw[h >> 5], 1u << (h & 31));
-    }
-    const uint32_t hmin = __reduce_min_sync(0xffffffffu, h);
-    const uint32_t who = __ffs(__ballot_sync(0xffffffffu, mine && h == hmin)) - 1;
-    E f = shfl_elem(e, who);
-    f.value = 0;
-    __syncwarp();
-    for (uint32_t x = lane; x < s * s; x += 32)
-      if (!((bitsw[x >> 5] >> (x & 31)) & 1)) slots[soff + x] = f;
-    __syncwarp();
-  }
-}
-
-// Dynamic shared memory of k_bucket (all offsets 16-byte aligned).  Regions
-// are reused once their first use is over (see the phase comments).
-struct BucketSmem {
-  size_t skey, sA, sidx, tmp, whist, sstart, st, total;
-};
 __host__ __device__ __forceinline__ size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
-__host__ __device__ __forceinline__ uint32_t bucket_chunk(uint32_t BP) {  // buckets per owner thread
-  return BP / kBThreads > 2 ? BP / kBThreads : 2;
-}
-__host__ __device__ __forceinline__ BucketSmem bucket_smem_layout(uint32_t cap, uint32_t BP) {
-  const uint32_t CH = bucket_chunk(BP), nown = BP / CH;
-  size_t wh = size_t(kBWarps) * nown * 2;                      // P1-P3: per-warp owner counters
-  wh = wh > size_t(CH) * kBThreads * 2 ? wh : size_t(CH) * kBThreads * 2;  // P4: per-thread bucket counters
-  wh = wh > (size_t(cap) / 2 + 8) * 2 ? wh : (size_t(cap) / 2 + 8) * 2;   // then: class lists
+// Dynamic shared memory of k_bucket (all offsets 16-byte aligned), computed on
+// the host and passed in BuildParams (kernel parameters live in the constant
+// bank: no registers, no recomputation inside the kernel's loops).
+__host__ __device__ __forceinline__ BucketSmem bucket_smem_layout(uint32_t cap, uint32_t BP, uint32_t esz) {
   BucketSmem L;
-  L.skey = 0;                                           // u64[cap]: the partition's keys (item order)
-  L.sA = L.skey + al16(size_t(cap) * 8);                // u16[cap]: bucket of item i; later level-2 slot of position
-  L.sidx = L.sA + al16(size_t(cap) * 2);                // u16[cap]: P1-P3 warp rank of item; P4+ position -> item
-  L.tmp = L.sidx + al16(size_t(cap) * 2);               // u16[max(cap,BP)]: owner-grouped items; P4c+ slot offset in chunk
-  L.whist = L.tmp + al16(size_t(cap > BP ? cap : BP) * 2);
-  L.sstart = L.whist + al16(wh);                        // u16[BP+1]: first position of each bucket
-  L.st = L.sstart + al16((size_t(BP) + 1) * 2);         // u8[BP]: attempt t of each bucket
-  L.total = L.st + al16(BP);
+  L.smax = 2 * cap + 256;  // slots of the partition staged in shared memory (S_p is ~2 cnt)
+  if (L.smax > 32768u) L.smax = 32768u;
+  L.cls_off[0] = 0;                           // s = 2..8 (regions s = 2 | 3..4 | 5..8): at most cap/2 buckets
+  L.cls_off[1] = L.cls_off[0];
+  L.cls_off[2] = L.cls_off[1] + cap / 2 + 1;  // s = 9..32: cap/9
+  L.cls_off[3] = L.cls_off[2] + cap / 9 + 1;
+  L.skv = 0;                                               // E[cap]: the partition's elements
+  L.lbk = L.skv + al16(size_t(cap) * esz);                 // u16[cap]: local bucket of item i
+  L.rk = L.lbk + al16(size_t(cap) * 2);                    // u16[cap]: rank of item i in its bucket
+  L.sidx = L.rk + al16(size_t(cap) * 2);                   // u16[cap]: grouped position -> item
+  L.sA = L.sidx + al16(size_t(cap) * 2);                   // u16[cap]: level-2 slot of a grouped position
+  L.src = L.sA + al16(size_t(cap) * 2);                    // u16[smax]: slot -> item (bit 15: filler, value 0)
+  L.slist = L.src + al16(size_t(L.smax) * 2);              // u16[]: class lists
+  L.queue = L.slist + al16(size_t(L.cls_off[kNCls]) * 2);  // u32[2][cap/2+1]: search queues (lb | t<<16)
+  L.ss = L.queue + al16(size_t(cap / 2 + 1) * 8);          // u8[BP]: bucket size s
+  L.sstart = L.ss + al16(BP);                              // u16[BP]: first grouped position of each bucket
+  L.soff = L.sstart + al16(size_t(BP) * 2);                // u32[BP]: histogram, then slot offset in the partition
+  L.st = L.soff + al16(size_t(BP) * 4);                    // u8[BP]: attempt t of each bucket
+  L.total = uint32_t(L.st + al16(BP));
   return L;
+}
+
+// Block-wide exclusive scan of two u64 values at once (kBThreads threads).
+__device__ __forceinline__ void block_excl_scan2(unsigned long long& a, unsigned long long& b,
+                                                 unsigned long long* ta, unsigned long long* tb,
+                                                 unsigned long long (*s_red)[kBWarps]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned long long x = a, y = b;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long u = __shfl_up_sync(0xffffffffu, x, o), v = __shfl_up_sync(0xffffffffu, y, o);
+    if (lane >= o) {
+      x += u;
+      y += v;
+    }
+  }
+  if (lane == 31) {
+    s_red[0][warp] = x;
+    s_red[1][warp] = y;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    unsigned long long u = lane < kBWarps ? s_red[0][lane] : 0ull, v = lane < kBWarps ? s_red[1][lane] : 0ull;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long p = __shfl_up_sync(0xffffffffu, u, o), q = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) {
+        u += p;
+        v += q;
+      }
+    }
+    if (lane < kBWarps) {
+      s_red[0][lane] = u;
+      s_red[1][lane] = v;
+    }
+  }
+  __syncthreads();
+  const unsigned long long ba = warp ? s_red[0][warp - 1] : 0ull, bb = warp ? s_red[1][warp - 1] : 0ull;
+  *ta = s_red[0][kBWarps - 1];
+  *tb = s_red[1][kBWarps - 1];
+  a = ba + x - a;
+  b = bb + y - b;
+  __syncthreads();
 }
 
 template <class E, class Same>
@@ -656,224 +820,173 @@ __global__ void __launch_bounds__(kBThreads, 1024 / kBThreads)
              E* __restrict__ slots, DevStatus* __restrict__ stt, Same same) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint64_t s_m2[33];
+  __shared__ __align__(8) unsigned long long s_bar;
   __shared__ uint32_t s_p;
-  __shared__ unsigned long long s_red[kBWarps];
+  __shared__ unsigned long long s_red2[2][kBWarps];
   __shared__ unsigned long long s_base;
-  __shared__ uint32_t s_cls_off[kNCls + 1];
-  __shared__ uint32_t s_bits[kBWarps][32];
-  __shared__ uint32_t s_cbase[kBThreads];  // slot offset of each thread's bucket chunk in the partition
-  __shared__ uint32_t s_next[kNCls];        // work counters of the search classes
+  __shared__ uint32_t s_c9, s_qn[2];
+  __shared__ uint32_t s_bitsw[kBWarps][32];
 
-  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) s_p = atomicAdd(&stt->ticket, 1u);
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, lt = (1u << lane) - 1u;
+  const uint32_t cap = bp.cap;
+  const uint32_t BP = 1u << bp.log2_bp;
+  const uint32_t CH = BP > uint32_t(kBThreads) ? BP / kBThreads : 1u;  // buckets per thread in the scans
+  const BucketSmem& SL = bp.sl;
+  E* skv = reinterpret_cast<E*>(smem + SL.skv);
+  uint16_t* lbk = reinterpret_cast<uint16_t*>(smem + SL.lbk);
+  uint16_t* rk = reinterpret_cast<uint16_t*>(smem + SL.rk);
+  uint16_t* sidx = reinterpret_cast<uint16_t*>(smem + SL.sidx);
+  uint16_t* sA = reinterpret_cast<uint16_t*>(smem + SL.sA);
+  uint16_t* src = reinterpret_cast<uint16_t*>(smem + SL.src);
+  uint16_t* slist = reinterpret_cast<uint16_t*>(smem + SL.slist);
+  uint8_t* ss = smem + SL.ss;
+  uint16_t* sstart = reinterpret_cast<uint16_t*>(smem + SL.sstart);
+  uint32_t* soff = reinterpret_cast<uint32_t*>(smem + SL.soff);
+  uint8_t* s_t = smem + SL.st;
+
+  if (tid == 0) {
+    s_p = atomicAdd(&stt->ticket, 1u);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    s_c9 = 0;
+    s_qn[0] = s_qn[1] = 0;
+  }
   if (tid < 33) s_m2[tid] = tid ? ~0ull / (uint64_t(tid) * tid) : 0ull;
+  for (uint32_t j = tid; j < BP; j += kBThreads) soff[j] = 0;  // the histogram
   __syncthreads();
   const uint32_t p = s_p;
   HM_TMARK(0);
-  const uint32_t cap = bp.cap;
-  const uint32_t BP = 1u << bp.log2_bp;
-  const uint32_t CH = bucket_chunk(BP), lgch = 31 - __clz(CH), nown = BP / CH, obits = 31 - __clz(nown);
   const uint64_t lb0 = uint64_t(p) << bp.log2_bp;
   const uint32_t nbp = uint32_t(bp.nb - lb0 < uint64_t(BP) ? bp.nb - lb0 : uint64_t(BP));
   const uint32_t cnt_raw = pcount[p];
   const bool ovf = cnt_raw > cap;
   const uint32_t cnt = ovf ? 0u : cnt_raw;
-  const BucketSmem SL = bucket_smem_layout(cap, BP);
-  uint64_t* skey = reinterpret_cast<uint64_t*>(smem + SL.skey);
-  uint16_t* sA = reinterpret_cast<uint16_t*>(smem + SL.sA);
-  uint16_t* srk = reinterpret_cast<uint16_t*>(smem + SL.sidx);   // P1-P3
-  uint16_t* sidx = srk;                                           // P4+
-  uint16_t* tmp = reinterpret_cast<uint16_t*>(smem + SL.tmp);    // P3-P4b
-  uint16_t* srel = tmp;                                           // P4c+
-  uint16_t* whist = reinterpret_cast<uint16_t*>(smem + SL.whist); // P1-P3
-  uint16_t* scnt = whist;                                         // P4a-P4b
-  uint16_t* slist = whist;                                        // P4c+
-  uint16_t* sstart = reinterpret_cast<uint16_t*>(smem + SL.sstart);
-  uint8_t* s_t = smem + SL.st;
-  for (uint32_t w = tid; w < kBWarps * nown / 2; w += kBThreads) reinterpret_cast<uint32_t*>(whist)[w] = 0;
-  __syncthreads();
-  const E* part = pbuf + size_t(p) * cap;
   const uint64_t bbase = bp.b_lo + lb0;  // global id of the partition's first bucket
 
-  // groupby of the partition's items by bucket without shared
-  // atomics: P1 ranks every item among the items of its owner thread (the
-  // thread owning CH consecutive buckets) with `obits` warp ballots and
-  // per-warp counters; P2 scans the counters; P3 scatters into owner order;
-  // P4 groups each owner's ~CH items by bucket with thread-private counters.
+  // ---- load: one bulk copy (TMA) of the partition's elements into shared memory
+  if (tid == 0) {
+    const uint32_t bytes = cnt * uint32_t(sizeof(E));
+    if (bytes) {
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&s_bar)), "r"(bytes)
+                   : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_u32(skv)),
+          "l"(pbuf + size_t(p) * cap), "r"(bytes), "r"(smem_u32(&s_bar))
+          : "memory");
+    } else {
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&s_bar)) : "memory");
+    }
+  }
+  if (warp == 0) {  // the other warps wait at the CTA barrier (no issue slots)
+    uint32_t done = 0;
+    do {
+      asm volatile(
+          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+          : "=r"(done)
+          : "r"(smem_u32(&s_bar))
+          : "memory");
+      if (!done) __nanosleep(64);
+    } while (!done);
+  }
+  __syncthreads();
   HM_TMARK(1);
-  // ---- P1: level-1 bucket g k, warp-level owner rank
-  const uint32_t lt = (1u << lane) - 1u;
-  uint16_t* wh = whist + warp * nown;
-  for (uint32_t i0 = warp * 32; i0 < cnt; i0 += 8 * kBThreads) {
-    uint64_t ks[8];
-    uint32_t lbs[8];
+
+  // ---- hist: g k of every item; its rank among
+  // the items of its bucket comes from the shared-memory counter
+  for (uint32_t i0 = 0; i0 < cnt; i0 += 2 * kBThreads) {
+    uint64_t k2[2];
 #pragma unroll
-    for (int j = 0; j < 8; j++) {  // the partition's keys are read from HBM once, 8 loads in flight
-      const uint32_t i = i0 + j * kBThreads + lane;
-      ks[j] = i < cnt ? part[i].key : 0ull;
+    for (int u = 0; u < 2; u++) {
+      const uint32_t i = i0 + u * kBThreads + tid;
+      k2[u] = i < cnt ? skv[i].key : 0ull;
     }
 #pragma unroll
-    for (int j = 0; j < 8; j++) {
-      const uint32_t i = i0 + j * kBThreads + lane;
-      lbs[j] = 0;
+    for (int u = 0; u < 2; u++) {
+      const uint32_t i = i0 + u * kBThreads + tid;
       if (i < cnt) {
-        skey[i] = ks[j];
-        lbs[j] = uint32_t(level1_bucket(bp.l1, ks[j]) - bbase);
-        if (lbs[j] >= nbp) {  // cannot happen for a well-routed partition; never index out of range
+        uint32_t lb = uint32_t(level1_bucket(bp.l1, k2[u]) - bbase);
+        if (lb >= nbp) {  // cannot happen for a well-routed partition; never index out of range
           atomicOr(&stt->pad, 1u);
-          lbs[j] = 0;
+          lb = 0;
         }
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < 8; j++) {
-      const uint32_t i = i0 + j * kBThreads + lane;
-      const bool valid = i < cnt;
-      const uint32_t o = lbs[j] >> lgch;
-      uint32_t m = __ballot_sync(0xffffffffu, valid);
-      for (uint32_t bit = 0; bit < obits; bit++) {
-        const uint32_t bl = __ballot_sync(0xffffffffu, (o >> bit) & 1u);
-        m &= ((o >> bit) & 1u) ? bl : ~bl;
-      }
-      const uint32_t below = m & lt;
-      const uint32_t wc = valid ? wh[o] : 0u;
-      __syncwarp();
-      if (valid && below == 0) wh[o] = uint16_t(wc + __popc(m));
-      __syncwarp();
-      if (valid) {
-        sA[i] = uint16_t(lbs[j]);
-        srk[i] = uint16_t(wc + __popc(below));
+        lbk[i] = uint16_t(lb);
+        rk[i] = uint16_t(atomicAdd(&soff[lb], 1u));
       }
     }
   }
   __syncthreads();
   HM_TMARK(2);
-  // ---- P2: owner totals and offsets (owner-major, warp-minor)
-  uint32_t ostart = 0, otot = 0;
+
+  // ---- exclusive scans of s and s^2 (presum, R1/R2) and of
+  // the class counts; thread t owns buckets [t*CH, t*CH + CH)
+  bool huge = false, bfail = false;
+  unsigned long long S_p;
   {
-    uint32_t pre[kBWarps];
-    if (tid < nown) {
-#pragma unroll
-      for (int w = 0; w < kBWarps; w++) {
-        pre[w] = otot;
-        otot += whist[w * nown + tid];
+    const uint32_t c0 = tid * CH, c1 = min(c0 + CH, nbp);
+    unsigned long long a = 0, b = 0;  // a = s | s^2 << 32, b = #(s=2) | #(s=3..4) << 21 | #(s=5..8) << 42
+    for (uint32_t j = c0; j < c1; j++) {
+      const uint32_t v = soff[j];
+      a += uint64_t(v) | (uint64_t(v * v) << 32);
+      if (uint64_t(v) * v <= bp.bound4n) {  // (a bucket over the bound is never searched: level one redraws)
+        if (v == 2) b += 1;
+        else if (v >= 3 && v <= 4) b += 1ull << 21;
+        else if (v >= 5 && v <= 8) b += 1ull << 42;
       }
     }
-    unsigned long long tot;
-    ostart = uint32_t(block_excl_scan(otot, &tot, s_red));
-    if (tid < nown) {
-#pragma unroll
-      for (int w = 0; w < kBWarps; w++) whist[w * nown + tid] = uint16_t(ostart + pre[w]);
+    unsigned long long ta, tb;
+    block_excl_scan2(a, b, &ta, &tb, s_red2);
+    S_p = ta >> 32;
+    const uint32_t T2 = uint32_t(tb & 0x1FFFFF), T4 = uint32_t((tb >> 21) & 0x1FFFFF);
+    uint32_t pos = uint32_t(a), sq = uint32_t(a >> 32);
+    uint32_t n2 = uint32_t(b & 0x1FFFFF), n4 = T2 + uint32_t((b >> 21) & 0x1FFFFF), n8 = T2 + T4 + uint32_t(b >> 42);
+    for (uint32_t j = c0; j < c1; j++) {
+      const uint32_t v = soff[j];
+      ss[j] = uint8_t(v > 255 ? 255 : v);
+      sstart[j] = uint16_t(pos);
+      soff[j] = sq;
+      s_t[j] = 0;
+      pos += v;
+      sq += v * v;
+      if (v >= 2) {
+        if (uint64_t(v) * v > bp.bound4n) bfail = true;  // S > 4n: level one redraws
+        else if (v > 32) huge = true;
+        else if (v == 2) slist[n2++] = uint16_t(j);
+        else if (v <= 4) slist[n4++] = uint16_t(j);
+        else if (v <= 8) slist[n8++] = uint16_t(j);
+        else slist[SL.cls_off[2] + atomicAdd(&s_c9, 1u)] = uint16_t(j);
+      }
+    }
+    if (huge) atomicOr(&stt->huge, 1u);
+    if (bfail) atomicOr(&stt->bound_fail, 1u);
+    if (tid == 0) {
+      s_qn[0] = 0;
+      s_red2[0][0] = tb;  // class counts (read after the next barrier)
     }
   }
+  // publish the partition's aggregate S_p now (decoupled look-back)
+  if (tid == 0) st_release(&lbstate[p], (p == 0 ? kFlagInc : kFlagAgg) | (S_p & kValMask));
+  __syncthreads();
+  const unsigned long long tcls = s_red2[0][0];
+  const uint32_t Lc2 = uint32_t(tcls & 0x1FFFFF), Lc4 = Lc2 + uint32_t((tcls >> 21) & 0x1FFFFF),
+                 Lc8 = Lc4 + uint32_t(tcls >> 42);
+  // groupby: grouped position of every item
+  for (uint32_t i = tid; i < cnt; i += kBThreads) sidx[sstart[lbk[i]] + rk[i]] = uint16_t(i);
   __syncthreads();
   HM_TMARK(3);
-  // ---- P3: scatter items into owner order
-  for (uint32_t i0 = warp * 32; i0 < cnt; i0 += kBThreads) {
-    const uint32_t i = i0 + lane;
-    if (i < cnt) tmp[wh[sA[i] >> lgch] + srk[i]] = uint16_t(i);
-  }
-  __syncthreads();
-  HM_TMARK(4);
-  // ---- P4a/b: each owner groups its items by bucket (thread-private counters)
-  if (tid < nown) {
-    for (uint32_t k = 0; k < CH; k++) scnt[k * kBThreads + tid] = 0;
-    for (uint32_t q = ostart; q < ostart + otot; q++) scnt[(sA[tmp[q]] & (CH - 1)) * kBThreads + tid]++;
-    uint32_t run = ostart;
-    for (uint32_t k = 0; k < CH; k++) {
-      const uint32_t c = scnt[k * kBThreads + tid];
-      scnt[k * kBThreads + tid] = uint16_t(run);
-      sstart[tid * CH + k] = uint16_t(run);
-      run += c;
-    }
-    for (uint32_t q = ostart; q < ostart + otot; q++) {
-      const uint32_t i = tmp[q];
-      uint16_t* c = &scnt[(sA[i] & (CH - 1)) * kBThreads + tid];
-      sidx[*c] = uint16_t(i);
-      *c = uint16_t(*c + 1);
-    }
-  }
-  if (tid == 0) sstart[BP] = uint16_t(cnt);
-  __syncthreads();
-  HM_TMARK(5);
-  // ---- P4c: sizes, s^2 offsets (presum, R1/R2), class lists
-  const uint32_t c0 = tid * CH, c1 = min(c0 + CH, nbp);
-  uint32_t lsq = 0, maxs = 0;
-  unsigned long long lcls = 0;
-  for (uint32_t j = c0; j < c1; j++) {
-    const uint32_t v = uint32_t(sstart[j + 1]) - sstart[j];
-    lsq += v * v;
-    maxs = max(maxs, v);
-    if (v >= 2) {
-      const int c = size_class(v);
-      if (c < kNCls && uint64_t(v) * v <= bp.bound4n) lcls += 1ull << (16 * c);
-    }
-  }
-  unsigned long long S_p, totB;
-  const uint32_t exsq = uint32_t(block_excl_scan(lsq, &S_p, s_red));
-  const unsigned long long exB = block_excl_scan(lcls, &totB, s_red);
-  if (tid == 0) {
-    s_cls_off[0] = 0;
-    for (int c = 0; c < kNCls; c++) s_cls_off[c + 1] = s_cls_off[c] + uint32_t((totB >> (16 * c)) & 0xFFFF);
-  }
-  s_cbase[tid] = exsq;
-  __syncthreads();
-  {
-    uint32_t ccur[kNCls];
-#pragma unroll
-    for (int c = 0; c < kNCls; c++) ccur[c] = s_cls_off[c] + uint32_t((exB >> (16 * c)) & 0xFFFF);
-    bool huge = false, bfail = false;
-    uint32_t fsq = 0;
-    for (uint32_t j = c0; j < c1; j++) {
-      const uint32_t v = uint32_t(sstart[j + 1]) - sstart[j];
-      srel[j] = uint16_t(fsq);
-      fsq += v * v;
-      s_t[j] = 0;
-      if (v >= 2) {
-        const int c = size_class(v);
-        if (uint64_t(v) * v > bp.bound4n) bfail = true;  // S > 4n: level one redraws
-        else if (c >= kNCls) huge = true;
-        else slist[ccur[c]++] = uint16_t(j);
-      }
-    }
-    if (fsq > 0xFFFFu) huge = true;
-    if (huge) atomicOr(&stt->huge, 1u);
-    if (bfail || uint64_t(maxs) * maxs > bp.bound4n) atomicOr(&stt->bound_fail, 1u);
-  }
-  // publish the partition's aggregate S_p now (decoupled look-back); the
-  // exclusive prefix is looked up after the search, when the predecessors
-  // have long published theirs
-  if (tid == 0) st_release(&lbstate[p], (p == 0 ? kFlagInc : kFlagAgg) | (S_p & kValMask));
-  if (tid < kNCls) s_next[tid] = 0;
-  __syncthreads();
 
-  // from here: bucket lb holds positions [sstart[lb], sstart[lb+1]); sidx[pos] = item;
-  // slot offset within the partition = s_cbase[lb / CH] + srel[lb]
-
-  HM_TMARK(6);
-  // level-2 seed search, map make2 over the multi-key buckets:
-  // warp-per-bucket for 9 <= s <= 32, then thread-per-bucket classes from the
-  // rarest (longest chains) to the most common, so the tail of the last class
-  // is short and early warps go on to the singleton slots
-  search_warp(bp, part, skey, slist + s_cls_off[3], s_cls_off[4] - s_cls_off[3], sstart, sidx, sA, s_t, s_m2, bbase, stt,
-              same);
-  search_threads<8>(bp, part, skey, slist + s_cls_off[2], s_cls_off[3] - s_cls_off[2], &s_next[2], sstart, sidx, sA, s_t,
-                    s_m2, bbase, stt, same);
-  search_threads<4>(bp, part, skey, slist + s_cls_off[1], s_cls_off[2] - s_cls_off[1], &s_next[1], sstart, sidx, sA, s_t,
-                    s_m2, bbase, stt, same);
-  search_threads<2>(bp, part, skey, slist + s_cls_off[0], s_cls_off[1] - s_cls_off[0], &s_next[0], sstart, sidx, sA, s_t,
-                    s_m2, bbase, stt, same);
-  HM_TMARK(7);
   // look-back: exclusive prefix of S over the partitions before p (warp 0,
-  // lane i inspects partition q0 - i: the closest inclusive prefix plus the
-  // aggregates in front of it give the base)
+  // lane i inspects partition qb - i: the closest inclusive prefix plus the
+  // aggregates in front of it give the base).  Done before the search so that
+  // the inclusive prefix is published early and successors find it one hop
+  // back; warp 0 then takes the smallest share of the search.
   if (warp == 0) {
     unsigned long long base = 0;
     if (p > 0) {
-      int64_t q0 = int64_t(p) - 1;
+      int64_t qb = int64_t(p) - 1;
       while (true) {
-        const int64_t q = q0 - int64_t(lane);
-        const unsigned long long v = q >= 0 ? ld_acquire(&lbstate[q]) : kFlagInc;
+        const int64_t qq = qb - int64_t(lane);
+        const unsigned long long v = qq >= 0 ? ld_acquire(&lbstate[qq]) : kFlagInc;
         const unsigned long long f = v & ~kValMask;
         const uint32_t notready = __ballot_sync(0xffffffffu, f == 0);
         const uint32_t incs = __ballot_sync(0xffffffffu, f == kFlagInc);
@@ -885,7 +998,7 @@ __global__ void __launch_bounds__(kBThreads, 1024 / kBThreads)
         for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
         base += x;
         if (incs) break;
-        q0 -= 32;
+        qb -= 32;
       }
       if (lane == 0) st_release(&lbstate[p], kFlagInc | ((base + S_p) & kValMask));
     }
@@ -894,7 +1007,40 @@ __global__ void __launch_bounds__(kBThreads, 1024 / kBThreads)
       s_base = base;
     }
   }
+  // ---- level-2 seed search, map make2 over the multi-key buckets
+  // (PAPER.md:286-292); every finished bucket maps its slots to their source
+  // items (bucket_done), the singletons are mapped here (R12: a singleton sits
+  // at soff)
+  const bool staged = S_p <= SL.smax;
+  SearchCtx X{sstart, ss, sidx, soff, sA, s_t, staged ? src : nullptr};
+  uint32_t* q0 = reinterpret_cast<uint32_t*>(smem + SL.queue);
+  uint32_t* q1 = q0 + (cap / 2 + 1);
+  search_warp(bp, skv, X, slist + SL.cls_off[2], s_c9, s_m2, bbase, stt, same, s_bitsw[warp]);
+  HM_TMARK(8);
+  search_round0(bp, skv, X, slist, Lc2, Lc4, Lc8, q0, &s_qn[0], s_m2, bbase, stt, same);
+  HM_TMARK(9);
+  if (staged) {
+    const uint32_t c0 = tid * CH, c1 = min(c0 + CH, nbp);
+    for (uint32_t j = c0; j < c1; j++)
+      if (ss[j] == 1) src[soff[j]] = sidx[sstart[j]];
+  }
   __syncthreads();
+  HM_TMARK(10);
+  for (uint32_t r = 0;; r++) {
+    const uint32_t L = s_qn[r & 1];
+    if (L == 0) break;
+    if (tid == 0) s_qn[(r + 1) & 1] = 0;
+    __syncthreads();
+    uint32_t logA = 0;
+    while (logA < 3 && (L << (logA + 1)) <= uint32_t(kBThreads)) logA++;
+    search_round(bp, skv, X, (r & 1) ? q1 : q0, L, logA, (r & 1) ? q0 : q1, &s_qn[(r + 1) & 1], s_m2, bbase, stt,
+                 same);
+    __syncthreads();
+  }
+  HM_TMARK(4);
+
+  __syncthreads();  // (s_base)
+  HM_TMARK(5);
   const unsigned long long base = s_base;
   if (ovf) {
     if (tid == 0) atomicOr(&stt->part_overflow, 1u);
@@ -905,42 +1051,70 @@ __global__ void __launch_bounds__(kBThreads, 1024 / kBThreads)
     return;
   }
 
-
-  // singleton slots (R12: a singleton sits at soff) need no search result;
-  // 8 element loads in flight per thread, then the stores
-  for (uint32_t lb0s = 0; lb0s < nbp; lb0s += 8 * kBThreads) {
-    E ev[8];
-    uint64_t so[8];
+  // ---- out: the partition's slots [base, base + S_p), consecutive lanes write
+  // consecutive records
+  if (staged) {
+    E* out = slots + base;
+    const uint32_t Sp = uint32_t(S_p);
+    for (uint32_t x0 = 0; x0 < Sp; x0 += 4 * kBThreads) {
+      E e[4];
 #pragma unroll
-    for (int j = 0; j < 8; j++) {
-      const uint32_t lb = lb0s + j * kBThreads + tid;
-      so[j] = ~0ull;
-      if (lb < nbp) {
-        const uint32_t st0 = sstart[lb];
-        if (uint32_t(sstart[lb + 1]) - st0 == 1) {
-          so[j] = base + s_cbase[lb >> lgch] + srel[lb];
-          ev[j] = part[sidx[st0]];
+      for (int j = 0; j < 4; j++) {
+        const uint32_t x = x0 + j * kBThreads + tid;
+        if (x < Sp) {
+          const uint32_t v = src[x], it = v & 0x7FFFu;
+          e[j] = skv[it < cnt ? it : 0u];  // (an unmapped slot only in a pass that is redone)
+          if (v & 0x8000u) e[j].value = 0;
         }
       }
-    }
 #pragma unroll
-    for (int j = 0; j < 8; j++)
-      if (so[j] != ~0ull) slots[so[j]] = ev[j];
+      for (int j = 0; j < 4; j++) {
+        const uint32_t x = x0 + j * kBThreads + tid;
+        if (x < Sp) out[x] = e[j];
+      }
+    }
+  } else {
+    // a partition with more slots than the staging map (adversarial level-1
+    // distribution within the global bound): direct writes, thread per bucket
+    for (uint32_t lb = tid; lb < nbp; lb += kBThreads) {
+      const uint32_t s = ss[lb];
+      if (s == 0 || s > 32) continue;
+      E* out = slots + base + soff[lb];
+      const uint32_t st0 = sstart[lb];
+      if (s == 1) {
+        out[0] = skv[sidx[st0]];
+        continue;
+      }
+      const uint32_t s2 = s * s;
+      uint32_t hmin = 0xFFFFu, fill = 0;
+      for (uint32_t j = 0; j < s; j++) {
+        const uint32_t h = sA[st0 + j];
+        if (h < hmin) {
+          hmin = h;
+          fill = sidx[st0 + j];
+        }
+      }
+      E f = skv[fill];
+      f.value = 0;
+      for (uint32_t x = 0; x < s2; x++) out[x] = f;
+      for (uint32_t j = 0; j < s; j++) {
+        const uint32_t h = sA[st0 + j];
+        if (h < s2) out[h] = skv[sidx[st0 + j]];
+      }
+    }
   }
-
-  HM_TMARK(8);
+  HM_TMARK(6);
   // directory (coalesced) and compact directory record per 32 buckets (one per
   // warp iteration)
   for (uint32_t cb = 0; cb < nbp; cb += kBThreads) {
     const uint32_t lb = cb + tid;
-    uint32_t s = 0, t = 0, st0 = 0;
-    uint64_t soff = 0;
+    uint32_t s = 0, t = 0;
+    uint64_t so = 0;
     if (lb < nbp) {
-      st0 = sstart[lb];
-      s = uint32_t(sstart[lb + 1]) - st0;
+      s = ss[lb];
       t = s_t[lb];
-      soff = base + s_cbase[lb >> lgch] + srel[lb];
-      dir[lb0 + lb] = dir_entry(soff, s, t);
+      so = base + soff[lb];
+      dir[lb0 + lb] = dir_entry(so, s, t);
     }
     uint32_t pa = __ballot_sync(0xffffffffu, s & 4), pb = __ballot_sync(0xffffffffu, s & 2),
              pc = __ballot_sync(0xffffffffu, s & 1);
@@ -950,7 +1124,7 @@ __global__ void __launch_bounds__(kBThreads, 1024 / kBThreads)
       pa = pb = pc = 0xffffffffu;
     if (lane == 0 && lb < nbp) {
       CDir r;
-      r.w[0] = uint32_t(soff);
+      r.w[0] = uint32_t(so);
       r.w[1] = pa;
       r.w[2] = pb;
       r.w[3] = pc;
@@ -961,23 +1135,12 @@ __global__ void __launch_bounds__(kBThreads, 1024 / kBThreads)
       cdir[(lb0 + lb) >> 5] = r;
     }
   }
-  HM_TMARK(9);
-  // multi-key buckets: members at soff + h, every unused slot gets the
-  // lowest-slot member with value 0 (R10)
-  write_threads<2>(slist + s_cls_off[0], s_cls_off[1] - s_cls_off[0], sstart, sidx, sA, part, slots, base, s_cbase,
-                   srel, lgch);
-  write_threads<4>(slist + s_cls_off[1], s_cls_off[2] - s_cls_off[1], sstart, sidx, sA, part, slots, base, s_cbase,
-                   srel, lgch);
-  write_threads<8>(slist + s_cls_off[2], s_cls_off[3] - s_cls_off[2], sstart, sidx, sA, part, slots, base, s_cbase,
-                   srel, lgch);
-  write_warp(slist + s_cls_off[3], s_cls_off[4] - s_cls_off[3], sstart, sidx, sA, part, slots, base, s_cbase, srel,
-             lgch, s_bits[warp]);
-  HM_TMARK(10);
+  HM_TMARK(7);
 }
 
 // ------------------------------------------------------------- host side
-static size_t bucket_smem_bytes(uint32_t cap, uint32_t log2_bp) {
-  return bucket_smem_layout(cap, 1u << log2_bp).total;
+static size_t bucket_smem_bytes(uint32_t cap, uint32_t log2_bp, uint32_t esz) {
+  return bucket_smem_layout(cap, 1u << log2_bp, esz).total;
 }
 
 struct Plan {
@@ -985,12 +1148,17 @@ struct Plan {
   size_t smemB;
 };
 
-static Plan make_plan(uint64_t n_in, uint64_t nb, uint32_t log2_req, size_t smem_limit) {
+// Partition geometry: the largest BP = 2^lg (at most 2^12: 64 groups of 64
+// buckets) whose k_bucket shared memory lets 1024 / kBThreads CTAs share an SM
+// (smem_two: the register-limited occupancy at 64 registers per thread); with
+// at least 4 partitions per SM for small tables.  An
+// explicit log2_req only has to fit one CTA per SM (smem_one).
+static Plan make_plan(uint64_t n_in, uint64_t nb, uint32_t log2_req, uint32_t esz, size_t smem_two,
+                      size_t smem_one) {
   Plan pl{};
   const int sms = num_sms();
-  // 8K buckets per partition (two CTAs of k_bucket per SM); 16K when that
-  // would make more than 32K partitions (k_partition's shared histogram)
-  uint32_t lg = log2_req ? log2_req : ((nb >> HM_KB_LOG2BP) > 32768 ? 14 : HM_KB_LOG2BP);
+  uint32_t lg = log2_req ? std::min<uint32_t>(log2_req, 12u) : 12u;
+  const size_t limit = log2_req ? smem_one : smem_two;
   if (!log2_req) {
     while (lg > 6 && (nb >> lg) < uint64_t(4 * sms)) lg--;
   }
@@ -998,10 +1166,9 @@ static Plan make_plan(uint64_t n_in, uint64_t nb, uint32_t log2_req, size_t smem
     const double BP = double(uint64_t(1) << lg);
     const double m = double(n_in) * BP / double(std::max<uint64_t>(nb, 1));
     double c = m + 8.0 * std::sqrt(std::max(m, 1.0)) + 64.0;
-    uint32_t cap = uint32_t(std::min(65535.0, std::ceil(c / 32.0) * 32.0));
-    if (cap > 65535u) cap = 65535u;
-    const size_t sm = bucket_smem_bytes(cap, lg);
-    if ((sm <= smem_limit && c <= 65535.0) || lg <= 1) {
+    uint32_t cap = uint32_t(std::min(16383.0, std::ceil(c / 32.0) * 32.0));
+    const size_t sm = bucket_smem_bytes(cap, lg, esz);
+    if ((sm <= limit && c <= 16383.0) || lg <= 1) {
       pl.log2_bp = lg;
       pl.cap = cap;
       pl.smemB = sm;
@@ -1094,10 +1261,13 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
   HM_CUDA_TRY(cudaGetDevice(&dev));
   int smem_optin = 0;
   HM_CUDA_TRY(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-  const size_t static_smem_B = 6144;  // upper bound for k_bucket static shared memory (4.5 KB)
+  int smem_sm = 0;
+  HM_CUDA_TRY(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
+  const size_t static_smem_B = 4096;  // upper bound for k_bucket static shared memory (~2 KB)
   const uint32_t knob_flags = log2_req >> 16;
   log2_req &= 0xFFFFu;
-  const Plan pl = make_plan(n_in, nb, log2_req, size_t(smem_optin) - static_smem_B);
+  const Plan pl = make_plan(n_in, nb, log2_req, uint32_t(sizeof(E)), size_t(smem_sm) / (1024 / kBThreads) - 1024 - static_smem_B,
+                            size_t(smem_optin) - static_smem_B);
   if (pl.smemB + static_smem_B > size_t(smem_optin)) {
     set_error("build plan does not fit in shared memory");
     return HM_ERR_TOO_LARGE;
@@ -1155,17 +1325,20 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
   const uint64_t T = uint64_t(kAThreads) * KPT;
   const uint64_t ntiles = (n_in + T - 1) / T;
   const unsigned gridA = unsigned(std::max<uint64_t>(1, std::min<uint64_t>(ntiles, uint64_t(sms) * occA)));
-  // large tables: two coalesced 128-way passes instead of one 16K-way scatter
-  const bool two_pass = sizeof(E) == 16 && pl.np > 1024 && pl.np <= 65536 && !getenv("HM_ONE_PASS");
+  // large tables: two coalesced radix passes (256- or 512-way) over the
+  // partition id instead of one np-way scatter
+  const bool two_pass = sizeof(E) == 16 && pl.np > 1024 && pl.np <= (1u << 18) && !getenv("HM_ONE_PASS");
+  const int sbits = pl.np <= 65536 ? 8 : 9;
+  const uint32_t sdig = 1u << sbits;
   uint32_t ncoarse = 0, ccap = 0, tpc = 0;
   E* cbuf = nullptr;
   unsigned int* ccount = nullptr;
-  const size_t smemS = size_t(kSTile) * (sizeof(E) + 1);
-  auto kS1 = k_split<Src, E, 1>;
-  auto kS2 = k_split<Src, E, 2>;
+  const size_t smemS = size_t(kSTile) * (sizeof(E) + 2);
+  auto kS1 = sbits == 8 ? k_split<Src, E, 1, 8> : k_split<Src, E, 1, 9>;
+  auto kS2 = sbits == 8 ? k_split<Src, E, 2, 8> : k_split<Src, E, 2, 9>;
   if (two_pass) {
-    ncoarse = (pl.np + kSDigits - 1) / kSDigits;
-    const double mc = double(n_in) * double(kSDigits) * double(uint64_t(1) << pl.log2_bp) / double(nb);
+    ncoarse = (pl.np + sdig - 1) / sdig;
+    const double mc = double(n_in) * double(sdig) * double(uint64_t(1) << pl.log2_bp) / double(nb);
     ccap = uint32_t(mc + 8.0 * std::sqrt(mc + 1.0) + 1024.0);
     tpc = (ccap + kSTile - 1) / kSTile;
     if ((s = sc.alloc(WS_CBUF, &cbuf, size_t(ncoarse) * ccap * sizeof(E))) != HM_OK) return fail(s);
@@ -1173,7 +1346,6 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
     HM_CUDA_TRY(cudaFuncSetAttribute(kS1, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smemS)));
     HM_CUDA_TRY(cudaFuncSetAttribute(kS2, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smemS)));
   }
-
   BuildParams bp{};
   bp.smix = smix;
   bp.b_lo = b_lo;
@@ -1184,6 +1356,7 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
   bp.np = pl.np;
   bp.cap = pl.cap;
   bp.flags = knob_flags;
+  bp.sl = bucket_smem_layout(pl.cap, 1u << pl.log2_bp, uint32_t(sizeof(E)));
 
   DevStatus hs{};
   const uint32_t t1_lo = t1_fixed >= 0 ? uint32_t(t1_fixed) : 0u;

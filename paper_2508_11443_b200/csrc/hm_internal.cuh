@@ -38,6 +38,14 @@ struct DevStatus {
 
 constexpr int kMaxHuge = 1024;
 
+// Shared-memory layout of k_bucket (byte offsets into the dynamic region).
+constexpr int kNClsL = 3;
+struct BucketSmem {
+  uint32_t skv, lbk, rk, sidx, sA, src, slist, queue, ss, sstart, soff, st, total;
+  uint32_t smax;                 // capacity of the slot source map
+  uint32_t cls_off[kNClsL + 1];  // class-list regions in slist
+};
+
 struct BuildParams {
   L1Params l1;
   uint64_t smix;      // seed_mix(seed)
@@ -50,6 +58,7 @@ struct BuildParams {
   uint32_t np;        // partitions
   uint32_t cap;       // partition capacity (elements)
   uint32_t flags;     // HM_FLAG_* (hm.h)
+  BucketSmem sl;      // k_bucket shared-memory layout
 };
 
 struct LookupParams {

@@ -1,7 +1,7 @@
 """Summarise an ncu --set full report per CUDA source line (samples, instructions)."""
 import csv, subprocess, sys
 rep = sys.argv[1]; top = int(sys.argv[2]) if len(sys.argv) > 2 else 25
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"] + (["-k", "regex:" + __import__("os").environ["KN"]] if __import__("os").environ.get("KN") else []),
                      capture_output=True, text=True).stdout.splitlines()
 rows = list(csv.reader(out))
 hdr = None; lines = []; fname = None

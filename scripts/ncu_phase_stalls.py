@@ -2,7 +2,7 @@
 import csv, subprocess, sys
 rep, fsuffix = sys.argv[1], sys.argv[2]
 ranges = [(int(r.split(':')[0].split('-')[0]), int(r.split(':')[0].split('-')[1]), r.split(':')[1]) for r in sys.argv[3:]]
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"], capture_output=True, text=True).stdout.splitlines()
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"] + (["-k", "regex:" + __import__("os").environ["KN"]] if __import__("os").environ.get("KN") else []), capture_output=True, text=True).stdout.splitlines()
 rows = list(csv.reader(out)); hdr = None; fname = ""; cur = "other"; agg = {}
 def num(x):
     try: return int(x)

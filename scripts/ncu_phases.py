@@ -1,7 +1,7 @@
 """Aggregate ncu source-view samples / instructions over line ranges of build.cu."""
 import csv, subprocess, sys
 rep = sys.argv[1]; fsuffix = sys.argv[2]; ranges = sys.argv[3:]  # "a-b:name"
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"], capture_output=True, text=True).stdout.splitlines()
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"] + (["-k", "regex:" + __import__("os").environ["KN"]] if __import__("os").environ.get("KN") else []), capture_output=True, text=True).stdout.splitlines()
 rows = list(csv.reader(out)); hdr = None; fname = None; agg = {}; tot = [0, 0]
 def num(x):
     try: return int(x)

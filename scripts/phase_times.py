@@ -1,4 +1,5 @@
-"""Per-phase durations of k_bucket from the debug build (HM_LIB_PATH=.../libhm_timing.so)."""
+"""Per-phase durations of k_bucket from the debug build (HM_LIB_PATH=.../libhm_timing.so):
+globaltimer stamps at the HM_TMARK points of every CTA."""
 import os, sys, ctypes as C
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 os.environ.setdefault("HM_LIB_PATH", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2508_11443_b200", "libhm_timing.so"))
@@ -16,14 +17,18 @@ print('event ms per kernel', hm.profile_read()); hm.profile_enable(False)
 L = hm.lib(); L.hm_debug_phase_times.argtypes = [C.c_void_p, C.c_uint64]
 buf = np.zeros(65536 * 12 + 8192, np.uint64)
 L.hm_debug_phase_times(buf.ctypes.data_as(C.c_void_p), 65536 * 12)
-ka = buf[65536*12:].reshape(4096, 2).astype(np.int64); ka = ka[ka[:,0] > 0]
-print('k_partition CTA span us', (ka[:,1].max()-ka[:,0].min())/1e3, 'ctas', len(ka))
-KA_END = ka[:,1].max(); KA_START = ka[:,0].min()
-np_ = n >> (int(sys.argv[2]) if len(sys.argv) > 2 else 12)
-t = buf[: np_ * 12].reshape(np_, 12).astype(np.int64)
-names = ["start", "P1", "P2", "P3", "P4ab", "P4c", "search", "lookback", "dir/cdir/single", "multiwrite", "end"]
-d = np.diff(t[:, :11], axis=1)
-print("partitions", np_, "kernel span us", (t[:, 10].max() - t[:, 0].min()) / 1e3, "gap K_A end -> first K_B CTA us", (t[:, 0].min() - KA_END) / 1e3, "K_A start -> K_B end us", (t[:,10].max()-KA_START)/1e3)
-print("CTA lifetime us: mean %.1f median %.1f max %.1f" % (np.mean(t[:, 10] - t[:, 0]) / 1e3, np.median(t[:, 10] - t[:, 0]) / 1e3, np.max(t[:, 10] - t[:, 0]) / 1e3))
-for i in range(10):
-    print(f"{names[i]:>16s} -> {names[i+1]:<16s} mean {d[:, i].mean()/1e3:8.2f} us  p50 {np.median(d[:, i])/1e3:8.2f}  max {d[:, i].max()/1e3:8.2f}")
+names = ["start", "load", "hist", "scan+group", "search", "lookback", "out", "dir"]
+t = buf[: 65536 * 12].reshape(65536, 12).astype(np.int64)
+t = t[t[:, 0] > 0][:, :len(names)]
+d = np.diff(t, axis=1)
+life = t[:, -1] - t[:, 0]
+print("partitions", len(t), "kernel span us %.1f" % ((t[:, -1].max() - t[:, 0].min()) / 1e3))
+print("CTA lifetime us: mean %.2f median %.2f max %.2f" % (life.mean() / 1e3, np.median(life) / 1e3, life.max() / 1e3))
+for i in range(len(names) - 1):
+    print(f"{names[i]:>12s} -> {names[i+1]:<12s} mean {d[:, i].mean()/1e3:7.2f} us  p50 {np.median(d[:, i])/1e3:7.2f}  p99 {np.percentile(d[:, i], 99)/1e3:7.2f}  share {100*d[:, i].mean()/life.mean():5.1f}%")
+t2 = buf[: 65536 * 12].reshape(65536, 12).astype(np.int64)
+t2 = t2[t2[:, 0] > 0]
+if (t2[:, 8] > 0).all():
+    for a, b, nm in [(3, 8, "search_warp"), (8, 9, "round0 (thread 0)"), (9, 10, "singles+sync"), (10, 4, "retry rounds")]:
+        x = t2[:, b] - t2[:, a]
+        print(f"  search part {nm:18s} mean {x.mean()/1e3:7.2f} us  p50 {np.median(x)/1e3:7.2f}")
