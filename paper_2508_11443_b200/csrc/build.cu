@@ -254,12 +254,12 @@ __global__ void __launch_bounds__(kAThreads) k_partition(Src src, BuildParams bp
 
 // ------------------------------------------------------------ K_A, two passes
 // For large tables the partition step runs as two 128-way radix-partition
-// passes over the partition id (high 7 bits, then low 7 bits): a 16K-way
-// single pass writes ~one 16-byte element per partition per tile (scattered
-// partial-sector stores), a 128-way pass writes runs of ~32 elements from a
-// shared-memory staging tile, fully coalesced.  Ranking inside the tile uses
-// warp ballots over the 7 digit bits and per-warp counters (no atomics).
-constexpr int kSThreads = 512, kSPT = 4, kSTile = kSThreads * kSPT;
+// passes over the partition id (high bits, then low bits; 8- or 9-bit digits):
+// an np-way single pass writes ~one 16-byte element per partition per tile
+// (scattered partial-sector stores), a 256-way pass writes runs of ~16
+// elements from a shared-memory staging tile.  Ranking inside the tile uses
+// one shared-memory atomicAdd per element.
+constexpr int kSThreads = 512, kSPT = 8, kSTile = kSThreads * kSPT;
 constexpr int kSWarps = kSThreads / 32;  // BITS-bit digits: up to 2^(2 BITS) partitions in two passes
 
 struct SplitArgs {
@@ -283,12 +283,11 @@ __global__ void __launch_bounds__(kSThreads, 2) k_split(Src src, BuildParams bp,
   constexpr int kSDigits = 1 << BITS, kSBits = BITS;
   E* stage = reinterpret_cast<E*>(smem);
   uint16_t* sdig = reinterpret_cast<uint16_t*>(smem + size_t(kSTile) * sizeof(E));
-  __shared__ uint16_t s_wh[kSWarps][kSDigits];
-  __shared__ uint32_t s_dstart[kSDigits], s_gbase[kSDigits];
+  __shared__ uint32_t s_cnt[kSDigits], s_dstart[kSDigits], s_gbase[kSDigits];
   __shared__ unsigned long long s_red[kSWarps];
 
-  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, lt = (1u << lane) - 1u;
-  for (uint32_t i = tid; i < kSWarps * kSDigits / 2; i += kSThreads) reinterpret_cast<uint32_t*>(&s_wh[0][0])[i] = 0;
+  const uint32_t tid = threadIdx.x;
+  for (uint32_t i = tid; i < kSDigits; i += kSThreads) s_cnt[i] = 0;
   // this CTA's elements
   uint64_t base;
   uint32_t nvalid, coarse = 0;
@@ -324,39 +323,20 @@ __global__ void __launch_bounds__(kSThreads, 2) k_split(Src src, BuildParams bp,
       dg[j] = PASS == 1 ? ((p >> kSBits) & (kSDigits - 1)) : (p & (kSDigits - 1));
     }
   }
-  // warp-ballot rank of every element among the warp's elements with its digit
+  // rank of every element among the tile's elements with its digit: one
+  // shared-memory atomicAdd (cheap on sm_100 for spread addresses,
+  // scripts/micro/smem_atomics.cu); the order inside a digit is irrelevant
+  // (the table is a function of the key set, R13)
 #pragma unroll
-  for (int j = 0; j < kSPT; j++) {
-    const bool valid = j * kSThreads + tid < nvalid;
-    uint32_t m = __ballot_sync(0xffffffffu, valid);
-#pragma unroll
-    for (int bit = 0; bit < kSBits; bit++) {
-      const uint32_t bl = __ballot_sync(0xffffffffu, (dg[j] >> bit) & 1u);
-      m &= ((dg[j] >> bit) & 1u) ? bl : ~bl;
-    }
-    const uint32_t below = m & lt;
-    const uint32_t c = valid ? s_wh[warp][dg[j]] : 0u;
-    __syncwarp();
-    if (valid && below == 0) s_wh[warp][dg[j]] = uint16_t(c + __popc(m));
-    __syncwarp();
-    rk[j] = c + __popc(below);
-  }
+  for (int j = 0; j < kSPT; j++)
+    if (j * kSThreads + tid < nvalid) rk[j] = atomicAdd(&s_cnt[dg[j]], 1u);
   __syncthreads();
   // digit-major offsets inside the tile; one global reservation per digit
   {
-    uint32_t pre[kSWarps], tot = 0;
-    if (tid < kSDigits) {
-#pragma unroll
-      for (int w = 0; w < kSWarps; w++) {
-        pre[w] = tot;
-        tot += s_wh[w][tid];
-      }
-    }
+    const uint32_t tot = tid < kSDigits ? s_cnt[tid] : 0u;
     unsigned long long t_all;
     const uint32_t ds = uint32_t(block_excl_scan<kSThreads>(tot, &t_all, s_red));
     if (tid < kSDigits) {
-#pragma unroll
-      for (int w = 0; w < kSWarps; w++) s_wh[w][tid] = uint16_t(ds + pre[w]);
       s_dstart[tid] = ds;
       if (tot) {
         const uint32_t reg = PASS == 1 ? tid : coarse * kSDigits + tid;
@@ -368,7 +348,7 @@ __global__ void __launch_bounds__(kSThreads, 2) k_split(Src src, BuildParams bp,
 #pragma unroll
   for (int j = 0; j < kSPT; j++) {
     if (j * kSThreads + tid < nvalid) {
-      const uint32_t pos = s_wh[warp][dg[j]] + rk[j];
+      const uint32_t pos = s_dstart[dg[j]] + rk[j];
       stage[pos] = e[j];
       sdig[pos] = uint16_t(dg[j]);
     }
