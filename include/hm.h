@@ -68,6 +68,13 @@ typedef struct {
  * full directory entry for every query (a testing/diagnostic knob: the
  * results are identical, only slower).  The table itself is unchanged. */
 #define HM_FLAG_FULL_DIRECTORY 1u
+/* Testing knobs of the construction (the table is identical, only the route
+ * differs): DIRECT_SLOTS makes every build partition write its slots straight
+ * from the search (the path of a partition whose slots exceed the shared-memory
+ * staging map); NO_ROUND0_ILP tries one attempt per bucket in round 0 and
+ * leaves the rest to the lane-parallel rounds. */
+#define HM_FLAG_DIRECT_SLOTS 2u
+#define HM_FLAG_NO_ROUND0_ILP 4u
 
 /* Table header, 56 bytes, little-endian (DESIGN.md §4 "Table layout"). */
 typedef struct {

@@ -259,7 +259,16 @@ __global__ void __launch_bounds__(kAThreads) k_partition(Src src, BuildParams bp
 // (scattered partial-sector stores), a 256-way pass writes runs of ~16
 // elements from a shared-memory staging tile.  Ranking inside the tile uses
 // one shared-memory atomicAdd per element.
-constexpr int kSThreads = 512, kSPT = 8, kSTile = kSThreads * kSPT;
+constexpr int kSThreads = 512;
+// elements per thread: 8 x 16-byte or 4 x 32-byte records in registers
+template <class E>
+__host__ __device__ constexpr int split_pt() {
+  return sizeof(E) == 16 ? 8 : 4;
+}
+template <class E>
+__host__ __device__ constexpr int split_tile() {
+  return kSThreads * split_pt<E>();
+}
 constexpr int kSWarps = kSThreads / 32;  // BITS-bit digits: up to 2^(2 BITS) partitions in two passes
 
 struct SplitArgs {
@@ -280,7 +289,7 @@ template <class Src, class E, int PASS, int BITS>
 __global__ void __launch_bounds__(kSThreads, 2) k_split(Src src, BuildParams bp, SplitArgs a,
                                                         DevStatus* __restrict__ stt) {
   extern __shared__ __align__(16) uint8_t smem[];
-  constexpr int kSDigits = 1 << BITS, kSBits = BITS;
+  constexpr int kSDigits = 1 << BITS, kSBits = BITS, kSPT = split_pt<E>(), kSTile = split_tile<E>();
   E* stage = reinterpret_cast<E*>(smem);
   uint16_t* sdig = reinterpret_cast<uint16_t*>(smem + size_t(kSTile) * sizeof(E));
   __shared__ uint32_t s_cnt[kSDigits], s_dstart[kSDigits], s_gbase[kSDigits];
@@ -537,7 +546,7 @@ __device__ __forceinline__ uint32_t round0_bucket(const BuildParams& bp, const E
   constexpr bool kTwo = K <= 4;  // (two attempts in flight; the rare s = 5..8 buckets try one)
   uint32_t h0[K], h1[kTwo ? K : 1];
   uint64_t b0, b1 = 0;
-  if (kTwo) {
+  if (kTwo && !(bp.flags & HM_FLAG_NO_ROUND0_ILP)) {
     const Consts c0 = derive(bp.smix, 2, bbase + lb, 0), c1 = derive(bp.smix, 2, bbase + lb, 1);
     b0 = slots_of<K>(c0, k, s, fm, h0);
     b1 = slots_of<K>(c1, k, s, fm, h1);
@@ -563,11 +572,11 @@ __device__ __forceinline__ uint32_t round0_bucket(const BuildParams& bp, const E
     X.s_t[lb] = 0;
     return 0;
   }
-  if (kTwo && b1) {
+  if (kTwo && !(bp.flags & HM_FLAG_NO_ROUND0_ILP) && b1) {
     bucket_done_regs<K>(X, lb, st0, s, 1, h1, b1);
     return 0;
   }
-  return kTwo ? 2 : 1;
+  return (kTwo && !(bp.flags & HM_FLAG_NO_ROUND0_ILP)) ? 2 : 1;
 }
 
 // Round 0 over the multi-key list ([s = 2 | s = 3..4 | s = 5..8] regions, so
@@ -991,7 +1000,7 @@ __global__ void __launch_bounds__(kBThreads, 1024 / kBThreads)
   // (PAPER.md:286-292); every finished bucket maps its slots to their source
   // items (bucket_done), the singletons are mapped here (R12: a singleton sits
   // at soff)
-  const bool staged = S_p <= SL.smax;
+  const bool staged = S_p <= SL.smax && !(bp.flags & HM_FLAG_DIRECT_SLOTS);
   SearchCtx X{sstart, ss, sidx, soff, sA, s_t, staged ? src : nullptr};
   uint32_t* q0 = reinterpret_cast<uint32_t*>(smem + SL.queue);
   uint32_t* q1 = q0 + (cap / 2 + 1);
@@ -1307,12 +1316,13 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
   const unsigned gridA = unsigned(std::max<uint64_t>(1, std::min<uint64_t>(ntiles, uint64_t(sms) * occA)));
   // large tables: two coalesced radix passes (256- or 512-way) over the
   // partition id instead of one np-way scatter
-  const bool two_pass = sizeof(E) == 16 && pl.np > 1024 && pl.np <= (1u << 18) && !getenv("HM_ONE_PASS");
+  const bool two_pass = pl.np > 1024 && pl.np <= (1u << 18) && !getenv("HM_ONE_PASS");
   const int sbits = pl.np <= 65536 ? 8 : 9;
   const uint32_t sdig = 1u << sbits;
   uint32_t ncoarse = 0, ccap = 0, tpc = 0;
   E* cbuf = nullptr;
   unsigned int* ccount = nullptr;
+  constexpr int kSTile = split_tile<E>();
   const size_t smemS = size_t(kSTile) * (sizeof(E) + 2);
   auto kS1 = sbits == 8 ? k_split<Src, E, 1, 8> : k_split<Src, E, 1, 9>;
   auto kS2 = sbits == 8 ? k_split<Src, E, 2, 8> : k_split<Src, E, 2, 9>;

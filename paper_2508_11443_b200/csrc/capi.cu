@@ -258,7 +258,7 @@ hm_status hm_build_u64(const uint64_t* keys, const uint64_t* vals, uint64_t n, c
   if (n == 0) return HM_ERR_EMPTY;
   if (!keys || !vals) return HM_ERR_INVALID_ARG;
   if (n > (1ull << 30)) return HM_ERR_TOO_LARGE;
-  if (opts && (opts->flags & ~uint32_t(HM_FLAG_FULL_DIRECTORY))) return HM_ERR_INVALID_ARG;
+  if (opts && (opts->flags & ~uint32_t(HM_FLAG_FULL_DIRECTORY | HM_FLAG_DIRECT_SLOTS | HM_FLAG_NO_ROUND0_ILP))) return HM_ERR_INVALID_ARG;
   hm_status s = check_device();
   if (s != HM_OK) return s;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -295,7 +295,7 @@ hm_status hm_build_bytes(const uint8_t* bytes, const uint64_t* offsets, const ui
   if (n == 0) return HM_ERR_EMPTY;
   if (!offsets || !vals) return HM_ERR_INVALID_ARG;
   if (n > (1ull << 30)) return HM_ERR_TOO_LARGE;
-  if (opts && (opts->flags & ~uint32_t(HM_FLAG_FULL_DIRECTORY))) return HM_ERR_INVALID_ARG;
+  if (opts && (opts->flags & ~uint32_t(HM_FLAG_FULL_DIRECTORY | HM_FLAG_DIRECT_SLOTS | HM_FLAG_NO_ROUND0_ILP))) return HM_ERR_INVALID_ARG;
   hm_status s = check_device();
   if (s != HM_OK) return s;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);

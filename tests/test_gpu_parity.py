@@ -235,3 +235,31 @@ def test_bytes_edge_strings_and_offsets():
         c, o = gen.pack_bytes_list([b"hello", b"world", b"hello"])
         hm.HashMap.build_bytes(torch.from_numpy(c).cuda(), dev(o), dev(np.arange(3, dtype=np.uint64)))
     assert e.value.name == "DUPLICATE_KEY"
+
+
+@pytest.mark.parametrize("flags_name", ["FLAG_DIRECT_SLOTS", "FLAG_NO_ROUND0_ILP"])
+@pytest.mark.parametrize("n,seed,log2_bp", [(5, 0, 0), (4133, 5, 0), (70_001, 3, 6), (300_007, 1, 0)])
+def test_u64_construction_routes_same_table(flags_name, n, seed, log2_bp):
+    """The testing knobs change how k_bucket gets there (direct slot writes
+    instead of the shared-memory source map; one round-0 attempt instead of
+    two), never the table: both must still equal the oracle byte for byte."""
+    hm = _hm()
+    keys, vals = gen.u64_keys(n, lo=3 * n), gen.u64_values(n)
+    ot = O.build_u64(keys, vals, seed)
+    m = hm.HashMap.build_u64(dev(keys), dev(vals), seed=seed, log2_bp=log2_bp, flags=getattr(hm, flags_name))
+    assert_table_equal(m, ot)
+    q, _, _ = gen.u64_queries(n, 2 * n + 100)
+    ov, of = O.lookup_u64(ot, q)
+    gv, gf = m.lookup(dev(q))
+    assert np.array_equal(host(gv), ov) and np.array_equal(host(gf), of)
+    m.free()
+
+
+@pytest.mark.parametrize("flags_name", ["FLAG_DIRECT_SLOTS", "FLAG_NO_ROUND0_ILP"])
+def test_u64_construction_routes_duplicates(flags_name):
+    hm = _hm()
+    keys = gen.u64_keys(100_000)
+    keys[91_234] = keys[5]
+    with pytest.raises(hm.HMError) as e:
+        hm.HashMap.build_u64(dev(keys), dev(gen.u64_values(100_000)), flags=getattr(hm, flags_name))
+    assert e.value.name == "DUPLICATE_KEY"
