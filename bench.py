@@ -200,15 +200,20 @@ def run_ours(args):
     of = torch.empty(n, dtype=torch.uint8, device=dev)
     torch.cuda.synchronize()
 
+    s_over_n = 2.0  # replaced by the table's actual S / n after the first step
+
     def step(ev_b=None):
+        nonlocal s_over_n
         if world == 1:
             m = hm.HashMap.build_u64(keys, vals, seed=0)
+            s_over_n = m.info().S / n
             if ev_b is not None:
                 ev_b.record()
             m.lookup(q, ov, of)
             m.free()
         else:
             dm = dist.build_dist(keys, vals, seed=0)
+            s_over_n = dm.S_local / n
             if ev_b is not None:
                 ev_b.record()
             v, f = dist.lookup_dist(dm, q)
@@ -261,12 +266,14 @@ def run_ours(args):
     if dom:
         launches_dom, ms_dom = kstats[dom]
         avg_ms = ms_dom / launches_dom
+        # algorithmic bytes of each kernel: what it must move
+        # per unit, with the table's actual S/n for the slot writes
         if dom.startswith("k_lookup"):
             units, bpu, what = n * args.steps / launches_dom, LOOKUP_BYTES_PER_QUERY, "queries"
-        elif dom == "k_partition":
-            units, bpu, what = n * args.steps / launches_dom, 16.0, "keys"
-        else:
-            units, bpu, what = n * args.steps / launches_dom, BUILD_BYTES_PER_KEY - 16.0, "keys"
+        elif dom in ("k_partition", "k_split1", "k_split2"):
+            units, bpu, what = n * args.steps / launches_dom, 32.0, "keys"  # read + write a 16-byte record
+        else:  # k_bucket: read the partition (16), write dir (8) + slots (16 S/n)
+            units, bpu, what = n * args.steps / launches_dom, 16.0 + 8.0 + 16.0 * s_over_n, "keys"
         achieved = units * bpu / (avg_ms / 1e3) / 1e9
         traffic = None
         try:
