@@ -613,6 +613,24 @@ __device__ __forceinline__ void search_round0(const BuildParams& bp, const E* sk
   }
 }
 
+// One attempt of a queued bucket with K key registers; the lowest successful
+// lane of the group finishes the bucket from its registers.  Returns whether
+// this lane's attempt succeeded.
+template <int K, class E>
+__device__ __forceinline__ bool retry_attempt(const BuildParams& bp, const E* skv, const SearchCtx& X, uint32_t lb,
+                                              uint32_t st0, uint32_t s, uint32_t t, const uint64_t* s_m2,
+                                              uint64_t bbase, uint32_t gmask) {
+  uint64_t k[K];
+#pragma unroll
+  for (int j = 0; j < K; j++) k[j] = uint32_t(j) < s ? skv[X.sidx[st0 + j]].key : 0ull;
+  const FastMod fm{uint64_t(s) * s, s_m2[s]};
+  uint32_t h[K];
+  const uint64_t bits = t < kT2Cap ? slots_of<K>(derive(bp.smix, 2, bbase + lb, t), k, s, fm, h) : 0ull;
+  const uint32_t om = __ballot_sync(__activemask(), bits != 0) & gmask;
+  if (bits && (threadIdx.x & 31) == uint32_t(__ffs(om) - 1)) bucket_done_regs<K>(X, lb, st0, s, t, h, bits);
+  return bits != 0;
+}
+
 // Round r >= 1: A = 2^logA adjacent lanes per queued bucket, attempt tb + j on lane j.
 template <class E, class Same>
 __device__ __forceinline__ void search_round(const BuildParams& bp, const E* skv, const SearchCtx& X,
@@ -626,7 +644,6 @@ __device__ __forceinline__ void search_round(const BuildParams& bp, const E* skv
     const uint32_t w = w0 + lane;
     bool ok = false, lead = false;
     uint32_t lb = 0, st0 = 0, s = 2, t = 0, tb = 0;
-    FastMod fm{4, 0};
     if (w < W) {
       const uint32_t q = queue[w >> logA];
       lb = q & 0xFFFFu;
@@ -635,11 +652,12 @@ __device__ __forceinline__ void search_round(const BuildParams& bp, const E* skv
       lead = (w & (A - 1u)) == 0;
       st0 = X.sstart[lb];
       s = X.ss[lb];
-      fm = FastMod{uint64_t(s) * s, s_m2[s]};
-      if (t < kT2Cap) ok = attempt_ok(bp.smix, bbase + lb, t, skv, X.sidx, st0, s, fm);
+      // keys in registers, the winner finishes from its registers (a group
+      // never straddles the two widths: its lanes share the bucket)
+      if (s <= 4) ok = retry_attempt<4>(bp, skv, X, lb, st0, s, t, s_m2, bbase, gmask);
+      else ok = retry_attempt<8>(bp, skv, X, lb, st0, s, t, s_m2, bbase, gmask);
     }
     const uint32_t om = __ballot_sync(0xffffffffu, ok) & gmask;
-    if (ok && lane == uint32_t(__ffs(om) - 1)) bucket_done(X, bp.smix, bbase + lb, lb, st0, s, t, skv, fm);
     bool retry = false;
     if (lead && om == 0 && tb == 0) {  // equal keys collide under every t: check once
       for (uint32_t i = 0; i < s && !retry; i++) {
@@ -1464,16 +1482,39 @@ hm_status build_u64_core(const uint64_t* keys, const uint64_t* vals, uint64_t n_
 }
 
 // ------------------------------------------------------------ byte keys
-// Fingerprints (R5) of all keys, thread per key, expanded form (fingerprint_pw).
-__global__ void __launch_bounds__(256) k_fingerprint(const uint8_t* __restrict__ bytes,
-                                                     const uint64_t* __restrict__ offs, uint64_t n, uint64_t r,
-                                                     uint64_t* __restrict__ fp) {
+// Fingerprints (R5) of all keys, expanded form.  A warp takes 32 consecutive
+// keys, stages their contiguous byte range in shared memory with coalesced
+// word loads, and every lane fingerprints its key from there (fingerprint_sm);
+// a range longer than the stage (keys of hundreds of bytes) is read directly.
+constexpr int kFpThreads = 256, kFpWarps = kFpThreads / 32, kFpStageWords = 512;
+__global__ void __launch_bounds__(kFpThreads) k_fingerprint(const uint8_t* __restrict__ bytes,
+                                                            const uint64_t* __restrict__ offs, uint64_t n, uint64_t r,
+                                                            uint64_t* __restrict__ fp) {
   __shared__ FpPow s_pw;
+  __shared__ uint32_t s_stage[kFpWarps][kFpStageWords];
   if (threadIdx.x == 0) fp_pow_fill(&s_pw, r);
   __syncthreads();
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
-    const uint64_t o = offs[i], o1 = offs[i + 1];
-    fp[i] = fingerprint_pw(bytes, o, o1 - o, r, &s_pw);
+  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t* sb = s_stage[w];
+  for (uint64_t i0 = (uint64_t(blockIdx.x) * kFpWarps + w) * 32; i0 < n; i0 += uint64_t(gridDim.x) * kFpWarps * 32) {
+    const uint64_t i = i0 + lane;
+    const bool valid = i < n;
+    const uint64_t o = valid ? __ldg(offs + i) : 0, o1 = valid ? __ldg(offs + i + 1) : 0;
+    const uint32_t lastl = n - 1 - i0 < 31 ? uint32_t(n - 1 - i0) : 31u;
+    const uint64_t start = __shfl_sync(0xffffffffu, o, 0), end = __shfl_sync(0xffffffffu, o1, lastl);
+    const uint64_t g0 = start & ~uint64_t(3);
+    const uint64_t nw = end > start ? (end - g0 + 3) >> 2 : 0;
+    if (nw <= uint64_t(kFpStageWords)) {  // (warp-uniform)
+      const uint32_t* gw = reinterpret_cast<const uint32_t*>(bytes + g0);
+      for (uint32_t k = lane; k < uint32_t(nw); k += 32) sb[k] = __ldg(gw + k);
+      __syncwarp();
+      if (valid)
+        fp[i] = o1 - o <= 4ull * kFpPowMax ? fingerprint_sm(sb, uint32_t(o - g0), uint32_t(o1 - o), &s_pw)
+                                           : fingerprint_pw(bytes, o, o1 - o, r, &s_pw);
+      __syncwarp();
+    } else if (valid) {
+      fp[i] = fingerprint_pw(bytes, o, o1 - o, r, &s_pw);
+    }
   }
 }
 
@@ -1487,10 +1528,10 @@ __global__ void k_check_offsets(const uint64_t* __restrict__ offs, uint64_t n, u
 
 void launch_fingerprint(const uint8_t* bytes, const uint64_t* offs, uint64_t n, uint64_t r, uint64_t* fp,
                         cudaStream_t st) {
-  const unsigned grid = unsigned(std::min<uint64_t>((n + 255) / 256, uint64_t(num_sms()) * 8));
+  const unsigned grid = unsigned(std::min<uint64_t>((n + kFpThreads - 1) / kFpThreads, uint64_t(num_sms()) * 8));
   {
     LaunchScope ls_("k_fingerprint", st);
-    k_fingerprint<<<std::max(grid, 1u), 256, 0, st>>>(bytes, offs, n, r, fp);
+    k_fingerprint<<<std::max(grid, 1u), kFpThreads, 0, st>>>(bytes, offs, n, r, fp);
   }
 }
 

@@ -254,6 +254,31 @@ __device__ __forceinline__ uint64_t fingerprint_pw(const uint8_t* bytes, uint64_
   return f >= kP ? f - kP : f;
 }
 
+// fingerprint_pw over a shared-memory copy of the context: sb holds the
+// 4-byte words of the bytes starting at a 4-aligned position, the key starts
+// rel bytes in (len <= 4 * kFpPowMax).
+__device__ __forceinline__ uint64_t fingerprint_sm(const uint32_t* sb, uint32_t rel, uint32_t len, const FpPow* pw) {
+  if (len == 0) return 0;
+  const uint32_t a0 = rel >> 2, sh = (rel & 3) * 8;
+  const uint32_t last = (rel + len - 1) >> 2;
+  const uint32_t nw = (len + 3) >> 2;
+  uint64_t acc = 0;
+  uint32_t cur = sb[a0];
+  for (uint32_t i = 0; i < nw; i++) {
+    const uint32_t na = a0 + i + 1;
+    const uint32_t nxt = na <= last ? sb[na] : 0u;
+    uint32_t w = sh ? __funnelshift_r(cur, nxt, sh) : cur;
+    const uint32_t rem = len - 4 * i;
+    if (rem < 4) w &= (1u << (8 * rem)) - 1u;
+    acc += mul32_p(w, pw->lo[nw - i], pw->hi[nw - i]);
+    acc = (acc & kP) + (acc >> 61);
+    cur = nxt;
+  }
+  uint64_t f = acc + len;
+  f = (f & kP) + (f >> 61);
+  return f >= kP ? f - kP : f;
+}
+
 #endif
 
 }  // namespace hm
