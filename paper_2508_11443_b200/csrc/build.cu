@@ -858,7 +858,7 @@ __global__ void __launch_bounds__(kBThreads, 1024 / kBThreads)
     s_c9 = 0;
     s_qn[0] = s_qn[1] = 0;
   }
-  if (tid < 33) s_m2[tid] = tid ? ~0ull / (uint64_t(tid) * tid) : 0ull;
+  if (tid < 33) s_m2[tid] = bp.m2[tid];  // (host-computed: no 64-bit division per CTA)
   for (uint32_t j = tid; j < BP; j += kBThreads) soff[j] = 0;  // the histogram
   __syncthreads();
   const uint32_t p = s_p;
@@ -1365,6 +1365,7 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
   bp.cap = pl.cap;
   bp.flags = knob_flags;
   bp.sl = bucket_smem_layout(pl.cap, 1u << pl.log2_bp, uint32_t(sizeof(E)));
+  for (int i = 0; i < 33; i++) bp.m2[i] = i ? ~0ull / (uint64_t(i) * i) : 0ull;
 
   DevStatus hs{};
   const uint32_t t1_lo = t1_fixed >= 0 ? uint32_t(t1_fixed) : 0u;

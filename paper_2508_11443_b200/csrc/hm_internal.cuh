@@ -59,6 +59,7 @@ struct BuildParams {
   uint32_t cap;       // partition capacity (elements)
   uint32_t flags;     // HM_FLAG_* (hm.h)
   BucketSmem sl;      // k_bucket shared-memory layout
+  uint64_t m2[33];    // floor((2^64 - 1) / s^2) for the exact mod s^2 (R22), s <= 32
 };
 
 struct LookupParams {
