@@ -912,13 +912,15 @@ __global__ void __launch_bounds__(kBThreads, 1024 / kBThreads)
     for (int u = 0; u < 2; u++) {
       const uint32_t i = i0 + u * kBThreads + tid;
       if (i < cnt) {
-        uint32_t lb = uint32_t(level1_bucket(bp.l1, k2[u]) - bbase);
+        const uint64_t h1 = hash64(bp.l1.c1, k2[u]);
+        uint32_t lb = uint32_t(level1_of_hash(bp.l1, h1) - bbase);
         if (lb >= nbp) {  // cannot happen for a well-routed partition; never index out of range
           atomicOr(&stt->pad, 1u);
           lb = 0;
         }
         lbk[i] = uint16_t(lb);
         rk[i] = uint16_t(atomicAdd(&soff[lb], 1u));
+        s_t[lb] = uint8_t(tag4_of_hash(h1));  // kept for singletons only (the scan resets the rest)
       }
     }
   }
@@ -952,7 +954,7 @@ __global__ void __launch_bounds__(kBThreads, 1024 / kBThreads)
       ss[j] = uint8_t(v > 255 ? 255 : v);
       sstart[j] = uint16_t(pos);
       soff[j] = sq;
-      s_t[j] = 0;
+      if (v != 1) s_t[j] = 0;  // (a singleton keeps its key's tag for the compact directory)
       pos += v;
       sq += v * v;
       if (v >= 2) {
@@ -1119,15 +1121,15 @@ __global__ void __launch_bounds__(kBThreads, 1024 / kBThreads)
     uint64_t so = 0;
     if (lb < nbp) {
       s = ss[lb];
-      t = s_t[lb];
+      t = s_t[lb];  // (a singleton: its key's tag; t = 0 in the directory, R12)
       so = base + soff[lb];
-      dir[lb0 + lb] = dir_entry(so, s, t);
+      dir[lb0 + lb] = dir_entry(so, s, s == 1 ? 0u : t);
     }
     uint32_t pa = __ballot_sync(0xffffffffu, s & 4), pb = __ballot_sync(0xffffffffu, s & 2),
              pc = __ballot_sync(0xffffffffu, s & 1);
     const uint32_t t0 = __ballot_sync(0xffffffffu, t & 1), t1 = __ballot_sync(0xffffffffu, t & 2),
                    t2 = __ballot_sync(0xffffffffu, t & 4), t3 = __ballot_sync(0xffffffffu, t & 8);
-    if (__any_sync(0xffffffffu, s >= kCdirEscS || t >= kCdirEscT) || (bp.flags & HM_FLAG_FULL_DIRECTORY))
+    if (__any_sync(0xffffffffu, s >= kCdirEscS || (s >= 2 && t >= kCdirEscT)) || (bp.flags & HM_FLAG_FULL_DIRECTORY))
       pa = pb = pc = 0xffffffffu;
     if (lane == 0 && lb < nbp) {
       CDir r;

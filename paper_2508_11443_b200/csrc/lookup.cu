@@ -115,7 +115,7 @@ __device__ __forceinline__ uint64_t cdir_entry(const CDir& r, uint64_t lb, const
   const uint32_t s = ((r.w[1] & bit) ? 4u : 0u) | ((r.w[2] & bit) ? 2u : 0u) | ((r.w[3] & bit) ? 1u : 0u);
   const uint32_t t = ((r.w[4] & bit) ? 1u : 0u) | ((r.w[5] & bit) ? 2u : 0u) | ((r.w[6] & bit) ? 4u : 0u) |
                      ((r.w[7] & bit) ? 8u : 0u);
-  *escaped = s == kCdirEscS || t == kCdirEscT;
+  *escaped = s == kCdirEscS || (s >= 2 && t == kCdirEscT);  // (a singleton's t planes hold its tag)
   const uint64_t soff = uint64_t(r.w[0]) + cdir_prefix_sq(r.w[1] & below, r.w[2] & below, r.w[3] & below);
   return dir_entry(soff, s, t);
 }
@@ -134,6 +134,7 @@ __global__ void __launch_bounds__(kLThreads) k_lookup_u64(LookupParams lp, const
   const uint64_t per = uint64_t(kLThreads) * QPT;
   for (uint64_t base = blockIdx.x * per; base < nq; base += uint64_t(gridDim.x) * per) {
     uint64_t key[QPT], b[QPT], d[QPT];
+    uint32_t tag[QPT];
     CDir rec[QPT];
 #pragma unroll
     for (int j = 0; j < QPT; j++) {
@@ -144,7 +145,9 @@ __global__ void __launch_bounds__(kLThreads) k_lookup_u64(LookupParams lp, const
 #pragma unroll
     for (int j = 0; j < QPT; j++) {
       const uint64_t idx = base + uint64_t(j) * kLThreads + threadIdx.x;
-      b[j] = level1_bucket(lp.l1, key[j]) - lp.b_lo;
+      const uint64_t h1 = hash64(lp.l1.c1, key[j]);
+      b[j] = level1_of_hash(lp.l1, h1) - lp.b_lo;
+      tag[j] = tag4_of_hash(h1);
       const bool ok = idx < nq && b[j] < lp.nb;
       if (!ok) b[j] = 0;
       rec[j] = ld_cdir(lp.cdir + (b[j] >> 5), pol_keep);
@@ -155,6 +158,8 @@ __global__ void __launch_bounds__(kLThreads) k_lookup_u64(LookupParams lp, const
       bool esc;
       d[j] = cdir_entry(rec[j], b[j], lp.dir, &esc);
       if (esc) d[j] = ld_dir(lp.dir + b[j]);
+      // a singleton whose key tag differs: a miss without the slot probe
+      else if (((d[j] >> 40) & 0xFFFF) == 1 && uint32_t(d[j] >> 56) != tag[j]) d[j] = 0;
     }
     // L3 + L4: slot index and the slot probe
     KV16 e[QPT];
@@ -260,10 +265,13 @@ __global__ void __launch_bounds__(kLThreads) k_lookup_bytes(LookupParams lp, con
         fp[j] = fingerprint_pw(qb, off[j], len[j], lp.r_fp, &s_pw);
       }
     }
+    uint32_t tag[QPT];
 #pragma unroll
     for (int j = 0; j < QPT; j++) {
       const uint64_t idx = base + uint64_t(j) * kLThreads + threadIdx.x;
-      b[j] = level1_bucket(lp.l1, fp[j]) - lp.b_lo;
+      const uint64_t h1 = hash64(lp.l1.c1, fp[j]);
+      b[j] = level1_of_hash(lp.l1, h1) - lp.b_lo;
+      tag[j] = tag4_of_hash(h1);
       const bool ok = idx < nq && b[j] < lp.nb;
       if (!ok) b[j] = 0;
       rec[j] = ld_cdir(lp.cdir + (b[j] >> 5), pol_keep);
@@ -274,6 +282,8 @@ __global__ void __launch_bounds__(kLThreads) k_lookup_bytes(LookupParams lp, con
       bool esc;
       d[j] = cdir_entry(rec[j], b[j], lp.dir, &esc);
       if (esc) d[j] = ld_dir(lp.dir + b[j]);
+      // a singleton whose key tag differs: a miss without the slot probe
+      else if (((d[j] >> 40) & 0xFFFF) == 1 && uint32_t(d[j] >> 56) != tag[j]) d[j] = 0;
     }
 #pragma unroll
     for (int j = 0; j < QPT; j++) {
