@@ -127,14 +127,14 @@ __device__ __forceinline__ unsigned long long block_excl_scan(unsigned long long
 
 // Debug-only phase timestamps (compile with -DHM_PHASE_TIMING).
 #ifdef HM_PHASE_TIMING
-__device__ unsigned long long g_hm_phase[65536 * 12];
+__device__ unsigned long long g_hm_phase[65536 * 16];
 __device__ unsigned long long g_hm_ka[4096 * 2];
 #define HM_TMARK(k)                                                     \
   do {                                                                  \
     if (threadIdx.x == 0) {                                             \
       unsigned long long t_;                                            \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));            \
-      g_hm_phase[(s_p & 65535u) * 12 + (k)] = t_;                       \
+      g_hm_phase[(s_p & 65535u) * 16 + (k)] = t_;                       \
     }                                                                   \
   } while (0)
 extern "C" int hm_debug_phase_times(unsigned long long* host, unsigned long long n) {
@@ -1045,6 +1045,10 @@ __global__ void __launch_bounds__(kBThreads, 1024 / kBThreads)
     search_round(bp, skv, X, (r & 1) ? q1 : q0, L, logA, (r & 1) ? q0 : q1, &s_qn[(r + 1) & 1], s_m2, bbase, stt,
                  same);
     __syncthreads();
+#ifdef HM_PHASE_TIMING
+    if (r == 0) HM_TMARK(11);
+    if (tid == 0) g_hm_phase[(s_p & 65535u) * 16 + 12] = r + 1;  // (the round count)
+#endif
   }
   HM_TMARK(4);
 

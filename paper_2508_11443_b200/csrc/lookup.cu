@@ -193,7 +193,10 @@ hm_status lookup_u64_launch(const hm_map* m, const uint64_t* q, uint64_t nq, uin
   lp.dir = m->dir;
   lp.cdir = m->cdir;
   lp.slots = m->slots;
-  constexpr int QPT = 4;
+#ifndef HM_LOOKUP_QPT
+#define HM_LOOKUP_QPT 4
+#endif
+  constexpr int QPT = HM_LOOKUP_QPT;
   const uint64_t per = uint64_t(kLThreads) * QPT;
   const uint64_t blocks = (nq + per - 1) / per;
   const unsigned grid = unsigned(std::min<uint64_t>(blocks, uint64_t(num_sms()) * 8));

@@ -15,10 +15,10 @@ hm.profile_read(); hm.profile_enable(True)
 m = hm.HashMap.build_u64(k, v); torch.cuda.synchronize()
 print('event ms per kernel', hm.profile_read()); hm.profile_enable(False)
 L = hm.lib(); L.hm_debug_phase_times.argtypes = [C.c_void_p, C.c_uint64]
-buf = np.zeros(65536 * 12 + 8192, np.uint64)
-L.hm_debug_phase_times(buf.ctypes.data_as(C.c_void_p), 65536 * 12)
+buf = np.zeros(65536 * 16 + 8192, np.uint64)
+L.hm_debug_phase_times(buf.ctypes.data_as(C.c_void_p), 65536 * 16)
 names = ["start", "load", "hist", "scan+group", "search", "lookback", "out", "dir"]
-t = buf[: 65536 * 12].reshape(65536, 12).astype(np.int64)
+t = buf[: 65536 * 16].reshape(65536, 16).astype(np.int64)
 t = t[t[:, 0] > 0][:, :len(names)]
 d = np.diff(t, axis=1)
 life = t[:, -1] - t[:, 0]
@@ -26,9 +26,13 @@ print("partitions", len(t), "kernel span us %.1f" % ((t[:, -1].max() - t[:, 0].m
 print("CTA lifetime us: mean %.2f median %.2f max %.2f" % (life.mean() / 1e3, np.median(life) / 1e3, life.max() / 1e3))
 for i in range(len(names) - 1):
     print(f"{names[i]:>12s} -> {names[i+1]:<12s} mean {d[:, i].mean()/1e3:7.2f} us  p50 {np.median(d[:, i])/1e3:7.2f}  p99 {np.percentile(d[:, i], 99)/1e3:7.2f}  share {100*d[:, i].mean()/life.mean():5.1f}%")
-t2 = buf[: 65536 * 12].reshape(65536, 12).astype(np.int64)
+t2 = buf[: 65536 * 16].reshape(65536, 16).astype(np.int64)
 t2 = t2[t2[:, 0] > 0]
 if (t2[:, 8] > 0).all():
     for a, b, nm in [(3, 8, "search_warp"), (8, 9, "round0 (thread 0)"), (9, 10, "singles+sync"), (10, 4, "retry rounds")]:
         x = t2[:, b] - t2[:, a]
         print(f"  search part {nm:18s} mean {x.mean()/1e3:7.2f} us  p50 {np.median(x)/1e3:7.2f}")
+    nr = t2[:, 12]
+    x = t2[:, 11] - t2[:, 10]
+    ok = t2[:, 11] > 0
+    print("  rounds per CTA: mean %.2f, dist %s; first retry round mean %.2f us" % (nr.mean(), np.bincount(nr.astype(int))[:6], (x[ok]).mean() / 1e3 if ok.any() else 0))
