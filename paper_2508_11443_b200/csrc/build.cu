@@ -534,7 +534,7 @@ __device__ __forceinline__ void bucket_done_regs(const SearchCtx& X, uint32_t lb
 // hides the first one's latency), the lower successful one wins.  Equal keys
 // -> duplicate / fingerprint collision (checked once: equal keys collide under
 // every t).  Returns the first attempt still to try (0: the bucket is done).
-template <int K, class E, class Same>
+template <int K, bool kTwoOK, class E, class Same>
 __device__ __forceinline__ uint32_t round0_bucket(const BuildParams& bp, const E* skv, const SearchCtx& X, uint32_t lb,
                                               const uint64_t* s_m2, uint64_t bbase, DevStatus* stt,
                                               const Same& same) {
@@ -543,7 +543,7 @@ __device__ __forceinline__ uint32_t round0_bucket(const BuildParams& bp, const E
 #pragma unroll
   for (int j = 0; j < K; j++) k[j] = uint32_t(j) < s ? skv[X.sidx[st0 + j]].key : 0ull;
   const FastMod fm{uint64_t(s) * s, s_m2[s]};
-  constexpr bool kTwo = K <= 4;  // (two attempts in flight; the rare s = 5..8 buckets try one)
+  constexpr bool kTwo = kTwoOK && K <= 4;  // (two attempts in flight; the rare s = 5..8 buckets try one)
   uint32_t h0[K], h1[kTwo ? K : 1];
   uint64_t b0, b1 = 0;
   if (kTwo && !(bp.flags & HM_FLAG_NO_ROUND0_ILP)) {
@@ -579,36 +579,66 @@ __device__ __forceinline__ uint32_t round0_bucket(const BuildParams& bp, const E
   return (kTwo && !(bp.flags & HM_FLAG_NO_ROUND0_ILP)) ? 2 : 1;
 }
 
-// Round 0 over the multi-key list ([s = 2 | s = 3..4 | s = 5..8] regions, so
-// almost every warp runs one key-register width): the buckets that need t >= 2
-// are queued.
+// Round 0 over the multi-key list ([s = 5..8 | s = 3..4 | s = 2] regions),
+// one iteration for every warp and one key-register width per warp: the rare
+// s = 5..8 buckets go straight to the queue (t = 0); warps [0, w4) take the
+// s = 3..4 buckets, a lane per bucket with attempts 0 and 1 in flight; the
+// other warps take the s = 2 buckets the same way — and when there are more of
+// them than lanes, the last lanes take two s = 2 buckets each with one attempt
+// per bucket (the same two independent chains per lane).  The buckets that
+// need more attempts are queued.
 template <class E, class Same>
 __device__ __forceinline__ void search_round0(const BuildParams& bp, const E* skv, const SearchCtx& X,
-                                              const uint16_t* list, uint32_t n2, uint32_t n4, uint32_t L,
+                                              const uint16_t* list, uint32_t e8, uint32_t e4, uint32_t L,
                                               uint32_t* queue, uint32_t* qn, const uint64_t* s_m2, uint64_t bbase,
                                               DevStatus* stt, const Same& same) {
-  const uint32_t lane = threadIdx.x & 31, lt = (1u << lane) - 1u;
-  // one entry per thread, warps in reverse order (warp 0, which did the
-  // look-back, gets the fewest); entries beyond kBThreads go to the queue with
-  // t = 0 — every warp runs one round-0 iteration
-  const uint32_t e = (kBWarps - 1 - (threadIdx.x >> 5)) * 32 + lane;
-  for (uint32_t x = kBThreads + threadIdx.x; x < L; x += kBThreads) queue[atomicAdd(qn, 1u)] = list[x];
-  if (e - lane < L) {
-    uint32_t lb = 0, tn = 0;
-    if (e < L) {
-      lb = list[e];
-      if (e < n2) tn = round0_bucket<2>(bp, skv, X, lb, s_m2, bbase, stt, same);
-      else if (e < n4) tn = round0_bucket<4>(bp, skv, X, lb, s_m2, bbase, stt, same);
-      else tn = round0_bucket<8>(bp, skv, X, lb, s_m2, bbase, stt, same);
+  const uint32_t lane = threadIdx.x & 31, lt = (1u << lane) - 1u, warp = threadIdx.x >> 5;
+  const uint32_t n4 = e4 - e8, n2 = L - e4;
+  const uint32_t w4 = min((n4 + 31) / 32, uint32_t(kBWarps));
+  for (uint32_t x = threadIdx.x; x < e8; x += kBThreads) queue[atomicAdd(qn, 1u)] = list[x];
+  uint32_t lb = 0, tn = 0, lb2 = 0, tn2 = 0;
+  if (warp < w4) {
+    for (uint32_t i = warp * 32 + lane; i < n4; i += w4 * 32) {  // (more than one pass only if n4 > 512)
+      lb = list[e8 + i];
+      const uint32_t t = round0_bucket<4, true>(bp, skv, X, lb, s_m2, bbase, stt, same);
+      if (t) queue[atomicAdd(qn, 1u)] = lb | (t << 16);
     }
-    const bool retry = tn != 0;
-    const uint32_t m = __ballot_sync(0xffffffffu, retry);
+  } else {
+    const uint32_t lanes = (kBWarps - w4) * 32, e = threadIdx.x - w4 * 32;
+    uint32_t pbase = lanes;  // lanes >= pbase take two s = 2 buckets
+    if (n2 > lanes) {
+      if (n2 - lanes <= lanes) {
+        pbase = lanes - (n2 - lanes);
+      } else {  // (not enough lanes even in pairs: the rest is queued)
+        for (uint32_t x = 2 * lanes + e; x < n2; x += lanes) queue[atomicAdd(qn, 1u)] = list[e4 + x];
+        pbase = 0;
+      }
+    }
+    if (e >= pbase) {
+      const uint32_t i0 = pbase + 2 * (e - pbase);
+      if (i0 < n2) {
+        lb = list[e4 + i0];
+        tn = round0_bucket<2, false>(bp, skv, X, lb, s_m2, bbase, stt, same);
+      }
+      if (i0 + 1 < n2) {
+        lb2 = list[e4 + i0 + 1];
+        tn2 = round0_bucket<2, false>(bp, skv, X, lb2, s_m2, bbase, stt, same);
+      }
+    } else if (e < n2) {
+      lb = list[e4 + e];
+      tn = round0_bucket<2, true>(bp, skv, X, lb, s_m2, bbase, stt, same);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 2; u++) {
+    const uint32_t tq = u ? tn2 : tn, lq = u ? lb2 : lb;
+    const uint32_t m = __ballot_sync(0xffffffffu, tq != 0);
     if (m) {
       const uint32_t leader = __ffs(m) - 1;
       uint32_t q0 = 0;
       if (lane == leader) q0 = atomicAdd(qn, uint32_t(__popc(m)));
       q0 = __shfl_sync(0xffffffffu, q0, leader);
-      if (retry) queue[q0 + __popc(m & lt)] = lb | (tn << 16);
+      if (tq) queue[q0 + __popc(m & lt)] = lq | (tq << 16);
     }
   }
 }
@@ -636,11 +666,12 @@ template <class E, class Same>
 __device__ __forceinline__ void search_round(const BuildParams& bp, const E* skv, const SearchCtx& X,
                                              const uint32_t* queue, uint32_t L, uint32_t logA, uint32_t* nqueue,
                                              uint32_t* nqn, const uint64_t* s_m2, uint64_t bbase, DevStatus* stt,
-                                             const Same& same) {
+                                             const Same& same, uint32_t first) {
+  // (threads first.. take part; first is a multiple of 32)
   const uint32_t lane = threadIdx.x & 31, lt = (1u << lane) - 1u;
   const uint32_t A = 1u << logA, W = L << logA;
   const uint32_t gmask = A == 32 ? 0xffffffffu : (((1u << A) - 1u) << (lane & ~(A - 1u)));
-  for (uint32_t w0 = threadIdx.x & ~31u; w0 < W; w0 += kBThreads) {
+  for (uint32_t w0 = (threadIdx.x - first) & ~31u; w0 < W; w0 += kBThreads - first) {
     const uint32_t w = w0 + lane;
     bool ok = false, lead = false;
     uint32_t lb = 0, st0 = 0, s = 2, t = 0, tb = 0;
@@ -946,9 +977,10 @@ __global__ void __launch_bounds__(kBThreads, 1024 / kBThreads)
     unsigned long long ta, tb;
     block_excl_scan2(a, b, &ta, &tb, s_red2);
     S_p = ta >> 32;
-    const uint32_t T2 = uint32_t(tb & 0x1FFFFF), T4 = uint32_t((tb >> 21) & 0x1FFFFF);
+    const uint32_t T4 = uint32_t((tb >> 21) & 0x1FFFFF), T8 = uint32_t(tb >> 42);
     uint32_t pos = uint32_t(a), sq = uint32_t(a >> 32);
-    uint32_t n2 = uint32_t(b & 0x1FFFFF), n4 = T2 + uint32_t((b >> 21) & 0x1FFFFF), n8 = T2 + T4 + uint32_t(b >> 42);
+    // list regions: [s = 5..8 | s = 3..4 | s = 2]
+    uint32_t n8 = uint32_t(b >> 42), n4 = T8 + uint32_t((b >> 21) & 0x1FFFFF), n2 = T8 + T4 + uint32_t(b & 0x1FFFFF);
     for (uint32_t j = c0; j < c1; j++) {
       const uint32_t v = soff[j];
       ss[j] = uint8_t(v > 255 ? 255 : v);
@@ -977,19 +1009,38 @@ __global__ void __launch_bounds__(kBThreads, 1024 / kBThreads)
   if (tid == 0) st_release(&lbstate[p], (p == 0 ? kFlagInc : kFlagAgg) | (S_p & kValMask));
   __syncthreads();
   const unsigned long long tcls = s_red2[0][0];
-  const uint32_t Lc2 = uint32_t(tcls & 0x1FFFFF), Lc4 = Lc2 + uint32_t((tcls >> 21) & 0x1FFFFF),
-                 Lc8 = Lc4 + uint32_t(tcls >> 42);
+  const uint32_t Le8 = uint32_t(tcls >> 42), Le4 = Le8 + uint32_t((tcls >> 21) & 0x1FFFFF),
+                 Lall = Le4 + uint32_t(tcls & 0x1FFFFF);
   // groupby: grouped position of every item
   for (uint32_t i = tid; i < cnt; i += kBThreads) sidx[sstart[lbk[i]] + rk[i]] = uint16_t(i);
   __syncthreads();
   HM_TMARK(3);
 
+  // ---- level-2 seed search, map make2 over the multi-key buckets
+  // (PAPER.md:286-292); every finished bucket maps its slots to their source
+  // items (bucket_done), the singletons are mapped here (R12: a singleton sits
+  // at soff)
+  const bool staged = S_p <= SL.smax && !(bp.flags & HM_FLAG_DIRECT_SLOTS);
+  SearchCtx X{sstart, ss, sidx, soff, sA, s_t, staged ? src : nullptr};
+  uint32_t* q0 = reinterpret_cast<uint32_t*>(smem + SL.queue);
+  uint32_t* q1 = q0 + (cap / 2 + 1);
+  search_warp(bp, skv, X, slist + SL.cls_off[2], s_c9, s_m2, bbase, stt, same, s_bitsw[warp]);
+  HM_TMARK(8);
+  search_round0(bp, skv, X, slist, Le8, Le4, Lall, q0, &s_qn[0], s_m2, bbase, stt, same);
+  HM_TMARK(9);
+  if (staged) {
+    const uint32_t c0 = tid * CH, c1 = min(c0 + CH, nbp);
+    for (uint32_t j = c0; j < c1; j++)
+      if (ss[j] == 1) src[soff[j]] = sidx[sstart[j]];
+  }
+  __syncthreads();
+  HM_TMARK(10);
   // look-back: exclusive prefix of S over the partitions before p (warp 0,
   // lane i inspects partition qb - i: the closest inclusive prefix plus the
-  // aggregates in front of it give the base).  Done before the search so that
-  // the inclusive prefix is published early and successors find it one hop
-  // back; warp 0 then takes the smallest share of the search.
-  if (warp == 0) {
+  // aggregates in front of it give the base).  Warp 0 runs it while warps
+  // 1..15 run the first retry round (or right after round 0 when no bucket
+  // needs one).
+  auto look_back = [&]() {
     unsigned long long base = 0;
     if (p > 0) {
       int64_t qb = int64_t(p) - 1;
@@ -1015,41 +1066,28 @@ __global__ void __launch_bounds__(kBThreads, 1024 / kBThreads)
       if (p == bp.np - 1) stt->S = base + S_p;
       s_base = base;
     }
-  }
-  // ---- level-2 seed search, map make2 over the multi-key buckets
-  // (PAPER.md:286-292); every finished bucket maps its slots to their source
-  // items (bucket_done), the singletons are mapped here (R12: a singleton sits
-  // at soff)
-  const bool staged = S_p <= SL.smax && !(bp.flags & HM_FLAG_DIRECT_SLOTS);
-  SearchCtx X{sstart, ss, sidx, soff, sA, s_t, staged ? src : nullptr};
-  uint32_t* q0 = reinterpret_cast<uint32_t*>(smem + SL.queue);
-  uint32_t* q1 = q0 + (cap / 2 + 1);
-  search_warp(bp, skv, X, slist + SL.cls_off[2], s_c9, s_m2, bbase, stt, same, s_bitsw[warp]);
-  HM_TMARK(8);
-  search_round0(bp, skv, X, slist, Lc2, Lc4, Lc8, q0, &s_qn[0], s_m2, bbase, stt, same);
-  HM_TMARK(9);
-  if (staged) {
-    const uint32_t c0 = tid * CH, c1 = min(c0 + CH, nbp);
-    for (uint32_t j = c0; j < c1; j++)
-      if (ss[j] == 1) src[soff[j]] = sidx[sstart[j]];
-  }
-  __syncthreads();
-  HM_TMARK(10);
+  };
+  bool looked = false;  // (CTA-uniform)
   for (uint32_t r = 0;; r++) {
     const uint32_t L = s_qn[r & 1];
     if (L == 0) break;
     if (tid == 0) s_qn[(r + 1) & 1] = 0;
     __syncthreads();
+    const uint32_t first = r == 0 ? 32u : 0u, lanes = kBThreads - first;
     uint32_t logA = 0;
-    while (logA < 3 && (L << (logA + 1)) <= uint32_t(kBThreads)) logA++;
-    search_round(bp, skv, X, (r & 1) ? q1 : q0, L, logA, (r & 1) ? q0 : q1, &s_qn[(r + 1) & 1], s_m2, bbase, stt,
-                 same);
+    while (logA < 3 && (L << (logA + 1)) <= lanes) logA++;  // A <= 8
+    if (tid < first) look_back();
+    else
+      search_round(bp, skv, X, (r & 1) ? q1 : q0, L, logA, (r & 1) ? q0 : q1, &s_qn[(r + 1) & 1], s_m2, bbase, stt,
+                   same, first);
+    looked = true;
     __syncthreads();
 #ifdef HM_PHASE_TIMING
     if (r == 0) HM_TMARK(11);
     if (tid == 0) g_hm_phase[(s_p & 65535u) * 16 + 12] = r + 1;  // (the round count)
 #endif
   }
+  if (!looked && warp == 0) look_back();
   HM_TMARK(4);
 
   __syncthreads();  // (s_base)
