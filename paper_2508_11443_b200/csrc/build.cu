@@ -39,6 +39,9 @@ constexpr int kAThreads = 512;
 #define HM_KB_THREADS 512
 #endif
 constexpr int kBThreads = HM_KB_THREADS;
+#ifndef HM_RETRY_LOGA
+#define HM_RETRY_LOGA 3  // at most 2^3 lanes (attempts) per queued bucket and round
+#endif
 constexpr int kBWarps = kBThreads / 32;
 constexpr unsigned long long kFlagAgg = 1ull << 62, kFlagInc = 2ull << 62, kValMask = (1ull << 62) - 1;
 
@@ -261,9 +264,15 @@ __global__ void __launch_bounds__(kAThreads) k_partition(Src src, BuildParams bp
 // one shared-memory atomicAdd per element.
 constexpr int kSThreads = 512;
 // elements per thread: 8 x 16-byte or 4 x 32-byte records in registers
+#ifndef HM_SPLIT_PT
+#define HM_SPLIT_PT 6
+#endif
+#ifndef HM_SPLIT_MINB
+#define HM_SPLIT_MINB 2
+#endif
 template <class E>
 __host__ __device__ constexpr int split_pt() {
-  return sizeof(E) == 16 ? 8 : 4;
+  return sizeof(E) == 16 ? HM_SPLIT_PT : 4;
 }
 template <class E>
 __host__ __device__ constexpr int split_tile() {
@@ -286,7 +295,7 @@ struct SplitArgs {
 };
 
 template <class Src, class E, int PASS, int BITS>
-__global__ void __launch_bounds__(kSThreads, 2) k_split(Src src, BuildParams bp, SplitArgs a,
+__global__ void __launch_bounds__(kSThreads, HM_SPLIT_MINB) k_split(Src src, BuildParams bp, SplitArgs a,
                                                         DevStatus* __restrict__ stt) {
   extern __shared__ __align__(16) uint8_t smem[];
   constexpr int kSDigits = 1 << BITS, kSBits = BITS, kSPT = split_pt<E>(), kSTile = split_tile<E>();
@@ -1075,7 +1084,7 @@ __global__ void __launch_bounds__(kBThreads, 1024 / kBThreads)
     __syncthreads();
     const uint32_t first = r == 0 ? 32u : 0u, lanes = kBThreads - first;
     uint32_t logA = 0;
-    while (logA < 3 && (L << (logA + 1)) <= lanes) logA++;  // A <= 8
+    while (logA < HM_RETRY_LOGA && (L << (logA + 1)) <= lanes) logA++;
     if (tid < first) look_back();
     else
       search_round(bp, skv, X, (r & 1) ? q1 : q0, L, logA, (r & 1) ? q0 : q1, &s_qn[(r + 1) & 1], s_m2, bbase, stt,
@@ -1187,6 +1196,32 @@ __global__ void __launch_bounds__(kBThreads, 1024 / kBThreads)
     }
   }
   HM_TMARK(7);
+}
+
+// ------------------------------------------------------- overflow check
+// A build partition that overflowed its buffer (a degenerate level-1
+// distribution: many equal keys, or an adversarial key set) lost records, so
+// its S_p is unknown.  These two kernels recount the level-1 histogram of the
+// suspect partitions straight from the input and sum their s^2, so that the
+// space bound R7 decides as the oracle does (redraw level one, and after 16
+// draws SEED_EXHAUSTED); if the bound holds the build reports TOO_LARGE (a
+// bucket this version cannot hold).
+template <class Src>
+__global__ void k_heavy_hist(Src src, BuildParams bp, const uint32_t* __restrict__ hidx, uint32_t* __restrict__ hcnt) {
+  const uint32_t BP = 1u << bp.log2_bp;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < bp.n_in; i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t lb = level1_bucket(bp.l1, src.load(i).key) - bp.b_lo;
+    if (lb >= bp.nb) continue;
+    const uint32_t h = hidx[lb >> bp.log2_bp];
+    if (h != ~0u) atomicAdd(&hcnt[size_t(h) * BP + (lb & (BP - 1))], 1u);
+  }
+}
+__global__ void k_heavy_sq(const uint32_t* __restrict__ hcnt, uint64_t total, unsigned long long* out) {
+  unsigned long long acc = 0;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total; i += uint64_t(gridDim.x) * blockDim.x)
+    acc += uint64_t(hcnt[i]) * hcnt[i];
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
 }
 
 // ------------------------------------------------------------- host side
@@ -1457,7 +1492,54 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
         return fail(HM_ERR_INVALID_ARG);
       }
       if (hs.part_overflow) {
-        set_error("build partition overflow (degenerate key distribution); not supported in this version");
+        // recount the suspect partitions (k_heavy_*) for the space bound R7
+        std::vector<unsigned int> hp(pl.np), hc(two_pass ? ncoarse : 0);
+        HM_CUDA_TRY(cudaMemcpyAsync(hp.data(), pcount, size_t(pl.np) * 4, cudaMemcpyDeviceToHost, st));
+        if (two_pass) HM_CUDA_TRY(cudaMemcpyAsync(hc.data(), ccount, size_t(ncoarse) * 4, cudaMemcpyDeviceToHost, st));
+        HM_CUDA_TRY(cudaStreamSynchronize(st));
+        std::vector<uint32_t> hidx(pl.np, ~0u);
+        uint32_t nh = 0;
+        for (uint32_t q = 0; q < pl.np; q++)
+          if (hp[q] > pl.cap) hidx[q] = nh++;
+        for (uint32_t c = 0; c < hc.size(); c++)
+          if (hc[c] > ccap)
+            for (uint32_t d = 0; d < sdig && c * sdig + d < pl.np; d++)
+              if (hidx[c * sdig + d] == ~0u) hidx[c * sdig + d] = nh++;
+        if (nh == 0 || nh > 1024) {
+          set_error("build partition overflow (degenerate key distribution); not supported in this version");
+          return fail(HM_ERR_TOO_LARGE);
+        }
+        const size_t BPz = size_t(1) << pl.log2_bp;
+        uint32_t *d_hidx = nullptr, *d_hcnt = nullptr;
+        unsigned long long* d_sq = nullptr;
+        if ((s = dmalloc(&d_hidx, size_t(pl.np) * 4, st)) != HM_OK) return fail(s);
+        if ((s = dmalloc(&d_hcnt, size_t(nh) * BPz * 4, st)) != HM_OK) return fail(s);
+        if ((s = dmalloc(&d_sq, 8, st)) != HM_OK) return fail(s);
+        HM_CUDA_TRY(cudaMemcpyAsync(d_hidx, hidx.data(), size_t(pl.np) * 4, cudaMemcpyHostToDevice, st));
+        HM_CUDA_TRY(cudaMemsetAsync(d_hcnt, 0, size_t(nh) * BPz * 4, st));
+        HM_CUDA_TRY(cudaMemsetAsync(d_sq, 0, 8, st));
+        {
+          LaunchScope ls_("k_heavy_hist", st);
+          k_heavy_hist<Src><<<unsigned(sms) * 8, 256, 0, st>>>(src, bp, d_hidx, d_hcnt);
+        }
+        {
+          LaunchScope ls_("k_heavy_sq", st);
+          k_heavy_sq<<<unsigned(sms) * 4, 256, 0, st>>>(d_hcnt, uint64_t(nh) * BPz, d_sq);
+        }
+        unsigned long long heavy = 0;
+        HM_CUDA_TRY(cudaMemcpyAsync(&heavy, d_sq, 8, cudaMemcpyDeviceToHost, st));
+        HM_CUDA_TRY(cudaStreamSynchronize(st));
+        cudaFreeAsync(d_hidx, st);
+        cudaFreeAsync(d_hcnt, st);
+        cudaFreeAsync(d_sq, st);
+        if (hs.S + heavy > 4 * n_global) {  // R7: level one redraws, as the oracle does
+          hs.S += heavy;
+          hs.bound_fail = 1;
+          hs.part_overflow = 0;
+          break;
+        }
+        set_error("build partition overflow (degenerate key distribution) within the space bound; "
+                  "not supported in this version");
         return fail(HM_ERR_TOO_LARGE);
       }
       if (hs.S > 4 * n_global || hs.bound_fail) break;  // R7: redraw level one

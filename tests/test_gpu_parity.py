@@ -263,3 +263,31 @@ def test_u64_construction_routes_duplicates(flags_name):
     with pytest.raises(hm.HMError) as e:
         hm.HashMap.build_u64(dev(keys), dev(gen.u64_values(100_000)), flags=getattr(hm, flags_name))
     assert e.value.name == "DUPLICATE_KEY"
+
+
+def test_u64_duplicate_heavy_overflow_matches_oracle():
+    """Thousands of copies of one key overflow a build partition; the GPU
+    recounts the suspect partitions for the space bound (R7) and, like the
+    oracle, exhausts level one (SEED_EXHAUSTED, R26).  With the bound holding
+    (a huge n) such an input is outside this version (TOO_LARGE)."""
+    hm = _hm()
+    n = 200_000
+    keys = gen.u64_keys(n)
+    keys[:2000] = keys[7]
+    vals = gen.u64_values(n)
+    with pytest.raises(O.OracleError) as eo:
+        O.build_u64(keys, vals, 0)
+    with pytest.raises(hm.HMError) as e:
+        hm.HashMap.build_u64(dev(keys), dev(vals))
+    assert e.value.name == eo.value.name == "SEED_EXHAUSTED"
+    n = 2_000_000
+    keys = gen.u64_keys(n)
+    keys[:1500] = keys[11]
+    with pytest.raises(hm.HMError) as e:
+        hm.HashMap.build_u64(dev(keys), dev(gen.u64_values(n)))
+    assert e.value.name == "TOO_LARGE"
+    # the map and the workspace stay usable after the degenerate builds
+    keys, vals = gen.u64_keys(5000), gen.u64_values(5000)
+    m = hm.HashMap.build_u64(dev(keys), dev(vals))
+    assert_table_equal(m, O.build_u64(keys, vals, 0))
+    m.free()
