@@ -336,15 +336,27 @@ __device__ __forceinline__ uint32_t owner_of(uint64_t b, uint64_t n, int world) 
   return uint32_t((b * uint64_t(world)) / n);
 }
 
-__global__ void k_route_count(const uint64_t* __restrict__ keys, uint64_t n, L1Params l1, int world,
-                              unsigned long long* __restrict__ counts) {
-  __shared__ unsigned long long s_c[64];
+__global__ void __launch_bounds__(512) k_route_count(const uint64_t* __restrict__ keys, uint64_t n, L1Params l1,
+                                                     int world, unsigned long long* __restrict__ counts) {
+  __shared__ unsigned int s_c[64];
   if (threadIdx.x < 64) s_c[threadIdx.x] = 0;
   __syncthreads();
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
-    atomicAdd(&s_c[owner_of(level1_bucket(l1, keys[i]), l1.n, world)], 1ull);
+  constexpr int U = 8;  // keys in flight per thread
+  for (uint64_t b0 = uint64_t(blockIdx.x) * blockDim.x * U; b0 < n; b0 += uint64_t(gridDim.x) * blockDim.x * U) {
+    uint64_t k[U];
+#pragma unroll
+    for (int j = 0; j < U; j++) {
+      const uint64_t i = b0 + uint64_t(j) * blockDim.x + threadIdx.x;
+      k[j] = i < n ? __ldg(keys + i) : 0ull;
+    }
+#pragma unroll
+    for (int j = 0; j < U; j++) {
+      const uint64_t i = b0 + uint64_t(j) * blockDim.x + threadIdx.x;
+      if (i < n) atomicAdd(&s_c[owner_of(level1_bucket(l1, k[j]), l1.n, world)], 1u);
+    }
+  }
   __syncthreads();
-  if (threadIdx.x < world && s_c[threadIdx.x]) atomicAdd(&counts[threadIdx.x], s_c[threadIdx.x]);
+  if (threadIdx.x < world && s_c[threadIdx.x]) atomicAdd(&counts[threadIdx.x], (unsigned long long)s_c[threadIdx.x]);
 }
 
 __global__ void k_route_prefix(const unsigned long long* counts, int world, unsigned long long* cursors) {
@@ -357,29 +369,87 @@ __global__ void k_route_prefix(const unsigned long long* counts, int world, unsi
   }
 }
 
-// Scatter by owner rank; warp-aggregated cursor reservation per destination.
-__global__ void k_route_scatter(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ vals, uint64_t n,
-                                L1Params l1, int world, unsigned long long* __restrict__ cursors,
-                                uint64_t* __restrict__ sk, uint64_t* __restrict__ sv, uint64_t* __restrict__ perm) {
-  const uint32_t lane = threadIdx.x & 31;
-  for (uint64_t base = (blockIdx.x * uint64_t(blockDim.x)) & ~uint64_t(31); base < n;
-       base += uint64_t(gridDim.x) * blockDim.x) {
-    const uint64_t i = base + (threadIdx.x & ~31u) + lane;
-    const bool live = i < n;
-    uint64_t k = live ? keys[i] : 0;
-    const uint32_t r = live ? owner_of(level1_bucket(l1, k), l1.n, world) : 0xFFFFFFFFu;
-    const uint32_t peers = __match_any_sync(0xffffffffu, r);
-    const uint32_t leader = __ffs(peers) - 1;
-    const uint32_t rank_in = __popc(peers & ((1u << lane) - 1u));
-    unsigned long long pos0 = 0;
-    if (live && lane == leader) pos0 = atomicAdd(&cursors[r], (unsigned long long)__popc(peers));
-    pos0 = __shfl_sync(0xffffffffu, pos0, leader);
-    if (live) {
-      const uint64_t pos = pos0 + rank_in;
-      sk[pos] = k;
-      if (sv) sv[pos] = vals[i];
-      if (perm) perm[i] = pos;
+// Scatter by owner rank, a tile of kRTile keys per CTA: the rank of every key
+// among the tile's keys with the same destination comes from a shared-memory
+// atomicAdd, one global atomicAdd per (tile, destination) reserves its run in
+// the send buffer (counts are exact: k_route_count ran first), and the tile is
+// staged in shared memory in destination order so that the runs are written
+// with consecutive lanes.  perm[i] (queries) = the routed position of input i.
+constexpr int kRThreads = 512, kRPT = 8, kRTile = kRThreads * kRPT;
+__global__ void __launch_bounds__(kRThreads) k_route_scatter(const uint64_t* __restrict__ keys,
+                                                             const uint64_t* __restrict__ vals, uint64_t n, L1Params l1,
+                                                             int world, unsigned long long* __restrict__ cursors,
+                                                             uint64_t* __restrict__ sk, uint64_t* __restrict__ sv,
+                                                             uint64_t* __restrict__ perm) {
+  __shared__ uint64_t s_k[kRTile];
+  __shared__ uint8_t s_d[kRTile];
+  __shared__ uint32_t s_cnt[64], s_pre[64];
+  __shared__ unsigned long long s_base[64];
+  const uint32_t tid = threadIdx.x;
+  for (uint64_t t0 = uint64_t(blockIdx.x) * kRTile; t0 < n; t0 += uint64_t(gridDim.x) * kRTile) {
+    const uint32_t nv = n - t0 < uint64_t(kRTile) ? uint32_t(n - t0) : uint32_t(kRTile);
+    if (tid < 64) s_cnt[tid] = 0;
+    __syncthreads();
+    uint64_t k[kRPT];
+    uint32_t d[kRPT], rk[kRPT];
+#pragma unroll
+    for (int j = 0; j < kRPT; j++) {
+      const uint32_t i = j * kRThreads + tid;
+      k[j] = i < nv ? __ldg(keys + t0 + i) : 0ull;
     }
+#pragma unroll
+    for (int j = 0; j < kRPT; j++) {
+      const uint32_t i = j * kRThreads + tid;
+      d[j] = 0;
+      if (i < nv) {
+        d[j] = owner_of(level1_bucket(l1, k[j]), l1.n, world);
+        rk[j] = atomicAdd(&s_cnt[d[j]], 1u);
+      }
+    }
+    __syncthreads();
+    if (tid < 32) {  // tile prefix over the destinations (world <= 64: two per lane)
+      const uint32_t a = s_cnt[2 * tid], b = s_cnt[2 * tid + 1];
+      uint32_t x = a + b;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (tid >= uint32_t(o)) x += y;
+      }
+      x -= a + b;
+      s_pre[2 * tid] = x;
+      s_pre[2 * tid + 1] = x + a;
+    }
+    if (tid < uint32_t(world) && s_cnt[tid]) s_base[tid] = atomicAdd(&cursors[tid], (unsigned long long)s_cnt[tid]);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kRPT; j++) {
+      const uint32_t i = j * kRThreads + tid;
+      if (i < nv) {
+        const uint32_t pos = s_pre[d[j]] + rk[j];
+        s_k[pos] = k[j];
+        s_d[pos] = uint8_t(d[j]);
+        if (perm) perm[t0 + i] = s_base[d[j]] + rk[j];
+      }
+    }
+    __syncthreads();
+    for (uint32_t i = tid; i < nv; i += kRThreads) {
+      const uint32_t dd = s_d[i];
+      sk[s_base[dd] + (i - s_pre[dd])] = s_k[i];
+    }
+    if (sv) {  // values follow the same permutation (staged through the same buffer)
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < kRPT; j++) {
+        const uint32_t i = j * kRThreads + tid;
+        if (i < nv) s_k[s_pre[d[j]] + rk[j]] = __ldg(vals + t0 + i);
+      }
+      __syncthreads();
+      for (uint32_t i = tid; i < nv; i += kRThreads) {
+        const uint32_t dd = s_d[i];
+        sv[s_base[dd] + (i - s_pre[dd])] = s_k[i];
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -393,7 +463,8 @@ static hm_status route_common(const uint64_t* keys, const uint64_t* vals, uint64
   if (e == cudaSuccess && n) {
     {
       LaunchScope ls_("k_route_count", st);
-      k_route_count<<<grid, 256, 0, st>>>(keys, n, l1, world, reinterpret_cast<unsigned long long*>(counts));
+      const unsigned gc = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((n + 4095) / 4096, uint64_t(num_sms()) * 4)));
+      k_route_count<<<gc, 512, 0, st>>>(keys, n, l1, world, reinterpret_cast<unsigned long long*>(counts));
     }
     {
       LaunchScope ls_("k_route_prefix", st);
@@ -401,7 +472,8 @@ static hm_status route_common(const uint64_t* keys, const uint64_t* vals, uint64
     }
     {
       LaunchScope ls_("k_route_scatter", st);
-      k_route_scatter<<<grid, 256, 0, st>>>(keys, vals, n, l1, world, cur, sk, sv, perm);
+      const unsigned gs = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((n + kRTile - 1) / kRTile, uint64_t(num_sms()) * 2)));
+      k_route_scatter<<<gs, kRThreads, 0, st>>>(keys, vals, n, l1, world, cur, sk, sv, perm);
     }
     e = cudaGetLastError();
   }
