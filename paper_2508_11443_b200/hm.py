@@ -220,6 +220,16 @@ class HashMap:
         _check(lib().hm_lookup_bytes(self._h, cp, op, nq, vp, fp, _stream(stream)))
         return out_vals, out_found
 
+    def contains_bytes(self, qctx, qoffsets, out_found=None, stream=None):
+        """Membership of byte-string needles: no value is written."""
+        nq = _numel(qoffsets) - 1
+        _, out_found = self._outputs(qoffsets, nq, False, out_found)
+        cp, ck = _ptr(qctx)
+        op, ok = _ptr(qoffsets)
+        fp, fk = _ptr(out_found)
+        _check(lib().hm_lookup_bytes(self._h, cp, op, nq, None, fp, _stream(stream)))
+        return out_found
+
     @staticmethod
     def _outputs(like, nq, out_vals, out_found):
         try:

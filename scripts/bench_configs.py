@@ -112,8 +112,61 @@ def str_config(name, log2n, reps=5):
             "build_kernels_ms": bk, "lookup_kernels_ms": lk}
 
 
+def paper_shape(reps=5):
+    """NEXT-3: the paper's Table 1 shape: n = 10^7 keys, u64 keys and 5..25-byte
+    strings, construction, lookup of every key (100 % hit) and membership of every key.  Values
+    are u64 here (the paper's are i32).  Context only: the paper's numbers are A100."""
+    n = 10_000_000
+    out = []
+    k, v = gen_cuda.u64_keys(n)
+    maps = []
+
+    def build():
+        m = hm.HashMap.build_u64(k, v)
+        if maps:
+            maps.pop().free()
+        maps.append(m)
+
+    bmed, _, bk = timed(build, reps)
+    m = maps[0]
+    ov = torch.empty(n, dtype=torch.int64, device="cuda")
+    of = torch.empty(n, dtype=torch.uint8, device="cuda")
+    lmed, _, lk = timed(lambda: m.lookup(k, ov, of), reps)
+    assert bool(torch.equal(ov, v)) and bool(of.all())
+    mmed, _, mk = timed(lambda: m.contains(k), reps)
+    m.free()
+    out.append({"config": "P1 paper Table 1 shape, u64 keys, n = 10^7", "n": n,
+                "construction_ms": round(bmed, 4), "lookup_all_ms": round(lmed, 4), "membership_all_ms": round(mmed, 4),
+                "paper_a100_ms": {"construction": 18.3, "lookup": 3.3, "membership": 1.6},
+                "build_kernels_ms": bk, "lookup_kernels_ms": lk, "membership_kernels_ms": mk})
+    del k, v, ov, of
+    ctx, offs = gen_cuda.string_keys(n, lens_range=(5, 25))
+    vals = torch.arange(n, dtype=torch.int64, device="cuda")
+    maps = []
+
+    def build_s():
+        m = hm.HashMap.build_bytes(ctx, offs, vals)
+        if maps:
+            maps.pop().free()
+        maps.append(m)
+
+    bmed, _, bk = timed(build_s, reps)
+    m = maps[0]
+    lmed, _, lk = timed(lambda: m.lookup_bytes(ctx, offs), reps)
+    gv, gf = m.lookup_bytes(ctx, offs)
+    assert bool(torch.equal(gv, vals)) and bool(gf.all())
+    mmed, _, mk = timed(lambda: m.contains_bytes(ctx, offs), reps)
+    m.free()
+    out.append({"config": "P1 paper Table 1 shape, 5..25-byte strings, n = 10^7", "n": n, "ctx_bytes": int(ctx.numel()),
+                "construction_ms": round(bmed, 4), "lookup_all_ms": round(lmed, 4), "membership_all_ms": round(mmed, 4),
+                "paper_a100_ms": {"construction": 33.2, "lookup": 4.3, "membership": 2.8},
+                "build_kernels_ms": bk, "lookup_kernels_ms": lk, "membership_kernels_ms": mk})
+    torch.cuda.empty_cache()
+    return out
+
+
 def main():
-    only = os.environ.get("ONLY", "C1,C2,C3,C4,C5").split(",")
+    only = os.environ.get("ONLY", "C1,C2,C3,C4,C5,P1").split(",")
     todo = [
         ("C1", lambda: u64_config("C1 2^16 u64 + 2^16 lookups", 16, 16, reps=20)),
         ("C2", lambda: u64_config("C2 2^26 u64 + 2^26 lookups", 26, 26)),
@@ -122,6 +175,8 @@ def main():
         ("C5", lambda: u64_config("C5 2^30 lookups on a 2^27 table (1 GPU)", 27, 30, reps=3)),
     ]
     res = [fn() for tag, fn in todo if tag in only]
+    if "P1" in only:
+        res += paper_shape()
     meta = {"gpu": torch.cuda.get_device_name(0), "peak_gbs": PEAK, "when": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime())}
     for r in res:
         print(json.dumps(r))

@@ -27,3 +27,14 @@ def test_device_generators_match_numpy():
     hqc, hqo, _, _ = gen.string_queries(20_000, 7_000)
     assert np.array_equal(qo.cpu().numpy().view(np.uint64), hqo)
     assert np.array_equal(qc.cpu().numpy(), hqc)
+
+
+def test_device_paper_shape_strings_match_numpy():
+    """The paper's Table 1 string shape (5..25 characters)."""
+    from workloads import gen_cuda
+    ctx, offs = gen_cuda.string_keys(30_001, lo=9, lens_range=(5, 25))
+    hc, ho = gen.pack_strings(np.arange(9, 9 + 30_001, dtype=np.uint64), lens_range=(5, 25))
+    lens = np.diff(ho.astype(np.int64))
+    assert lens.min() == 5 and lens.max() == 25
+    assert np.array_equal(offs.cpu().numpy().view(np.uint64), ho)
+    assert np.array_equal(ctx.cpu().numpy(), hc)

@@ -111,8 +111,11 @@ def fmix32(h: np.ndarray) -> np.ndarray:
     return h
 
 
-def string_lengths(idx: np.ndarray, seed_l: int = SEED_L) -> np.ndarray:
-    return (np.uint64(4) + stream(seed_l, idx) % np.uint64(61)).astype(np.int64)
+def string_lengths(idx: np.ndarray, seed_l: int = SEED_L, lens_range=(4, 64)) -> np.ndarray:
+    """len = lmin + stream(SEED_L, id) mod (lmax - lmin + 1): 4..64 by default, 5..25 for the
+    paper's Table 1 shape."""
+    lmin, lmax = lens_range
+    return (np.uint64(lmin) + stream(seed_l, idx) % np.uint64(lmax - lmin + 1)).astype(np.int64)
 
 
 def string_rows(idx: np.ndarray, seed_b: int = SEED_B) -> np.ndarray:
@@ -126,10 +129,10 @@ def string_rows(idx: np.ndarray, seed_b: int = SEED_B) -> np.ndarray:
     return rows
 
 
-def pack_strings(idx: np.ndarray, seed_l: int = SEED_L, seed_b: int = SEED_B):
+def pack_strings(idx: np.ndarray, seed_l: int = SEED_L, seed_b: int = SEED_B, lens_range=(4, 64)):
     """Flat context + CSR offsets (n+1, uint64) for the strings with ids idx."""
     idx = np.asarray(idx, dtype=np.uint64)
-    lens = string_lengths(idx, seed_l)
+    lens = string_lengths(idx, seed_l, lens_range)
     offs = np.zeros(idx.shape[0] + 1, dtype=np.uint64)
     np.cumsum(lens, out=offs[1:])
     total = int(offs[-1])

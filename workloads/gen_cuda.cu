@@ -48,10 +48,11 @@ __global__ void k_query_ids(uint64_t start_q, uint64_t n, uint64_t lo, uint64_t 
   }
 }
 
-__global__ void k_str_lens(uint64_t start_l, const uint64_t* ids, uint64_t lo, uint64_t n, int64_t* lens) {
+__global__ void k_str_lens(uint64_t start_l, const uint64_t* ids, uint64_t lo, uint64_t n, int64_t* lens,
+                           uint64_t lmin, uint64_t lspan) {
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
     const uint64_t id = ids ? ids[i] : lo + i;
-    lens[i] = int64_t(4 + stream_at(start_l, id) % 61);
+    lens[i] = int64_t(lmin + stream_at(start_l, id) % lspan);
   }
 }
 
@@ -95,9 +96,12 @@ int hg_query_ids(uint64_t seed_q, uint64_t n, uint64_t lo, uint64_t nq, uint64_t
   k_query_ids<<<1184, 256, 0, (cudaStream_t)stream>>>(hg_stream_start(seed_q), n, lo, nq, ids);
   return (int)cudaGetLastError();
 }
-int hg_str_lens(uint64_t seed_l, const uint64_t* ids, uint64_t lo, uint64_t n, int64_t* lens, void* stream) {
+// lengths lmin + stream(SEED_L, id) mod lspan (the default recipe: 4 + mod 61, i.e. 4..64 bytes;
+// the paper's Table 1 shape: 5 + mod 21, i.e. 5..25)
+int hg_str_lens(uint64_t seed_l, const uint64_t* ids, uint64_t lo, uint64_t n, int64_t* lens, void* stream,
+                uint64_t lmin, uint64_t lspan) {
   if (!n) return 0;
-  k_str_lens<<<1184, 256, 0, (cudaStream_t)stream>>>(hg_stream_start(seed_l), ids, lo, n, lens);
+  k_str_lens<<<1184, 256, 0, (cudaStream_t)stream>>>(hg_stream_start(seed_l), ids, lo, n, lens, lmin, lspan);
   return (int)cudaGetLastError();
 }
 int hg_str_bytes(uint64_t seed_b, const uint64_t* ids, uint64_t lo, uint64_t n, const uint64_t* offs, uint8_t* ctx,

@@ -35,7 +35,7 @@ def lib():
         L.hg_u64_keys.argtypes = [u64, u64, u64, p, p, p]
         L.hg_queries.argtypes = [u64, u64, u64, u64, u64, p, p, p, p]
         L.hg_query_ids.argtypes = [u64, u64, u64, u64, p, p]
-        L.hg_str_lens.argtypes = [u64, p, u64, u64, p, p]
+        L.hg_str_lens.argtypes = [u64, p, u64, u64, p, p, u64, u64]
         L.hg_str_bytes.argtypes = [u64, p, u64, u64, p, p, p]
         _lib = L
     return _lib
@@ -67,10 +67,11 @@ def u64_queries(n, nq, lo=0, with_expect=False, device="cuda"):
     return q, ev, ef
 
 
-def _strings(ids, lo, n, device):
+def _strings(ids, lo, n, device, lens_range=(4, 64)):
     import torch
     lens = torch.empty(n, dtype=torch.int64, device=device)
-    assert lib().hg_str_lens(gen.SEED_L, _p(ids), lo, n, _p(lens), _s()) == 0
+    lmin, lmax = lens_range
+    assert lib().hg_str_lens(gen.SEED_L, _p(ids), lo, n, _p(lens), _s(), lmin, lmax - lmin + 1) == 0
     offs = torch.zeros(n + 1, dtype=torch.int64, device=device)
     torch.cumsum(lens, 0, out=offs[1:])
     total = int(offs[-1].item())
@@ -79,13 +80,13 @@ def _strings(ids, lo, n, device):
     return ctx[:total], offs
 
 
-def string_keys(n, lo=0, device="cuda"):
-    return _strings(None, lo, n, device)
+def string_keys(n, lo=0, device="cuda", lens_range=(4, 64)):
+    return _strings(None, lo, n, device, lens_range)
 
 
-def string_queries(n, nq, lo=0, device="cuda"):
+def string_queries(n, nq, lo=0, device="cuda", lens_range=(4, 64)):
     import torch
     ids = torch.empty(nq, dtype=torch.int64, device=device)
     assert lib().hg_query_ids(gen.SEED_Q, n, lo, nq, _p(ids), _s()) == 0
-    ctx, offs = _strings(ids, 0, nq, device)
+    ctx, offs = _strings(ids, 0, nq, device, lens_range)
     return ctx, offs, ids
