@@ -39,6 +39,9 @@ constexpr int kAThreads = 512;
 #define HM_KB_THREADS 512
 #endif
 constexpr int kBThreads = HM_KB_THREADS;
+#ifndef HM_KB_MINB
+#define HM_KB_MINB (1024 / HM_KB_THREADS)  // CTAs per SM the registers must allow
+#endif
 #ifndef HM_RETRY_LOGA
 #define HM_RETRY_LOGA 3  // at most 2^3 lanes (attempts) per queued bucket and round
 #endif
@@ -861,7 +864,7 @@ __device__ __forceinline__ void block_excl_scan2(unsigned long long& a, unsigned
 }
 
 template <class E, class Same>
-__global__ void __launch_bounds__(kBThreads, 1024 / kBThreads)
+__global__ void __launch_bounds__(kBThreads, HM_KB_MINB)
     k_bucket(BuildParams bp, const E* __restrict__ pbuf, const unsigned int* __restrict__ pcount,
              unsigned long long* __restrict__ lbstate, uint64_t* __restrict__ dir, CDir* __restrict__ cdir,
              E* __restrict__ slots, DevStatus* __restrict__ stt, Same same) {
@@ -877,7 +880,7 @@ __global__ void __launch_bounds__(kBThreads, 1024 / kBThreads)
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, lt = (1u << lane) - 1u;
   const uint32_t cap = bp.cap;
   const uint32_t BP = 1u << bp.log2_bp;
-  const uint32_t CH = BP > uint32_t(kBThreads) ? BP / kBThreads : 1u;  // buckets per thread in the scans
+  const uint32_t CH = (BP + kBThreads - 1) / kBThreads;  // buckets per thread in the scans
   const BucketSmem& SL = bp.sl;
   E* skv = reinterpret_cast<E*>(smem + SL.skv);
   uint16_t* lbk = reinterpret_cast<uint16_t*>(smem + SL.lbk);
@@ -1352,7 +1355,7 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
   const size_t static_smem_B = 4096;  // upper bound for k_bucket static shared memory (~2 KB)
   const uint32_t knob_flags = log2_req >> 16;
   log2_req &= 0xFFFFu;
-  const Plan pl = make_plan(n_in, nb, log2_req, uint32_t(sizeof(E)), size_t(smem_sm) / (1024 / kBThreads) - 1024 - static_smem_B,
+  const Plan pl = make_plan(n_in, nb, log2_req, uint32_t(sizeof(E)), size_t(smem_sm) / HM_KB_MINB - 1024 - static_smem_B,
                             size_t(smem_optin) - static_smem_B);
   if (pl.smemB + static_smem_B > size_t(smem_optin)) {
     set_error("build plan does not fit in shared memory");
