@@ -236,6 +236,22 @@ def build_u64(keys, vals, seed: int = 0) -> Table:
     return _wrap(h.value, 0)
 
 
+def from_array_u64(keys, vals, seed: int = 0) -> Table:
+    """from_array: duplicates are
+    allowed, the first occurrence (lowest input index) of every key keeps its
+    value, and the map is the one from_array_nodup builds from those distinct
+    keys (the table is a function of the key set, R13, so their order does not
+    matter).  Plain definition: numpy's unique with return_index gives the
+    first occurrence of each key."""
+    keys, vals = _u64(keys), _u64(vals)
+    assert len(keys) == len(vals)
+    if len(keys) == 0:
+        raise OracleError(2)
+    _, first = np.unique(keys, return_index=True)
+    first = np.sort(first)
+    return build_u64(keys[first], vals[first], seed)
+
+
 def build_u64_shard(keys, vals, n_global: int, b_lo: int, b_hi: int, t1: int, seed: int = 0):
     """(status_name, Table) of one bucket-range shard (fks_oracle.c or_build_u64_shard)."""
     keys, vals = _u64(keys), _u64(vals)

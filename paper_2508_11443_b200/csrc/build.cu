@@ -1288,7 +1288,7 @@ static hm_status dmalloc(T** p, size_t bytes, cudaStream_t st) {
 // maps' own arrays), so they stay allocated until hm_release_workspace().
 // Reuse is safe because everything that touches a stream's workspace is
 // ordered on that stream.
-enum WsRole { WS_FP, WS_BAD, WS_PBUF, WS_PCOUNT, WS_LBSTATE, WS_DSTAT, WS_CBUF, WS_CCOUNT, WS_NROLES };
+enum WsRole { WS_FP, WS_BAD, WS_PBUF, WS_PCOUNT, WS_LBSTATE, WS_DSTAT, WS_CBUF, WS_CCOUNT, WS_DEDUP, WS_NROLES };
 struct Workspace {
   void* p[WS_NROLES] = {};
   size_t bytes[WS_NROLES] = {};
@@ -1319,6 +1319,15 @@ struct Scratch {
     return HM_OK;
   }
 };
+
+// The from_array dedup set (dedup.cu) lives in the same cache.
+hm_status dedup_workspace(void** p, size_t bytes, cudaStream_t st) {
+  Scratch sc{st};
+  uint8_t* q = nullptr;
+  hm_status s = sc.alloc(WS_DEDUP, &q, bytes);
+  *p = q;
+  return s;
+}
 
 // Frees every cached workspace of the current device (stream-ordered on the
 // stream that owns it).

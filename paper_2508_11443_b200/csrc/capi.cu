@@ -258,7 +258,9 @@ hm_status hm_build_u64(const uint64_t* keys, const uint64_t* vals, uint64_t n, c
   if (n == 0) return HM_ERR_EMPTY;
   if (!keys || !vals) return HM_ERR_INVALID_ARG;
   if (n > (1ull << 30)) return HM_ERR_TOO_LARGE;
-  if (opts && (opts->flags & ~uint32_t(HM_FLAG_FULL_DIRECTORY | HM_FLAG_DIRECT_SLOTS | HM_FLAG_NO_ROUND0_ILP))) return HM_ERR_INVALID_ARG;
+  if (opts && (opts->flags & ~uint32_t(HM_FLAG_FULL_DIRECTORY | HM_FLAG_DIRECT_SLOTS | HM_FLAG_NO_ROUND0_ILP |
+                                         HM_FLAG_FROM_ARRAY)))
+    return HM_ERR_INVALID_ARG;
   hm_status s = check_device();
   if (s != HM_OK) return s;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -267,8 +269,20 @@ hm_status hm_build_u64(const uint64_t* keys, const uint64_t* vals, uint64_t n, c
   if ((s = sg.in(keys, n, &dk)) != HM_OK) return s;
   if ((s = sg.in(vals, n, &dv)) != HM_OK) return s;
   const uint64_t seed = opts ? opts->seed : 0;
+  uint64_t *uk = nullptr, *uv = nullptr;
+  if (opts && (opts->flags & HM_FLAG_FROM_ARRAY)) {  // from_array: the distinct keys first
+    uint64_t nu = 0;
+    if ((s = dedup_u64(dk, dv, n, st, &uk, &uv, &nu)) != HM_OK) return s;
+    dk = uk;
+    dv = uv;
+    n = nu;
+  }
   BuildOut bo;
   s = build_u64_core(dk, dv, n, n, 0, n, -1, seed, opts ? (opts->log2_bp | (opts->flags << 16)) : 0, st, &bo);
+  if (uk) {
+    cudaFreeAsync(uk, st);
+    cudaFreeAsync(uv, st);
+  }
   if (s != HM_OK) return s;
   hm_map* m = new_map();
   m->key_kind = 0;

@@ -291,3 +291,45 @@ def test_u64_duplicate_heavy_overflow_matches_oracle():
     m = hm.HashMap.build_u64(dev(keys), dev(vals))
     assert_table_equal(m, O.build_u64(keys, vals, 0))
     m.free()
+
+
+@pytest.mark.parametrize("n,ndistinct,seed", [(1, 1, 0), (10, 3, 1), (5000, 5000, 2), (300_000, 70_000, 3),
+                                              (1 << 20, 1 << 18, 0)])
+def test_u64_from_array_parity(n, ndistinct, seed):
+    """from_array (HM_FLAG_FROM_ARRAY): duplicates allowed, the first occurrence
+    keeps its value; the table equals the oracle's from_array byte for byte."""
+    hm = _hm()
+    rng = np.random.default_rng(n + seed)
+    base = gen.u64_keys(ndistinct, lo=11)
+    keys = base[rng.integers(0, ndistinct, size=n)] if n > ndistinct else base[rng.permutation(ndistinct)]
+    vals = gen.u64_values(n, lo=100)
+    ot = O.from_array_u64(keys, vals, seed)
+    m = hm.HashMap.build_u64(dev(keys), dev(vals), seed=seed, flags=hm.FLAG_FROM_ARRAY)
+    assert_table_equal(m, ot)
+    q = np.concatenate([base, gen.u64_keys(1000, lo=10 * n + 7)])
+    ov, of = O.lookup_u64(ot, q)
+    gv, gf = m.lookup(dev(q))
+    assert np.array_equal(host(gv), ov) and np.array_equal(host(gf), of)
+    m.free()
+
+
+def test_u64_from_array_heavy_duplication():
+    """A million copies of one key among a few distinct ones: the dedup set
+    meets them in one slot; the map holds 4 keys."""
+    hm = _hm()
+    n = 1_000_000
+    keys = np.full(n, np.uint64(0xDEADBEEF12345678))
+    keys[[10, 500_000, 999_999]] = gen.u64_keys(3, lo=5)
+    vals = gen.u64_values(n, lo=0)
+    ot = O.from_array_u64(keys, vals, 0)
+    m = hm.HashMap.build_u64(dev(keys), dev(vals), flags=hm.FLAG_FROM_ARRAY)
+    assert m.info().n == 4
+    assert_table_equal(m, ot)
+    gv, gf = m.lookup(dev(np.array([0xDEADBEEF12345678], np.uint64)))
+    assert host(gv)[0] == 0 and host(gf)[0] == 1  # the first copy is input 0 with value 0
+    m.free()
+    with pytest.raises(hm.HMError) as e:  # byte keys: not in this version
+        ctx, offs = gen.string_keys(10)
+        hm.HashMap.build_bytes(torch.from_numpy(ctx).cuda(), dev(offs), dev(gen.u64_values(10)),
+                               flags=hm.FLAG_FROM_ARRAY)
+    assert e.value.name == "INVALID_ARG"

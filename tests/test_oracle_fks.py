@@ -261,3 +261,32 @@ def test_statistics_universal_family():
     # (singletons take exactly one attempt, R12)
     mean_attempts = (att_obs + singles) / nonempty
     assert abs(mean_attempts - 1.1555) < 0.01
+
+
+def test_oracle_from_array_first_occurrence_wins():
+    """from_array: a brute-force scan of the
+    input for every key's first occurrence gives each lookup; the header counts
+    the distinct keys; distinct inputs give exactly from_array_nodup's table."""
+    rng = np.random.default_rng(7)
+    base = gen.u64_keys(40, lo=900)
+    keys = base[rng.integers(0, 40, size=150)]  # many duplicates, 40 candidates
+    vals = np.arange(1000, 1150, dtype=np.uint64)
+    t = O.from_array_u64(keys, vals, 3)
+    distinct = set(int(k) for k in keys)
+    assert int(t.header["n"]) == len(distinct)
+    q = np.concatenate([base, gen.u64_keys(60, lo=5000)])
+    ov, of = O.lookup_u64(t, q)
+    for x, v, f in zip(q.tolist(), ov.tolist(), of.tolist()):
+        first = next((i for i, k in enumerate(keys.tolist()) if k == x), None)
+        if first is None:
+            assert f == 0 and v == 0
+        else:
+            assert f == 1 and v == 1000 + first
+    k2, v2 = gen.u64_keys(500, lo=3), gen.u64_values(500)
+    a, b = O.from_array_u64(k2, v2, 1), O.build_u64(k2, v2, 1)
+    assert a.dir.tobytes() == b.dir.tobytes() and a.slots.tobytes() == b.slots.tobytes()
+    # the order of the later duplicates does not matter
+    keys3 = np.concatenate([k2, k2[rng.permutation(500)]])
+    vals3 = np.concatenate([v2, np.full(500, 7, np.uint64)])
+    c = O.from_array_u64(keys3, vals3, 1)
+    assert c.dir.tobytes() == b.dir.tobytes() and c.slots.tobytes() == b.slots.tobytes()
