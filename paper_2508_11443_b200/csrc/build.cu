@@ -75,6 +75,20 @@ struct SrcBytes {
     return e;
   }
 };
+// from_array's dedup: {key, value, input index} records (KV32 with ctx_off = i).
+struct SrcU64Idx {
+  const uint64_t* keys;
+  const uint64_t* vals;
+  __device__ __forceinline__ KV32 load(uint64_t i) const {
+    KV32 e;
+    e.key = __ldg(keys + i);
+    e.value = __ldg(vals + i);
+    e.ctx_off = i;
+    e.len = 0;
+    e.reserved = 0;
+    return e;
+  }
+};
 // Equal hashed keys: the same key (duplicate) or a fingerprint collision?
 struct SameU64 {
   __device__ __forceinline__ bool same(const KV16&, const KV16&) const { return true; }
@@ -1722,6 +1736,142 @@ hm_status build_bytes_core(const uint8_t* bytes, const uint64_t* offsets, const 
   }
   set_error("fingerprint redraws exhausted (16)");
   return HM_ERR_FP_EXHAUSTED;
+}
+
+// --------------------------------------------------- from_array, dedup
+// The first occurrence of every key, through the build's own radix passes:
+// {key, value, input index} records are partitioned by a level-1 hash (equal
+// keys share a partition), and one CTA per partition keeps, in a shared-memory
+// set keyed by the key, the lowest input index of every key; the records
+// holding it go to the output.  A partition that overflows its buffer (heavy
+// duplication) makes the caller fall back to the global set (dedup.cu).
+constexpr int kDThreads = 512, kDTab = 4096;
+__global__ void __launch_bounds__(kDThreads, 2) k_dedup_part(const KV32* __restrict__ pbuf,
+                                                             const unsigned int* __restrict__ pcount, uint32_t cap,
+                                                             uint64_t* __restrict__ okeys, uint64_t* __restrict__ ovals,
+                                                             unsigned long long* __restrict__ cursor,
+                                                             DevStatus* __restrict__ stt) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  KV32* skv = reinterpret_cast<KV32*>(smem);
+  uint32_t* tab = reinterpret_cast<uint32_t*>(smem + size_t(cap) * sizeof(KV32));  // local item index
+  uint32_t* tmin = tab + kDTab;                                                    // lowest input index
+  __shared__ uint32_t s_n;
+  __shared__ unsigned long long s_base;
+  const uint32_t p = blockIdx.x, tid = threadIdx.x;
+  const uint32_t cnt_raw = pcount[p];
+  if (cnt_raw > cap) {  // (records were lost: the global set decides)
+    if (tid == 0) atomicOr(&stt->part_overflow, 1u);
+    return;
+  }
+  const uint32_t cnt = cnt_raw;
+  for (uint32_t i = tid; i < kDTab; i += kDThreads) {
+    tab[i] = ~0u;
+    tmin[i] = ~0u;
+  }
+  if (tid == 0) s_n = 0;
+  for (uint32_t i = tid; i < cnt; i += kDThreads) skv[i] = pbuf[size_t(p) * cap + i];
+  __syncthreads();
+  for (uint32_t i = tid; i < cnt; i += kDThreads) {
+    const uint64_t k = skv[i].key;
+    uint32_t h = uint32_t(mix64(k ^ 0x5851F42D4C957F2Dull)) & (kDTab - 1);
+    while (true) {
+      const uint32_t cur = atomicCAS(&tab[h], ~0u, i);
+      if (cur == ~0u || skv[cur].key == k) break;
+      h = (h + 1) & (kDTab - 1);
+    }
+    atomicMin(&tmin[h], uint32_t(skv[i].ctx_off));
+    skv[i].len = h;  // (the item's slot, for the survivor test)
+  }
+  __syncthreads();
+  uint32_t rk[(8192 + kDThreads - 1) / kDThreads];
+  uint32_t nloc = 0;
+  for (uint32_t i = tid, j = 0; i < cnt; i += kDThreads, j++) {
+    rk[j] = ~0u;
+    if (tmin[skv[i].len] == uint32_t(skv[i].ctx_off)) {
+      rk[j] = atomicAdd(&s_n, 1u);
+      nloc++;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) s_base = atomicAdd(cursor, (unsigned long long)s_n);
+  __syncthreads();
+  for (uint32_t i = tid, j = 0; i < cnt; i += kDThreads, j++)
+    if (rk[j] != ~0u) {
+      okeys[s_base + rk[j]] = skv[i].key;
+      ovals[s_base + rk[j]] = skv[i].value;
+    }
+}
+
+// Returns HM_OK with *n_out distinct keys in (okeys, ovals) (device arrays of n
+// entries the caller owns), or HM_ERR_TOO_LARGE when a partition overflowed.
+hm_status dedup_partitioned(const uint64_t* keys, const uint64_t* vals, uint64_t n, cudaStream_t st,
+                            uint64_t* okeys, uint64_t* ovals, uint64_t* n_out) {
+  const int sms = num_sms();
+  // partitions of ~2048 records (cap 2496): 2 CTAs per SM for k_dedup_part
+  uint32_t lg = 11;
+  while (lg > 6 && (n >> lg) < uint64_t(4 * sms)) lg--;
+  const double m = double(uint64_t(1) << lg);
+  const uint32_t cap = uint32_t(std::ceil((m + 8.0 * std::sqrt(m) + 64.0) / 32.0) * 32.0);
+  const uint32_t np = uint32_t((n + (uint64_t(1) << lg) - 1) >> lg);
+  if (np > (1u << 18) || cap * 4 > kDTab * 3) return HM_ERR_TOO_LARGE;
+  BuildParams bp{};
+  bp.smix = seed_mix(0x46524F4D41525241ull);  // (any level-1 function groups equal keys)
+  bp.l1 = make_l1(bp.smix, 0, n);
+  bp.b_lo = 0;
+  bp.nb = n;
+  bp.n_in = n;
+  bp.log2_bp = lg;
+  bp.np = np;
+  bp.cap = cap;
+  Scratch sc{st};
+  KV32 *pbuf = nullptr, *cbuf = nullptr;
+  unsigned int *pcount = nullptr, *ccount = nullptr;
+  DevStatus* dstat = nullptr;
+  hm_status s;
+  const int sbits = np <= 65536 ? 8 : 9;
+  const uint32_t sdig = 1u << sbits, ncoarse = (np + sdig - 1) / sdig;
+  const double mc = double(n) * double(sdig) * m / double(n);
+  const uint32_t ccap = uint32_t(mc + 8.0 * std::sqrt(mc + 1.0) + 1024.0);
+  constexpr int kSTile = split_tile<KV32>();
+  const uint32_t tpc = (ccap + kSTile - 1) / kSTile;
+  if ((s = sc.alloc(WS_PBUF, &pbuf, size_t(np) * cap * sizeof(KV32))) != HM_OK) return s;
+  if ((s = sc.alloc(WS_PCOUNT, &pcount, size_t(np) * 4)) != HM_OK) return s;
+  if ((s = sc.alloc(WS_CBUF, &cbuf, size_t(ncoarse) * ccap * sizeof(KV32))) != HM_OK) return s;
+  if ((s = sc.alloc(WS_CCOUNT, &ccount, size_t(ncoarse) * 4)) != HM_OK) return s;
+  if ((s = sc.alloc(WS_DSTAT, &dstat, sizeof(DevStatus))) != HM_OK) return s;
+  unsigned long long* cur = reinterpret_cast<unsigned long long*>(&dstat->S);  // (S is unused here)
+  HM_CUDA_TRY(cudaMemsetAsync(pcount, 0, size_t(np) * 4, st));
+  HM_CUDA_TRY(cudaMemsetAsync(ccount, 0, size_t(ncoarse) * 4, st));
+  HM_CUDA_TRY(cudaMemsetAsync(dstat, 0, sizeof(DevStatus), st));
+  const size_t smemS = size_t(kSTile) * (sizeof(KV32) + 2);
+  auto kS1 = sbits == 8 ? k_split<SrcU64Idx, KV32, 1, 8> : k_split<SrcU64Idx, KV32, 1, 9>;
+  auto kS2 = sbits == 8 ? k_split<SrcU64Idx, KV32, 2, 8> : k_split<SrcU64Idx, KV32, 2, 9>;
+  HM_CUDA_TRY(cudaFuncSetAttribute(kS1, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smemS)));
+  HM_CUDA_TRY(cudaFuncSetAttribute(kS2, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smemS)));
+  const SrcU64Idx src{keys, vals};
+  const SplitArgs a1{nullptr, nullptr, 0, 0, cbuf, ccount, ccap, ncoarse, 0};
+  {
+    LaunchScope ls_("k_split1", st);
+    kS1<<<unsigned((n + kSTile - 1) / kSTile), kSThreads, smemS, st>>>(src, bp, a1, dstat);
+  }
+  const SplitArgs a2{cbuf, ccount, ccap, tpc, pbuf, pcount, cap, np, ncoarse};
+  {
+    LaunchScope ls_("k_split2", st);
+    kS2<<<ncoarse * tpc, kSThreads, smemS, st>>>(src, bp, a2, dstat);
+  }
+  const size_t smemD = size_t(cap) * sizeof(KV32) + size_t(kDTab) * 8;
+  HM_CUDA_TRY(cudaFuncSetAttribute(k_dedup_part, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smemD)));
+  {
+    LaunchScope ls_("k_dedup_part", st);
+    k_dedup_part<<<np, kDThreads, smemD, st>>>(pbuf, pcount, cap, okeys, ovals, cur, dstat);
+  }
+  HM_CUDA_TRY(cudaGetLastError());
+  DevStatus hs{};
+  HM_CUDA_TRY(cudaMemcpyAsync(&hs, dstat, sizeof(hs), cudaMemcpyDeviceToHost, st));
+  HM_CUDA_TRY(cudaStreamSynchronize(st));
+  if (hs.part_overflow || hs.pad) return HM_ERR_TOO_LARGE;
+  *n_out = hs.S;
+  return HM_OK;
 }
 
 }  // namespace hm

@@ -110,12 +110,6 @@ hm_status dedup_u64(const uint64_t* keys, const uint64_t* vals, uint64_t n, cuda
     if (cur) cudaFreeAsync(cur, st);
   };
   cudaError_t e;
-  {  // the set is cached build scratch (hm_release_workspace frees it)
-    void* v = nullptr;
-    hm_status s = dedup_workspace(&v, cap * sizeof(DedupSlot), st);
-    if (s != HM_OK) return s;
-    set = reinterpret_cast<DedupSlot*>(v);
-  }
   if ((e = cudaMallocAsync(reinterpret_cast<void**>(&cur), 8, st)) != cudaSuccess ||
       (e = cudaMallocAsync(reinterpret_cast<void**>(&ok), n * 8, st)) != cudaSuccess ||
       (e = cudaMallocAsync(reinterpret_cast<void**>(&ov), n * 8, st)) != cudaSuccess) {
@@ -124,6 +118,36 @@ hm_status dedup_u64(const uint64_t* keys, const uint64_t* vals, uint64_t n, cuda
     if (ok) cudaFreeAsync(ok, st);
     set_error("from_array: out of device memory for the dedup set");
     return HM_ERR_OOM;
+  }
+  {  // the fast path: the build's radix passes and a shared-memory set per partition
+    uint64_t m = 0;
+    const hm_status ps = dedup_partitioned(keys, vals, n, st, ok, ov, &m);
+    if (ps == HM_OK) {
+      release();
+      *out_keys = ok;
+      *out_vals = ov;
+      *n_out = m;
+      return HM_OK;
+    }
+    if (ps != HM_ERR_TOO_LARGE) {
+      release();
+      cudaFreeAsync(ok, st);
+      cudaFreeAsync(ov, st);
+      return ps;
+    }
+  }
+  // heavy duplication (a partition overflowed): the global set, cached build
+  // scratch (hm_release_workspace frees it)
+  {
+    void* v = nullptr;
+    const hm_status s = dedup_workspace(&v, cap * sizeof(DedupSlot), st);
+    if (s != HM_OK) {
+      release();
+      cudaFreeAsync(ok, st);
+      cudaFreeAsync(ov, st);
+      return s;
+    }
+    set = reinterpret_cast<DedupSlot*>(v);
   }
   HM_CUDA_TRY(cudaMemsetAsync(set, 0, cap * sizeof(DedupSlot), st));
   HM_CUDA_TRY(cudaMemsetAsync(cur, 0, 8, st));
