@@ -42,6 +42,19 @@ constexpr int kBThreads = HM_KB_THREADS;
 #ifndef HM_KB_MINB
 #define HM_KB_MINB (1024 / HM_KB_THREADS)  // CTAs per SM the registers must allow
 #endif
+#ifndef HM_KB_THREADS_BYTES
+#define HM_KB_THREADS_BYTES 256  // byte keys: 32-byte records, BP = 2^10, 3 CTAs per SM
+#endif
+#ifndef HM_KB_MINB_BYTES
+#define HM_KB_MINB_BYTES 3
+#endif
+// k_bucket geometry per record type: threads per CTA, warps, CTAs per SM
+template <class E>
+struct KBCfg {
+  static constexpr int T = sizeof(E) == 16 ? HM_KB_THREADS : HM_KB_THREADS_BYTES;
+  static constexpr int W = T / 32;
+  static constexpr int MINB = sizeof(E) == 16 ? HM_KB_MINB : HM_KB_MINB_BYTES;
+};
 #ifndef HM_RETRY_LOGA
 #define HM_RETRY_LOGA 3  // at most 2^3 lanes (attempts) per queued bucket and round
 #endif
@@ -620,8 +633,8 @@ __device__ __forceinline__ void search_round0(const BuildParams& bp, const E* sk
                                               DevStatus* stt, const Same& same) {
   const uint32_t lane = threadIdx.x & 31, lt = (1u << lane) - 1u, warp = threadIdx.x >> 5;
   const uint32_t n4 = e4 - e8, n2 = L - e4;
-  const uint32_t w4 = min((n4 + 31) / 32, uint32_t(kBWarps));
-  for (uint32_t x = threadIdx.x; x < e8; x += kBThreads) queue[atomicAdd(qn, 1u)] = list[x];
+  const uint32_t w4 = min((n4 + 31) / 32, uint32_t(KBCfg<E>::W));
+  for (uint32_t x = threadIdx.x; x < e8; x += KBCfg<E>::T) queue[atomicAdd(qn, 1u)] = list[x];
   uint32_t lb = 0, tn = 0, lb2 = 0, tn2 = 0;
   if (warp < w4) {
     for (uint32_t i = warp * 32 + lane; i < n4; i += w4 * 32) {  // (more than one pass only if n4 > 512)
@@ -630,7 +643,7 @@ __device__ __forceinline__ void search_round0(const BuildParams& bp, const E* sk
       if (t) queue[atomicAdd(qn, 1u)] = lb | (t << 16);
     }
   } else {
-    const uint32_t lanes = (kBWarps - w4) * 32, e = threadIdx.x - w4 * 32;
+    const uint32_t lanes = (KBCfg<E>::W - w4) * 32, e = threadIdx.x - w4 * 32;
     uint32_t pbase = lanes;  // lanes >= pbase take two s = 2 buckets
     if (n2 > lanes) {
       if (n2 - lanes <= lanes) {
@@ -697,7 +710,7 @@ __device__ __forceinline__ void search_round(const BuildParams& bp, const E* skv
   const uint32_t lane = threadIdx.x & 31, lt = (1u << lane) - 1u;
   const uint32_t A = 1u << logA, W = L << logA;
   const uint32_t gmask = A == 32 ? 0xffffffffu : (((1u << A) - 1u) << (lane & ~(A - 1u)));
-  for (uint32_t w0 = (threadIdx.x - first) & ~31u; w0 < W; w0 += kBThreads - first) {
+  for (uint32_t w0 = (threadIdx.x - first) & ~31u; w0 < W; w0 += KBCfg<E>::T - first) {
     const uint32_t w = w0 + lane;
     bool ok = false, lead = false;
     uint32_t lb = 0, st0 = 0, s = 2, t = 0, tb = 0;
@@ -759,7 +772,7 @@ __device__ __forceinline__ void search_warp(const BuildParams& bp, const E* skv,
                                             const uint16_t* list, uint32_t L, const uint64_t* s_m2, uint64_t bbase,
                                             DevStatus* stt, const Same& same, uint32_t* bitsw) {
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (uint32_t idx = warp; idx < L; idx += kBWarps) {
+  for (uint32_t idx = warp; idx < L; idx += KBCfg<E>::W) {
     const uint32_t lb = list[idx], st0 = X.sstart[lb], s = X.ss[lb];
     const bool mine = lane < s;
     const uint32_t item = mine ? X.sidx[st0 + lane] : 0u;
@@ -834,10 +847,11 @@ __host__ __device__ __forceinline__ BucketSmem bucket_smem_layout(uint32_t cap, 
   return L;
 }
 
-// Block-wide exclusive scan of two u64 values at once (kBThreads threads).
+// Block-wide exclusive scan of two u64 values at once (NW warps).
+template <int NW>
 __device__ __forceinline__ void block_excl_scan2(unsigned long long& a, unsigned long long& b,
                                                  unsigned long long* ta, unsigned long long* tb,
-                                                 unsigned long long (*s_red)[kBWarps]) {
+                                                 unsigned long long (*s_red)[NW]) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   unsigned long long x = a, y = b;
 #pragma unroll
@@ -854,7 +868,7 @@ __device__ __forceinline__ void block_excl_scan2(unsigned long long& a, unsigned
   }
   __syncthreads();
   if (warp == 0) {
-    unsigned long long u = lane < kBWarps ? s_red[0][lane] : 0ull, v = lane < kBWarps ? s_red[1][lane] : 0ull;
+    unsigned long long u = lane < NW ? s_red[0][lane] : 0ull, v = lane < NW ? s_red[1][lane] : 0ull;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const unsigned long long p = __shfl_up_sync(0xffffffffu, u, o), q = __shfl_up_sync(0xffffffffu, v, o);
@@ -863,22 +877,22 @@ __device__ __forceinline__ void block_excl_scan2(unsigned long long& a, unsigned
         v += q;
       }
     }
-    if (lane < kBWarps) {
+    if (lane < NW) {
       s_red[0][lane] = u;
       s_red[1][lane] = v;
     }
   }
   __syncthreads();
   const unsigned long long ba = warp ? s_red[0][warp - 1] : 0ull, bb = warp ? s_red[1][warp - 1] : 0ull;
-  *ta = s_red[0][kBWarps - 1];
-  *tb = s_red[1][kBWarps - 1];
+  *ta = s_red[0][NW - 1];
+  *tb = s_red[1][NW - 1];
   a = ba + x - a;
   b = bb + y - b;
   __syncthreads();
 }
 
 template <class E, class Same>
-__global__ void __launch_bounds__(kBThreads, HM_KB_MINB)
+__global__ void __launch_bounds__(KBCfg<E>::T, KBCfg<E>::MINB)
     k_bucket(BuildParams bp, const E* __restrict__ pbuf, const unsigned int* __restrict__ pcount,
              unsigned long long* __restrict__ lbstate, uint64_t* __restrict__ dir, CDir* __restrict__ cdir,
              E* __restrict__ slots, DevStatus* __restrict__ stt, Same same) {
@@ -886,15 +900,15 @@ __global__ void __launch_bounds__(kBThreads, HM_KB_MINB)
   __shared__ uint64_t s_m2[33];
   __shared__ __align__(8) unsigned long long s_bar;
   __shared__ uint32_t s_p;
-  __shared__ unsigned long long s_red2[2][kBWarps];
+  __shared__ unsigned long long s_red2[2][KBCfg<E>::W];
   __shared__ unsigned long long s_base;
   __shared__ uint32_t s_c9, s_qn[2];
-  __shared__ uint32_t s_bitsw[kBWarps][32];
+  __shared__ uint32_t s_bitsw[KBCfg<E>::W][32];
 
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, lt = (1u << lane) - 1u;
   const uint32_t cap = bp.cap;
   const uint32_t BP = 1u << bp.log2_bp;
-  const uint32_t CH = (BP + kBThreads - 1) / kBThreads;  // buckets per thread in the scans
+  const uint32_t CH = (BP + KBCfg<E>::T - 1) / KBCfg<E>::T;  // buckets per thread in the scans
   const BucketSmem& SL = bp.sl;
   E* skv = reinterpret_cast<E*>(smem + SL.skv);
   uint16_t* lbk = reinterpret_cast<uint16_t*>(smem + SL.lbk);
@@ -916,7 +930,7 @@ __global__ void __launch_bounds__(kBThreads, HM_KB_MINB)
     s_qn[0] = s_qn[1] = 0;
   }
   if (tid < 33) s_m2[tid] = bp.m2[tid];  // (host-computed: no 64-bit division per CTA)
-  for (uint32_t j = tid; j < BP; j += kBThreads) soff[j] = 0;  // the histogram
+  for (uint32_t j = tid; j < BP; j += KBCfg<E>::T) soff[j] = 0;  // the histogram
   __syncthreads();
   const uint32_t p = s_p;
   HM_TMARK(0);
@@ -958,16 +972,16 @@ __global__ void __launch_bounds__(kBThreads, HM_KB_MINB)
 
   // ---- hist: g k of every item; its rank among
   // the items of its bucket comes from the shared-memory counter
-  for (uint32_t i0 = 0; i0 < cnt; i0 += 2 * kBThreads) {
+  for (uint32_t i0 = 0; i0 < cnt; i0 += 2 * KBCfg<E>::T) {
     uint64_t k2[2];
 #pragma unroll
     for (int u = 0; u < 2; u++) {
-      const uint32_t i = i0 + u * kBThreads + tid;
+      const uint32_t i = i0 + u * KBCfg<E>::T + tid;
       k2[u] = i < cnt ? skv[i].key : 0ull;
     }
 #pragma unroll
     for (int u = 0; u < 2; u++) {
-      const uint32_t i = i0 + u * kBThreads + tid;
+      const uint32_t i = i0 + u * KBCfg<E>::T + tid;
       if (i < cnt) {
         const uint64_t h1 = hash64(bp.l1.c1, k2[u]);
         uint32_t lb = uint32_t(level1_of_hash(bp.l1, h1) - bbase);
@@ -1001,7 +1015,7 @@ __global__ void __launch_bounds__(kBThreads, HM_KB_MINB)
       }
     }
     unsigned long long ta, tb;
-    block_excl_scan2(a, b, &ta, &tb, s_red2);
+    block_excl_scan2<KBCfg<E>::W>(a, b, &ta, &tb, s_red2);
     S_p = ta >> 32;
     const uint32_t T4 = uint32_t((tb >> 21) & 0x1FFFFF), T8 = uint32_t(tb >> 42);
     uint32_t pos = uint32_t(a), sq = uint32_t(a >> 32);
@@ -1038,7 +1052,7 @@ __global__ void __launch_bounds__(kBThreads, HM_KB_MINB)
   const uint32_t Le8 = uint32_t(tcls >> 42), Le4 = Le8 + uint32_t((tcls >> 21) & 0x1FFFFF),
                  Lall = Le4 + uint32_t(tcls & 0x1FFFFF);
   // groupby: grouped position of every item
-  for (uint32_t i = tid; i < cnt; i += kBThreads) sidx[sstart[lbk[i]] + rk[i]] = uint16_t(i);
+  for (uint32_t i = tid; i < cnt; i += KBCfg<E>::T) sidx[sstart[lbk[i]] + rk[i]] = uint16_t(i);
   __syncthreads();
   HM_TMARK(3);
 
@@ -1099,7 +1113,7 @@ __global__ void __launch_bounds__(kBThreads, HM_KB_MINB)
     if (L == 0) break;
     if (tid == 0) s_qn[(r + 1) & 1] = 0;
     __syncthreads();
-    const uint32_t first = r == 0 ? 32u : 0u, lanes = kBThreads - first;
+    const uint32_t first = r == 0 ? 32u : 0u, lanes = KBCfg<E>::T - first;
     uint32_t logA = 0;
     while (logA < HM_RETRY_LOGA && (L << (logA + 1)) <= lanes) logA++;
     if (tid < first) look_back();
@@ -1133,11 +1147,11 @@ __global__ void __launch_bounds__(kBThreads, HM_KB_MINB)
   if (staged) {
     E* out = slots + base;
     const uint32_t Sp = uint32_t(S_p);
-    for (uint32_t x0 = 0; x0 < Sp; x0 += 4 * kBThreads) {
+    for (uint32_t x0 = 0; x0 < Sp; x0 += 4 * KBCfg<E>::T) {
       E e[4];
 #pragma unroll
       for (int j = 0; j < 4; j++) {
-        const uint32_t x = x0 + j * kBThreads + tid;
+        const uint32_t x = x0 + j * KBCfg<E>::T + tid;
         if (x < Sp) {
           const uint32_t v = src[x], it = v & 0x7FFFu;
           e[j] = skv[it < cnt ? it : 0u];  // (an unmapped slot only in a pass that is redone)
@@ -1146,14 +1160,14 @@ __global__ void __launch_bounds__(kBThreads, HM_KB_MINB)
       }
 #pragma unroll
       for (int j = 0; j < 4; j++) {
-        const uint32_t x = x0 + j * kBThreads + tid;
+        const uint32_t x = x0 + j * KBCfg<E>::T + tid;
         if (x < Sp) out[x] = e[j];
       }
     }
   } else {
     // a partition with more slots than the staging map (adversarial level-1
     // distribution within the global bound): direct writes, thread per bucket
-    for (uint32_t lb = tid; lb < nbp; lb += kBThreads) {
+    for (uint32_t lb = tid; lb < nbp; lb += KBCfg<E>::T) {
       const uint32_t s = ss[lb];
       if (s == 0 || s > 32) continue;
       E* out = slots + base + soff[lb];
@@ -1183,7 +1197,7 @@ __global__ void __launch_bounds__(kBThreads, HM_KB_MINB)
   HM_TMARK(6);
   // directory (coalesced) and compact directory record per 32 buckets (one per
   // warp iteration)
-  for (uint32_t cb = 0; cb < nbp; cb += kBThreads) {
+  for (uint32_t cb = 0; cb < nbp; cb += KBCfg<E>::T) {
     const uint32_t lb = cb + tid;
     uint32_t s = 0, t = 0;
     uint64_t so = 0;
@@ -1252,7 +1266,7 @@ struct Plan {
 };
 
 // Partition geometry: the largest BP = 2^lg (at most 2^12: 64 groups of 64
-// buckets) whose k_bucket shared memory lets 1024 / kBThreads CTAs share an SM
+// buckets) whose k_bucket shared memory lets KBCfg<E>::MINB CTAs share an SM
 // (smem_two: the register-limited occupancy at 64 registers per thread); with
 // at least 4 partitions per SM for small tables.  An
 // explicit log2_req only has to fit one CTA per SM (smem_one).
@@ -1375,10 +1389,15 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
   HM_CUDA_TRY(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   int smem_sm = 0;
   HM_CUDA_TRY(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
-  const size_t static_smem_B = 4096;  // upper bound for k_bucket static shared memory (~2 KB)
+  size_t static_smem_B = 4096;  // k_bucket's static shared memory (queried below; ~1.5-2.6 KB)
+  {
+    cudaFuncAttributes fa{};
+    if (cudaFuncGetAttributes(&fa, k_bucket<E, Same>) == cudaSuccess) static_smem_B = fa.sharedSizeBytes;
+    else cudaGetLastError();
+  }
   const uint32_t knob_flags = log2_req >> 16;
   log2_req &= 0xFFFFu;
-  const Plan pl = make_plan(n_in, nb, log2_req, uint32_t(sizeof(E)), size_t(smem_sm) / HM_KB_MINB - 1024 - static_smem_B,
+  const Plan pl = make_plan(n_in, nb, log2_req, uint32_t(sizeof(E)), size_t(smem_sm) / KBCfg<E>::MINB - 1024 - static_smem_B,
                             size_t(smem_optin) - static_smem_B);
   if (pl.smemB + static_smem_B > size_t(smem_optin)) {
     set_error("build plan does not fit in shared memory");
@@ -1508,7 +1527,7 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
       run_a = false;
       {
         LaunchScope ls_("k_bucket", st);
-        kB<<<pl.np, kBThreads, pl.smemB, st>>>(bp, pbuf, pcount, lbstate, dir, cdir, slots, dstat, same);
+        kB<<<pl.np, KBCfg<E>::T, pl.smemB, st>>>(bp, pbuf, pcount, lbstate, dir, cdir, slots, dstat, same);
       }
       HM_CUDA_TRY(cudaGetLastError());
       HM_CUDA_TRY(cudaMemcpyAsync(&hs, dstat, sizeof(hs), cudaMemcpyDeviceToHost, st));
