@@ -177,9 +177,13 @@ const char* hm_version(void);
 uint64_t hm_kernel_launches(void);
 
 /* hm_release_workspace — free the build scratch this library caches between
- * builds (per device and stream: partition buffers, fingerprints; about
- * 40 B per key for u64 builds, 48 B per key for byte-key builds) on the
- * current device.  Maps are not affected.  Synchronises the device. */
+ * builds (per device and stream: partition buffers and their bucket codes,
+ * fingerprints, the from_array dedup set; about 44 B per key for u64 builds,
+ * 52 B per key for byte-key builds) on the current device, and trim the
+ * device's default stream-ordered memory pool, whose release threshold the
+ * library raises on first use (freed table memory otherwise goes back to the
+ * driver at every synchronisation and is re-mapped by the next build).  Maps
+ * are not affected.  Synchronises the device. */
 hm_status hm_release_workspace(void);
 
 /* Per-kernel device timing (diagnostics, used by bench.py for the roofline).

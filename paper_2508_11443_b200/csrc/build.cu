@@ -204,7 +204,7 @@ extern "C" int hm_debug_phase_times(unsigned long long* host, unsigned long long
 // ------------------------------------------------------------------ K_A
 template <class Src, class E, int KPT, bool kSmemHist>
 __global__ void __launch_bounds__(kAThreads) k_partition(Src src, BuildParams bp, E* __restrict__ pbuf,
-                                                         unsigned int* __restrict__ pcount,
+                                                         uint16_t* __restrict__ plb, unsigned int* __restrict__ pcount,
                                                          DevStatus* __restrict__ stt) {
   constexpr uint32_t kNone = 0x7FFFFFFFu, kLead = 0x80000000u;
   extern __shared__ unsigned int s_hist[];
@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(kAThreads) k_partition(Src src, BuildParams bp
   bool ovf = false, bad = false;
   for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     E e[KPT];
-    uint32_t pp[KPT], rk[KPT];
+    uint32_t pp[KPT], rk[KPT], lc[KPT];
     const uint64_t base = tile * T;
 #pragma unroll
     for (int j = 0; j < KPT; j++) {
@@ -233,12 +233,14 @@ __global__ void __launch_bounds__(kAThreads) k_partition(Src src, BuildParams bp
     for (int j = 0; j < KPT; j++) {
       const uint64_t idx = base + uint64_t(j) * kAThreads + tid;
       if (idx < bp.n_in) {
-        const uint64_t lb = level1_bucket(bp.l1, e[j].key) - bp.b_lo;
+        const uint64_t h1 = hash64(bp.l1.c1, e[j].key);
+        const uint64_t lb = level1_of_hash(bp.l1, h1) - bp.b_lo;
         if (lb >= bp.nb) {
           bad = true;
           continue;
         }
         pp[j] = uint32_t(lb >> bp.log2_bp);
+        lc[j] = uint32_t(lb & ((1u << bp.log2_bp) - 1)) | (tag4_of_hash(h1) << 12);
         rk[j] = kSmemHist ? atomicAdd(&s_hist[pp[j]], 1u) : atomicAdd(&pcount[pp[j]], 1u);
       }
     }
@@ -269,8 +271,12 @@ __global__ void __launch_bounds__(kAThreads) k_partition(Src src, BuildParams bp
     for (int j = 0; j < KPT; j++) {
       if (pp[j] == kNone) continue;
       const uint32_t pos = (kSmemHist ? s_hist[pp[j]] : 0u) + rk[j];
-      if (pos < bp.cap) pbuf[size_t(pp[j]) * bp.cap + pos] = e[j];
-      else ovf = true;
+      if (pos < bp.cap) {
+        pbuf[size_t(pp[j]) * bp.cap + pos] = e[j];
+        plb[size_t(pp[j]) * bp.cap + pos] = uint16_t(lc[j]);
+      } else {
+        ovf = true;
+      }
     }
     if (kSmemHist) {
       __syncthreads();
@@ -322,6 +328,7 @@ struct SplitArgs {
   uint32_t dcap;
   uint32_t nreg;      // destination regions
   uint32_t nreg_src;  // pass 2: source (coarse) regions
+  uint16_t* dst_lb;   // pass 2: the record's local bucket | tag4 << 12 for k_bucket (nullptr: none)
 };
 
 template <class Src, class E, int PASS, int BITS>
@@ -331,6 +338,7 @@ __global__ void __launch_bounds__(kSThreads, HM_SPLIT_MINB) k_split(Src src, Bui
   constexpr int kSDigits = 1 << BITS, kSBits = BITS, kSPT = split_pt<E>(), kSTile = split_tile<E>();
   E* stage = reinterpret_cast<E*>(smem);
   uint16_t* sdig = reinterpret_cast<uint16_t*>(smem + size_t(kSTile) * sizeof(E));
+  uint16_t* slbc = sdig + kSTile;  // pass 2: local bucket | tag4 << 12 of the staged record
   __shared__ uint32_t s_cnt[kSDigits], s_dstart[kSDigits], s_gbase[kSDigits];
   __shared__ unsigned long long s_red[kSWarps];
 
@@ -353,7 +361,7 @@ __global__ void __launch_bounds__(kSThreads, HM_SPLIT_MINB) k_split(Src src, Bui
   __syncthreads();
   if (nvalid == 0) return;
   E e[kSPT];
-  uint32_t dg[kSPT], rk[kSPT];
+  uint32_t dg[kSPT], rk[kSPT], lc[kSPT];
   bool bad = false;
 #pragma unroll
   for (int j = 0; j < kSPT; j++) {
@@ -365,10 +373,12 @@ __global__ void __launch_bounds__(kSThreads, HM_SPLIT_MINB) k_split(Src src, Bui
     const uint32_t i = j * kSThreads + tid;
     dg[j] = 0;
     if (i < nvalid) {
-      const uint64_t lb = level1_bucket(bp.l1, e[j].key) - bp.b_lo;
+      const uint64_t h1 = hash64(bp.l1.c1, e[j].key);
+      const uint64_t lb = level1_of_hash(bp.l1, h1) - bp.b_lo;
       if (lb >= bp.nb) bad = true;
       const uint32_t p = uint32_t(lb >> bp.log2_bp);
       dg[j] = PASS == 1 ? ((p >> kSBits) & (kSDigits - 1)) : (p & (kSDigits - 1));
+      lc[j] = uint32_t(lb & ((1u << bp.log2_bp) - 1)) | (tag4_of_hash(h1) << 12);
     }
   }
   // rank of every element among the tile's elements with its digit: one
@@ -399,6 +409,7 @@ __global__ void __launch_bounds__(kSThreads, HM_SPLIT_MINB) k_split(Src src, Bui
       const uint32_t pos = s_dstart[dg[j]] + rk[j];
       stage[pos] = e[j];
       sdig[pos] = uint16_t(dg[j]);
+      if (PASS == 2) slbc[pos] = uint16_t(lc[j]);
     }
   }
   __syncthreads();
@@ -409,8 +420,12 @@ __global__ void __launch_bounds__(kSThreads, HM_SPLIT_MINB) k_split(Src src, Bui
     const uint32_t d = sdig[i];
     const uint32_t reg = PASS == 1 ? d : coarse * kSDigits + d;
     const uint32_t pos = s_gbase[d] + (i - s_dstart[d]);
-    if (reg < a.nreg && pos < a.dcap) dst[size_t(reg) * a.dcap + pos] = stage[i];
-    else ovf = true;
+    if (reg < a.nreg && pos < a.dcap) {
+      dst[size_t(reg) * a.dcap + pos] = stage[i];
+      if (PASS == 2 && a.dst_lb) a.dst_lb[size_t(reg) * a.dcap + pos] = slbc[i];
+    } else {
+      ovf = true;
+    }
   }
   if (ovf) atomicOr(&stt->part_overflow, 1u);
   if (bad) atomicOr(&stt->pad, 1u);
@@ -893,7 +908,8 @@ __device__ __forceinline__ void block_excl_scan2(unsigned long long& a, unsigned
 
 template <class E, class Same>
 __global__ void __launch_bounds__(KBCfg<E>::T, KBCfg<E>::MINB)
-    k_bucket(BuildParams bp, const E* __restrict__ pbuf, const unsigned int* __restrict__ pcount,
+    k_bucket(BuildParams bp, const E* __restrict__ pbuf, const uint16_t* __restrict__ plb,
+             const unsigned int* __restrict__ pcount,
              unsigned long long* __restrict__ lbstate, uint64_t* __restrict__ dir, CDir* __restrict__ cdir,
              E* __restrict__ slots, DevStatus* __restrict__ stt, Same same) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -944,13 +960,20 @@ __global__ void __launch_bounds__(KBCfg<E>::T, KBCfg<E>::MINB)
   // ---- load: one bulk copy (TMA) of the partition's elements into shared memory
   if (tid == 0) {
     const uint32_t bytes = cnt * uint32_t(sizeof(E));
+    const uint32_t lbytes = ((cnt + 7) & ~7u) * 2;  // (16-byte multiple; cap is a multiple of 32)
     if (bytes) {
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&s_bar)), "r"(bytes)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&s_bar)),
+                   "r"(bytes + lbytes)
                    : "memory");
       asm volatile(
           "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
               smem_u32(skv)),
           "l"(pbuf + size_t(p) * cap), "r"(bytes), "r"(smem_u32(&s_bar))
+          : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_u32(lbk)),
+          "l"(plb + size_t(p) * cap), "r"(lbytes), "r"(smem_u32(&s_bar))
           : "memory");
     } else {
       asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&s_bar)) : "memory");
@@ -970,30 +993,20 @@ __global__ void __launch_bounds__(KBCfg<E>::T, KBCfg<E>::MINB)
   __syncthreads();
   HM_TMARK(1);
 
-  // ---- hist: g k of every item; its rank among
-  // the items of its bucket comes from the shared-memory counter
-  for (uint32_t i0 = 0; i0 < cnt; i0 += 2 * KBCfg<E>::T) {
-    uint64_t k2[2];
-#pragma unroll
-    for (int u = 0; u < 2; u++) {
-      const uint32_t i = i0 + u * KBCfg<E>::T + tid;
-      k2[u] = i < cnt ? skv[i].key : 0ull;
+  // ---- hist: the local bucket of g k and the
+  // key's tag came with the record from the partition pass (k_split pass 2 /
+  // k_partition hashed it already); the rank among the items of its bucket
+  // comes from the shared-memory counter
+  for (uint32_t i = tid; i < cnt; i += KBCfg<E>::T) {
+    const uint32_t code = lbk[i];
+    uint32_t lb = code & 0xFFFu;
+    if (lb >= nbp) {  // cannot happen for a well-routed partition; never index out of range
+      atomicOr(&stt->pad, 1u);
+      lb = 0;
     }
-#pragma unroll
-    for (int u = 0; u < 2; u++) {
-      const uint32_t i = i0 + u * KBCfg<E>::T + tid;
-      if (i < cnt) {
-        const uint64_t h1 = hash64(bp.l1.c1, k2[u]);
-        uint32_t lb = uint32_t(level1_of_hash(bp.l1, h1) - bbase);
-        if (lb >= nbp) {  // cannot happen for a well-routed partition; never index out of range
-          atomicOr(&stt->pad, 1u);
-          lb = 0;
-        }
-        lbk[i] = uint16_t(lb);
-        rk[i] = uint16_t(atomicAdd(&soff[lb], 1u));
-        s_t[lb] = uint8_t(tag4_of_hash(h1));  // kept for singletons only (the scan resets the rest)
-      }
-    }
+    lbk[i] = uint16_t(lb);
+    rk[i] = uint16_t(atomicAdd(&soff[lb], 1u));
+    s_t[lb] = uint8_t(code >> 12);  // kept for singletons only (the scan resets the rest)
   }
   __syncthreads();
   HM_TMARK(2);
@@ -1316,7 +1329,7 @@ static hm_status dmalloc(T** p, size_t bytes, cudaStream_t st) {
 // maps' own arrays), so they stay allocated until hm_release_workspace().
 // Reuse is safe because everything that touches a stream's workspace is
 // ordered on that stream.
-enum WsRole { WS_FP, WS_BAD, WS_PBUF, WS_PCOUNT, WS_LBSTATE, WS_DSTAT, WS_CBUF, WS_CCOUNT, WS_DEDUP, WS_NROLES };
+enum WsRole { WS_FP, WS_BAD, WS_PBUF, WS_PLB, WS_PCOUNT, WS_LBSTATE, WS_DSTAT, WS_CBUF, WS_CCOUNT, WS_DEDUP, WS_NROLES };
 struct Workspace {
   void* p[WS_NROLES] = {};
   size_t bytes[WS_NROLES] = {};
@@ -1373,6 +1386,9 @@ hm_status release_workspace() {
     }
   }
   HM_CUDA_TRY(cudaDeviceSynchronize());
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+  cudaGetLastError();
   return HM_OK;
 }
 
@@ -1413,6 +1429,8 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
   DevStatus* dstat = nullptr;
   hm_status s;
   if ((s = sc.alloc(WS_PBUF, &pbuf, size_t(pl.np) * pl.cap * sizeof(E))) != HM_OK) return s;
+  uint16_t* plb = nullptr;
+  if ((s = sc.alloc(WS_PLB, &plb, size_t(pl.np) * pl.cap * 2)) != HM_OK) return s;
   if ((s = sc.alloc(WS_PCOUNT, &pcount, size_t(pl.np) * 4)) != HM_OK) return s;
   if ((s = sc.alloc(WS_LBSTATE, &lbstate, size_t(pl.np) * 8)) != HM_OK) return s;
   if ((s = sc.alloc(WS_DSTAT, &dstat, sizeof(DevStatus))) != HM_OK) return s;
@@ -1465,7 +1483,7 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
   E* cbuf = nullptr;
   unsigned int* ccount = nullptr;
   constexpr int kSTile = split_tile<E>();
-  const size_t smemS = size_t(kSTile) * (sizeof(E) + 2);
+  const size_t smemS = size_t(kSTile) * (sizeof(E) + 4);
   auto kS1 = sbits == 8 ? k_split<Src, E, 1, 8> : k_split<Src, E, 1, 9>;
   auto kS2 = sbits == 8 ? k_split<Src, E, 2, 8> : k_split<Src, E, 2, 9>;
   if (two_pass) {
@@ -1510,7 +1528,7 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
           kS1<<<unsigned((n_in + kSTile - 1) / kSTile), kSThreads, smemS, st>>>(src, bp, a1, dstat);
         }
         HM_CUDA_TRY(cudaGetLastError());
-        const SplitArgs a2{cbuf, ccount, ccap, tpc, pbuf, pcount, pl.cap, pl.np, ncoarse};
+        const SplitArgs a2{cbuf, ccount, ccap, tpc, pbuf, pcount, pl.cap, pl.np, ncoarse, plb};
         {
           LaunchScope ls_("k_split2", st);
           kS2<<<ncoarse * tpc, kSThreads, smemS, st>>>(src, bp, a2, dstat);
@@ -1519,15 +1537,15 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
       } else if (run_a && ntiles > 0) {
         {
           LaunchScope ls_("k_partition", st);
-          if (smemHist) kA_s<<<gridA, kAThreads, smemA, st>>>(src, bp, pbuf, pcount, dstat);
-          else kA_g<<<gridA, kAThreads, 0, st>>>(src, bp, pbuf, pcount, dstat);
+          if (smemHist) kA_s<<<gridA, kAThreads, smemA, st>>>(src, bp, pbuf, plb, pcount, dstat);
+          else kA_g<<<gridA, kAThreads, 0, st>>>(src, bp, pbuf, plb, pcount, dstat);
         }
         HM_CUDA_TRY(cudaGetLastError());
       }
       run_a = false;
       {
         LaunchScope ls_("k_bucket", st);
-        kB<<<pl.np, KBCfg<E>::T, pl.smemB, st>>>(bp, pbuf, pcount, lbstate, dir, cdir, slots, dstat, same);
+        kB<<<pl.np, KBCfg<E>::T, pl.smemB, st>>>(bp, pbuf, plb, pcount, lbstate, dir, cdir, slots, dstat, same);
       }
       HM_CUDA_TRY(cudaGetLastError());
       HM_CUDA_TRY(cudaMemcpyAsync(&hs, dstat, sizeof(hs), cudaMemcpyDeviceToHost, st));
@@ -1862,7 +1880,7 @@ hm_status dedup_partitioned(const uint64_t* keys, const uint64_t* vals, uint64_t
   HM_CUDA_TRY(cudaMemsetAsync(pcount, 0, size_t(np) * 4, st));
   HM_CUDA_TRY(cudaMemsetAsync(ccount, 0, size_t(ncoarse) * 4, st));
   HM_CUDA_TRY(cudaMemsetAsync(dstat, 0, sizeof(DevStatus), st));
-  const size_t smemS = size_t(kSTile) * (sizeof(KV32) + 2);
+  const size_t smemS = size_t(kSTile) * (sizeof(KV32) + 4);
   auto kS1 = sbits == 8 ? k_split<SrcU64Idx, KV32, 1, 8> : k_split<SrcU64Idx, KV32, 1, 9>;
   auto kS2 = sbits == 8 ? k_split<SrcU64Idx, KV32, 2, 8> : k_split<SrcU64Idx, KV32, 2, 9>;
   HM_CUDA_TRY(cudaFuncSetAttribute(kS1, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smemS)));

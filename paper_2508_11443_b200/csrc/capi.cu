@@ -118,6 +118,20 @@ static hm_status check_device() {
     set_error("libhm is built for sm_100a (B200) only");
     return HM_ERR_NO_DEVICE;
   }
+  // Keep freed stream-ordered memory in the device's pool instead of handing it
+  // back to the driver at every synchronisation (the default threshold, 0):
+  // re-mapping a table's gigabytes costs ~10 ms per build otherwise.
+  // hm_release_workspace() trims the pool.
+  static bool configured[64] = {};
+  if (dev >= 0 && dev < 64 && !configured[dev]) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+    configured[dev] = true;
+  }
   return HM_OK;
 }
 
