@@ -216,9 +216,7 @@ def run_ours(args):
             s_over_n = dm.S_local / n
             if ev_b is not None:
                 ev_b.record()
-            v, f = dist.lookup_dist(dm, q)
-            ov.copy_(v)
-            of.copy_(f)
+            dist.lookup_dist(dm, q, ov, of)
             dist.free_dist(dm)
 
     for _ in range(args.warmup):

@@ -90,13 +90,18 @@ class DistMap:
     group: object = None
 
 
-def _all_to_all_v(send, in_counts, group, device):
-    """Variable all-to-all of a 1-D tensor grouped by destination rank."""
-    world = len(in_counts)
+def _exchange_counts(in_counts, group, device):
+    """How many elements every rank sends here (all_to_all of the split sizes)."""
     cin = torch.tensor(in_counts, dtype=torch.int64, device=device)
     cout = torch.empty_like(cin)
     tdist.all_to_all_single(cout, cin, group=group)
-    out_counts = [int(x) for x in cout.tolist()]
+    return [int(x) for x in cout.tolist()]
+
+
+def _all_to_all_v(send, in_counts, group, device, out_counts=None):
+    """Variable all-to-all of a 1-D tensor grouped by destination rank."""
+    if out_counts is None:
+        out_counts = _exchange_counts(in_counts, group, device)
     recv = torch.empty(sum(out_counts), dtype=send.dtype, device=send.device)
     tdist.all_to_all_single(recv, send, out_counts, list(in_counts), group=group)
     return recv, out_counts
@@ -117,8 +122,8 @@ def build_dist(keys, vals, seed: int = 0, ops=None, group=None) -> DistMap:
     for t1 in range(16):
         sk, sv, counts = ops.route(keys, vals, n, seed, t1, world)
         in_counts = [int(x) for x in counts.tolist()]
-        rk, _ = _all_to_all_v(sk, in_counts, group, dev)
-        rv, _ = _all_to_all_v(sv, in_counts, group, dev)
+        rk, out_counts = _all_to_all_v(sk, in_counts, group, dev)
+        rv, _ = _all_to_all_v(sv, in_counts, group, dev, out_counts)  # (same splits)
         shard, S_local, code = ops.build_shard(rk, rv, n, lo, hi, t1, seed)
         # agree on the outcome: the space bound is global (R7), errors are global
         red = torch.tensor([S_local, code], dtype=torch.int64, device=dev)
@@ -139,8 +144,9 @@ def build_dist(keys, vals, seed: int = 0, ops=None, group=None) -> DistMap:
     return DistMap(shard, n, lo, hi, t1, S_local, base, S_total, world, rank, ops, group)
 
 
-def lookup_dist(dm: DistMap, q):
-    """Collective lookup: every rank passes its own queries, gets its own answers."""
+def lookup_dist(dm: DistMap, q, out_vals=None, out_found=None):
+    """Collective lookup: every rank passes its own queries, gets its own answers
+    (written into out_vals / out_found when given)."""
     ops, group, world = dm.ops, dm.group, dm.world
     dev = q.device
     sq, perm, counts = ops.route_queries(dm.shard, q, world)
@@ -152,8 +158,8 @@ def lookup_dist(dm: DistMap, q):
     tdist.all_to_all_single(back_v, v, in_counts, out_counts, group=group)
     back_f = torch.empty(sum(in_counts), dtype=f.dtype, device=dev)
     tdist.all_to_all_single(back_f, f, in_counts, out_counts, group=group)
-    out_v = torch.empty_like(q)
-    out_f = torch.empty(q.numel(), dtype=torch.uint8, device=dev)
+    out_v = torch.empty_like(q) if out_vals is None else out_vals
+    out_f = torch.empty(q.numel(), dtype=torch.uint8, device=dev) if out_found is None else out_found
     ops.unroute(back_v, back_f, perm, out_v, out_f)
     return out_v, out_f
 
