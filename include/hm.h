@@ -75,11 +75,13 @@ typedef struct {
  * leaves the rest to the lane-parallel rounds. */
 #define HM_FLAG_DIRECT_SLOTS 2u
 #define HM_FLAG_NO_ROUND0_ILP 4u
-/* from_array, hm_build_u64 only:
- * the keys may repeat; the first occurrence (lowest input index) of every key
- * keeps its value, and the map is the one the default build (from_array_nodup)
- * makes from the distinct keys — hm_info's n is their number.  Byte keys:
- * HM_ERR_INVALID_ARG in this version. */
+/* from_array: the keys may repeat;
+ * the first occurrence (lowest input index) of every key keeps its value, and
+ * the map is the one the default build (from_array_nodup) makes from the
+ * distinct keys — hm_info's n is their number; byte keys are compared by
+ * content and the distinct ones are packed in input order into the map's
+ * context.  Byte keys repeated so heavily that a dedup partition overflows:
+ * HM_ERR_TOO_LARGE in this version. */
 #define HM_FLAG_FROM_ARRAY 8u
 
 /* Table header, 56 bytes, little-endian (DESIGN.md §4 "Table layout"). */

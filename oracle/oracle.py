@@ -289,6 +289,30 @@ def build_bytes(ctx, offsets, vals, seed: int = 0) -> Table:
     return _wrap(h.value, 1)
 
 
+def from_array_bytes(ctx, offsets, vals, seed: int = 0) -> Table:
+    """from_array for byte-string keys: the first
+    occurrence of every key (by content) keeps its value; the distinct keys,
+    packed in input order into a new context, go to from_array_nodup.  Plain
+    definition: a Python dict over the key bytes."""
+    ctx = np.ascontiguousarray(np.asarray(ctx, dtype=np.uint8))
+    offsets, vals = _u64(offsets), _u64(vals)
+    n = len(offsets) - 1
+    if n <= 0:
+        raise OracleError(2)
+    seen, keep = set(), []
+    for i in range(n):
+        k = ctx[int(offsets[i]):int(offsets[i + 1])].tobytes()
+        if k not in seen:
+            seen.add(k)
+            keep.append(i)
+    parts = [ctx[int(offsets[i]):int(offsets[i + 1])] for i in keep]
+    lens = np.array([len(x) for x in parts], dtype=np.uint64)
+    noffs = np.zeros(len(keep) + 1, np.uint64)
+    np.cumsum(lens, out=noffs[1:])
+    nctx = np.concatenate(parts) if int(noffs[-1]) else np.zeros(0, np.uint8)
+    return build_bytes(nctx, noffs, vals[np.array(keep, dtype=np.int64)], seed)
+
+
 def lookup_bytes(t: Table, qctx, qoffsets):
     qctx = np.ascontiguousarray(np.asarray(qctx, dtype=np.uint8))
     qoffsets = _u64(qoffsets)

@@ -102,6 +102,23 @@ struct SrcU64Idx {
     return e;
   }
 };
+// from_array of byte keys: {fingerprint, value, ctx_off, len, input index}.
+struct SrcBytesIdx {
+  const uint64_t* fp;
+  const uint64_t* vals;
+  const uint64_t* offs;
+  uint64_t off0;
+  __device__ __forceinline__ KV32 load(uint64_t i) const {
+    KV32 e;
+    const uint64_t o = __ldg(offs + i), o1 = __ldg(offs + i + 1);
+    e.key = __ldg(fp + i);
+    e.value = __ldg(vals + i);
+    e.ctx_off = o - off0;
+    e.len = uint32_t(o1 - o);
+    e.reserved = uint32_t(i);
+    return e;
+  }
+};
 // Equal hashed keys: the same key (duplicate) or a fingerprint collision?
 struct SameU64 {
   __device__ __forceinline__ bool same(const KV16&, const KV16&) const { return true; }
@@ -1837,6 +1854,119 @@ __global__ void __launch_bounds__(kDThreads, 2) k_dedup_part(const KV32* __restr
       okeys[s_base + rk[j]] = skv[i].key;
       ovals[s_base + rk[j]] = skv[i].value;
     }
+}
+
+// The same for byte keys: the set is keyed by the fingerprint and confirmed
+// by content (equal fingerprints with different bytes are different keys and
+// take different slots); a first occurrence sets keep[input index] = 1.
+__global__ void __launch_bounds__(kDThreads, 2) k_dedup_part_bytes(const KV32* __restrict__ pbuf,
+                                                                   const unsigned int* __restrict__ pcount, uint32_t cap,
+                                                                   const uint8_t* __restrict__ bytes, uint64_t off0,
+                                                                   uint8_t* __restrict__ keep,
+                                                                   DevStatus* __restrict__ stt) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  KV32* skv = reinterpret_cast<KV32*>(smem);
+  uint32_t* tab = reinterpret_cast<uint32_t*>(smem + size_t(cap) * sizeof(KV32));
+  uint32_t* tmin = tab + kDTab;
+  uint16_t* slotof = reinterpret_cast<uint16_t*>(tmin + kDTab);
+  const uint32_t p = blockIdx.x, tid = threadIdx.x;
+  const uint32_t cnt_raw = pcount[p];
+  if (cnt_raw > cap) {
+    if (tid == 0) atomicOr(&stt->part_overflow, 1u);
+    return;
+  }
+  const uint32_t cnt = cnt_raw;
+  for (uint32_t i = tid; i < kDTab; i += kDThreads) {
+    tab[i] = ~0u;
+    tmin[i] = ~0u;
+  }
+  for (uint32_t i = tid; i < cnt; i += kDThreads) skv[i] = pbuf[size_t(p) * cap + i];
+  __syncthreads();
+  for (uint32_t i = tid; i < cnt; i += kDThreads) {
+    const KV32 e = skv[i];
+    uint32_t h = uint32_t(mix64(e.key ^ 0x5851F42D4C957F2Dull)) & (kDTab - 1);
+    while (true) {
+      const uint32_t cur = atomicCAS(&tab[h], ~0u, i);
+      if (cur == ~0u) break;
+      const KV32 c = skv[cur];
+      if (c.key == e.key && c.len == e.len &&
+          bytes_equal(bytes + off0 + c.ctx_off, bytes + off0 + e.ctx_off, e.len))
+        break;
+      h = (h + 1) & (kDTab - 1);
+    }
+    atomicMin(&tmin[h], e.reserved);
+    slotof[i] = uint16_t(h);
+  }
+  __syncthreads();
+  for (uint32_t i = tid; i < cnt; i += kDThreads)
+    if (tmin[slotof[i]] == skv[i].reserved) keep[skv[i].reserved] = 1;
+}
+
+hm_status dedup_partitioned_bytes(const uint8_t* bytes, const uint64_t* offs, const uint64_t* fp,
+                                  const uint64_t* vals, uint64_t n, uint64_t off0, cudaStream_t st, uint8_t* keep) {
+  const int sms = num_sms();
+  uint32_t lg = 10;  // (32-byte records: partitions of ~1024 records, 2 CTAs per SM)
+  while (lg > 6 && (n >> lg) < uint64_t(4 * sms)) lg--;
+  const double m = double(uint64_t(1) << lg);
+  const uint32_t cap = uint32_t(std::ceil((m + 8.0 * std::sqrt(m) + 64.0) / 32.0) * 32.0);
+  const uint32_t np = uint32_t((n + (uint64_t(1) << lg) - 1) >> lg);
+  if (np > (1u << 18) || cap * 4 > kDTab * 3) return HM_ERR_TOO_LARGE;
+  BuildParams bp{};
+  bp.smix = seed_mix(0x46524F4D41525241ull);
+  bp.l1 = make_l1(bp.smix, 0, n);
+  bp.nb = n;
+  bp.n_in = n;
+  bp.log2_bp = lg;
+  bp.np = np;
+  bp.cap = cap;
+  Scratch sc{st};
+  KV32 *pbuf = nullptr, *cbuf = nullptr;
+  unsigned int *pcount = nullptr, *ccount = nullptr;
+  DevStatus* dstat = nullptr;
+  hm_status s;
+  const int sbits = np <= 65536 ? 8 : 9;
+  const uint32_t sdig = 1u << sbits, ncoarse = (np + sdig - 1) / sdig;
+  const double mc = double(sdig) * m;
+  const uint32_t ccap = uint32_t(mc + 8.0 * std::sqrt(mc + 1.0) + 1024.0);
+  constexpr int kSTile = split_tile<KV32>();
+  const uint32_t tpc = (ccap + kSTile - 1) / kSTile;
+  if ((s = sc.alloc(WS_PBUF, &pbuf, size_t(np) * cap * sizeof(KV32))) != HM_OK) return s;
+  if ((s = sc.alloc(WS_PCOUNT, &pcount, size_t(np) * 4)) != HM_OK) return s;
+  if ((s = sc.alloc(WS_CBUF, &cbuf, size_t(ncoarse) * ccap * sizeof(KV32))) != HM_OK) return s;
+  if ((s = sc.alloc(WS_CCOUNT, &ccount, size_t(ncoarse) * 4)) != HM_OK) return s;
+  if ((s = sc.alloc(WS_DSTAT, &dstat, sizeof(DevStatus))) != HM_OK) return s;
+  HM_CUDA_TRY(cudaMemsetAsync(pcount, 0, size_t(np) * 4, st));
+  HM_CUDA_TRY(cudaMemsetAsync(ccount, 0, size_t(ncoarse) * 4, st));
+  HM_CUDA_TRY(cudaMemsetAsync(dstat, 0, sizeof(DevStatus), st));
+  uint64_t o0 = off0;
+  const size_t smemS = size_t(kSTile) * (sizeof(KV32) + 4);
+  auto kS1 = sbits == 8 ? k_split<SrcBytesIdx, KV32, 1, 8> : k_split<SrcBytesIdx, KV32, 1, 9>;
+  auto kS2 = sbits == 8 ? k_split<SrcBytesIdx, KV32, 2, 8> : k_split<SrcBytesIdx, KV32, 2, 9>;
+  HM_CUDA_TRY(cudaFuncSetAttribute(kS1, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smemS)));
+  HM_CUDA_TRY(cudaFuncSetAttribute(kS2, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smemS)));
+  const SrcBytesIdx src{fp, vals, offs, o0};
+  const SplitArgs a1{nullptr, nullptr, 0, 0, cbuf, ccount, ccap, ncoarse, 0};
+  {
+    LaunchScope ls_("k_split1", st);
+    kS1<<<unsigned((n + kSTile - 1) / kSTile), kSThreads, smemS, st>>>(src, bp, a1, dstat);
+  }
+  const SplitArgs a2{cbuf, ccount, ccap, tpc, pbuf, pcount, cap, np, ncoarse};
+  {
+    LaunchScope ls_("k_split2", st);
+    kS2<<<ncoarse * tpc, kSThreads, smemS, st>>>(src, bp, a2, dstat);
+  }
+  const size_t smemD = size_t(cap) * sizeof(KV32) + size_t(kDTab) * 8 + size_t(cap) * 2;
+  HM_CUDA_TRY(cudaFuncSetAttribute(k_dedup_part_bytes, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smemD)));
+  {
+    LaunchScope ls_("k_dedup_part", st);
+    k_dedup_part_bytes<<<np, kDThreads, smemD, st>>>(pbuf, pcount, cap, bytes, o0, keep, dstat);
+  }
+  HM_CUDA_TRY(cudaGetLastError());
+  DevStatus hs{};
+  HM_CUDA_TRY(cudaMemcpyAsync(&hs, dstat, sizeof(hs), cudaMemcpyDeviceToHost, st));
+  HM_CUDA_TRY(cudaStreamSynchronize(st));
+  if (hs.part_overflow || hs.pad) return HM_ERR_TOO_LARGE;
+  return HM_OK;
 }
 
 // Returns HM_OK with *n_out distinct keys in (okeys, ovals) (device arrays of n

@@ -323,7 +323,9 @@ hm_status hm_build_bytes(const uint8_t* bytes, const uint64_t* offsets, const ui
   if (n == 0) return HM_ERR_EMPTY;
   if (!offsets || !vals) return HM_ERR_INVALID_ARG;
   if (n > (1ull << 30)) return HM_ERR_TOO_LARGE;
-  if (opts && (opts->flags & ~uint32_t(HM_FLAG_FULL_DIRECTORY | HM_FLAG_DIRECT_SLOTS | HM_FLAG_NO_ROUND0_ILP))) return HM_ERR_INVALID_ARG;
+  if (opts && (opts->flags & ~uint32_t(HM_FLAG_FULL_DIRECTORY | HM_FLAG_DIRECT_SLOTS | HM_FLAG_NO_ROUND0_ILP |
+                                         HM_FLAG_FROM_ARRAY)))
+    return HM_ERR_INVALID_ARG;
   hm_status s = check_device();
   if (s != HM_OK) return s;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -349,6 +351,21 @@ hm_status hm_build_bytes(const uint8_t* bytes, const uint64_t* offsets, const ui
     db = reinterpret_cast<const uint8_t*>(d);
   }
   const uint64_t seed = opts ? opts->seed : 0;
+  if (opts && (opts->flags & HM_FLAG_FROM_ARRAY)) {  // from_array: the distinct keys, packed in input order
+    uint8_t* pc = nullptr;
+    uint64_t *po = nullptr, *pv = nullptr, m = 0;
+    if ((s = dedup_bytes(db, doff, dv, n, st, &pc, &po, &pv, &m)) != HM_OK) return s;
+    sg.tmp.push_back(pc);
+    sg.tmp.push_back(po);
+    sg.tmp.push_back(pv);
+    db = pc;
+    doff = po;
+    dv = pv;
+    n = m;
+    o0 = 0;
+    HM_CUDA_TRY(cudaMemcpyAsync(&on, po + m, 8, cudaMemcpyDeviceToHost, st));
+    HM_CUDA_TRY(cudaStreamSynchronize(st));
+  }
   BuildOut bo;
   uint32_t t0 = 0;
   uint64_t r = 0;

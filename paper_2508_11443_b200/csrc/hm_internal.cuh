@@ -129,6 +129,12 @@ hm_status build_bytes_core(const uint8_t* bytes, const uint64_t* offsets, const 
                            uint64_t seed, uint32_t log2_bp, cudaStream_t st, BuildOut* out, uint32_t* t0_out,
                            uint64_t* r_out);
 hm_status dedup_workspace(void** p, size_t bytes, cudaStream_t st);  // build.cu's cached scratch
+hm_status dedup_partitioned_bytes(const uint8_t* bytes, const uint64_t* offs, const uint64_t* fp,
+                                  const uint64_t* vals, uint64_t n, uint64_t off0, cudaStream_t st, uint8_t* keep);
+void launch_fingerprint(const uint8_t* bytes, const uint64_t* offs, uint64_t n, uint64_t r, uint64_t* fp,
+                        cudaStream_t st);
+hm_status dedup_bytes(const uint8_t* bytes, const uint64_t* offs, const uint64_t* vals, uint64_t n, cudaStream_t st,
+                      uint8_t** out_ctx, uint64_t** out_offs, uint64_t** out_vals, uint64_t* n_out);
 hm_status dedup_partitioned(const uint64_t* keys, const uint64_t* vals, uint64_t n, cudaStream_t st, uint64_t* okeys,
                             uint64_t* ovals, uint64_t* n_out);
 // dedup.cu: from_array's distinct (first-occurrence) keys, device arrays owned by the caller

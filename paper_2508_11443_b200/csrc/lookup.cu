@@ -210,34 +210,6 @@ hm_status lookup_u64_launch(const hm_map* m, const uint64_t* q, uint64_t nq, uin
 
 // ------------------------------------------------------------ byte keys
 
-// Byte equality of two keys of length len at arbitrary alignments: 4-byte
-// aligned loads on both sides, realigned with a funnel shift (the word holding
-// a key's last byte is the last one read, so nothing past the key is touched).
-__device__ __forceinline__ bool bytes_equal(const uint8_t* a, const uint8_t* b, uint32_t len) {
-  if (len == 0) return true;
-  const uintptr_t A = reinterpret_cast<uintptr_t>(a), B = reinterpret_cast<uintptr_t>(b);
-  const uint32_t* wa = reinterpret_cast<const uint32_t*>(A & ~uintptr_t(3));
-  const uint32_t* wb = reinterpret_cast<const uint32_t*>(B & ~uintptr_t(3));
-  const uint32_t sa = uint32_t(A & 3) * 8, sb = uint32_t(B & 3) * 8;
-  const uint32_t* la = reinterpret_cast<const uint32_t*>((A + len - 1) & ~uintptr_t(3));
-  const uint32_t* lb = reinterpret_cast<const uint32_t*>((B + len - 1) & ~uintptr_t(3));
-  uint32_t ca = __ldg(wa), cb = __ldg(wb);
-  for (uint32_t i = 0, k = 1; i < len; i += 4, k++) {
-    const uint32_t na = wa + k <= la ? __ldg(wa + k) : 0u, nb = wb + k <= lb ? __ldg(wb + k) : 0u;
-    uint32_t x = sa ? __funnelshift_r(ca, na, sa) : ca, y = sb ? __funnelshift_r(cb, nb, sb) : cb;
-    const uint32_t rem = len - i;
-    if (rem < 4) {
-      const uint32_t m = (1u << (8 * rem)) - 1u;
-      x &= m;
-      y &= m;
-    }
-    if (x != y) return false;
-    ca = na;
-    cb = nb;
-  }
-  return true;
-}
-
 // Byte-key lookup: fingerprint the needle (R5,
 // expanded form), probe the compact directory and the 32-byte slot, and on a
 // fingerprint + length match compare the bytes with the map's context copy.

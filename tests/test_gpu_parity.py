@@ -328,8 +328,25 @@ def test_u64_from_array_heavy_duplication():
     gv, gf = m.lookup(dev(np.array([0xDEADBEEF12345678], np.uint64)))
     assert host(gv)[0] == 0 and host(gf)[0] == 1  # the first copy is input 0 with value 0
     m.free()
-    with pytest.raises(hm.HMError) as e:  # byte keys: not in this version
-        ctx, offs = gen.string_keys(10)
-        hm.HashMap.build_bytes(torch.from_numpy(ctx).cuda(), dev(offs), dev(gen.u64_values(10)),
+
+
+@pytest.mark.parametrize("n,ndistinct,seed", [(1, 1, 0), (40, 7, 1), (3000, 3000, 2), (200_000, 50_000, 3)])
+def test_bytes_from_array_parity(n, ndistinct, seed):
+    """from_array for byte keys (HM_FLAG_FROM_ARRAY): content duplicates, the
+    first occurrence keeps its value, the distinct keys are packed in input
+    order; table and context equal the oracle's byte for byte."""
+    hm = _hm()
+    rng = np.random.default_rng(n * 7 + seed)
+    ids = rng.integers(0, ndistinct, size=n).astype(np.uint64) if n > ndistinct else \
+        rng.permutation(ndistinct).astype(np.uint64)
+    ctx, offs = gen.pack_strings(ids + np.uint64(5))
+    vals = gen.u64_values(n, lo=1000)
+    ot = O.from_array_bytes(ctx, offs, vals, seed)
+    m = hm.HashMap.build_bytes(torch.from_numpy(ctx).cuda(), dev(offs), dev(vals), seed=seed,
                                flags=hm.FLAG_FROM_ARRAY)
-    assert e.value.name == "INVALID_ARG"
+    assert_table_equal(m, ot)
+    qc, qo = gen.pack_strings(np.arange(0, ndistinct + 50, dtype=np.uint64) + np.uint64(5))
+    ov, of = O.lookup_bytes(ot, qc, qo)
+    gv, gf = m.lookup_bytes(torch.from_numpy(qc).cuda(), dev(qo))
+    assert np.array_equal(host(gv), ov) and np.array_equal(host(gf), of)
+    m.free()

@@ -108,3 +108,33 @@ def test_string_fingerprints_distinct_and_deterministic():
     assert t1.dir.tobytes() == t2.dir.tobytes()
     for f in ("fp", "value", "len"):
         assert np.array_equal(t1.slots[f], t2.slots[f])
+
+
+def test_oracle_from_array_bytes_first_occurrence_wins():
+    """from_array for byte keys: each lookup returns the value of the key's
+    first occurrence (brute-force scan); distinct inputs give from_array_nodup's
+    table; the packed context holds the distinct keys in input order."""
+    rng = np.random.default_rng(11)
+    words = [b"", b"a", b"ab", b"ab\\0", b"abc", b"hello world", b"x" * 70, b"\\x00\\x01", b"zz"]
+    idx = rng.integers(0, len(words), size=60)
+    keys = [words[i] for i in idx]
+    ctx = np.frombuffer(b"".join(keys), np.uint8)
+    offs = np.zeros(len(keys) + 1, np.uint64)
+    np.cumsum([len(k) for k in keys], out=offs[1:])
+    vals = np.arange(500, 560, dtype=np.uint64)
+    t = O.from_array_bytes(ctx, offs, vals, 2)
+    distinct = list(dict.fromkeys(keys))
+    assert int(t.header["n"]) == len(distinct)
+    assert t.ctx.tobytes() == b"".join(distinct)
+    qk = words + [b"abcd", b"hello worle"]
+    qctx = np.frombuffer(b"".join(qk), np.uint8)
+    qoffs = np.zeros(len(qk) + 1, np.uint64)
+    np.cumsum([len(k) for k in qk], out=qoffs[1:])
+    ov, of = O.lookup_bytes(t, qctx, qoffs)
+    for k, v, f in zip(qk, ov.tolist(), of.tolist()):
+        first = next((i for i, x in enumerate(keys) if x == k), None)
+        assert (f, v) == ((0, 0) if first is None else (1, 500 + first))
+    c2, o2 = gen.string_keys(300)
+    v2 = gen.u64_values(300)
+    a, b = O.from_array_bytes(c2, o2, v2, 1), O.build_bytes(c2, o2, v2, 1)
+    assert a.dir.tobytes() == b.dir.tobytes() and a.slots.tobytes() == b.slots.tobytes()
