@@ -469,7 +469,6 @@ __global__ void __launch_bounds__(kSThreads, HM_SPLIT_MINB) k_split(Src src, Bui
 // Size classes of multi-key buckets for the search: s=2, 3..8 (a thread per
 // bucket and attempt, K = 2/8 key registers) and 9..32 (a warp per bucket).
 constexpr int kNCls = 3;
-__device__ __forceinline__ int size_class(uint32_t s) { return s == 2 ? 0 : s <= 8 ? 1 : s <= 32 ? 2 : 3; }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -477,10 +476,11 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 
 // make2 for buckets with 2 <= s <= 8, in CTA-wide rounds.
 // One attempt = derive(seed,2,b,t), the s level-2 slots hash mod s^2 and the
-// occupancy bitmap as `collision`.  Round 0 tries t = 0 for
-// every multi-key bucket (a thread per bucket); the buckets that collide are
+// occupancy bitmap as `collision`.  Round 0 gives every
+// multi-key bucket a lane (attempts 0 and 1 in flight for s <= 4, attempt 0 for
+// the paired s = 2 lanes and s = 5..8); the buckets that still collide are
 // queued, and every later round tries A consecutive attempts of each queued
-// bucket on A adjacent lanes (A = 512 / queue length, up to 8), the lowest
+// bucket on A adjacent lanes (A = lanes / queue length, up to 8), the lowest
 // successful attempt winning — the same t as trying them one by one (R13),
 // without the long per-bucket chains that leave most lanes idle.
 
@@ -495,58 +495,6 @@ struct SearchCtx {
   uint16_t* src;  // slot -> item map (nullptr: not staged)
 };
 
-__device__ __forceinline__ uint32_t l2_slot(const Consts& c, uint64_t key, uint32_t s, const FastMod& fm) {
-  const uint64_t hv = hash64(c, key);
-  // mod s^2: a mask when s is a power of two
-  return (s & (s - 1)) == 0 ? uint32_t(hv) & (s * s - 1) : uint32_t(fastmod(hv, fm));
-}
-
-// Is attempt t injective on the bucket?  Keys are read from shared memory, s
-// is a runtime bound (no predicated-off work for small buckets).
-template <class E>
-__device__ __forceinline__ bool attempt_ok(uint64_t smix, uint64_t b, uint32_t t, const E* skv, const uint16_t* sidx,
-                                           uint32_t st0, uint32_t s, const FastMod& fm) {
-  const Consts c = derive(smix, 2, b, t);
-  uint64_t bits = 0;
-  for (uint32_t j = 0; j < s; j++) {
-    const uint64_t bit = 1ull << l2_slot(c, skv[sidx[st0 + j]].key, s, fm);
-    if (bits & bit) return false;
-    bits |= bit;
-  }
-  return true;
-}
-
-// The bucket is done with attempt t: record t and the level-2 slot of every
-// member, and map its s^2 slots to their source items — the members, and the
-// lowest-slot member as value-0 filler everywhere else (R10).
-template <class E>
-__device__ __forceinline__ void bucket_done(const SearchCtx& X, uint64_t smix, uint64_t b, uint32_t lb, uint32_t st0,
-                                            uint32_t s, uint32_t t, const E* skv, const FastMod& fm) {
-  X.s_t[lb] = uint8_t(t);
-  const Consts c = derive(smix, 2, b, t);
-  uint64_t bits = 0;
-  uint32_t hmin = 0xFFFFu, fill = 0;
-  for (uint32_t j = 0; j < s; j++) {
-    const uint32_t it = X.sidx[st0 + j];
-    const uint32_t h = l2_slot(c, skv[it].key, s, fm);
-    X.sA[st0 + j] = uint16_t(h);
-    bits |= 1ull << h;
-    if (h < hmin) {
-      hmin = h;
-      fill = it;
-    }
-  }
-  if (X.src) {
-    uint16_t* o = X.src + X.soff[lb];
-    const uint32_t s2 = s * s;
-    uint64_t fr = ~bits & (s2 == 64 ? ~0ull : ((1ull << s2) - 1));  // the unused slots
-    while (fr) {
-      o[__ffsll(fr) - 1] = uint16_t(fill | 0x8000u);
-      fr &= fr - 1;
-    }
-    for (uint32_t j = 0; j < s; j++) o[X.sA[st0 + j]] = X.sidx[st0 + j];
-  }
-}
 
 // Slots h[] of bucket lb under constants c (K keys in registers); returns the
 // occupancy bitmap, or 0 on a collision (s >= 2, so a valid map is never 0).
