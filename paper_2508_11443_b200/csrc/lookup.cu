@@ -33,7 +33,7 @@ __device__ __forceinline__ KV16 ld_slot16(const KV16* p) {
 __device__ __forceinline__ KV32 ld_slot32(const KV32* p) {
   KV32 e;
   uint64_t w3;
-  asm volatile("ld.global.cg.v4.u64 {%0, %1, %2, %3}, [%4];"
+  asm volatile("ld.global.cg.L2::64B.v4.u64 {%0, %1, %2, %3}, [%4];"
                : "=l"(e.key), "=l"(e.value), "=l"(e.ctx_off), "=l"(w3)
                : "l"(p));
   e.len = uint32_t(w3);
@@ -84,7 +84,7 @@ __device__ __forceinline__ uint64_t ld_q(const uint64_t* p, uint64_t pol) {
 __device__ __forceinline__ CDir ld_cdir(const CDir* p, uint64_t pol) {
   CDir r;
   uint64_t a, b, c, d;
-  asm volatile("ld.global.cg.L2::cache_hint.v4.u64 {%0, %1, %2, %3}, [%4], %5;"
+  asm volatile("ld.global.cg.L2::cache_hint.L2::64B.v4.u64 {%0, %1, %2, %3}, [%4], %5;"
                : "=l"(a), "=l"(b), "=l"(c), "=l"(d)
                : "l"(p), "l"(pol));
   r.w[0] = uint32_t(a);
@@ -99,7 +99,7 @@ __device__ __forceinline__ CDir ld_cdir(const CDir* p, uint64_t pol) {
 }
 __device__ __forceinline__ KV16 ld_slot16_ef(const KV16* p, uint64_t pol) {
   KV16 e;
-  asm volatile("ld.global.cg.L2::cache_hint.v2.u64 {%0, %1}, [%2], %3;"
+  asm volatile("ld.global.cg.L2::cache_hint.L2::64B.v2.u64 {%0, %1}, [%2], %3;"
                : "=l"(e.key), "=l"(e.value)
                : "l"(p), "l"(pol));
   return e;

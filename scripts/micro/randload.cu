@@ -13,6 +13,11 @@ template<int F> __device__ __forceinline__ uint64_t ld(const uint64_t* p){
   if (F==4) asm volatile("ld.global.nc.u64 %0,[%1];":"=l"(v):"l"(p));
   if (F==5) asm volatile("ld.relaxed.gpu.global.u64 %0,[%1];":"=l"(v):"l"(p));
   if (F==6) asm volatile("ld.global.lu.u64 %0,[%1];":"=l"(v):"l"(p));
+  if (F==8) asm volatile("ld.global.nc.L2::64B.u64 %0,[%1];":"=l"(v):"l"(p));
+  if (F==9) asm volatile("ld.global.L2::64B.u64 %0,[%1];":"=l"(v):"l"(p));
+  if (F==10) asm volatile("ld.global.nc.L1::no_allocate.L2::64B.u64 %0,[%1];":"=l"(v):"l"(p));
+  if (F==11) asm volatile("ld.global.cg.L2::64B.u64 %0,[%1];":"=l"(v):"l"(p));
+  if (F==12) asm volatile("ld.global.nc.L2::128B.u64 %0,[%1];":"=l"(v):"l"(p));
   if (F==7) { uint64_t pol; asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;":"=l"(pol)); asm volatile("ld.global.L2::cache_hint.u64 %0,[%1], %2;":"=l"(v):"l"(p),"l"(pol)); }
   return v;
 }
@@ -43,5 +48,6 @@ int main(){
   cudaEvent_t e0,e1; cudaEventCreate(&e0); cudaEventCreate(&e1); float ms;
 #define RUN(K,name) K<<<148*8,256>>>(a,n,m,o); cudaEventRecord(e0); K<<<148*8,256>>>(a,n,m,o); cudaEventRecord(e1); cudaEventSynchronize(e1); cudaEventElapsedTime(&ms,e0,e1); printf("%-12s %7.3f ms  %6.2f Gld/s\n", name, ms, m/ms/1e6);
   RUN(k<0>,"ca") RUN(k<1>,"cg") RUN(k<2>,"cs") RUN(k<3>,"cv") RUN(k<4>,"nc") RUN(k<5>,"relaxed") RUN(k<6>,"lu") RUN(k<7>,"evict_first") RUN(kca,"cp.async8")
+  RUN(k<8>,"nc.L2::64B") RUN(k<9>,"L2::64B") RUN(k<10>,"nc.noal.L2::64B") RUN(k<11>,"cg.L2::64B") RUN(k<12>,"nc.L2::128B")
   return 0;
 }
