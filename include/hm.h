@@ -83,6 +83,13 @@ typedef struct {
  * context.  Byte keys repeated so heavily that a dedup partition overflows:
  * HM_ERR_TOO_LARGE in this version. */
 #define HM_FLAG_FROM_ARRAY 8u
+/* Ablation (u64 keys only; byte keys -> HM_ERR_INVALID_ARG): build level two
+ * with the paper's sortless round-based construction (PAPER.md:443-499,
+ * §2.5: flat arrays, hist for collisions, presum renumbering, one grid-wide
+ * pass per round) instead of the partitioned warp-per-bucket search.  The
+ * table is identical (R13); only the construction route and its speed
+ * differ.  log2_bp is ignored. */
+#define HM_FLAG_ROUNDS 16u
 
 /* Table header, 56 bytes, little-endian (DESIGN.md §4 "Table layout"). */
 typedef struct {
@@ -158,7 +165,10 @@ hm_status hm_lookup_bytes(const hm_map* map, const uint8_t* qbytes, const uint64
                           uint64_t nq, uint64_t* out_vals, uint8_t* out_found, void* stream);
 
 /* ---------------------------------------------------------------- lifetime */
-void hm_free(hm_map* map); /* NULL-safe; waits for the map's pending work */
+/* NULL-safe; waits for the device's pending work.  The map's device arrays are
+ * kept for reuse by the next build of the same size (see
+ * hm_release_workspace) unless that cache is full. */
+void hm_free(hm_map* map);
 
 /* Header of the (logical) table.  host_out: host pointer. */
 hm_status hm_info(const hm_map* map, hm_header* host_out);
@@ -184,8 +194,10 @@ uint64_t hm_kernel_launches(void);
  * 52 B per key for byte-key builds) on the current device, and trim the
  * device's default stream-ordered memory pool, whose release threshold the
  * library raises on first use (freed table memory otherwise goes back to the
- * driver at every synchronisation and is re-mapped by the next build).  Maps
- * are not affected.  Synchronises the device. */
+ * driver at every synchronisation and is re-mapped by the next build), and
+ * free the arrays of freed maps that the library keeps (per device and size,
+ * at most 32 GB) for the next build of the same size.  Live maps are not
+ * affected.  Synchronises the device. */
 hm_status hm_release_workspace(void);
 
 /* Per-kernel device timing (diagnostics, used by bench.py for the roofline).

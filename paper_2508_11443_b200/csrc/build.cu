@@ -1326,6 +1326,47 @@ struct Scratch {
   }
 };
 
+// Map arrays freed by hm_free, kept per (device, size) for the next build.
+// Builds of a size take their dir/cdir/slots from here; without it the
+// stream-ordered pool, fragmented by the other sizes, mapped fresh memory for
+// a 2 GB slot array on build after build (50-100 ms each at 2^26, measured).
+// Capped at kMapCacheCap bytes; hm_release_workspace() empties it.
+static std::multimap<std::pair<int, size_t>, void*> g_mapcache;
+static size_t g_mapcache_bytes = 0;
+constexpr size_t kMapCacheCap = size_t(32) << 30;
+
+hm_status map_alloc(void** p, size_t bytes, cudaStream_t st) {
+  bytes = std::max<size_t>(bytes, 16);
+  int dev = 0;
+  HM_CUDA_TRY(cudaGetDevice(&dev));
+  {
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    auto it = g_mapcache.find({dev, bytes});
+    if (it != g_mapcache.end()) {
+      *p = it->second;
+      g_mapcache.erase(it);
+      g_mapcache_bytes -= bytes;
+      return HM_OK;
+    }
+  }
+  return dmalloc(p, bytes, st);
+}
+
+void map_release(void* p, size_t bytes) {
+  if (!p) return;
+  bytes = std::max<size_t>(bytes, 16);
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) {
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    if (g_mapcache_bytes + bytes <= kMapCacheCap) {
+      g_mapcache.insert({{dev, bytes}, p});
+      g_mapcache_bytes += bytes;
+      return;
+    }
+  }
+  cudaFree(p);
+}
+
 // The from_array dedup set (dedup.cu) lives in the same cache.
 hm_status dedup_workspace(void** p, size_t bytes, cudaStream_t st) {
   Scratch sc{st};
@@ -1346,6 +1387,15 @@ hm_status release_workspace() {
       for (int r = 0; r < WS_NROLES; r++)
         if (it->second.p[r]) cudaFreeAsync(it->second.p[r], it->first.second);
       it = g_ws.erase(it);
+    } else {
+      ++it;
+    }
+  }
+  for (auto it = g_mapcache.begin(); it != g_mapcache.end();) {
+    if (it->first.first == dev) {
+      cudaFree(it->second);
+      g_mapcache_bytes -= it->first.second;
+      it = g_mapcache.erase(it);
     } else {
       ++it;
     }
@@ -1403,15 +1453,16 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
   uint64_t* dir = nullptr;
   E* slots = nullptr;
   CDir* cdir = nullptr;
-  if ((s = dmalloc(&dir, nb * 8, st)) != HM_OK) return s;
-  if ((s = dmalloc(&cdir, ((nb + 31) / 32) * sizeof(CDir), st)) != HM_OK) {
+  const size_t dir_bytes = nb * 8, cdir_bytes = ((nb + 31) / 32) * sizeof(CDir);
+  if ((s = map_alloc(reinterpret_cast<void**>(&dir), dir_bytes, st)) != HM_OK) return s;
+  if ((s = map_alloc(reinterpret_cast<void**>(&cdir), cdir_bytes, st)) != HM_OK) {
     cudaFreeAsync(dir, st);
     return s;
   }
   const double sn = double(n_in);
   uint64_t slot_cap = uint64_t(2.0 * sn + 8.0 * std::sqrt(2.0 * sn + 1.0) + 1024.0);
   if (n_in <= 4096) slot_cap = std::max<uint64_t>(slot_cap, 4 * std::max<uint64_t>(n_in, 1));
-  if ((s = dmalloc(&slots, slot_cap * sizeof(E), st)) != HM_OK) {
+  if ((s = map_alloc(reinterpret_cast<void**>(&slots), slot_cap * sizeof(E), st)) != HM_OK) {
     cudaFreeAsync(dir, st);
     cudaFreeAsync(cdir, st);
     return s;
@@ -1577,7 +1628,7 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
         slots = nullptr;
         slot_cap = hs.S;
         bp.slot_cap = slot_cap;
-        if ((s = dmalloc(&slots, slot_cap * sizeof(E), st)) != HM_OK) {
+        if ((s = map_alloc(reinterpret_cast<void**>(&slots), slot_cap * sizeof(E), st)) != HM_OK) {
           cudaFreeAsync(dir, st);
           cudaFreeAsync(cdir, st);
           return s;
@@ -1620,6 +1671,9 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
     out->dir = dir;
     out->cdir = cdir;
     out->slots = slots;
+    out->bytes[0] = dir_bytes;
+    out->bytes[1] = cdir_bytes;
+    out->bytes[2] = slot_cap * sizeof(E);
     out->S = hs.S;
     out->t1 = t1;
     return HM_OK;

@@ -273,7 +273,7 @@ hm_status hm_build_u64(const uint64_t* keys, const uint64_t* vals, uint64_t n, c
   if (!keys || !vals) return HM_ERR_INVALID_ARG;
   if (n > (1ull << 30)) return HM_ERR_TOO_LARGE;
   if (opts && (opts->flags & ~uint32_t(HM_FLAG_FULL_DIRECTORY | HM_FLAG_DIRECT_SLOTS | HM_FLAG_NO_ROUND0_ILP |
-                                         HM_FLAG_FROM_ARRAY)))
+                                         HM_FLAG_FROM_ARRAY | HM_FLAG_ROUNDS)))
     return HM_ERR_INVALID_ARG;
   hm_status s = check_device();
   if (s != HM_OK) return s;
@@ -292,7 +292,8 @@ hm_status hm_build_u64(const uint64_t* keys, const uint64_t* vals, uint64_t n, c
     n = nu;
   }
   BuildOut bo;
-  s = build_u64_core(dk, dv, n, n, 0, n, -1, seed, opts ? (opts->log2_bp | (opts->flags << 16)) : 0, st, &bo);
+  if (opts && (opts->flags & HM_FLAG_ROUNDS)) s = build_u64_rounds(dk, dv, n, seed, opts->flags, st, &bo);
+  else s = build_u64_core(dk, dv, n, n, 0, n, -1, seed, opts ? (opts->log2_bp | (opts->flags << 16)) : 0, st, &bo);
   if (uk) {
     cudaFreeAsync(uk, st);
     cudaFreeAsync(uv, st);
@@ -311,6 +312,7 @@ hm_status hm_build_u64(const uint64_t* keys, const uint64_t* vals, uint64_t n, c
   m->dir = bo.dir;
   m->cdir = bo.cdir;
   m->slots = bo.slots;
+  for (int a = 0; a < 3; a++) m->abytes[a] = bo.bytes[a];
   *out = m;
   return HM_OK;
 }
@@ -385,6 +387,7 @@ hm_status hm_build_bytes(const uint8_t* bytes, const uint64_t* offsets, const ui
   m->dir = bo.dir;
   m->cdir = bo.cdir;
   m->slots = bo.slots;
+  for (int a = 0; a < 3; a++) m->abytes[a] = bo.bytes[a];
   m->ctx_bytes = on - o0;
   void* c = nullptr;
   cudaError_t e = cudaMallocAsync(&c, std::max<uint64_t>(m->ctx_bytes + 16, 16), st);
@@ -480,9 +483,12 @@ void hm_free(hm_map* map) {
   cudaGetDevice(&cur);
   if (cur != map->device) cudaSetDevice(map->device);
   cudaDeviceSynchronize();
-  if (map->dir) cudaFree(map->dir);
-  if (map->cdir) cudaFree(map->cdir);
-  if (map->slots) cudaFree(map->slots);
+  void* arr[3] = {map->dir, map->cdir, map->slots};
+  for (int a = 0; a < 3; a++) {
+    if (!arr[a]) continue;
+    if (map->abytes[a]) map_release(arr[a], map->abytes[a]);
+    else cudaFree(arr[a]);
+  }
   if (map->ctx) cudaFree(map->ctx);
   if (cur != map->device) cudaSetDevice(cur);
   delete map;
@@ -581,6 +587,7 @@ hm_status hm_build_u64_shard(const uint64_t* keys, const uint64_t* vals, uint64_
   m->dir = bo.dir;
   m->cdir = bo.cdir;
   m->slots = bo.slots;
+  for (int a = 0; a < 3; a++) m->abytes[a] = bo.bytes[a];
   *S_local = bo.S;
   *out = m;
   return HM_OK;

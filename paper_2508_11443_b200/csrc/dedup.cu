@@ -253,7 +253,10 @@ __global__ void k_scan_add(uint64_t* __restrict__ v, uint64_t n, const uint64_t*
     v[i] += sums[i / kScanTile];
 }
 
-static hm_status scan_excl(uint64_t* v, uint64_t n, uint64_t* sums, cudaStream_t st) {
+uint64_t scan_sums_len(uint64_t n) { return (n + kScanTile - 1) / kScanTile; }
+
+// in-place exclusive scan of v[0, n); sums holds scan_sums_len(n) entries
+hm_status scan_excl(uint64_t* v, uint64_t n, uint64_t* sums, cudaStream_t st) {
   const uint64_t tiles = (n + kScanTile - 1) / kScanTile;
   {
     LaunchScope ls_("k_scan_tiles", st);

@@ -89,6 +89,7 @@ struct hm_map {
   hm::L1Params l1;
   uint64_t smix;
   uint64_t r_fp;         // byte keys: fingerprint point (a1 of derive(seed,0,0,t0))
+  size_t abytes[3];      // map_alloc sizes of dir, cdir, slots (0: plain cudaMalloc)
   uint64_t* dir;         // nb entries, local soff
   hm::CDir* cdir;        // compact lookup directory, ceil(nb/32) records
   void* slots;           // S records
@@ -119,7 +120,13 @@ struct BuildOut {
   void* slots = nullptr;
   uint64_t S = 0;
   uint32_t t1 = 0;
+  size_t bytes[3] = {0, 0, 0};  // allocation sizes of dir, cdir, slots (map_alloc)
 };
+// Device arrays of a map (dir, cdir, slots) come from map_alloc and go back
+// through map_release when the map is freed (after a device synchronisation):
+// freed arrays are kept, up to a cap, for the next build of the same sizes.
+hm_status map_alloc(void** p, size_t bytes, cudaStream_t st);
+void map_release(void* p, size_t bytes);
 // t1_fixed < 0: search t1 = 0..15 with the space bound of this table.
 hm_status release_workspace();
 hm_status build_u64_core(const uint64_t* keys, const uint64_t* vals, uint64_t n_in, uint64_t n_global,
@@ -140,6 +147,9 @@ hm_status dedup_partitioned(const uint64_t* keys, const uint64_t* vals, uint64_t
 // dedup.cu: from_array's distinct (first-occurrence) keys, device arrays owned by the caller
 hm_status dedup_u64(const uint64_t* keys, const uint64_t* vals, uint64_t n, cudaStream_t st, uint64_t** out_keys,
                     uint64_t** out_vals, uint64_t* n_out);
+// rounds.cu: the sortless round-based construction (HM_FLAG_ROUNDS ablation)
+hm_status build_u64_rounds(const uint64_t* keys, const uint64_t* vals, uint64_t n, uint64_t seed, uint32_t flags,
+                           cudaStream_t st, BuildOut* out);
 // lookup.cu
 hm_status lookup_u64_launch(const hm_map* m, const uint64_t* q, uint64_t nq, uint64_t* out_vals,
                             uint8_t* out_found, cudaStream_t st);

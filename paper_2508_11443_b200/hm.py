@@ -139,6 +139,7 @@ FLAG_FULL_DIRECTORY = 1  # HM_FLAG_FULL_DIRECTORY
 FLAG_DIRECT_SLOTS = 2  # HM_FLAG_DIRECT_SLOTS (testing knob)
 FLAG_NO_ROUND0_ILP = 4  # HM_FLAG_NO_ROUND0_ILP (testing knob)
 FLAG_FROM_ARRAY = 8  # HM_FLAG_FROM_ARRAY: from_array (duplicates allowed, first occurrence kept)
+FLAG_ROUNDS = 16  # HM_FLAG_ROUNDS: the paper's sortless round-based construction (ablation, u64 keys)
 
 
 def _opts(seed: int, log2_bp: int = 0, flags: int = 0):

@@ -237,12 +237,13 @@ def test_bytes_edge_strings_and_offsets():
     assert e.value.name == "DUPLICATE_KEY"
 
 
-@pytest.mark.parametrize("flags_name", ["FLAG_DIRECT_SLOTS", "FLAG_NO_ROUND0_ILP"])
+@pytest.mark.parametrize("flags_name", ["FLAG_DIRECT_SLOTS", "FLAG_NO_ROUND0_ILP", "FLAG_ROUNDS"])
 @pytest.mark.parametrize("n,seed,log2_bp", [(5, 0, 0), (4133, 5, 0), (70_001, 3, 6), (300_007, 1, 0)])
 def test_u64_construction_routes_same_table(flags_name, n, seed, log2_bp):
     """The testing knobs change how k_bucket gets there (direct slot writes
     instead of the shared-memory source map; one round-0 attempt instead of
-    two), never the table: both must still equal the oracle byte for byte."""
+    two), and FLAG_ROUNDS replaces it with the paper's sortless rounds
+     — never the table: all must equal the oracle byte for byte."""
     hm = _hm()
     keys, vals = gen.u64_keys(n, lo=3 * n), gen.u64_values(n)
     ot = O.build_u64(keys, vals, seed)
@@ -255,7 +256,7 @@ def test_u64_construction_routes_same_table(flags_name, n, seed, log2_bp):
     m.free()
 
 
-@pytest.mark.parametrize("flags_name", ["FLAG_DIRECT_SLOTS", "FLAG_NO_ROUND0_ILP"])
+@pytest.mark.parametrize("flags_name", ["FLAG_DIRECT_SLOTS", "FLAG_NO_ROUND0_ILP", "FLAG_ROUNDS"])
 def test_u64_construction_routes_duplicates(flags_name):
     hm = _hm()
     keys = gen.u64_keys(100_000)
@@ -350,3 +351,36 @@ def test_bytes_from_array_parity(n, ndistinct, seed):
     gv, gf = m.lookup_bytes(torch.from_numpy(qc).cuda(), dev(qo))
     assert np.array_equal(host(gv), ov) and np.array_equal(host(gf), of)
     m.free()
+
+
+def test_u64_rounds_ablation_large_and_from_array():
+    """The sortless round-based construction (HM_FLAG_ROUNDS) at a
+    size with tens of rounds: the same table as the default build (whose
+    parity with the oracle is tested above) and, for from_array input, as the
+    oracle's; byte keys are outside the ablation."""
+    hm = _hm()
+    n = 1 << 21
+    keys, vals = gen.u64_keys(n), gen.u64_values(n)
+    a = hm.HashMap.build_u64(dev(keys), dev(vals), seed=9)
+    b = hm.HashMap.build_u64(dev(keys), dev(vals), seed=9, flags=hm.FLAG_ROUNDS)
+    da, sa, _ = a.export()
+    db, sb, _ = b.export()
+    assert a.header_bytes() == b.header_bytes()
+    assert np.array_equal(da, db) and sa.tobytes() == sb.tobytes()
+    q, _, _ = gen.u64_queries(n, 1 << 20)
+    va, fa = a.lookup(dev(q))
+    vb, fb = b.lookup(dev(q))
+    assert torch.equal(va, vb) and torch.equal(fa, fb)
+    a.free()
+    b.free()
+    rng = np.random.default_rng(4)
+    base = gen.u64_keys(50_000, lo=11)
+    keys = base[rng.integers(0, 50_000, size=200_000)]
+    vals = gen.u64_values(200_000, lo=3)
+    m = hm.HashMap.build_u64(dev(keys), dev(vals), seed=2, flags=hm.FLAG_ROUNDS | hm.FLAG_FROM_ARRAY)
+    assert_table_equal(m, O.from_array_u64(keys, vals, 2))
+    m.free()
+    c, o = gen.string_keys(100)
+    with pytest.raises(hm.HMError) as e:
+        hm.HashMap.build_bytes(torch.from_numpy(c).cuda(), dev(o), dev(gen.u64_values(100)), flags=hm.FLAG_ROUNDS)
+    assert e.value.name == "INVALID_ARG"
