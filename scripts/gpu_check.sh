@@ -15,4 +15,5 @@ timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"k_
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_lookup_bytes|k_bucket|k_split|k_fingerprint" -c 8 -o $OUT/full_bytes python scripts/prof_once.py 24 bytes > $OUT/ncu_full_bytes.log 2>&1
 fi
 timeout 600 python scripts/bench_configs.py > $OUT/configs.jsonl 2> $OUT/configs.err
+timeout 300 python scripts/rounds_bench.py > $OUT/rounds_ablation.jsonl 2> $OUT/rounds.err
 tail -3 $OUT/pytest_gpu.log; tail -2 $OUT/smoke.log; cat $OUT/bench.json $OUT/bench_ref.json
