@@ -173,13 +173,31 @@ void hm_free(hm_map* map);
 /* Header of the (logical) table.  host_out: host pointer. */
 hm_status hm_info(const hm_map* map, hm_header* host_out);
 
-/* hm_export — copy the table to HOST memory for parity checks:
+/* hm_export — copy the table out for parity checks and for replication
+ * (DESIGN.md §4).  Each destination may be host or device memory (of the
+ * map's device); a device directory is rebased on the device:
  *   host_dir:   u64[n]  entry b = soff_b | s_b<<40 | t_b<<56 (may be NULL)
  *   host_slots: S slots of 16 B (u64 keys) or 32 B (byte keys) (may be NULL)
  *   host_ctx:   ctx_bytes bytes of the map's context copy (byte keys; may be NULL)
  * For a shard (hm_build_u64_shard) the directory covers the shard's bucket
  * range and soff is GLOBAL (the shard's slot base is added). Synchronous. */
 hm_status hm_export(const hm_map* map, uint64_t* host_dir, void* host_slots, uint8_t* host_ctx);
+
+/* hm_assemble_u64 — a map (u64 keys) from a complete table in the layout of
+ * dir u64[n] (soff | s<<40 | t<<56, soff global), slots
+ * {u64 key, u64 value}[S], as hm_export writes them — for a distributed build,
+ * the shards' exports concatenated in rank order, which is the single table
+ * (the replicated-lookup mode; dist.replicate_dist).
+ * seed and t1 are the table's (hm_info).  dir/slots: host or device pointers,
+ * copied (the caller keeps ownership).  The compact lookup directory is
+ * derived on the device.  Checked: soff_0 = 0, soff_{b+1} = soff_b + s_b^2,
+ * soff_{n-1} + s_{n-1}^2 = S and t = 0 where s < 2 (else HM_ERR_INVALID_ARG),
+ * so that no lookup probe leaves the slots; the keys themselves are trusted
+ * (a table whose keys do not hash to their slots gives misses, not faults).
+ * n == 0: HM_ERR_EMPTY; S > 4n or n > 2^30: HM_ERR_TOO_LARGE; opts: seed and
+ * log2_bp ignored, flags 0 or HM_FLAG_FULL_DIRECTORY. */
+hm_status hm_assemble_u64(const uint64_t* dir, const void* slots, uint64_t n, uint64_t S, uint64_t seed, uint32_t t1,
+                          const hm_opts* opts, void* stream, hm_map** out);
 
 const char* hm_status_str(hm_status s);
 const char* hm_last_error(void); /* thread-local; "" if none */

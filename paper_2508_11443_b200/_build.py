@@ -8,7 +8,7 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libhm.so")
-SOURCES = ["capi.cu", "build.cu", "lookup.cu", "dedup.cu", "rounds.cu"]
+SOURCES = ["capi.cu", "build.cu", "lookup.cu", "dedup.cu", "rounds.cu", "assemble.cu"]
 HEADERS = ["hm_internal.cuh", "hm_math.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [

@@ -38,7 +38,6 @@ constexpr int kAThreads = 512;
 #ifndef HM_KB_THREADS
 #define HM_KB_THREADS 512
 #endif
-constexpr int kBThreads = HM_KB_THREADS;
 #ifndef HM_KB_MINB
 #define HM_KB_MINB (1024 / HM_KB_THREADS)  // CTAs per SM the registers must allow
 #endif
@@ -58,7 +57,6 @@ struct KBCfg {
 #ifndef HM_RETRY_LOGA
 #define HM_RETRY_LOGA 3  // at most 2^3 lanes (attempts) per queued bucket and round
 #endif
-constexpr int kBWarps = kBThreads / 32;
 constexpr unsigned long long kFlagAgg = 1ull << 62, kFlagInc = 2ull << 62, kValMask = (1ull << 62) - 1;
 
 // ----------------------------------------------------------------- sources
@@ -886,7 +884,7 @@ __global__ void __launch_bounds__(KBCfg<E>::T, KBCfg<E>::MINB)
   __shared__ uint32_t s_c9, s_qn[2];
   __shared__ uint32_t s_bitsw[KBCfg<E>::W][32];
 
-  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, lt = (1u << lane) - 1u;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t cap = bp.cap;
   const uint32_t BP = 1u << bp.log2_bp;
   const uint32_t CH = (BP + KBCfg<E>::T - 1) / KBCfg<E>::T;  // buckets per thread in the scans

@@ -512,16 +512,91 @@ hm_status hm_info(const hm_map* map, hm_header* h) {
 hm_status hm_export(const hm_map* map, uint64_t* host_dir, void* host_slots, uint8_t* host_ctx) {
   if (!map) return HM_ERR_INVALID_ARG;
   if (host_dir) {
-    HM_CUDA_TRY(cudaMemcpy(host_dir, map->dir, map->nb * 8, cudaMemcpyDeviceToHost));
-    if (map->slot_base)
-      for (uint64_t i = 0; i < map->nb; i++) {
-        const uint64_t d = host_dir[i];
-        host_dir[i] = (d & ~kMask40) | ((d & kMask40) + map->slot_base);
+    if (is_device_ptr(host_dir)) {  // device destination: copy and rebase on the device
+      HM_CUDA_TRY(cudaMemcpy(host_dir, map->dir, map->nb * 8, cudaMemcpyDeviceToDevice));
+      if (map->slot_base) {
+        hm_status s = dir_rebase_launch(host_dir, map->nb, map->slot_base, 0);
+        if (s != HM_OK) return s;
       }
+    } else {
+      HM_CUDA_TRY(cudaMemcpy(host_dir, map->dir, map->nb * 8, cudaMemcpyDeviceToHost));
+      if (map->slot_base)
+        for (uint64_t i = 0; i < map->nb; i++) {
+          const uint64_t d = host_dir[i];
+          host_dir[i] = (d & ~kMask40) | ((d & kMask40) + map->slot_base);
+        }
+    }
   }
   if (host_slots && map->S)
-    HM_CUDA_TRY(cudaMemcpy(host_slots, map->slots, map->S * (map->key_kind ? 32 : 16), cudaMemcpyDeviceToHost));
-  if (host_ctx && map->ctx_bytes) HM_CUDA_TRY(cudaMemcpy(host_ctx, map->ctx, map->ctx_bytes, cudaMemcpyDeviceToHost));
+    HM_CUDA_TRY(cudaMemcpy(host_slots, map->slots, map->S * (map->key_kind ? 32 : 16), cudaMemcpyDefault));
+  if (host_ctx && map->ctx_bytes) HM_CUDA_TRY(cudaMemcpy(host_ctx, map->ctx, map->ctx_bytes, cudaMemcpyDefault));
+  HM_CUDA_TRY(cudaDeviceSynchronize());
+  return HM_OK;
+}
+
+hm_status hm_assemble_u64(const uint64_t* dir, const void* slots, uint64_t n, uint64_t S, uint64_t seed, uint32_t t1,
+                          const hm_opts* opts, void* stream, hm_map** out) {
+  g_last_error.clear();
+  if (!out) return HM_ERR_INVALID_ARG;
+  *out = nullptr;
+  if (n == 0) return HM_ERR_EMPTY;
+  if (!dir || !slots || S == 0) return HM_ERR_INVALID_ARG;
+  if (n > (1ull << 30) || S > 4 * n) return HM_ERR_TOO_LARGE;
+  if (t1 >= kT1Cap || (opts && (opts->flags & ~uint32_t(HM_FLAG_FULL_DIRECTORY)))) return HM_ERR_INVALID_ARG;
+  hm_status s = check_device();
+  if (s != HM_OK) return s;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const size_t bytes[3] = {n * 8, ((n + 31) / 32) * sizeof(CDir), S * 16};
+  void* arr[3] = {nullptr, nullptr, nullptr};
+  auto fail = [&](hm_status code) {
+    for (int a = 0; a < 3; a++)
+      if (arr[a]) cudaFreeAsync(arr[a], st);
+    return code;
+  };
+  for (int a = 0; a < 3; a++)
+    if ((s = map_alloc(&arr[a], bytes[a], st)) != HM_OK) return fail(s);
+  unsigned int* bad = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&bad), 4, st);
+  if (e != cudaSuccess) return fail(cuda_fail(e, "assemble"));
+  auto fail2 = [&](hm_status code) {
+    cudaFreeAsync(bad, st);
+    return fail(code);
+  };
+  if ((e = cudaMemcpyAsync(arr[0], dir, bytes[0], cudaMemcpyDefault, st)) != cudaSuccess ||
+      (e = cudaMemcpyAsync(arr[2], slots, bytes[2], cudaMemcpyDefault, st)) != cudaSuccess ||
+      (e = cudaMemsetAsync(bad, 0, 4, st)) != cudaSuccess)
+    return fail2(cuda_fail(e, "assemble copies"));
+  const uint64_t smix = seed_mix(seed);
+  const L1Params l1 = make_l1(smix, t1, n);
+  if ((s = assemble_cdir_launch(static_cast<uint64_t*>(arr[0]), arr[2], n, S, l1,
+                                opts ? (opts->flags & HM_FLAG_FULL_DIRECTORY) : 0u, static_cast<CDir*>(arr[1]), bad,
+                                st)) != HM_OK)
+    return fail2(s);
+  unsigned int hbad = 0;
+  if ((e = cudaMemcpyAsync(&hbad, bad, 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+      (e = cudaStreamSynchronize(st)) != cudaSuccess)
+    return fail2(cuda_fail(e, "assemble"));
+  cudaFreeAsync(bad, st);
+  if (hbad) {
+    set_error("not a table: directory offsets do not follow soff_{b+1} = soff_b + s_b^2 up to S, or a bucket "
+              "with s < 2 has t != 0");
+    return fail(HM_ERR_INVALID_ARG);
+  }
+  hm_map* m = new_map();
+  m->key_kind = 0;
+  m->n_global = n;
+  m->b_lo = 0;
+  m->nb = n;
+  m->S = S;
+  m->seed = seed;
+  m->t1 = t1;
+  m->smix = smix;
+  m->l1 = l1;
+  m->dir = static_cast<uint64_t*>(arr[0]);
+  m->cdir = static_cast<CDir*>(arr[1]);
+  m->slots = arr[2];
+  for (int a = 0; a < 3; a++) m->abytes[a] = bytes[a];
+  *out = m;
   return HM_OK;
 }
 

@@ -116,7 +116,7 @@ hm_status dedup_u64(const uint64_t* keys, const uint64_t* vals, uint64_t n, cuda
     cudaGetLastError();
     release();
     if (ok) cudaFreeAsync(ok, st);
-    set_error("from_array: out of device memory for the dedup set");
+    set_error(std::string("from_array: out of device memory for the dedup set: ") + cudaGetErrorString(e));
     return HM_ERR_OOM;
   }
   {  // the fast path: the build's radix passes and a shared-memory set per partition

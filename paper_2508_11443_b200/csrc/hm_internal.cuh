@@ -150,6 +150,10 @@ hm_status dedup_u64(const uint64_t* keys, const uint64_t* vals, uint64_t n, cuda
 // rounds.cu: the sortless round-based construction (HM_FLAG_ROUNDS ablation)
 hm_status build_u64_rounds(const uint64_t* keys, const uint64_t* vals, uint64_t n, uint64_t seed, uint32_t flags,
                            cudaStream_t st, BuildOut* out);
+// assemble.cu
+hm_status assemble_cdir_launch(const uint64_t* dir, const void* slots, uint64_t n, uint64_t S, const L1Params& l1,
+                               uint32_t full_dir, CDir* cdir, unsigned int* bad, cudaStream_t st);
+hm_status dir_rebase_launch(uint64_t* d, uint64_t n, uint64_t base, cudaStream_t st);
 // lookup.cu
 hm_status lookup_u64_launch(const hm_map* m, const uint64_t* q, uint64_t nq, uint64_t* out_vals,
                             uint8_t* out_found, cudaStream_t st);

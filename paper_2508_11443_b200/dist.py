@@ -18,6 +18,8 @@ Build (all ranks, collectively):
   4. slot base of rank r = sum_{q<r} S_q (allgather)             (C3)
 Lookup: route queries by owner, all_to_all, local lookup, all_to_all back,
 unroute by the recorded permutation.
+Replicated lookups: all-gather the exported shards into the single table on
+every rank (hm_assemble_u64), then local lookups without an exchange.
 """
 from __future__ import annotations
 
@@ -73,6 +75,16 @@ class GpuOps:
         if shard is not None:
             shard.free()
 
+    def export_shard(self, shard, nb, S_local, device):
+        d = torch.empty(max(nb, 1), dtype=torch.int64, device=device)
+        sl = torch.empty(max(2 * S_local, 2), dtype=torch.int64, device=device)
+        if shard is not None:
+            shard.export_to(d, sl)
+        return d[:nb], sl[: 2 * S_local]
+
+    def assemble(self, dir_, slots, n, S, seed, t1):
+        return _hm.HashMap.assemble_u64(dir_, slots, n, S, seed, t1)
+
 
 @dataclass
 class DistMap:
@@ -88,6 +100,8 @@ class DistMap:
     rank: int
     ops: object
     group: object = None
+    seed: int = 0
+    S_all: tuple = ()
 
 
 def _exchange_counts(in_counts, group, device):
@@ -141,7 +155,8 @@ def build_dist(keys, vals, seed: int = 0, ops=None, group=None) -> DistMap:
     tdist.all_gather(allS, torch.tensor([S_local], dtype=torch.int64, device=dev), group=group)
     base = sum(int(x.item()) for x in allS[:rank])
     ops.set_base(shard, base)
-    return DistMap(shard, n, lo, hi, t1, S_local, base, S_total, world, rank, ops, group)
+    return DistMap(shard, n, lo, hi, t1, S_local, base, S_total, world, rank, ops, group, seed,
+                   tuple(int(x.item()) for x in allS))
 
 
 def lookup_dist(dm: DistMap, q, out_vals=None, out_found=None):
@@ -162,6 +177,32 @@ def lookup_dist(dm: DistMap, q, out_vals=None, out_found=None):
     out_f = torch.empty(q.numel(), dtype=torch.uint8, device=dev) if out_found is None else out_found
     ops.unroute(back_v, back_f, perm, out_v, out_f)
     return out_v, out_f
+
+
+def _all_gather_v(x, sizes, group):
+    """All-gather of 1-D pieces of different lengths (padded to the largest)."""
+    world = len(sizes)
+    mx = max(max(sizes), 1)
+    pad = torch.zeros(mx, dtype=x.dtype, device=x.device)
+    pad[: x.numel()] = x
+    parts = [torch.empty_like(pad) for _ in range(world)]
+    tdist.all_gather(parts, pad, group=group)
+    return torch.cat([p[:n] for p, n in zip(parts, sizes)])
+
+
+def replicate_dist(dm: DistMap):
+    """Replicated-lookup mode: every rank receives
+    all shards (all-gather of the exported directories, whose soff are
+    global, and of the slots) and assembles the single table, so lookups are
+    local with no exchange.  Returns that map (a HashMap on this rank's GPU);
+    the shards stay as they are.  Costs 8 + 16*S/n bytes per key per rank."""
+    ops, group, world = dm.ops, dm.group, dm.world
+    nb_all = [hi - lo for lo, hi in (bucket_range(r, world, dm.n_global) for r in range(world))]
+    dev = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else torch.device("cpu")
+    d, sl = ops.export_shard(dm.shard, dm.hi - dm.lo, dm.S_local, dev)
+    full_dir = _all_gather_v(d, nb_all, group)
+    full_slots = _all_gather_v(sl, [2 * x for x in dm.S_all], group)
+    return ops.assemble(full_dir, full_slots, dm.n_global, dm.S_total, dm.seed, dm.t1)
 
 
 def free_dist(dm: DistMap):

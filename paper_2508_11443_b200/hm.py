@@ -88,7 +88,8 @@ def lib():
         L.hm_shard_set_base.argtypes = [p, u64]
         L.hm_route_queries_u64.argtypes = [p, p, u64, i32, p, p, p, p]
         L.hm_unroute_u64.argtypes = [p, p, p, u64, p, p, p]
-        for f in ("hm_build_u64", "hm_build_bytes", "hm_lookup_u64", "hm_lookup_bytes", "hm_info", "hm_export",
+        L.hm_assemble_u64.argtypes = [p, p, u64, u64, u64, u32, C.POINTER(_Opts), p, C.POINTER(p)]
+        for f in ("hm_assemble_u64", "hm_build_u64", "hm_build_bytes", "hm_lookup_u64", "hm_lookup_bytes", "hm_info", "hm_export",
                   "hm_route_u64", "hm_build_u64_shard", "hm_shard_set_base", "hm_route_queries_u64",
                   "hm_unroute_u64"):
             getattr(L, f).restype = C.c_int
@@ -175,6 +176,19 @@ class HashMap:
         h = C.c_void_p()
         o = _opts(seed, log2_bp, flags)
         _check(lib().hm_build_u64(kp, vp, n, C.byref(o), _stream(stream), C.byref(h)))
+        return cls(h.value, 0)
+
+    @classmethod
+    def assemble_u64(cls, dir_, slots, n: int, S: int, seed: int, t1: int, flags: int = 0,
+                     stream=None) -> "HashMap":
+        """A map from a complete table (dir uint64[n], slots {key, value}[S] as
+        2*S int64/uint64 words or the structured export), host or device."""
+        dp, dk = _ptr(dir_)
+        sp, sk = _ptr(slots)
+        h = C.c_void_p()
+        o = _opts(seed, 0, flags)
+        _check(lib().hm_assemble_u64(dp, sp, n, S, seed & ((1 << 64) - 1), t1, C.byref(o), _stream(stream),
+                                     C.byref(h)))
         return cls(h.value, 0)
 
     @classmethod
@@ -290,6 +304,14 @@ class HashMap:
             self.free()
         except Exception:
             pass
+
+    def export_to(self, dir_out, slots_out):
+        """Copy the directory (global soff for a shard) and the slots into
+        caller tensors (device or host): dir_out int64[nb], slots_out int64[2*S]
+        (u64 keys)."""
+        dp, dk = _ptr(dir_out)
+        sp, sk = _ptr(slots_out)
+        _check(lib().hm_export(self._h, dp, sp, None))
 
     # -- shards (multi-GPU)
     def set_base(self, slot_base: int):

@@ -9,6 +9,7 @@ rank order equal the single-table oracle.
 """
 import os
 import socket
+import types
 
 import numpy as np
 import pytest
@@ -89,6 +90,19 @@ class OracleOps:
     def free(self, shard):
         pass
 
+    def export_shard(self, shard, nb, S_local, device):
+        d = shard.t.dir.copy()
+        d = (d & ~MASK40) | ((d & MASK40) + np.uint64(shard.base))
+        sl = np.stack([shard.t.slots["key"], shard.t.slots["value"]], axis=1).reshape(-1)
+        return torch.from_numpy(d.view(np.int64)), torch.from_numpy(np.ascontiguousarray(sl).view(np.int64))
+
+    def assemble(self, dir_, slots, n, S, seed, t1):
+        sl = slots.numpy().view(np.uint64).reshape(-1, 2)
+        assert dir_.numel() == n and sl.shape[0] == S
+        t = types.SimpleNamespace(dir=dir_.numpy().view(np.uint64).copy(),
+                                  slots={"key": sl[:, 0].copy(), "value": sl[:, 1].copy()})
+        return OracleShard(t, n, 0, n, t1, seed)
+
 
 def _worker(rank, world, port, n, seed, nq, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -105,7 +119,12 @@ def _worker(rank, world, port, n, seed, nq, q):
         qlo, qhi = rank * nq // world, (rank + 1) * nq // world
         qq, _, _ = gen.u64_queries(n, qhi - qlo, lo=qlo)
         ov, of = dist.lookup_dist(dm, torch.from_numpy(qq.view(np.int64)))
-        out = (rank, dm.lo, dm.hi, dm.t1, d, dm.shard.t.slots.copy(), ov.numpy().view(np.uint64).copy(), of.numpy().copy())
+        # replicated mode: the all-gathered single table, local lookups
+        rep = dist.replicate_dist(dm)
+        rv, rf = dm.ops.lookup(rep, torch.from_numpy(qq.view(np.int64)))
+        assert torch.equal(rv, ov) and torch.equal(rf, of)
+        out = (rank, dm.lo, dm.hi, dm.t1, d, dm.shard.t.slots.copy(), ov.numpy().view(np.uint64).copy(), of.numpy().copy(),
+               rep.t.dir, rep.t.slots["key"])
         q.put(out)
     finally:
         tdist.destroy_process_group()
@@ -143,3 +162,5 @@ def test_sharded_build_equals_single_table(world, n, seed):
     ov, of = O.lookup_u64(t, qq)
     assert np.array_equal(np.concatenate([r[6] for r in res]), ov)
     assert np.array_equal(np.concatenate([r[7] for r in res]), of)
+    for r in res:  # every rank holds the whole single table after replicate_dist
+        assert np.array_equal(r[8], t.dir) and np.array_equal(r[9], t.slots["key"])

@@ -74,6 +74,17 @@ def test_sharded_build_and_routed_lookup_on_one_gpu(world, n, seed):
         slots.append(sl)
     assert np.concatenate(dirs).tobytes() == ot.dir.tobytes()
     assert np.concatenate(slots).tobytes() == ot.slots.tobytes()
+    # replicated mode: the shards' device exports, concatenated, assembled into
+    # the single table (hm_assemble_u64) — identical to the oracle's
+    dd, ss = [], []
+    for d_ in range(world):
+        lo, hi = dist.bucket_range(d_, world, n)
+        a, b = ops.export_shard(shards[d_][0], hi - lo, shards[d_][1], torch.device("cuda"))
+        dd.append(a)
+        ss.append(b)
+    rep = ops.assemble(torch.cat(dd), torch.cat(ss), n, ot.S, seed, t1)
+    rd, rs, _ = rep.export()
+    assert rd.tobytes() == ot.dir.tobytes() and rs.tobytes() == ot.slots.tobytes()
     # routed lookups: rank r asks its own queries
     q, _, _ = gen.u64_queries(n, 3 * n)
     ov, of = O.lookup_u64(ot, q)
@@ -94,8 +105,45 @@ def test_sharded_build_and_routed_lookup_on_one_gpu(world, n, seed):
         ops.unroute(back_v, back_f, rq[r][1], out_v, out_f)
         assert np.array_equal(host(out_v), ov[qcut[r]:qcut[r + 1]])
         assert np.array_equal(host(out_f), of[qcut[r]:qcut[r + 1]])
+    rv, rf = rep.lookup(dev(q))
+    assert np.array_equal(host(rv), ov) and np.array_equal(host(rf), of)
+    rep.free()
     for m, _, _ in shards:
         ops.free(m)
+
+
+def test_assemble_from_export_and_rejects_non_tables():
+    """hm_assemble_u64 on a host export of a built map gives the same table and
+    the same lookups (the compact directory re-derived, singleton tags included);
+    a directory whose offsets do not add up is refused."""
+    from paper_2508_11443_b200 import hm
+    n = 200_003
+    keys, vals = gen.u64_keys(n), gen.u64_values(n)
+    m = hm.HashMap.build_u64(dev(keys), dev(vals), seed=6)
+    d, sl, _ = m.export()
+    inf = m.info()
+    a = hm.HashMap.assemble_u64(d, sl, n, inf.S, 6, inf.t1)
+    d2, sl2, _ = a.export()
+    assert d2.tobytes() == d.tobytes() and sl2.tobytes() == sl.tobytes()
+    assert a.header_bytes() == m.header_bytes()
+    q, _, _ = gen.u64_queries(n, 3 * n)
+    v1, f1 = m.lookup(dev(q))
+    v2, f2 = a.lookup(dev(q))
+    assert torch.equal(v1, v2) and torch.equal(f1, f2)
+    full = hm.HashMap.assemble_u64(d, sl, n, inf.S, 6, inf.t1, flags=hm.FLAG_FULL_DIRECTORY)
+    v3, f3 = full.lookup(dev(q))
+    assert torch.equal(v1, v3) and torch.equal(f1, f3)
+    for x in (a, full):
+        x.free()
+    bad = d.copy()
+    bad[n // 2] += np.uint64(1)  # an soff off by one
+    with pytest.raises(hm.HMError) as e:
+        hm.HashMap.assemble_u64(bad, sl, n, inf.S, 6, inf.t1)
+    assert e.value.name == "INVALID_ARG"
+    with pytest.raises(hm.HMError) as e:
+        hm.HashMap.assemble_u64(d, sl, n, inf.S - 1, 6, inf.t1)
+    assert e.value.name == "INVALID_ARG"
+    m.free()
 
 
 def _free_port():
@@ -125,6 +173,10 @@ def test_dist_build_and_lookup_through_nccl_one_rank():
         v, f = dist.lookup_dist(dm, dev(q))
         ov, of = O.lookup_u64(ot, q)
         assert np.array_equal(host(v), ov) and np.array_equal(host(f), of)
+        rep = dist.replicate_dist(dm)
+        rv, rf = rep.lookup(dev(q))
+        assert np.array_equal(host(rv), ov) and np.array_equal(host(rf), of)
+        rep.free()
         dist.free_dist(dm)
     finally:
         tdist.destroy_process_group()
