@@ -150,7 +150,11 @@ hm_status hm_build_bytes(const uint8_t* bytes, const uint64_t* offsets, const ui
  *   out_found[nq]: 1 on a hit, 0 on a miss.  May be NULL.  Not both NULL.
  * Asynchronous and stream-ordered when all arrays are device memory; when any
  * array is host memory the call stages it and returns after the results are
- * on the host.  A map may serve concurrent lookups from several streams.
+ * on the host; with host queries and host (or NULL) outputs beyond 2^24
+ * queries the batch moves in 2^23-query chunks whose upload, lookups and
+ * download overlap (two library copy streams, ordered with `stream` by
+ * events; pinned host memory is needed for the overlap).  A map may serve
+ * concurrent lookups from several streams.
  * Errors: HM_ERR_INVALID_ARG (NULL map/q with nq>0, both outputs NULL, wrong
  * key kind), HM_ERR_CUDA. */
 hm_status hm_lookup_u64(const hm_map* map, const uint64_t* q, uint64_t nq, uint64_t* out_vals,

@@ -430,11 +430,87 @@ static hm_status finish_outputs(uint64_t nq, uint64_t* out_vals, uint8_t* out_fo
   return HM_OK;
 }
 
+// Host queries and host outputs: the batch goes through in chunks so that the
+// upload of chunk c+1, the lookups of chunk c and the download of chunk c-1
+// overlap (copy engines in both directions, PCIe full duplex) instead of
+// upload, lookups, download one after the other.  Two library streams per
+// device carry the copies; events order them with the caller's stream.
+constexpr uint64_t kPipeChunk = uint64_t(1) << 23;
+static hm_status copy_streams(cudaStream_t* up, cudaStream_t* down) {
+  static std::mutex mu;
+  static cudaStream_t s_up[64] = {}, s_down[64] = {};
+  int dev = 0;
+  HM_CUDA_TRY(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return HM_ERR_INVALID_ARG;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!s_up[dev]) {
+    HM_CUDA_TRY(cudaStreamCreateWithFlags(&s_up[dev], cudaStreamNonBlocking));
+    HM_CUDA_TRY(cudaStreamCreateWithFlags(&s_down[dev], cudaStreamNonBlocking));
+  }
+  *up = s_up[dev];
+  *down = s_down[dev];
+  return HM_OK;
+}
+
+static hm_status lookup_u64_pipelined(const hm_map* map, const uint64_t* q, uint64_t nq, uint64_t* out_vals,
+                                      uint8_t* out_found, cudaStream_t st) {
+  cudaStream_t up, down;
+  hm_status s;
+  if ((s = copy_streams(&up, &down)) != HM_OK) return s;
+  uint64_t* dq = nullptr;
+  uint64_t* dv = nullptr;
+  uint8_t* df = nullptr;
+  std::vector<cudaEvent_t> ev;
+  auto cleanup = [&]() {
+    if (dq) cudaFreeAsync(dq, st);
+    if (dv) cudaFreeAsync(dv, st);
+    if (df) cudaFreeAsync(df, st);
+    for (cudaEvent_t e : ev) cudaEventDestroy(e);
+  };
+  auto event = [&](cudaEvent_t* e) {
+    cudaError_t r = cudaEventCreateWithFlags(e, cudaEventDisableTiming);
+    if (r == cudaSuccess) ev.push_back(*e);
+    return r;
+  };
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&dq), nq * 8, st);
+  if (e == cudaSuccess && out_vals) e = cudaMallocAsync(reinterpret_cast<void**>(&dv), nq * 8, st);
+  if (e == cudaSuccess && out_found) e = cudaMallocAsync(reinterpret_cast<void**>(&df), nq, st);
+  cudaEvent_t e0, e_end;
+  if (e == cudaSuccess) e = event(&e0);
+  if (e == cudaSuccess) e = cudaEventRecord(e0, st);  // (the buffers and the caller's prior work)
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(up, e0, 0);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(down, e0, 0);
+  for (uint64_t c0 = 0; e == cudaSuccess && c0 < nq; c0 += kPipeChunk) {
+    const uint64_t cn = std::min(kPipeChunk, nq - c0);
+    cudaEvent_t e_in, e_k;
+    if ((e = event(&e_in)) != cudaSuccess || (e = event(&e_k)) != cudaSuccess) break;
+    if ((e = cudaMemcpyAsync(dq + c0, q + c0, cn * 8, cudaMemcpyHostToDevice, up)) != cudaSuccess) break;
+    if ((e = cudaEventRecord(e_in, up)) != cudaSuccess || (e = cudaStreamWaitEvent(st, e_in, 0)) != cudaSuccess) break;
+    if ((s = lookup_u64_launch(map, dq + c0, cn, dv ? dv + c0 : nullptr, df ? df + c0 : nullptr, st)) != HM_OK) {
+      cleanup();
+      return s;
+    }
+    if ((e = cudaEventRecord(e_k, st)) != cudaSuccess || (e = cudaStreamWaitEvent(down, e_k, 0)) != cudaSuccess) break;
+    if (dv && (e = cudaMemcpyAsync(out_vals + c0, dv + c0, cn * 8, cudaMemcpyDeviceToHost, down)) != cudaSuccess) break;
+    if (df && (e = cudaMemcpyAsync(out_found + c0, df + c0, cn, cudaMemcpyDeviceToHost, down)) != cudaSuccess) break;
+  }
+  if (e == cudaSuccess) e = event(&e_end);
+  if (e == cudaSuccess) e = cudaEventRecord(e_end, down);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(st, e_end, 0);  // (frees after the last download)
+  cleanup();
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "pipelined lookup");
+  return HM_OK;
+}
+
 hm_status hm_lookup_u64(const hm_map* map, const uint64_t* q, uint64_t nq, uint64_t* out_vals, uint8_t* out_found,
                         void* stream) {
   if (!map || (!q && nq) || (!out_vals && !out_found) || map->key_kind != 0) return HM_ERR_INVALID_ARG;
   if (nq == 0) return HM_OK;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (nq > 2 * kPipeChunk && !is_device_ptr(q) && !getenv("HM_NO_PIPELINE") &&
+      (!out_vals || !is_device_ptr(out_vals)) && (!out_found || !is_device_ptr(out_found)))
+    return lookup_u64_pipelined(map, q, nq, out_vals, out_found, st);
   Staged sg{st, {}};
   const uint64_t* dq;
   uint64_t* dvo;

@@ -384,3 +384,29 @@ def test_u64_rounds_ablation_large_and_from_array():
     with pytest.raises(hm.HMError) as e:
         hm.HashMap.build_bytes(torch.from_numpy(c).cuda(), dev(o), dev(gen.u64_values(100)), flags=hm.FLAG_ROUNDS)
     assert e.value.name == "INVALID_ARG"
+
+
+@pytest.mark.parametrize("pinned", [True, False])
+def test_u64_lookup_host_buffers_pipelined(pinned):
+    """Host queries with host outputs above two chunks (2^23) take the chunked
+    upload/lookup/download pipeline of hm_lookup_u64; answers equal the device
+    path's (whose parity with the oracle is tested above), with and without
+    a value output, from pinned and from pageable memory."""
+    hm = _hm()
+    n = 1 << 20
+    keys, vals = gen.u64_keys(n), gen.u64_values(n)
+    m = hm.HashMap.build_u64(dev(keys), dev(vals), seed=1)
+    nq = (1 << 24) + (1 << 22) + 12345  # 2.5 chunks and a ragged tail
+    q, _, _ = gen.u64_queries(n, nq)
+    dv, df = m.lookup(dev(q))
+    hq = torch.from_numpy(q.view(np.int64))
+    hv = torch.empty(nq, dtype=torch.int64)
+    hf = torch.empty(nq, dtype=torch.uint8)
+    if pinned:
+        hq, hv, hf = hq.pin_memory(), hv.pin_memory(), hf.pin_memory()
+    m.lookup(hq, hv, hf)
+    assert torch.equal(hv, dv.cpu()) and torch.equal(hf, df.cpu())
+    hf2 = torch.zeros(nq, dtype=torch.uint8)
+    m.contains(hq, hf2)
+    assert torch.equal(hf2, df.cpu())
+    m.free()
