@@ -213,6 +213,9 @@ hm_status lookup_u64_launch(const hm_map* m, const uint64_t* q, uint64_t nq, uin
 // Byte-key lookup: fingerprint the needle (R5,
 // expanded form), probe the compact directory and the 32-byte slot, and on a
 // fingerprint + length match compare the bytes with the map's context copy.
+#ifndef HM_LOOKUP_BYTES_QPT
+#define HM_LOOKUP_BYTES_QPT 1
+#endif
 template <int QPT>
 __global__ void __launch_bounds__(kLThreads) k_lookup_bytes(LookupParams lp, const uint8_t* __restrict__ qb,
                                                             const uint64_t* __restrict__ qo, uint64_t nq,
@@ -237,7 +240,7 @@ __global__ void __launch_bounds__(kLThreads) k_lookup_bytes(LookupParams lp, con
       if (idx < nq) {
         off[j] = qo[idx];
         len[j] = qo[idx + 1] - off[j];
-        fp[j] = fingerprint_pw(qb, off[j], len[j], lp.r_fp, &s_pw);
+        fp[j] = fingerprint_pw64(qb, off[j], len[j], lp.r_fp, &s_pw);
       }
     }
     uint32_t tag[QPT];
@@ -260,18 +263,23 @@ __global__ void __launch_bounds__(kLThreads) k_lookup_bytes(LookupParams lp, con
       // a singleton whose key tag differs: a miss without the slot probe
       else if (((d[j] >> 40) & 0xFFFF) == 1 && uint32_t(d[j] >> 56) != tag[j]) d[j] = 0;
     }
+    // all slot probes in flight before the first comparison
+    KV32 e[QPT];
+#pragma unroll
+    for (int j = 0; j < QPT; j++) {
+      e[j].key = ~fp[j];  // (no probe: never equal)
+      e[j].len = 0;
+      if (((d[j] >> 40) & 0xFFFF) != 0) e[j] = ld_slot32(slots + slot_index(lp.smix, b[j] + lp.b_lo, d[j], fp[j], s_m2));
+    }
 #pragma unroll
     for (int j = 0; j < QPT; j++) {
       const uint64_t idx = base + uint64_t(j) * kLThreads + threadIdx.x;
       if (idx >= nq) continue;
       bool hit = false;
       uint64_t v = 0;
-      if (((d[j] >> 40) & 0xFFFF) != 0) {
-        const KV32 e = ld_slot32(slots + slot_index(lp.smix, b[j] + lp.b_lo, d[j], fp[j], s_m2));
-        if (e.key == fp[j] && e.len == len[j]) {
-          hit = bytes_equal(lp.ctx + e.ctx_off, qb + off[j], e.len);
-          if (hit) v = e.value;
-        }
+      if (e[j].key == fp[j] && e[j].len == len[j]) {
+        hit = bytes_equal64(lp.ctx + e[j].ctx_off, qb + off[j], e[j].len);
+        if (hit) v = e[j].value;
       }
       if (ov) ov[idx] = v;
       if (of) of[idx] = hit ? 1 : 0;
@@ -292,11 +300,11 @@ hm_status lookup_bytes_launch(const hm_map* m, const uint8_t* qb, const uint64_t
   lp.slots = m->slots;
   lp.ctx = m->ctx;
   lp.r_fp = m->r_fp;
-  const uint64_t blocks = (nq + kLThreads * 2 - 1) / (kLThreads * 2);
+  const uint64_t blocks = (nq + kLThreads * HM_LOOKUP_BYTES_QPT - 1) / (kLThreads * HM_LOOKUP_BYTES_QPT);
   const unsigned grid = unsigned(std::min<uint64_t>(blocks, uint64_t(num_sms()) * 8));
   {
     LaunchScope ls_("k_lookup_bytes", st);
-    k_lookup_bytes<2><<<grid, kLThreads, 0, st>>>(lp, qb, qo, nq, out_vals, out_found);
+    k_lookup_bytes<HM_LOOKUP_BYTES_QPT><<<grid, kLThreads, 0, st>>>(lp, qb, qo, nq, out_vals, out_found);
   }
   HM_CUDA_TRY(cudaGetLastError());
   return HM_OK;
