@@ -1691,36 +1691,36 @@ hm_status build_u64_core(const uint64_t* keys, const uint64_t* vals, uint64_t n_
 // ------------------------------------------------------------ byte keys
 // Fingerprints (R5) of all keys, expanded form.  A warp takes 32 consecutive
 // keys, stages their contiguous byte range in shared memory with coalesced
-// word loads, and every lane fingerprints its key from there (fingerprint_sm);
+// 8-byte word loads, and every lane fingerprints its key from there (fingerprint_sm64);
 // a range longer than the stage (keys of hundreds of bytes) is read directly.
-constexpr int kFpThreads = 256, kFpWarps = kFpThreads / 32, kFpStageWords = 512;
+constexpr int kFpThreads = 256, kFpWarps = kFpThreads / 32, kFpStageWords = 256;  // (8-byte words)
 __global__ void __launch_bounds__(kFpThreads) k_fingerprint(const uint8_t* __restrict__ bytes,
                                                             const uint64_t* __restrict__ offs, uint64_t n, uint64_t r,
                                                             uint64_t* __restrict__ fp) {
   __shared__ FpPow s_pw;
-  __shared__ uint32_t s_stage[kFpWarps][kFpStageWords];
+  __shared__ uint64_t s_stage[kFpWarps][kFpStageWords];
   if (threadIdx.x == 0) fp_pow_fill(&s_pw, r);
   __syncthreads();
   const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  uint32_t* sb = s_stage[w];
+  uint64_t* sb = s_stage[w];
   for (uint64_t i0 = (uint64_t(blockIdx.x) * kFpWarps + w) * 32; i0 < n; i0 += uint64_t(gridDim.x) * kFpWarps * 32) {
     const uint64_t i = i0 + lane;
     const bool valid = i < n;
     const uint64_t o = valid ? __ldg(offs + i) : 0, o1 = valid ? __ldg(offs + i + 1) : 0;
     const uint32_t lastl = n - 1 - i0 < 31 ? uint32_t(n - 1 - i0) : 31u;
     const uint64_t start = __shfl_sync(0xffffffffu, o, 0), end = __shfl_sync(0xffffffffu, o1, lastl);
-    const uint64_t g0 = start & ~uint64_t(3);
-    const uint64_t nw = end > start ? (end - g0 + 3) >> 2 : 0;
+    const uint64_t g0 = start & ~uint64_t(7);
+    const uint64_t nw = end > start ? (end - g0 + 7) >> 3 : 0;
     if (nw <= uint64_t(kFpStageWords)) {  // (warp-uniform)
-      const uint32_t* gw = reinterpret_cast<const uint32_t*>(bytes + g0);
+      const unsigned long long* gw = reinterpret_cast<const unsigned long long*>(bytes + g0);
       for (uint32_t k = lane; k < uint32_t(nw); k += 32) sb[k] = __ldg(gw + k);
       __syncwarp();
       if (valid)
-        fp[i] = o1 - o <= 4ull * kFpPowMax ? fingerprint_sm(sb, uint32_t(o - g0), uint32_t(o1 - o), &s_pw)
-                                           : fingerprint_pw(bytes, o, o1 - o, r, &s_pw);
+        fp[i] = o1 - o <= 4ull * kFpPowMax ? fingerprint_sm64(sb, uint32_t(o - g0), uint32_t(o1 - o), &s_pw)
+                                           : fingerprint_pw64(bytes, o, o1 - o, r, &s_pw);
       __syncwarp();
     } else if (valid) {
-      fp[i] = fingerprint_pw(bytes, o, o1 - o, r, &s_pw);
+      fp[i] = fingerprint_pw64(bytes, o, o1 - o, r, &s_pw);
     }
   }
 }

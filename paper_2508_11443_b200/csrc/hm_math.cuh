@@ -362,25 +362,29 @@ __device__ __forceinline__ uint64_t fingerprint_pw64(const uint8_t* bytes, uint6
   return f >= kP ? f - kP : f;
 }
 
-// fingerprint_pw over a shared-memory copy of the context: sb holds the
-// 4-byte words of the bytes starting at a 4-aligned position, the key starts
-// rel bytes in (len <= 4 * kFpPowMax).
-__device__ __forceinline__ uint64_t fingerprint_sm(const uint32_t* sb, uint32_t rel, uint32_t len, const FpPow* pw) {
+// fingerprint_pw64 over a shared-memory copy: sb holds the 8-byte words of
+// the bytes from an 8-aligned position, the key starts rel bytes in
+// (1 <= len <= 4 * kFpPowMax).
+__device__ __forceinline__ uint64_t fingerprint_sm64(const uint64_t* sb, uint32_t rel, uint32_t len,
+                                                     const FpPow* pw) {
   if (len == 0) return 0;
-  const uint32_t a0 = rel >> 2, sh = (rel & 3) * 8;
-  const uint32_t last = (rel + len - 1) >> 2;
-  const uint32_t nw = (len + 3) >> 2;
-  uint64_t acc = 0;
-  uint32_t cur = sb[a0];
-  for (uint32_t i = 0; i < nw; i++) {
-    const uint32_t na = a0 + i + 1;
-    const uint32_t nxt = na <= last ? sb[na] : 0u;
-    uint32_t w = sh ? __funnelshift_r(cur, nxt, sh) : cur;
-    const uint32_t rem = len - 4 * i;
-    if (rem < 4) w &= (1u << (8 * rem)) - 1u;
-    acc += mul32_p(w, pw->lo[nw - i], pw->hi[nw - i]);
-    acc = (acc & kP) + (acc >> 61);
+  const uint32_t a0 = rel >> 3, sh = (rel & 7) * 8, last = (rel + len - 1) >> 3, nw = (len + 3) >> 2;
+  uint64_t cur = sb[a0], acc = 0;
+  for (uint32_t i = 0, k = a0 + 1; i < nw; i += 2, k++) {
+    const uint64_t nxt = k <= last ? sb[k] : 0ull;
+    const uint64_t x = sh ? (cur >> sh) | (nxt << (64 - sh)) : cur;
     cur = nxt;
+    const uint32_t rem = len - 4 * i;
+    uint32_t w0 = uint32_t(x);
+    if (rem < 4) w0 &= (1u << (8 * rem)) - 1u;
+    acc += mul32_p(w0, pw->lo[nw - i], pw->hi[nw - i]);
+    acc = (acc & kP) + (acc >> 61);
+    if (i + 1 < nw) {
+      uint32_t w1 = uint32_t(x >> 32);
+      if (rem - 4 < 4) w1 &= (1u << (8 * (rem - 4))) - 1u;
+      acc += mul32_p(w1, pw->lo[nw - i - 1], pw->hi[nw - i - 1]);
+      acc = (acc & kP) + (acc >> 61);
+    }
   }
   uint64_t f = acc + len;
   f = (f & kP) + (f >> 61);
