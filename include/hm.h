@@ -58,10 +58,28 @@ typedef enum {
 typedef struct hm_map hm_map; /* opaque; immutable after build; bound to its device */
 
 /* Build options.  NULL means all defaults. */
+/* Allocator hooks for the arrays a map owns.  alloc returns
+ * `bytes` of device memory of the current device, at least 16-B aligned,
+ * usable in stream order on `stream` (NULL: failure -> HM_ERR_OOM); free gets
+ * back the pointer and the size it was allocated with. */
+typedef void* (*hm_alloc_fn)(size_t bytes, void* stream, void* ctx);
+typedef void (*hm_free_fn)(void* ptr, size_t bytes, void* stream, void* ctx);
+
 typedef struct {
   uint64_t seed;       /* table seed: selects the constant schedule (R6). default 0  */
   uint32_t log2_bp;    /* 0 = auto. log2 of the level-1 buckets per build partition   */
   uint32_t flags;      /* 0, or HM_FLAG_* below; other bits -> HM_ERR_INVALID_ARG     */
+  /* NULL, NULL: the library's stream-ordered pool (cudaMallocAsync, with freed
+   * maps' arrays cached per size, see hm_release_workspace).  Both set: every
+   * array the built map owns (directory, compact directory, slots, the byte
+   * context copy) comes from alloc(bytes, build stream, alloc_ctx) and returns
+   * through free(ptr, bytes, stream, alloc_ctx) — from hm_free (stream NULL,
+   * after a device synchronisation) or, on a failed build, on the build
+   * stream.  Build scratch stays library-managed.  One hook alone:
+   * HM_ERR_INVALID_ARG. */
+  hm_alloc_fn alloc;
+  hm_free_fn free;
+  void* alloc_ctx;
 } hm_opts;
 
 /* Lookups of this map bypass the L2-resident compact directory and read the

@@ -1333,8 +1333,18 @@ static std::multimap<std::pair<int, size_t>, void*> g_mapcache;
 static size_t g_mapcache_bytes = 0;
 constexpr size_t kMapCacheCap = size_t(32) << 30;
 
+thread_local UserAlloc tl_user_alloc;
+
 hm_status map_alloc(void** p, size_t bytes, cudaStream_t st) {
   bytes = std::max<size_t>(bytes, 16);
+  if (tl_user_alloc.alloc) {
+    *p = tl_user_alloc.alloc(bytes, reinterpret_cast<void*>(st), tl_user_alloc.ctx);
+    if (!*p) {
+      set_error("the user allocator (hm_opts.alloc) returned NULL for " + std::to_string(bytes) + " bytes");
+      return HM_ERR_OOM;
+    }
+    return HM_OK;
+  }
   int dev = 0;
   HM_CUDA_TRY(cudaGetDevice(&dev));
   {
@@ -1348,6 +1358,12 @@ hm_status map_alloc(void** p, size_t bytes, cudaStream_t st) {
     }
   }
   return dmalloc(p, bytes, st);
+}
+
+void map_discard(void* p, size_t bytes, cudaStream_t st) {
+  if (!p) return;
+  if (tl_user_alloc.free) tl_user_alloc.free(p, std::max<size_t>(bytes, 16), reinterpret_cast<void*>(st), tl_user_alloc.ctx);
+  else cudaFreeAsync(p, st);
 }
 
 void map_release(void* p, size_t bytes) {
@@ -1454,21 +1470,21 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
   const size_t dir_bytes = nb * 8, cdir_bytes = ((nb + 31) / 32) * sizeof(CDir);
   if ((s = map_alloc(reinterpret_cast<void**>(&dir), dir_bytes, st)) != HM_OK) return s;
   if ((s = map_alloc(reinterpret_cast<void**>(&cdir), cdir_bytes, st)) != HM_OK) {
-    cudaFreeAsync(dir, st);
+    map_discard(dir, dir_bytes, st);
     return s;
   }
   const double sn = double(n_in);
   uint64_t slot_cap = uint64_t(2.0 * sn + 8.0 * std::sqrt(2.0 * sn + 1.0) + 1024.0);
   if (n_in <= 4096) slot_cap = std::max<uint64_t>(slot_cap, 4 * std::max<uint64_t>(n_in, 1));
   if ((s = map_alloc(reinterpret_cast<void**>(&slots), slot_cap * sizeof(E), st)) != HM_OK) {
-    cudaFreeAsync(dir, st);
-    cudaFreeAsync(cdir, st);
+    map_discard(dir, dir_bytes, st);
+    map_discard(cdir, cdir_bytes, st);
     return s;
   }
   auto fail = [&](hm_status code) {
-    cudaFreeAsync(dir, st);
-    cudaFreeAsync(cdir, st);
-    cudaFreeAsync(slots, st);
+    map_discard(dir, dir_bytes, st);
+    map_discard(cdir, cdir_bytes, st);
+    map_discard(slots, slot_cap * sizeof(E), st);
     return code;
   };
 
@@ -1622,13 +1638,13 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
       if (hs.S > 4 * n_global || hs.bound_fail) break;  // R7: redraw level one
       if (hs.slot_overflow && !(hs.bound_fail)) {
         // more slots than the allocation: grow to exactly S and rerun K_B
-        cudaFreeAsync(slots, st);
+        map_discard(slots, slot_cap * sizeof(E), st);
         slots = nullptr;
         slot_cap = hs.S;
         bp.slot_cap = slot_cap;
         if ((s = map_alloc(reinterpret_cast<void**>(&slots), slot_cap * sizeof(E), st)) != HM_OK) {
-          cudaFreeAsync(dir, st);
-          cudaFreeAsync(cdir, st);
+          map_discard(dir, dir_bytes, st);
+          map_discard(cdir, cdir_bytes, st);
           return s;
         }
         continue;
@@ -1639,8 +1655,11 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
       if (t1_fixed < 0) continue;
       // a shard with a fixed t1: report the failed bound, the caller redraws
       out->dir = dir;
-    out->cdir = cdir;
+      out->cdir = cdir;
       out->slots = slots;
+      out->bytes[0] = dir_bytes;
+      out->bytes[1] = cdir_bytes;
+      out->bytes[2] = slot_cap * sizeof(E);
       out->S = std::max<uint64_t>(hs.S, 4 * n_global + 1);
       out->t1 = t1;
       return HM_OK;

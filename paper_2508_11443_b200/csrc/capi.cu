@@ -182,6 +182,16 @@ struct Staged {
   }
 };
 
+static bool hooks_ok(const hm_opts* o) { return !o || (!o->alloc) == (!o->free); }
+
+// the map takes the user's free hook when its arrays came from the user's alloc
+static void adopt_hooks(hm_map* m) {
+  if (tl_user_alloc.alloc) {
+    m->ufree = tl_user_alloc.free;
+    m->uctx = tl_user_alloc.ctx;
+  }
+}
+
 static hm_map* new_map() {
   hm_map* m = new hm_map;
   std::memset(m, 0, sizeof(*m));
@@ -275,6 +285,8 @@ hm_status hm_build_u64(const uint64_t* keys, const uint64_t* vals, uint64_t n, c
   if (opts && (opts->flags & ~uint32_t(HM_FLAG_FULL_DIRECTORY | HM_FLAG_DIRECT_SLOTS | HM_FLAG_NO_ROUND0_ILP |
                                          HM_FLAG_FROM_ARRAY | HM_FLAG_ROUNDS)))
     return HM_ERR_INVALID_ARG;
+  if (!hooks_ok(opts)) return HM_ERR_INVALID_ARG;
+  UserAllocScope ua_(opts);
   hm_status s = check_device();
   if (s != HM_OK) return s;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -313,6 +325,7 @@ hm_status hm_build_u64(const uint64_t* keys, const uint64_t* vals, uint64_t n, c
   m->cdir = bo.cdir;
   m->slots = bo.slots;
   for (int a = 0; a < 3; a++) m->abytes[a] = bo.bytes[a];
+  adopt_hooks(m);
   *out = m;
   return HM_OK;
 }
@@ -328,6 +341,8 @@ hm_status hm_build_bytes(const uint8_t* bytes, const uint64_t* offsets, const ui
   if (opts && (opts->flags & ~uint32_t(HM_FLAG_FULL_DIRECTORY | HM_FLAG_DIRECT_SLOTS | HM_FLAG_NO_ROUND0_ILP |
                                          HM_FLAG_FROM_ARRAY)))
     return HM_ERR_INVALID_ARG;
+  if (!hooks_ok(opts)) return HM_ERR_INVALID_ARG;
+  UserAllocScope ua_(opts);
   hm_status s = check_device();
   if (s != HM_OK) return s;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -388,9 +403,21 @@ hm_status hm_build_bytes(const uint8_t* bytes, const uint64_t* offsets, const ui
   m->cdir = bo.cdir;
   m->slots = bo.slots;
   for (int a = 0; a < 3; a++) m->abytes[a] = bo.bytes[a];
+  adopt_hooks(m);
   m->ctx_bytes = on - o0;
   void* c = nullptr;
-  cudaError_t e = cudaMallocAsync(&c, std::max<uint64_t>(m->ctx_bytes + 16, 16), st);
+  cudaError_t e = cudaSuccess;
+  if (tl_user_alloc.alloc) {
+    m->ctx_alloc = std::max<uint64_t>(m->ctx_bytes + 16, 16);
+    c = tl_user_alloc.alloc(m->ctx_alloc, stream, tl_user_alloc.ctx);
+    if (!c) {
+      hm_free(m);
+      set_error("the user allocator (hm_opts.alloc) returned NULL for the context copy");
+      return HM_ERR_OOM;
+    }
+  } else {
+    e = cudaMallocAsync(&c, std::max<uint64_t>(m->ctx_bytes + 16, 16), st);
+  }
   if (e != cudaSuccess) {
     hm_free(m);
     return cuda_fail(e, "context copy");
@@ -562,10 +589,14 @@ void hm_free(hm_map* map) {
   void* arr[3] = {map->dir, map->cdir, map->slots};
   for (int a = 0; a < 3; a++) {
     if (!arr[a]) continue;
-    if (map->abytes[a]) map_release(arr[a], map->abytes[a]);
+    if (map->ufree) map->ufree(arr[a], map->abytes[a], nullptr, map->uctx);
+    else if (map->abytes[a]) map_release(arr[a], map->abytes[a]);
     else cudaFree(arr[a]);
   }
-  if (map->ctx) cudaFree(map->ctx);
+  if (map->ctx) {
+    if (map->ufree) map->ufree(map->ctx, map->ctx_alloc, nullptr, map->uctx);
+    else cudaFree(map->ctx);
+  }
   if (cur != map->device) cudaSetDevice(cur);
   delete map;
 }
@@ -619,6 +650,8 @@ hm_status hm_assemble_u64(const uint64_t* dir, const void* slots, uint64_t n, ui
   if (!dir || !slots || S == 0) return HM_ERR_INVALID_ARG;
   if (n > (1ull << 30) || S > 4 * n) return HM_ERR_TOO_LARGE;
   if (t1 >= kT1Cap || (opts && (opts->flags & ~uint32_t(HM_FLAG_FULL_DIRECTORY)))) return HM_ERR_INVALID_ARG;
+  if (!hooks_ok(opts)) return HM_ERR_INVALID_ARG;
+  UserAllocScope ua_(opts);
   hm_status s = check_device();
   if (s != HM_OK) return s;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -626,7 +659,7 @@ hm_status hm_assemble_u64(const uint64_t* dir, const void* slots, uint64_t n, ui
   void* arr[3] = {nullptr, nullptr, nullptr};
   auto fail = [&](hm_status code) {
     for (int a = 0; a < 3; a++)
-      if (arr[a]) cudaFreeAsync(arr[a], st);
+      if (arr[a]) map_discard(arr[a], bytes[a], st);
     return code;
   };
   for (int a = 0; a < 3; a++)
@@ -672,6 +705,7 @@ hm_status hm_assemble_u64(const uint64_t* dir, const void* slots, uint64_t n, ui
   m->cdir = static_cast<CDir*>(arr[1]);
   m->slots = arr[2];
   for (int a = 0; a < 3; a++) m->abytes[a] = bytes[a];
+  adopt_hooks(m);
   *out = m;
   return HM_OK;
 }
@@ -699,6 +733,8 @@ hm_status hm_build_u64_shard(const uint64_t* keys, const uint64_t* vals, uint64_
   if (n_global > (1ull << 30)) return HM_ERR_TOO_LARGE;
   if (b_hi < b_lo || b_hi > n_global || t1 >= kT1Cap) return HM_ERR_INVALID_ARG;
   if (n_recv && (!keys || !vals)) return HM_ERR_INVALID_ARG;
+  if (!hooks_ok(opts)) return HM_ERR_INVALID_ARG;
+  UserAllocScope ua_(opts);
   hm_status s = check_device();
   if (s != HM_OK) return s;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -739,6 +775,7 @@ hm_status hm_build_u64_shard(const uint64_t* keys, const uint64_t* vals, uint64_
   m->cdir = bo.cdir;
   m->slots = bo.slots;
   for (int a = 0; a < 3; a++) m->abytes[a] = bo.bytes[a];
+  adopt_hooks(m);
   *S_local = bo.S;
   *out = m;
   return HM_OK;

@@ -90,6 +90,9 @@ struct hm_map {
   uint64_t smix;
   uint64_t r_fp;         // byte keys: fingerprint point (a1 of derive(seed,0,0,t0))
   size_t abytes[3];      // map_alloc sizes of dir, cdir, slots (0: plain cudaMalloc)
+  hm_free_fn ufree;      // the user's free hook (hm_opts) when the arrays came from its alloc
+  void* uctx;
+  size_t ctx_alloc;      // allocation size of ctx (user hook)
   uint64_t* dir;         // nb entries, local soff
   hm::CDir* cdir;        // compact lookup directory, ceil(nb/32) records
   void* slots;           // S records
@@ -127,6 +130,23 @@ struct BuildOut {
 // freed arrays are kept, up to a cap, for the next build of the same sizes.
 hm_status map_alloc(void** p, size_t bytes, cudaStream_t st);
 void map_release(void* p, size_t bytes);
+// A map array that is not handed out (a failed build): back to the user's
+// free hook when one is active on this thread, else to the pool.
+void map_discard(void* p, size_t bytes, cudaStream_t st);
+// The user's allocator hooks of the build running on this thread (hm_opts),
+// set by the C-ABI entry points for the duration of a build.
+struct UserAlloc {
+  hm_alloc_fn alloc = nullptr;
+  hm_free_fn free = nullptr;
+  void* ctx = nullptr;
+};
+extern thread_local UserAlloc tl_user_alloc;
+struct UserAllocScope {
+  explicit UserAllocScope(const hm_opts* o) {
+    tl_user_alloc = o && o->alloc && o->free ? UserAlloc{o->alloc, o->free, o->alloc_ctx} : UserAlloc{};
+  }
+  ~UserAllocScope() { tl_user_alloc = UserAlloc{}; }
+};
 // t1_fixed < 0: search t1 = 0..15 with the space bound of this table.
 hm_status release_workspace();
 hm_status build_u64_core(const uint64_t* keys, const uint64_t* vals, uint64_t n_in, uint64_t n_global,

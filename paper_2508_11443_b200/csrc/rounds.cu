@@ -385,11 +385,12 @@ hm_status build_u64_rounds(const uint64_t* keys, const uint64_t* vals, uint64_t 
   CDir* cdir = nullptr;
   KV16* slots = nullptr;
   std::vector<void*> res;
+  const size_t bytes_[3] = {n * 8, ((n + 31) / 32) * sizeof(CDir), S * sizeof(KV16)};
+  const size_t* bytes = bytes_;
   auto fail = [&](hm_status code) {
-    for (void* p : res) cudaFreeAsync(p, st);
+    for (size_t a = 0; a < res.size(); a++) map_discard(res[a], bytes_[a], st);
     return code;
   };
-  const size_t bytes[3] = {n * 8, ((n + 31) / 32) * sizeof(CDir), S * sizeof(KV16)};
   void* arr[3] = {nullptr, nullptr, nullptr};
   for (int a = 0; a < 3; a++) {
     if ((s = map_alloc(&arr[a], bytes[a], st)) != HM_OK) return fail(s);

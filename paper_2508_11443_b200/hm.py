@@ -44,8 +44,13 @@ class HMError(RuntimeError):
         super().__init__(f"hm status {code} ({self.name}){': ' + detail if detail else ''}")
 
 
+ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+
+
 class _Opts(C.Structure):
-    _fields_ = [("seed", C.c_uint64), ("log2_bp", C.c_uint32), ("flags", C.c_uint32)]
+    _fields_ = [("seed", C.c_uint64), ("log2_bp", C.c_uint32), ("flags", C.c_uint32),
+                ("alloc", ALLOC_FN), ("free", FREE_FN), ("alloc_ctx", C.c_void_p)]
 
 
 class _Header(C.Structure):
@@ -143,8 +148,32 @@ FLAG_FROM_ARRAY = 8  # HM_FLAG_FROM_ARRAY: from_array (duplicates allowed, first
 FLAG_ROUNDS = 16  # HM_FLAG_ROUNDS: the paper's sortless round-based construction (ablation, u64 keys)
 
 
+_allocator = None  # (alloc, free) ctypes callbacks of set_allocator
+_allocators_alive = []  # every pair ever set: maps built with one call its free hook until hm_free
+
+
+def set_allocator(alloc=None, free=None):
+    """Allocator hooks (hm_opts.alloc / .free) for the arrays of the maps built
+    from now on in this process: alloc(bytes, stream) -> device pointer (int),
+    free(ptr, bytes, stream).  None, None: the library's own pool.  Maps keep
+    the hooks they were built with until hm_free."""
+    global _allocator
+    if (alloc is None) != (free is None):
+        raise ValueError("set both hooks or neither")
+    if alloc is None:
+        _allocator = None
+        return
+    a = ALLOC_FN(lambda n, st, ctx: alloc(int(n), st) or None)
+    f = FREE_FN(lambda p, n, st, ctx: free(int(p), int(n), st))
+    _allocator = (a, f)
+    _allocators_alive.append(_allocator)
+
+
 def _opts(seed: int, log2_bp: int = 0, flags: int = 0):
-    return _Opts(seed & ((1 << 64) - 1), log2_bp, flags)
+    o = _Opts(seed & ((1 << 64) - 1), log2_bp, flags)
+    if _allocator is not None:
+        o.alloc, o.free = _allocator
+    return o
 
 
 @dataclass

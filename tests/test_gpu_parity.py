@@ -410,3 +410,48 @@ def test_u64_lookup_host_buffers_pipelined(pinned):
     m.contains(hq, hf2)
     assert torch.equal(hf2, df.cpu())
     m.free()
+
+
+def test_user_allocator_hooks():
+    """hm_opts.alloc / .free: every array a map owns comes from
+    the hook (here torch's caching allocator) and goes back through it in
+    hm_free, also on a failed build; the maps are the oracle's."""
+    hm = _hm()
+    live, calls = {}, {"alloc": 0, "free": 0}
+
+    def alloc(n, st):
+        p = torch.cuda.caching_allocator_alloc(n, device=0, stream=st or 0)
+        live[p] = n
+        calls["alloc"] += 1
+        return p
+
+    def free(p, n, st):
+        assert live.pop(p) == n
+        calls["free"] += 1
+        torch.cuda.caching_allocator_delete(p)
+
+    hm.set_allocator(alloc, free)
+    try:
+        n = 100_003
+        keys, vals = gen.u64_keys(n), gen.u64_values(n)
+        m = hm.HashMap.build_u64(dev(keys), dev(vals), seed=2)
+        assert calls["alloc"] == 3 and len(live) == 3
+        assert_table_equal(m, O.build_u64(keys, vals, 2))
+        m.free()
+        assert not live and calls["free"] == 3
+        ctx, offs = gen.string_keys(5000)
+        bv = gen.u64_values(5000)
+        mb = hm.HashMap.build_bytes(torch.from_numpy(ctx).cuda(), dev(offs), dev(bv), seed=1)
+        assert len(live) == 4  # dir, compact dir, slots, context copy
+        assert_table_equal(mb, O.build_bytes(ctx, offs, bv, 1))
+        mb.free()
+        assert not live
+        keys[777] = keys[3]
+        with pytest.raises(hm.HMError) as e:
+            hm.HashMap.build_u64(dev(keys), dev(vals))
+        assert e.value.name == "DUPLICATE_KEY" and not live
+    finally:
+        hm.set_allocator(None, None)
+    m = hm.HashMap.build_u64(dev(keys[:10]), dev(vals[:10]))  # the library's pool again
+    assert not live
+    m.free()
