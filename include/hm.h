@@ -51,7 +51,7 @@ typedef enum {
   HM_ERR_TOO_LARGE = 6,      /* n > 2^30, or a byte key longer than 65535 bytes (R23)     */
   HM_ERR_OOM = 7,            /* device allocation failed                                   */
   HM_ERR_CUDA = 8,           /* a CUDA runtime error (detail in hm_last_error)             */
-  HM_ERR_NCCL = 9,           /* reserved for the fused multi-GPU path                     */
+  HM_ERR_NCCL = 9,           /* an NCCL call of hm_*_dist failed (detail in hm_last_error) */
   HM_ERR_NO_DEVICE = 10      /* no CUDA device / wrong architecture                       */
 } hm_status;
 
@@ -273,6 +273,28 @@ hm_status hm_route_u64(const uint64_t* keys, const uint64_t* vals, uint64_t n_lo
                        uint64_t n_global, uint64_t seed, uint32_t t1, int world,
                        uint64_t* send_keys, uint64_t* send_vals, uint64_t* send_counts,
                        void* stream);
+
+/* hm_build_u64_dist — collective build of the bucket-range-sharded table over
+ * an NCCL communicator.  Every rank of
+ * `nccl_comm` (an ncclComm_t, e.g. torch's ProcessGroupNCCL._comm_ptr(); the
+ * library uses the libnccl.so.2 the process has loaded) calls it with its own
+ * keys/vals[n_local] (device pointers): the global n is their sum; rank r
+ * receives the shard of level-1 buckets [ceil(r n / G), ceil((r+1) n / G)).
+ * The shards together are exactly the single table hm_build_u64 builds from
+ * the union of the keys (hm_export of a shard writes global soff).  All ranks
+ * return the same status (max over ranks); duplicates anywhere in the union:
+ * HM_ERR_DUPLICATE_KEY.  Synchronous on `stream`.  Free with hm_free. */
+hm_status hm_build_u64_dist(const uint64_t* keys, const uint64_t* vals, uint64_t n_local, const hm_opts* opts,
+                            void* stream, void* nccl_comm, hm_map** out);
+
+/* hm_lookup_u64_dist — collective lookup on the shards of hm_build_u64_dist:
+ * each rank passes its own queries q[nq] (device) and receives its own
+ * answers in out_vals / out_found (device, as hm_lookup_u64).  Queries are
+ * routed to the owner of their level-1 bucket, answered there and routed
+ * back.  Every rank must call it (nq may be 0).  Synchronous for the count
+ * exchange; the results are complete in `stream` order. */
+hm_status hm_lookup_u64_dist(const hm_map* shard, const uint64_t* q, uint64_t nq, uint64_t* out_vals,
+                             uint8_t* out_found, void* stream, void* nccl_comm);
 
 /* hm_build_u64_shard — build the shard of the global table that holds level-1
  * buckets [b_lo, b_hi) of a table with n_global keys, from exactly the keys

@@ -94,7 +94,9 @@ def lib():
         L.hm_route_queries_u64.argtypes = [p, p, u64, i32, p, p, p, p]
         L.hm_unroute_u64.argtypes = [p, p, p, u64, p, p, p]
         L.hm_assemble_u64.argtypes = [p, p, u64, u64, u64, u32, C.POINTER(_Opts), p, C.POINTER(p)]
-        for f in ("hm_assemble_u64", "hm_build_u64", "hm_build_bytes", "hm_lookup_u64", "hm_lookup_bytes", "hm_info", "hm_export",
+        L.hm_build_u64_dist.argtypes = [p, p, u64, C.POINTER(_Opts), p, p, C.POINTER(p)]
+        L.hm_lookup_u64_dist.argtypes = [p, p, u64, p, p, p, p]
+        for f in ("hm_assemble_u64", "hm_build_u64_dist", "hm_lookup_u64_dist", "hm_build_u64", "hm_build_bytes", "hm_lookup_u64", "hm_lookup_bytes", "hm_info", "hm_export",
                   "hm_route_u64", "hm_build_u64_shard", "hm_shard_set_base", "hm_route_queries_u64",
                   "hm_unroute_u64"):
             getattr(L, f).restype = C.c_int
@@ -373,6 +375,29 @@ def build_u64_shard(keys, vals, n_global: int, b_lo: int, b_hi: int, t1: int, se
     _check(lib().hm_build_u64_shard(kp, vp, _numel(keys), n_global, b_lo, b_hi, t1, C.byref(o), _stream(stream),
                                     C.byref(h), C.byref(S)))
     return HashMap(h.value, 0), int(S.value)
+
+
+def build_u64_dist(keys, vals, nccl_comm: int, seed: int = 0, stream=None, log2_bp: int = 0) -> "HashMap":
+    """Collective sharded build over an NCCL communicator (hm_build_u64_dist;
+    e.g. nccl_comm = the process group's backend ._comm_ptr())."""
+    kp, kk = _ptr(keys)
+    vp, vk = _ptr(vals)
+    h = C.c_void_p()
+    o = _opts(seed, log2_bp)
+    _check(lib().hm_build_u64_dist(kp, vp, _numel(keys), C.byref(o), _stream(stream), C.c_void_p(int(nccl_comm)),
+                                   C.byref(h)))
+    return HashMap(h.value, 0)
+
+
+def lookup_u64_dist(shard: "HashMap", q, nccl_comm: int, out_vals=None, out_found=None, stream=None):
+    """Collective routed lookup on the shards of build_u64_dist (hm_lookup_u64_dist)."""
+    nq = _numel(q)
+    out_vals, out_found = shard._outputs(q, nq, out_vals, out_found)
+    qp, qk = _ptr(q)
+    vp, vk = _ptr(out_vals)
+    fp, fk = _ptr(out_found)
+    _check(lib().hm_lookup_u64_dist(shard._h, qp, nq, vp, fp, _stream(stream), C.c_void_p(int(nccl_comm))))
+    return out_vals, out_found
 
 
 def unroute_u64(vals_routed, found_routed, perm, out_vals, out_found, stream=None):

@@ -178,5 +178,19 @@ def test_dist_build_and_lookup_through_nccl_one_rank():
         assert np.array_equal(host(rv), ov) and np.array_equal(host(rf), of)
         rep.free()
         dist.free_dist(dm)
+        # the same through the single C calls over the process group's communicator
+        from paper_2508_11443_b200 import hm
+        comm = tdist.distributed_c10d._get_default_group()._get_backend(torch.device("cuda", 0))._comm_ptr()
+        m = hm.build_u64_dist(dev(keys), dev(vals), comm, seed=3)
+        d, sl, _ = m.export()
+        assert d.tobytes() == ot.dir.tobytes() and sl.tobytes() == ot.slots.tobytes()
+        v, f = hm.lookup_u64_dist(m, dev(q), comm)
+        assert np.array_equal(host(v), ov) and np.array_equal(host(f), of)
+        dup = keys.copy()
+        dup[5] = dup[99]
+        with pytest.raises(hm.HMError) as e:
+            hm.build_u64_dist(dev(dup), dev(vals), comm)
+        assert e.value.name == "DUPLICATE_KEY"
+        m.free()
     finally:
         tdist.destroy_process_group()
