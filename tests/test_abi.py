@@ -54,3 +54,28 @@ def test_header_layout_matches_oracle():
     assert hm.HEADER_DTYPE == O.HEADER_DTYPE and hm.HEADER_DTYPE.itemsize == 56
     assert C.sizeof(hm._Header) == 56
     assert hm.SLOT_U64_DTYPE.itemsize == 16 and hm.SLOT_BYTES_DTYPE.itemsize == 32
+
+
+def test_opts_layout_hooks_and_dist_argument_errors():
+    L = hm.lib()
+    assert C.sizeof(hm._Opts) == 40  # seed, log2_bp, flags, alloc, free, alloc_ctx
+    out = C.c_void_p()
+    k = np.zeros(4, np.uint64)
+    kp = k.ctypes.data_as(C.c_void_p)
+    o = hm._opts(0)
+    o.alloc = hm.ALLOC_FN(lambda n, st, ctx: None)  # one hook without the other
+    assert L.hm_build_u64(kp, kp, 4, C.byref(o), None, C.byref(out)) == 1
+    assert L.hm_build_u64_dist(kp, kp, 4, None, None, None, C.byref(out)) == 1  # no communicator
+    assert L.hm_lookup_u64_dist(None, kp, 4, kp, None, None, None) == 1
+    assert L.hm_assemble_u64(kp, kp, 0, 1, 0, 0, None, None, C.byref(out)) == 2  # n == 0
+    assert L.hm_assemble_u64(kp, kp, 4, 17, 0, 0, None, None, C.byref(out)) == 6  # S > 4n
+    assert L.hm_assemble_u64(kp, kp, 4, 16, 0, 16, None, None, C.byref(out)) == 1  # t1 >= 16
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    import subprocess
+    import sys
+    code = "from paper_2508_11443_b200 import hm\ntry:\n    hm.lib()\nexcept RuntimeError as e:\n    print('raised', e)\n"
+    env = dict(os.environ, HM_LIB_PATH=str(tmp_path / "nope.so"), PYTHONPATH=ROOT)
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=120)
+    assert "raised" in r.stdout, r.stdout + r.stderr
