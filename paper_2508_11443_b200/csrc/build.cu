@@ -318,12 +318,15 @@ constexpr int kSThreads = 512;
 #ifndef HM_SPLIT_PT
 #define HM_SPLIT_PT 6
 #endif
+#ifndef HM_SPLIT_PT_BYTES
+#define HM_SPLIT_PT_BYTES 4
+#endif
 #ifndef HM_SPLIT_MINB
 #define HM_SPLIT_MINB 2
 #endif
 template <class E>
 __host__ __device__ constexpr int split_pt() {
-  return sizeof(E) == 16 ? HM_SPLIT_PT : 4;
+  return sizeof(E) == 16 ? HM_SPLIT_PT : HM_SPLIT_PT_BYTES;
 }
 template <class E>
 __host__ __device__ constexpr int split_tile() {
