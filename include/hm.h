@@ -283,7 +283,10 @@ hm_status hm_route_u64(const uint64_t* keys, const uint64_t* vals, uint64_t n_lo
  * The shards together are exactly the single table hm_build_u64 builds from
  * the union of the keys (hm_export of a shard writes global soff).  All ranks
  * return the same status (max over ranks); duplicates anywhere in the union:
- * HM_ERR_DUPLICATE_KEY.  Synchronous on `stream`.  Free with hm_free. */
+ * HM_ERR_DUPLICATE_KEY.  Synchronous on `stream`.  Free with hm_free.
+ * A rank that fails before the status agreement (a device allocation, an
+ * NCCL error) returns alone and leaves the others inside NCCL: abort the
+ * communicator (ncclCommAbort) as for any collective. */
 hm_status hm_build_u64_dist(const uint64_t* keys, const uint64_t* vals, uint64_t n_local, const hm_opts* opts,
                             void* stream, void* nccl_comm, hm_map** out);
 
