@@ -98,8 +98,8 @@ typedef struct {
  * the map is the one the default build (from_array_nodup) makes from the
  * distinct keys — hm_info's n is their number; byte keys are compared by
  * content and the distinct ones are packed in input order into the map's
- * context.  Byte keys repeated so heavily that a dedup partition overflows:
- * HM_ERR_TOO_LARGE in this version. */
+ * context (any duplication pattern; heavy duplication of byte keys takes a
+ * global fingerprint set confirmed by content). */
 #define HM_FLAG_FROM_ARRAY 8u
 /* Ablation (u64 keys only; byte keys -> HM_ERR_INVALID_ARG): build level two
  * with the paper's sortless round-based construction (PAPER.md:443-499,

@@ -289,6 +289,88 @@ __global__ void k_pack_kept(const uint8_t* __restrict__ bytes, const uint64_t* _
   }
 }
 
+// Byte keys, the fallback of heavy duplication (a dedup partition overflowed):
+// the global set keyed by fingerprint, every hit confirmed by content against
+// the slot's current lowest index (all indices in a slot hold equal bytes),
+// so equal fingerprints of different keys take different slots.
+__global__ void k_dedup_insert_bytes(const uint8_t* __restrict__ bytes, const uint64_t* __restrict__ offs,
+                                     const uint64_t* __restrict__ fp, uint64_t n, uint64_t mask, DedupSlot* set) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t f = fp[i], o = offs[i];
+    const uint32_t len = uint32_t(offs[i + 1] - o);
+    uint64_t h = dedup_slot(f, mask);
+    const uint64_t mine = (i << 32) | kSlotReady;
+    while (true) {
+      uint64_t* meta = &set[h].meta;
+      uint64_t m = ld_acquire_u64(meta);
+      if ((m & 3) == kSlotEmpty) {
+        if (atomicCAS(reinterpret_cast<unsigned long long*>(meta), m, (i << 32) | kSlotBusy) == m) {
+          set[h].key = f;
+          st_release_u64(meta, mine);
+          break;
+        }
+        continue;
+      }
+      while ((m & 3) == kSlotBusy) m = ld_acquire_u64(meta);
+      if (set[h].key == f) {
+        const uint64_t r = m >> 32, ro = offs[r];
+        if (offs[r + 1] - ro == len && bytes_equal(bytes + ro, bytes + o, len)) {
+          if (mine < m) atomicMin(reinterpret_cast<unsigned long long*>(meta), mine);
+          break;
+        }
+      }
+      h = (h + 1) & mask;
+    }
+  }
+}
+
+__global__ void k_dedup_keep_bytes(const uint8_t* __restrict__ bytes, const uint64_t* __restrict__ offs,
+                                   const uint64_t* __restrict__ fp, uint64_t n, uint64_t mask,
+                                   const DedupSlot* __restrict__ set, uint8_t* __restrict__ keep) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t f = fp[i], o = offs[i];
+    const uint32_t len = uint32_t(offs[i + 1] - o);
+    uint64_t h = dedup_slot(f, mask);
+    while (true) {
+      const DedupSlot sl = set[h];
+      if (sl.key == f) {
+        const uint64_t r = sl.meta >> 32, ro = offs[r];
+        if (offs[r + 1] - ro == len && bytes_equal(bytes + ro, bytes + o, len)) {
+          keep[i] = r == i ? 1 : 0;
+          break;
+        }
+      }
+      h = (h + 1) & mask;
+    }
+  }
+}
+
+static hm_status dedup_global_bytes(const uint8_t* bytes, const uint64_t* offs, const uint64_t* fp, uint64_t n,
+                                    cudaStream_t st, uint8_t* keep) {
+  uint64_t cap = 1024;
+  while (cap < 2 * n) cap <<= 1;
+  DedupSlot* set = nullptr;
+  if (cudaMallocAsync(reinterpret_cast<void**>(&set), cap * sizeof(DedupSlot), st) != cudaSuccess) {
+    cudaGetLastError();
+    set_error("from_array: out of device memory for the dedup set");
+    return HM_ERR_OOM;
+  }
+  HM_CUDA_TRY(cudaMemsetAsync(set, 0, cap * sizeof(DedupSlot), st));
+  const unsigned g = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, uint64_t(num_sms()) * 8)));
+  {
+    LaunchScope ls_("k_dedup_insert_bytes", st);
+    k_dedup_insert_bytes<<<g, 256, 0, st>>>(bytes, offs, fp, n, cap - 1, set);
+  }
+  {
+    LaunchScope ls_("k_dedup_keep_bytes", st);
+    k_dedup_keep_bytes<<<g, 256, 0, st>>>(bytes, offs, fp, n, cap - 1, set, keep);
+  }
+  const cudaError_t e = cudaGetLastError();
+  cudaFreeAsync(set, st);
+  if (e != cudaSuccess) return cuda_fail(e, "dedup_global_bytes");
+  return HM_OK;
+}
+
 hm_status dedup_bytes(const uint8_t* bytes, const uint64_t* offs, const uint64_t* vals, uint64_t n, cudaStream_t st,
                       uint8_t** out_ctx, uint64_t** out_offs, uint64_t** out_vals, uint64_t* n_out) {
   *out_ctx = nullptr;
@@ -319,11 +401,12 @@ hm_status dedup_bytes(const uint8_t* bytes, const uint64_t* offs, const uint64_t
   HM_CUDA_TRY(cudaMemsetAsync(keep, 0, n, st));
   HM_CUDA_TRY(cudaStreamSynchronize(st));
   hm_status s = dedup_partitioned_bytes(bytes, offs, fp, vals, n, o0, st, keep);
+  if (s == HM_ERR_TOO_LARGE) {  // heavy duplication: the global set decides every key
+    set_error("");
+    s = dedup_global_bytes(bytes, offs, fp, n, st, keep);
+  }
   if (s != HM_OK) {
     release();
-    if (s == HM_ERR_TOO_LARGE)
-      set_error("from_array on byte keys: heavy duplication overflowed a dedup partition; not supported in this "
-                "version");
     return s;
   }
   const unsigned g = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, uint64_t(num_sms()) * 8)));

@@ -455,3 +455,25 @@ def test_user_allocator_hooks():
     m = hm.HashMap.build_u64(dev(keys[:10]), dev(vals[:10]))  # the library's pool again
     assert not live
     m.free()
+
+
+def test_bytes_from_array_heavy_duplication():
+    """Byte keys repeated so often that a dedup partition overflows take the
+    global fingerprint set (content-confirmed); the map equals the oracle's
+    from_array: 300 000 copies of one string among 2 000 distinct ones."""
+    hm = _hm()
+    strs = [bytes(x) for x in gen.string_list(*gen.string_keys(2000))]
+    idx = np.random.default_rng(5).integers(0, 2000, size=20_000)
+    keys = [strs[i] for i in idx] + [strs[7]] * 300_000 + [b""] * 1000
+    ctx, offs = gen.pack_bytes_list(keys)
+    vals = gen.u64_values(len(keys), lo=9)
+    ot = O.from_array_bytes(ctx, offs, vals, 4)
+    hm.profile_read()
+    hm.profile_enable(True)
+    m = hm.HashMap.build_bytes(torch.from_numpy(ctx).cuda(), dev(offs), dev(vals), seed=4, flags=hm.FLAG_FROM_ARRAY)
+    st = hm.profile_read()
+    hm.profile_enable(False)
+    assert "k_dedup_insert_bytes" in st  # (the global set decided)
+    assert m.info().n == ot.n
+    assert_table_equal(m, ot)
+    m.free()
