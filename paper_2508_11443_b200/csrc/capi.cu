@@ -304,8 +304,19 @@ hm_status hm_build_u64(const uint64_t* keys, const uint64_t* vals, uint64_t n, c
     n = nu;
   }
   BuildOut bo;
-  if (opts && (opts->flags & HM_FLAG_ROUNDS)) s = build_u64_rounds(dk, dv, n, seed, opts->flags, st, &bo);
-  else s = build_u64_core(dk, dv, n, n, 0, n, -1, seed, opts ? (opts->log2_bp | (opts->flags << 16)) : 0, st, &bo);
+  if (opts && (opts->flags & HM_FLAG_ROUNDS)) {
+    s = build_u64_rounds(dk, dv, n, seed, opts->flags, st, &bo);
+  } else {
+    s = build_u64_core(dk, dv, n, n, 0, n, -1, seed, opts ? (opts->log2_bp | (opts->flags << 16)) : 0, st, &bo);
+    // a degenerate level-1 distribution within the space bound (a bucket of more
+    // than 32 keys, an overflowing build partition: many equal keys, or an
+    // adversarial key set) is outside the partitioned search; the flat rounds
+    // handle any bucket size and report equal keys as DUPLICATE_KEY
+    if (s == HM_ERR_TOO_LARGE) {
+      set_error("");
+      s = build_u64_rounds(dk, dv, n, seed, opts ? opts->flags : 0u, st, &bo);
+    }
+  }
   if (uk) {
     cudaFreeAsync(uk, st);
     cudaFreeAsync(uv, st);

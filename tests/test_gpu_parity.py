@@ -270,7 +270,8 @@ def test_u64_duplicate_heavy_overflow_matches_oracle():
     """Thousands of copies of one key overflow a build partition; the GPU
     recounts the suspect partitions for the space bound (R7) and, like the
     oracle, exhausts level one (SEED_EXHAUSTED, R26).  With the bound holding
-    (a huge n) such an input is outside this version (TOO_LARGE)."""
+    (a huge n) the build falls back to the flat rounds (any bucket size), which
+    report the equal keys as the oracle does (DUPLICATE_KEY)."""
     hm = _hm()
     n = 200_000
     keys = gen.u64_keys(n)
@@ -286,7 +287,7 @@ def test_u64_duplicate_heavy_overflow_matches_oracle():
     keys[:1500] = keys[11]
     with pytest.raises(hm.HMError) as e:
         hm.HashMap.build_u64(dev(keys), dev(gen.u64_values(n)))
-    assert e.value.name == "TOO_LARGE"
+    assert e.value.name == "DUPLICATE_KEY"  # (the bound holds: the flat rounds take over and find them)
     # the map and the workspace stay usable after the degenerate builds
     keys, vals = gen.u64_keys(5000), gen.u64_values(5000)
     m = hm.HashMap.build_u64(dev(keys), dev(vals))
@@ -476,4 +477,33 @@ def test_bytes_from_array_heavy_duplication():
     assert "k_dedup_insert_bytes" in st  # (the global set decided)
     assert m.info().n == ot.n
     assert_table_equal(m, ot)
+    m.free()
+
+
+def test_u64_bucket_over_32_keys_takes_the_flat_rounds():
+    """33 distinct keys in one level-1 bucket within the space bound: outside
+    the partitioned search (s <= 32), so the build falls back to the flat
+    rounds (HM_FLAG_ROUNDS' kernels, any s) — the table is still the oracle's."""
+    hm = _hm()
+    n, seed = 1024, 0
+    c1 = O.derive(seed, 1, 0, 0)
+    cand = gen.u64_keys(120_000, lo=77)
+    b0 = O.hash_(c1, int(cand[0])) % n
+    same, other = [], []
+    for k in cand:
+        b = O.hash_(c1, int(k)) % n
+        if b == b0 and len(same) < 33:
+            same.append(k)
+        elif b != b0 and len(other) < n - 33:
+            other.append(k)
+        if len(same) == 33 and len(other) == n - 33:
+            break
+    keys = np.array(same + other, dtype=np.uint64)
+    vals = gen.u64_values(n, lo=1)
+    ot = O.build_u64(keys, vals, seed)
+    assert int(ot.header["t1"]) == 0 and (ot.dir >> np.uint64(40) & np.uint64(0xFFFF)).max() == 33
+    m = hm.HashMap.build_u64(dev(keys), dev(vals), seed=seed)
+    assert_table_equal(m, ot)
+    gv, gf = m.lookup(dev(keys))
+    assert bool(gf.all()) and np.array_equal(host(gv), vals)
     m.free()
