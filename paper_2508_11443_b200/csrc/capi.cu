@@ -398,6 +398,21 @@ hm_status hm_build_bytes(const uint8_t* bytes, const uint64_t* offsets, const ui
   uint32_t t0 = 0;
   uint64_t r = 0;
   s = build_bytes_core(db, doff, dv, n, seed, opts ? (opts->log2_bp | (opts->flags << 16)) : 0, st, &bo, &t0, &r);
+  if (s == HM_ERR_TOO_LARGE && !(opts && (opts->flags & HM_FLAG_FROM_ARRAY))) {
+    // a degenerate level-1 distribution within the bound: equal keys (the
+    // oracle's DUPLICATE_KEY) are found by counting the distinct ones
+    const std::string why = hm_last_error();
+    uint8_t* pc = nullptr;
+    uint64_t *po = nullptr, *pv = nullptr, mdist = 0;
+    if (dedup_bytes(db, doff, dv, n, st, &pc, &po, &pv, &mdist) == HM_OK) {
+      for (void* q : {static_cast<void*>(pc), static_cast<void*>(po), static_cast<void*>(pv)}) cudaFreeAsync(q, st);
+      if (mdist < n) {
+        set_error("duplicate keys in from_array_nodup input");
+        return HM_ERR_DUPLICATE_KEY;
+      }
+    }
+    set_error(why);
+  }
   if (s != HM_OK) return s;
   hm_map* m = new_map();
   m->key_kind = 1;

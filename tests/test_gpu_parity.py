@@ -507,3 +507,16 @@ def test_u64_bucket_over_32_keys_takes_the_flat_rounds():
     gv, gf = m.lookup(dev(keys))
     assert bool(gf.all()) and np.array_equal(host(gv), vals)
     m.free()
+
+
+def test_bytes_duplicate_heavy_reports_duplicate_key():
+    """Byte keys from_array_nodup with 1 500 copies of one string among 2*10^6
+    (the space bound holds): equal keys are reported as DUPLICATE_KEY, as the
+    oracle does, not TOO_LARGE."""
+    hm = _hm()
+    strs = gen.string_list(*gen.string_keys(2_000_000))
+    keys = strs[:1_998_500] + [strs[3]] * 1500
+    ctx, offs = gen.pack_bytes_list(keys)
+    with pytest.raises(hm.HMError) as e:
+        hm.HashMap.build_bytes(torch.from_numpy(ctx).cuda(), dev(offs), dev(gen.u64_values(len(keys))))
+    assert e.value.name == "DUPLICATE_KEY"
