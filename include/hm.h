@@ -306,7 +306,9 @@ hm_status hm_lookup_u64_dist(const hm_map* shard, const uint64_t* q, uint64_t nq
  * if it fails.  On return *S_local holds the shard's slot count.  The shard's
  * global slot base (exclusive prefix of S_r over ranks) is set with
  * hm_shard_set_base.  Errors as hm_build_u64 (duplicates within the shard are
- * reported; SEED_EXHAUSTED only for level-2 exhaustion). Synchronous. */
+ * reported; SEED_EXHAUSTED only for level-2 exhaustion). Synchronous.
+ * opts->flags: FULL_DIRECTORY and the construction testing knobs only
+ * (FROM_ARRAY, ROUNDS: HM_ERR_INVALID_ARG — single-table paths). */
 hm_status hm_build_u64_shard(const uint64_t* keys, const uint64_t* vals, uint64_t n_recv,
                              uint64_t n_global, uint64_t b_lo, uint64_t b_hi, uint32_t t1,
                              const hm_opts* opts, void* stream, hm_map** out, uint64_t* S_local);

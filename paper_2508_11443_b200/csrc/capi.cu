@@ -760,6 +760,9 @@ hm_status hm_build_u64_shard(const uint64_t* keys, const uint64_t* vals, uint64_
   if (b_hi < b_lo || b_hi > n_global || t1 >= kT1Cap) return HM_ERR_INVALID_ARG;
   if (n_recv && (!keys || !vals)) return HM_ERR_INVALID_ARG;
   if (!hooks_ok(opts)) return HM_ERR_INVALID_ARG;
+  // (from_array and the rounds ablation are single-table paths)
+  if (opts && (opts->flags & ~uint32_t(HM_FLAG_FULL_DIRECTORY | HM_FLAG_DIRECT_SLOTS | HM_FLAG_NO_ROUND0_ILP)))
+    return HM_ERR_INVALID_ARG;
   UserAllocScope ua_(opts);
   hm_status s = check_device();
   if (s != HM_OK) return s;

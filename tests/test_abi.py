@@ -79,3 +79,13 @@ def test_missing_library_fails_loudly(tmp_path):
     env = dict(os.environ, HM_LIB_PATH=str(tmp_path / "nope.so"), PYTHONPATH=ROOT)
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=120)
     assert "raised" in r.stdout, r.stdout + r.stderr
+
+
+def test_shard_build_rejects_single_table_flags():
+    L = hm.lib()
+    out, S = C.c_void_p(), C.c_uint64()
+    k = np.zeros(4, np.uint64)
+    kp = k.ctypes.data_as(C.c_void_p)
+    for f in (hm.FLAG_FROM_ARRAY, hm.FLAG_ROUNDS):
+        o = hm._opts(0, 0, f)
+        assert L.hm_build_u64_shard(kp, kp, 4, 8, 0, 4, 0, C.byref(o), None, C.byref(out), C.byref(S)) == 1
