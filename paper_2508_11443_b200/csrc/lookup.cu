@@ -84,7 +84,10 @@ __device__ __forceinline__ uint64_t ld_q(const uint64_t* p, uint64_t pol) {
 __device__ __forceinline__ CDir ld_cdir(const CDir* p, uint64_t pol) {
   CDir r;
   uint64_t a, b, c, d;
-  asm volatile("ld.global.cg.L2::cache_hint.L2::64B.v4.u64 {%0, %1, %2, %3}, [%4], %5;"
+#ifndef HM_CDIR_PF
+#define HM_CDIR_PF "128B"  // (neighbouring records are reused: 2^26 lookups 1.46 -> 1.41 ms vs 64B)
+#endif
+  asm volatile("ld.global.cg.L2::cache_hint.L2::" HM_CDIR_PF ".v4.u64 {%0, %1, %2, %3}, [%4], %5;"
                : "=l"(a), "=l"(b), "=l"(c), "=l"(d)
                : "l"(p), "l"(pol));
   r.w[0] = uint32_t(a);
