@@ -651,3 +651,173 @@ void or_level1_buckets(const uint64_t* keys, uint64_t m, uint64_t n, uint64_t se
   or_derive(seed, 1, 0, t1, c1);
   for (uint64_t i = 0; i < m; i++) out[i] = or_hash(c1, keys[i]) % n;
 }
+
+/* ------------------------------------------- T-thread variant (CPU baseline)
+ * SURVEY §8(d) "Oracle timing": the same construction with the level-1
+ * buckets split into T contiguous ranges, one thread per range — the
+ * multi-GPU partitioning (§8(e)) on host threads.  Steps, in the order of
+ * or_fks: level one (hash every key, shape by atomic increments, S; redraw
+ * t1 while S > 4n, R7); offsets = presum(shape^2) and the group starts; the
+ * keys grouped by bucket (any order inside a bucket: make2's first successful
+ * t, the member slots and the lowest-slot filler do not depend on it); then
+ * each thread runs make2 (the same or_make2) over its bucket range and writes
+ * that range's directory entries and slots.  Same table as or_build_u64 (a
+ * test checks the bytes); timing only, never called by the product. */
+#include <pthread.h>
+
+typedef struct {
+  const uint64_t* keys; const uint64_t* vals; uint64_t n, seed;
+  uint32_t t1; int T, id;
+  uint64_t* hashes; uint32_t* shape; uint64_t* offs; uint64_t* gstart; uint64_t* gcur; uint64_t* gitems;
+  uint64_t* dir; or_slot_u64* slots;
+  uint64_t partS; int dup, exhausted;
+} or_mt_arg;
+
+static void* or_mt_level1(void* p) {
+  or_mt_arg* a = (or_mt_arg*)p;
+  uint64_t c1[3];
+  or_derive(a->seed, 1, 0, a->t1, c1);
+  uint64_t lo = a->n * a->id / a->T, hi = a->n * (a->id + 1) / a->T;
+  for (uint64_t i = lo; i < hi; i++) {
+    a->hashes[i] = or_hash(c1, a->keys[i]) % a->n;
+    __atomic_fetch_add(&a->shape[a->hashes[i]], 1u, __ATOMIC_RELAXED);
+  }
+  return NULL;
+}
+
+static void* or_mt_sq(void* p) {
+  or_mt_arg* a = (or_mt_arg*)p;
+  uint64_t lo = a->n * a->id / a->T, hi = a->n * (a->id + 1) / a->T, S = 0;
+  for (uint64_t b = lo; b < hi; b++) S += (uint64_t)a->shape[b] * a->shape[b];
+  a->partS = S;
+  return NULL;
+}
+
+static void* or_mt_group(void* p) {
+  or_mt_arg* a = (or_mt_arg*)p;
+  uint64_t lo = a->n * a->id / a->T, hi = a->n * (a->id + 1) / a->T;
+  for (uint64_t i = lo; i < hi; i++) {
+    uint64_t pos = __atomic_fetch_add(&a->gcur[a->hashes[i]], 1ull, __ATOMIC_RELAXED);
+    a->gitems[pos] = i;
+  }
+  return NULL;
+}
+
+static void* or_mt_level2(void* p) {
+  or_mt_arg* a = (or_mt_arg*)p;
+  uint64_t lo = a->n * a->id / a->T, hi = a->n * (a->id + 1) / a->T;
+  uint64_t* bkeys = (uint64_t*)malloc(sizeof(uint64_t) * 64);
+  uint64_t* bhs = (uint64_t*)malloc(sizeof(uint64_t) * 64);
+  uint64_t cap = 64;
+  for (uint64_t b = lo; b < hi; b++) {
+    uint64_t s = a->shape[b], soff = a->offs[b];
+    const uint64_t* items = a->gitems + a->gstart[b];
+    if (s == 0) { a->dir[b] = OR_DIR(soff, 0, 0); continue; }
+    int skip = 0;
+    for (uint64_t i = 0; i < s && !skip; i++)
+      for (uint64_t j = i + 1; j < s; j++)
+        if (a->keys[items[i]] == a->keys[items[j]]) { a->dup = 1; skip = 1; break; }
+    if (skip) { a->dir[b] = OR_DIR(soff, s, 0); continue; }
+    if (s > cap) {
+      cap = s;
+      bkeys = (uint64_t*)realloc(bkeys, sizeof(uint64_t) * cap);
+      bhs = (uint64_t*)realloc(bhs, sizeof(uint64_t) * cap);
+    }
+    int t = 0;
+    if (s == 1) bhs[0] = 0; /* R12 */
+    else {
+      for (uint64_t i = 0; i < s; i++) bkeys[i] = a->keys[items[i]];
+      t = or_make2(a->seed, b, bkeys, s, bhs);
+      if (t < 0) { a->exhausted = 1; a->dir[b] = OR_DIR(soff, s, 0); continue; }
+    }
+    a->dir[b] = OR_DIR(soff, s, (uint64_t)t);
+    /* the bucket's slots (R10): members at h, the rest
+     * the member at the lowest occupied slot with value 0 */
+    uint64_t low = 0;
+    for (uint64_t i = 1; i < s; i++) if (bhs[i] < bhs[low]) low = i;
+    for (uint64_t j = 0; j < s * s; j++) {
+      a->slots[soff + j].key = a->keys[items[low]];
+      a->slots[soff + j].value = 0;
+    }
+    for (uint64_t i = 0; i < s; i++) {
+      a->slots[soff + bhs[i]].key = a->keys[items[i]];
+      a->slots[soff + bhs[i]].value = a->vals[items[i]];
+    }
+  }
+  free(bkeys);
+  free(bhs);
+  return NULL;
+}
+
+static void or_mt_run(or_mt_arg* args, int T, void* (*fn)(void*)) {
+  pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * T);
+  for (int i = 0; i < T; i++) pthread_create(&th[i], NULL, fn, &args[i]);
+  for (int i = 0; i < T; i++) pthread_join(th[i], NULL);
+  free(th);
+}
+
+int or_build_u64_mt(const uint64_t* keys, const uint64_t* vals, uint64_t n, uint64_t seed, int T,
+                    or_table** out) {
+  *out = NULL;
+  if (n == 0) return OR_ERR_EMPTY;
+  if (!keys || !vals || T < 1) return OR_ERR_INVALID_ARG;
+  if (n > OR_MAX_N) return OR_ERR_TOO_LARGE;
+  uint64_t* hashes = (uint64_t*)malloc(sizeof(uint64_t) * n);
+  uint32_t* shape = (uint32_t*)malloc(sizeof(uint32_t) * n);
+  uint64_t* offs = (uint64_t*)malloc(sizeof(uint64_t) * (n + 1));
+  uint64_t* gstart = (uint64_t*)malloc(sizeof(uint64_t) * (n + 1));
+  uint64_t* gcur = (uint64_t*)malloc(sizeof(uint64_t) * n);
+  uint64_t* gitems = (uint64_t*)malloc(sizeof(uint64_t) * n);
+  uint64_t* dir = (uint64_t*)malloc(sizeof(uint64_t) * n);
+  or_mt_arg* args = (or_mt_arg*)calloc(T, sizeof(or_mt_arg));
+  if (!hashes || !shape || !offs || !gstart || !gcur || !gitems || !dir || !args) return OR_ERR_OOM;
+  for (int i = 0; i < T; i++) {
+    args[i] = (or_mt_arg){keys, vals, n, seed, 0, T, i, hashes, shape, offs, gstart, gcur, gitems, dir, NULL, 0, 0, 0};
+  }
+  uint32_t t1 = 0;
+  uint64_t S = 0;
+  for (;; t1++) {
+    if (t1 >= OR_T1_CAP) {
+      free(hashes); free(shape); free(offs); free(gstart); free(gcur); free(gitems); free(dir); free(args);
+      return OR_ERR_SEED_EXHAUSTED;
+    }
+    memset(shape, 0, sizeof(uint32_t) * n);
+    for (int i = 0; i < T; i++) args[i].t1 = t1;
+    or_mt_run(args, T, or_mt_level1);
+    or_mt_run(args, T, or_mt_sq);
+    S = 0;
+    for (int i = 0; i < T; i++) S += args[i].partS;
+    if (S <= 4 * n) break;
+  }
+  /* presums (sequential: one pass over n) */
+  uint64_t acc = 0, accg = 0;
+  for (uint64_t b = 0; b < n; b++) {
+    offs[b] = acc;
+    gstart[b] = accg;
+    gcur[b] = accg;
+    acc += (uint64_t)shape[b] * shape[b];
+    accg += shape[b];
+  }
+  offs[n] = acc;
+  gstart[n] = accg;
+  or_mt_run(args, T, or_mt_group);
+  or_slot_u64* slots = (or_slot_u64*)calloc(S ? S : 1, sizeof(or_slot_u64));
+  for (int i = 0; i < T; i++) args[i].slots = slots;
+  or_mt_run(args, T, or_mt_level2);
+  int dup = 0, exhausted = 0;
+  for (int i = 0; i < T; i++) { dup |= args[i].dup; exhausted |= args[i].exhausted; }
+  free(hashes); free(shape); free(offs); free(gstart); free(gcur); free(gitems); free(args);
+  if (dup || exhausted) { free(dir); free(slots); return dup ? OR_ERR_DUPLICATE_KEY : OR_ERR_SEED_EXHAUSTED; }
+  or_table* t = (or_table*)calloc(1, sizeof(or_table));
+  t->hdr.magic = OR_MAGIC;
+  t->hdr.spec_version = OR_SPEC_VERSION;
+  t->hdr.key_kind = 0;
+  t->hdr.n = n;
+  t->hdr.S = S;
+  t->hdr.seed = seed;
+  t->hdr.t1 = t1;
+  t->dir = dir;
+  t->slots = slots;
+  *out = t;
+  return OR_OK;
+}

@@ -55,7 +55,7 @@ def build_lib(force: bool = False) -> str:
     """Compile the oracle with gcc (plain C, -O2)."""
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
         tmp = LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", "-O2", "-std=gnu11", "-shared", "-fPIC", "-o", tmp, SRC])
+        subprocess.check_call(["gcc", "-O2", "-std=gnu11", "-shared", "-fPIC", "-pthread", "-o", tmp, SRC])
         os.replace(tmp, LIB)
     return LIB
 
@@ -97,6 +97,7 @@ def lib():
         L.or_table_ctx.argtypes = [p]
         L.or_sizeof_header.restype = u64
         L.or_level1_buckets.argtypes = [p, u64, u64, u64, u32, p]
+        L.or_build_u64_mt.argtypes = [p, p, u64, u64, C.c_int, C.POINTER(C.c_void_p)]
         L.or_level1_S.restype = u64
         L.or_level1_S.argtypes = [p, u64, u64, u32, p]
         assert L.or_sizeof_header() == HEADER_DTYPE.itemsize
@@ -231,6 +232,18 @@ def build_u64(keys, vals, seed: int = 0) -> Table:
     h = C.c_void_p()
     st = lib().or_build_u64(_ptr(keys) if len(keys) else None, _ptr(vals) if len(vals) else None,
                             len(keys), seed, C.byref(h))
+    if st != 0:
+        raise OracleError(st)
+    return _wrap(h.value, 0)
+
+
+def build_u64_mt(keys, vals, seed: int = 0, threads: int = 0) -> Table:
+    """The T-thread oracle (bucket ranges per thread): the same
+    table as build_u64; CPU-baseline timing only."""
+    keys, vals = _u64(keys), _u64(vals)
+    T = threads or os.cpu_count() or 1
+    h = C.c_void_p()
+    st = lib().or_build_u64_mt(_ptr(keys), _ptr(vals), len(keys), seed, T, C.byref(h))
     if st != 0:
         raise OracleError(st)
     return _wrap(h.value, 0)

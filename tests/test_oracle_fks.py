@@ -290,3 +290,23 @@ def test_oracle_from_array_first_occurrence_wins():
     vals3 = np.concatenate([v2, np.full(500, 7, np.uint64)])
     c = O.from_array_u64(keys3, vals3, 1)
     assert c.dir.tobytes() == b.dir.tobytes() and c.slots.tobytes() == b.slots.tobytes()
+
+
+@pytest.mark.parametrize("n,seed,T", [(1, 0, 4), (5, 3, 2), (1000, 1, 3), (70_001, 7, 8), (1 << 17, 0, 5)])
+def test_threaded_oracle_builds_the_same_table(n, seed, T):
+    """The T-thread oracle (bucket ranges per thread, the CPU
+    baseline of bench.py) is the same construction: identical table bytes, and
+    the same status on degenerate inputs."""
+    keys, vals = gen.u64_keys(n), gen.u64_values(n)
+    a = O.build_u64(keys, vals, seed)
+    b = O.build_u64_mt(keys, vals, seed, T)
+    assert a.header_bytes() == b.header_bytes()
+    assert a.dir.tobytes() == b.dir.tobytes() and a.slots.tobytes() == b.slots.tobytes()
+    if n >= 1000:
+        k2 = keys.copy()
+        k2[n // 2] = k2[3]
+        with pytest.raises(O.OracleError) as e1:
+            O.build_u64(k2, vals, seed)
+        with pytest.raises(O.OracleError) as e2:
+            O.build_u64_mt(k2, vals, seed, T)
+        assert e1.value.name == e2.value.name == "DUPLICATE_KEY"
