@@ -59,9 +59,11 @@ typedef struct hm_map hm_map; /* opaque; immutable after build; bound to its dev
 
 /* Build options.  NULL means all defaults. */
 /* Allocator hooks for the arrays a map owns.  alloc returns
- * `bytes` of device memory of the current device, at least 16-B aligned,
- * usable in stream order on `stream` (NULL: failure -> HM_ERR_OOM); free gets
- * back the pointer and the size it was allocated with. */
+ * `bytes` of device memory of the current device, 32-B aligned (the slot and
+ * compact-directory records are read with 32-byte vector loads; a pointer that
+ * is not 32-B aligned is handed back to free and the build returns
+ * HM_ERR_INVALID_ARG), usable in stream order on `stream` (NULL: failure ->
+ * HM_ERR_OOM); free gets back the pointer and the size it was allocated with. */
 typedef void* (*hm_alloc_fn)(size_t bytes, void* stream, void* ctx);
 typedef void (*hm_free_fn)(void* ptr, size_t bytes, void* stream, void* ctx);
 

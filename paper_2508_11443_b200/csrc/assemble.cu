@@ -30,7 +30,7 @@ __global__ void k_assemble_cdir(const uint64_t* __restrict__ dir, const KV16* __
       t = uint32_t(d >> 56);
       const uint64_t next = b + 1 < n ? (dir[b + 1] & kMask40) : S;
       bool ok = so + uint64_t(s) * s == next && (b != 0 || so == 0) && (s >= 2 || t == 0);
-      if (ok && s == 1) t = tag4_of_hash(hash64(l1.c1, slots[so].key));  // the singleton tag (§6.2)
+      if (ok && s == 1 && so < S) t = tag4_of_hash(hash64(l1.c1, slots[so].key));  // the singleton tag (§6.2)
       if (!ok) atomicOr(bad, 1u);
     }
     uint32_t pa = __ballot_sync(0xffffffffu, s & 4), pb = __ballot_sync(0xffffffffu, s & 2),

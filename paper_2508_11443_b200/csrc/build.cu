@@ -54,6 +54,10 @@ struct KBCfg {
   static constexpr int W = T / 32;
   static constexpr int MINB = sizeof(E) == 16 ? HM_KB_MINB : HM_KB_MINB_BYTES;
 };
+#ifndef HM_R0_TWO
+#define HM_R0_TWO 1  // round 0: attempts 0 and 1 per lane (s <= 4)
+#endif
+constexpr bool kR0Two = HM_R0_TWO != 0;
 #ifndef HM_RETRY_LOGA
 #define HM_RETRY_LOGA 3  // at most 2^3 lanes (attempts) per queued bucket and round
 #endif
@@ -461,14 +465,12 @@ __global__ void __launch_bounds__(kSThreads, HM_SPLIT_MINB) k_split(Src src, Bui
 //          a warp-ballot rank over 11 bucket bits (scripts/micro/smem_atomics.cu)
 //   scan   exclusive scans of s and s^2 (presum, R1/R2) and of
 //          the size-class counts; groupby as a counting scatter
-//   search make2 per multi-key bucket (search_* above); a
-//          finished bucket maps its s^2 slots to their source items: members,
-//          and the lowest-slot member as value-0 filler elsewhere (R10)
+//   search make2 per multi-key bucket in CTA-wide rounds
+//          (below); a finished bucket maps its s^2 slots to their source items:
+//          members, and the lowest-slot member as value-0 filler elsewhere (R10)
 //   out    decoupled look-back for the global slot base, then the slots
 //          (consecutive lanes -> consecutive 16/32-byte records), the directory
 //          and the compact directory.
-// Size classes of multi-key buckets for the search: s=2, 3..8 (a thread per
-// bucket and attempt, K = 2/8 key registers) and 9..32 (a warp per bucket).
 constexpr int kNCls = 3;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -478,31 +480,36 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 // make2 for buckets with 2 <= s <= 8, in CTA-wide rounds.
 // One attempt = derive(seed,2,b,t), the s level-2 slots hash mod s^2 and the
 // occupancy bitmap as `collision`.  Round 0 gives every
-// multi-key bucket a lane (attempts 0 and 1 in flight for s <= 4, attempt 0 for
-// the paired s = 2 lanes and s = 5..8); the buckets that still collide are
-// queued, and every later round tries A consecutive attempts of each queued
-// bucket on A adjacent lanes (A = lanes / queue length, up to 8), the lowest
-// successful attempt winning — the same t as trying them one by one (R13),
-// without the long per-bucket chains that leave most lanes idle.
+// multi-key bucket one lane and attempt t = 0, the list ordered by size class
+// (s = 5..8 | 3..4 | 2) so that the lanes of a warp share one key-register
+// width K; warps take 32-bucket chunks from a shared counter (dynamic
+// balance).  The buckets that collide go to the next round's list (s >= 3 from
+// the front, s = 2 from the back: the order by width again), and round r >= 1
+// tries attempts tb .. tb + A - 1 of each listed bucket on A adjacent lanes
+// (A = lanes / list length, at most 2^HM_RETRY_LOGA); the lowest successful
+// lane wins — the same t as trying them one by one (R13).  Every attempt is
+// one lane's work from start to end, so the instruction count follows the
+// attempts actually made (SASS attribution in profiles/r02/).
 
-// Search state shared by the rounds (shared memory).
+// Search state (shared memory).
 struct SearchCtx {
   const uint16_t* sstart;
   const uint8_t* ss;
   const uint16_t* sidx;
   const uint32_t* soff;  // slot offset of each bucket inside the partition
-  uint16_t* sA;
-  uint8_t* s_t;
-  uint16_t* src;  // slot -> item map (nullptr: not staged)
+  uint16_t* sA;          // level-2 slot of each grouped position (direct-slot partitions only)
+  uint8_t* s_t;          // attempt t of each bucket (the next attempt to try while searching)
+  uint16_t* src;         // slot -> item map (nullptr: not staged)
 };
 
-
-// Slots h[] of bucket lb under constants c (K keys in registers); returns the
+// Slots h[] of a bucket under constants c (K keys in registers); returns the
 // occupancy bitmap, or 0 on a collision (s >= 2, so a valid map is never 0).
+// For K <= 4 (s^2 <= 16) the bitmap is 32-bit.
 template <int K>
 __device__ __forceinline__ uint64_t slots_of(const Consts& c, const uint64_t* k, uint32_t s, const FastMod& fm,
                                              uint32_t* h) {
-  uint64_t bits = 0;
+  using B = typename std::conditional<(K <= 4), uint32_t, uint64_t>::type;
+  B bits = 0;
   bool coll = false;
 #pragma unroll
   for (int j = 0; j < K; j++) {
@@ -510,237 +517,147 @@ __device__ __forceinline__ uint64_t slots_of(const Consts& c, const uint64_t* k,
     if (uint32_t(j) < s) {
       const uint64_t hv = hash64(c, k[j]);
       h[j] = (K == 2 || (s & (s - 1)) == 0) ? uint32_t(hv) & (s * s - 1) : uint32_t(fastmod(hv, fm));
-      const uint64_t bit = 1ull << h[j];
+      const B bit = B(1) << h[j];
       coll |= (bits & bit) != 0;
       bits |= bit;
     }
   }
-  return coll ? 0ull : bits;
+  return coll ? 0ull : uint64_t(bits);
 }
 
-// bucket_done with the slots already in registers.
+// A finished bucket: its t, and its s^2 slots in the slot source map — member
+// j at h[j], every other slot the member at the lowest occupied slot with
+// value 0 (R10, bit 15): every slot is first written as filler (unrolled
+// predicated stores) and the members over them.
 template <int K>
-__device__ __forceinline__ void bucket_done_regs(const SearchCtx& X, uint32_t lb, uint32_t st0, uint32_t s,
-                                                 uint32_t t, const uint32_t* h, uint64_t bits) {
+__device__ __forceinline__ void bucket_done(const SearchCtx& X, uint32_t lb, uint32_t st0, uint32_t s, uint32_t t,
+                                            const uint32_t* h, uint64_t bits) {
   X.s_t[lb] = uint8_t(t);
-  uint32_t hmin = 0xFFFFu, fill = 0;
-  uint32_t it[K];
+  uint32_t it[K], hmin = 0xFFFFu, fill = 0;
 #pragma unroll
   for (int j = 0; j < K; j++)
     if (uint32_t(j) < s) {
       it[j] = X.sidx[st0 + j];
-      X.sA[st0 + j] = uint16_t(h[j]);
       if (h[j] < hmin) {
         hmin = h[j];
         fill = it[j];
       }
     }
-  if (X.src) {
-    uint16_t* o = X.src + X.soff[lb];
-    const uint32_t s2 = s * s;
-    uint64_t fr = ~bits & (s2 == 64 ? ~0ull : ((1ull << s2) - 1));  // the unused slots
-    while (fr) {
-      o[__ffsll(fr) - 1] = uint16_t(fill | 0x8000u);
-      fr &= fr - 1;
-    }
+  if (!X.src) {
 #pragma unroll
     for (int j = 0; j < K; j++)
-      if (uint32_t(j) < s) o[h[j]] = uint16_t(it[j]);
+      if (uint32_t(j) < s) X.sA[st0 + j] = uint16_t(h[j]);
+    return;
   }
+  uint16_t* o = X.src + X.soff[lb];
+  const uint16_t fv = uint16_t(fill | 0x8000u);
+  const uint32_t s2 = s * s;
+#pragma unroll
+  for (int x = 0; x < K * K; x++)
+    if (uint32_t(x) < s2) o[x] = fv;
+#pragma unroll
+  for (int j = 0; j < K; j++)
+    if (uint32_t(j) < s) o[h[j]] = uint16_t(it[j]);
 }
 
-// Round 0 for one bucket with K key registers: attempts t = 0 and t = 1 are
-// evaluated together (two independent derive/hash chains: the second one
-// hides the first one's latency), the lower successful one wins.  Equal keys
-// -> duplicate / fingerprint collision (checked once: equal keys collide under
-// every t).  Returns the first attempt still to try (0: the bucket is done).
-template <int K, bool kTwoOK, class E, class Same>
-__device__ __forceinline__ uint32_t round0_bucket(const BuildParams& bp, const E* skv, const SearchCtx& X, uint32_t lb,
-                                              const uint64_t* s_m2, uint64_t bbase, DevStatus* stt,
-                                              const Same& same) {
-  const uint32_t st0 = X.sstart[lb], s = X.ss[lb];
+// Equal keys in a bucket (a duplicate, or equal fingerprints with different
+// bytes) never separate: record which, once, and retire the bucket.
+template <class E, class Same>
+__device__ __noinline__ bool bucket_equal_keys_(const E* skv, const uint16_t* sstart, const uint8_t* ss,
+                                                const uint16_t* sidx, uint8_t* s_t, uint32_t lb, DevStatus* stt,
+                                                Same same) {
+  const uint32_t st0 = sstart[lb], s = ss[lb];
+  for (uint32_t i = 0; i < s; i++) {
+    const uint32_t ii = sidx[st0 + i];
+    for (uint32_t j = i + 1; j < s; j++) {
+      const uint32_t jj = sidx[st0 + j];
+      if (skv[jj].key == skv[ii].key) {
+        atomicOr(same.same(skv[ii], skv[jj]) ? &stt->dup : &stt->fpcoll, 1u);
+        s_t[lb] = 0;
+        return true;
+      }
+    }
+  }
+  return false;
+}
+template <class E, class Same>
+__device__ __forceinline__ bool bucket_equal_keys(const E* skv, const SearchCtx& X, uint32_t lb, DevStatus* stt,
+                                                  const Same& same) {
+  return bucket_equal_keys_(skv, X.sstart, X.ss, X.sidx, X.s_t, lb, stt, same);
+}
+
+// Attempt t of bucket lb (s keys, K-wide registers) on this lane; with
+// `finish` a success maps the bucket at once.  Returns the occupancy bitmap
+// (0: collision, or no bucket on this lane).  kTwo (round 0, K <= 4):
+// attempts t and t + 1 as two independent chains (the second hides the first
+// one's latency); the lower success wins.  *tw: the successful attempt, else
+// the last one tried.
+template <int K, bool kTwo, class E>
+__device__ __forceinline__ uint64_t lane_attempt(const BuildParams& bp, const E* skv, const SearchCtx& X, bool act,
+                                                 uint32_t lb, uint32_t s, uint32_t t, const uint64_t* s_m2,
+                                                 uint64_t bbase, bool finish, uint32_t* h, uint32_t* tw) {
+  *tw = t;
+  if (!act) return 0;
+  const uint32_t st0 = X.sstart[lb];
   uint64_t k[K];
 #pragma unroll
   for (int j = 0; j < K; j++) k[j] = uint32_t(j) < s ? skv[X.sidx[st0 + j]].key : 0ull;
-  const FastMod fm{uint64_t(s) * s, s_m2[s]};
-  constexpr bool kTwo = kTwoOK && K <= 4;  // (two attempts in flight; the rare s = 5..8 buckets try one)
-  uint32_t h0[K], h1[kTwo ? K : 1];
-  uint64_t b0, b1 = 0;
-  if (kTwo && !(bp.flags & HM_FLAG_NO_ROUND0_ILP)) {
-    const Consts c0 = derive(bp.smix, 2, bbase + lb, 0), c1 = derive(bp.smix, 2, bbase + lb, 1);
-    b0 = slots_of<K>(c0, k, s, fm, h0);
-    b1 = slots_of<K>(c1, k, s, fm, h1);
-  } else {
-    b0 = slots_of<K>(derive(bp.smix, 2, bbase + lb, 0), k, s, fm, h0);
-  }
-  if (b0) {
-    bucket_done_regs<K>(X, lb, st0, s, 0, h0, b0);
-    return 0;
-  }
-  int di = -1, dj = -1;
+  FastMod fm{uint64_t(s) * s, 0};
+  if (K > 2) fm.m = s_m2[s];
+  constexpr bool kT2 = kTwo && K <= 4;
+  uint64_t bits;
+  if (kT2) {
+    uint32_t h1[K];
+    const Consts c0 = derive(bp.smix, 2, bbase + lb, t), c1 = derive(bp.smix, 2, bbase + lb, t + 1);
+    bits = slots_of<K>(c0, k, s, fm, h);
+    const uint64_t b1 = slots_of<K>(c1, k, s, fm, h1);
+    if (!bits) {  // (*tw: the successful attempt, else the last one tried)
 #pragma unroll
-  for (int i = 0; i < K; i++)
-#pragma unroll
-    for (int j = i + 1; j < K; j++)
-      if (uint32_t(j) < s && k[i] == k[j] && di < 0) {
-        di = i;
-        dj = j;
-      }
-  if (di >= 0) {
-    const bool d = same.same(skv[X.sidx[st0 + di]], skv[X.sidx[st0 + dj]]);
-    atomicOr(d ? &stt->dup : &stt->fpcoll, 1u);
-    X.s_t[lb] = 0;
-    return 0;
-  }
-  if (kTwo && !(bp.flags & HM_FLAG_NO_ROUND0_ILP) && b1) {
-    bucket_done_regs<K>(X, lb, st0, s, 1, h1, b1);
-    return 0;
-  }
-  return (kTwo && !(bp.flags & HM_FLAG_NO_ROUND0_ILP)) ? 2 : 1;
-}
-
-// Round 0 over the multi-key list ([s = 5..8 | s = 3..4 | s = 2] regions),
-// one iteration for every warp and one key-register width per warp: the rare
-// s = 5..8 buckets go straight to the queue (t = 0); warps [0, w4) take the
-// s = 3..4 buckets, a lane per bucket with attempts 0 and 1 in flight; the
-// other warps take the s = 2 buckets the same way — and when there are more of
-// them than lanes, the last lanes take two s = 2 buckets each with one attempt
-// per bucket (the same two independent chains per lane).  The buckets that
-// need more attempts are queued.
-template <class E, class Same>
-__device__ __forceinline__ void search_round0(const BuildParams& bp, const E* skv, const SearchCtx& X,
-                                              const uint16_t* list, uint32_t e8, uint32_t e4, uint32_t L,
-                                              uint32_t* queue, uint32_t* qn, const uint64_t* s_m2, uint64_t bbase,
-                                              DevStatus* stt, const Same& same) {
-  const uint32_t lane = threadIdx.x & 31, lt = (1u << lane) - 1u, warp = threadIdx.x >> 5;
-  const uint32_t n4 = e4 - e8, n2 = L - e4;
-  const uint32_t w4 = min((n4 + 31) / 32, uint32_t(KBCfg<E>::W));
-  for (uint32_t x = threadIdx.x; x < e8; x += KBCfg<E>::T) queue[atomicAdd(qn, 1u)] = list[x];
-  uint32_t lb = 0, tn = 0, lb2 = 0, tn2 = 0;
-  if (warp < w4) {
-    for (uint32_t i = warp * 32 + lane; i < n4; i += w4 * 32) {  // (more than one pass only if n4 > 512)
-      lb = list[e8 + i];
-      const uint32_t t = round0_bucket<4, true>(bp, skv, X, lb, s_m2, bbase, stt, same);
-      if (t) queue[atomicAdd(qn, 1u)] = lb | (t << 16);
+      for (int j = 0; j < K; j++) h[j] = h1[j];
+      bits = b1;
+      *tw = t + 1;
     }
   } else {
-    const uint32_t lanes = (KBCfg<E>::W - w4) * 32, e = threadIdx.x - w4 * 32;
-    uint32_t pbase = lanes;  // lanes >= pbase take two s = 2 buckets
-    if (n2 > lanes) {
-      if (n2 - lanes <= lanes) {
-        pbase = lanes - (n2 - lanes);
-      } else {  // (not enough lanes even in pairs: the rest is queued)
-        for (uint32_t x = 2 * lanes + e; x < n2; x += lanes) queue[atomicAdd(qn, 1u)] = list[e4 + x];
-        pbase = 0;
-      }
-    }
-    if (e >= pbase) {
-      const uint32_t i0 = pbase + 2 * (e - pbase);
-      if (i0 < n2) {
-        lb = list[e4 + i0];
-        tn = round0_bucket<2, false>(bp, skv, X, lb, s_m2, bbase, stt, same);
-      }
-      if (i0 + 1 < n2) {
-        lb2 = list[e4 + i0 + 1];
-        tn2 = round0_bucket<2, false>(bp, skv, X, lb2, s_m2, bbase, stt, same);
-      }
-    } else if (e < n2) {
-      lb = list[e4 + e];
-      tn = round0_bucket<2, true>(bp, skv, X, lb, s_m2, bbase, stt, same);
-    }
+    bits = t < kT2Cap ? slots_of<K>(derive(bp.smix, 2, bbase + lb, t), k, s, fm, h) : 0ull;
   }
-#pragma unroll
-  for (int u = 0; u < 2; u++) {
-    const uint32_t tq = u ? tn2 : tn, lq = u ? lb2 : lb;
-    const uint32_t m = __ballot_sync(0xffffffffu, tq != 0);
-    if (m) {
-      const uint32_t leader = __ffs(m) - 1;
-      uint32_t q0 = 0;
-      if (lane == leader) q0 = atomicAdd(qn, uint32_t(__popc(m)));
-      q0 = __shfl_sync(0xffffffffu, q0, leader);
-      if (tq) queue[q0 + __popc(m & lt)] = lq | (tq << 16);
-    }
-  }
+  if (bits && finish) bucket_done<K>(X, lb, st0, s, *tw, h, bits);
+  return bits;
 }
 
-// One attempt of a queued bucket with K key registers; the lowest successful
-// lane of the group finishes the bucket from its registers.  Returns whether
-// this lane's attempt succeeded.
-template <int K, class E>
-__device__ __forceinline__ bool retry_attempt(const BuildParams& bp, const E* skv, const SearchCtx& X, uint32_t lb,
-                                              uint32_t st0, uint32_t s, uint32_t t, const uint64_t* s_m2,
-                                              uint64_t bbase, uint32_t gmask) {
-  uint64_t k[K];
-#pragma unroll
-  for (int j = 0; j < K; j++) k[j] = uint32_t(j) < s ? skv[X.sidx[st0 + j]].key : 0ull;
-  const FastMod fm{uint64_t(s) * s, s_m2[s]};
-  uint32_t h[K];
-  const uint64_t bits = t < kT2Cap ? slots_of<K>(derive(bp.smix, 2, bbase + lb, t), k, s, fm, h) : 0ull;
-  const uint32_t om = __ballot_sync(__activemask(), bits != 0) & gmask;
-  if (bits && (threadIdx.x & 31) == uint32_t(__ffs(om) - 1)) bucket_done_regs<K>(X, lb, st0, s, t, h, bits);
-  return bits != 0;
+// The key-register width follows the largest bucket among the warp's lanes.
+template <bool kTwo, class E>
+__device__ __forceinline__ uint64_t lane_attempt_k(const BuildParams& bp, const E* skv, const SearchCtx& X, bool act,
+                                                   uint32_t lb, uint32_t s, uint32_t t, const uint64_t* s_m2,
+                                                   uint64_t bbase, bool finish, uint32_t* h, uint32_t* tw) {
+  const uint32_t smax = __reduce_max_sync(0xffffffffu, act ? s : 0u);
+  if (smax <= 2) return lane_attempt<2, kTwo>(bp, skv, X, act, lb, s, t, s_m2, bbase, finish, h, tw);
+  if (smax <= 4) return lane_attempt<4, kTwo>(bp, skv, X, act, lb, s, t, s_m2, bbase, finish, h, tw);
+  return lane_attempt<8, false>(bp, skv, X, act, lb, s, t, s_m2, bbase, finish, h, tw);
 }
 
-// Round r >= 1: A = 2^logA adjacent lanes per queued bucket, attempt tb + j on lane j.
-template <class E, class Same>
-__device__ __forceinline__ void search_round(const BuildParams& bp, const E* skv, const SearchCtx& X,
-                                             const uint32_t* queue, uint32_t L, uint32_t logA, uint32_t* nqueue,
-                                             uint32_t* nqn, const uint64_t* s_m2, uint64_t bbase, DevStatus* stt,
-                                             const Same& same, uint32_t first) {
-  // (threads first.. take part; first is a multiple of 32)
+__device__ __forceinline__ void bucket_done_any(const SearchCtx& X, uint32_t lb, uint32_t s, uint32_t t,
+                                                const uint32_t* h, uint64_t bits) {
+  const uint32_t st0 = X.sstart[lb];
+  if (s <= 2) bucket_done<2>(X, lb, st0, s, t, h, bits);
+  else if (s <= 4) bucket_done<4>(X, lb, st0, s, t, h, bits);
+  else bucket_done<8>(X, lb, st0, s, t, h, bits);
+}
+
+// Append lb to the next round's list (s >= 3 at the front, s = 2 at the back),
+// warp-aggregated: one shared atomic per warp and side.
+__device__ __forceinline__ void list_append(bool want, uint32_t lb, uint32_t s, uint16_t* nl, uint32_t lcap,
+                                            uint32_t* ncnt) {
   const uint32_t lane = threadIdx.x & 31, lt = (1u << lane) - 1u;
-  const uint32_t A = 1u << logA, W = L << logA;
-  const uint32_t gmask = A == 32 ? 0xffffffffu : (((1u << A) - 1u) << (lane & ~(A - 1u)));
-  for (uint32_t w0 = (threadIdx.x - first) & ~31u; w0 < W; w0 += KBCfg<E>::T - first) {
-    const uint32_t w = w0 + lane;
-    bool ok = false, lead = false;
-    uint32_t lb = 0, st0 = 0, s = 2, t = 0, tb = 0;
-    if (w < W) {
-      const uint32_t q = queue[w >> logA];
-      lb = q & 0xFFFFu;
-      tb = q >> 16;
-      t = tb + (w & (A - 1u));
-      lead = (w & (A - 1u)) == 0;
-      st0 = X.sstart[lb];
-      s = X.ss[lb];
-      // keys in registers, the winner finishes from its registers (a group
-      // never straddles the two widths: its lanes share the bucket)
-      if (s <= 4) ok = retry_attempt<4>(bp, skv, X, lb, st0, s, t, s_m2, bbase, gmask);
-      else ok = retry_attempt<8>(bp, skv, X, lb, st0, s, t, s_m2, bbase, gmask);
-    }
-    const uint32_t om = __ballot_sync(0xffffffffu, ok) & gmask;
-    bool retry = false;
-    if (lead && om == 0 && tb == 0) {  // equal keys collide under every t: check once
-      for (uint32_t i = 0; i < s && !retry; i++) {
-        const uint32_t ii = X.sidx[st0 + i];
-        for (uint32_t j = i + 1; j < s; j++) {
-          const uint32_t jj = X.sidx[st0 + j];
-          if (skv[jj].key == skv[ii].key) {
-            atomicOr(same.same(skv[ii], skv[jj]) ? &stt->dup : &stt->fpcoll, 1u);
-            X.s_t[lb] = 0;
-            retry = true;  // (marks "handled")
-            break;
-          }
-        }
-      }
-      lead = !retry;
-      retry = false;
-    }
-    if (lead && om == 0) {
-      if (tb + A >= kT2Cap) {
-        atomicOr(&stt->exhausted, 1u);
-        X.s_t[lb] = 0;
-      } else {
-        retry = true;
-      }
-    }
-    const uint32_t m = __ballot_sync(0xffffffffu, retry);
+#pragma unroll
+  for (int side = 0; side < 2; side++) {
+    const bool mine = want && ((s >= 3) == (side == 0));
+    const uint32_t m = __ballot_sync(0xffffffffu, mine);
     if (m) {
       const uint32_t leader = __ffs(m) - 1;
-      uint32_t q0 = 0;
-      if (lane == leader) q0 = atomicAdd(nqn, uint32_t(__popc(m)));
-      q0 = __shfl_sync(0xffffffffu, q0, leader);
-      if (retry) nqueue[q0 + __popc(m & lt)] = lb | ((tb + A) << 16);
+      uint32_t b = 0;
+      if (lane == leader) b = atomicAdd(&ncnt[side], uint32_t(__popc(m)));
+      b = __shfl_sync(0xffffffffu, b, leader) + __popc(m & lt);
+      if (mine) nl[side == 0 ? b : lcap - 1 - b] = uint16_t(lb);
     }
   }
 }
@@ -808,7 +725,7 @@ __host__ __device__ __forceinline__ BucketSmem bucket_smem_layout(uint32_t cap, 
   BucketSmem L;
   L.smax = 2 * cap + 256;  // slots of the partition staged in shared memory (S_p is ~2 cnt)
   if (L.smax > 32768u) L.smax = 32768u;
-  L.cls_off[0] = 0;                           // s = 2..8 (regions s = 2 | 3..4 | 5..8): at most cap/2 buckets
+  L.cls_off[0] = 0;                           // s = 2..8 (regions s = 5..8 | 3..4 | 2): at most cap/2 buckets
   L.cls_off[1] = L.cls_off[0];
   L.cls_off[2] = L.cls_off[1] + cap / 2 + 1;  // s = 9..32: cap/9
   L.cls_off[3] = L.cls_off[2] + cap / 9 + 1;
@@ -819,8 +736,8 @@ __host__ __device__ __forceinline__ BucketSmem bucket_smem_layout(uint32_t cap, 
   L.sA = L.sidx + al16(size_t(cap) * 2);                   // u16[cap]: level-2 slot of a grouped position
   L.src = L.sA + al16(size_t(cap) * 2);                    // u16[smax]: slot -> item (bit 15: filler, value 0)
   L.slist = L.src + al16(size_t(L.smax) * 2);              // u16[]: class lists
-  L.queue = L.slist + al16(size_t(L.cls_off[kNCls]) * 2);  // u32[2][cap/2+1]: search queues (lb | t<<16)
-  L.ss = L.queue + al16(size_t(cap / 2 + 1) * 8);          // u8[BP]: bucket size s
+  L.queue = L.slist + al16(size_t(L.cls_off[kNCls]) * 2);  // u16[3][cap/2+1]: the rounds' lists
+  L.ss = L.queue + al16(size_t(cap / 2 + 1) * 6);          // u8[BP]: bucket size s
   L.sstart = L.ss + al16(BP);                              // u16[BP]: first grouped position of each bucket
   L.soff = L.sstart + al16(size_t(BP) * 2);                // u32[BP]: histogram, then slot offset in the partition
   L.st = L.soff + al16(size_t(BP) * 4);                    // u8[BP]: attempt t of each bucket
@@ -851,7 +768,7 @@ __device__ __forceinline__ void block_excl_scan2(unsigned long long& a, unsigned
   if (warp == 0) {
     unsigned long long u = lane < NW ? s_red[0][lane] : 0ull, v = lane < NW ? s_red[1][lane] : 0ull;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
+    for (int o = 1; o < NW; o <<= 1) {
       const unsigned long long p = __shfl_up_sync(0xffffffffu, u, o), q = __shfl_up_sync(0xffffffffu, v, o);
       if (lane >= o) {
         u += p;
@@ -869,7 +786,6 @@ __device__ __forceinline__ void block_excl_scan2(unsigned long long& a, unsigned
   *tb = s_red[1][NW - 1];
   a = ba + x - a;
   b = bb + y - b;
-  __syncthreads();
 }
 
 template <class E, class Same>
@@ -884,7 +800,7 @@ __global__ void __launch_bounds__(KBCfg<E>::T, KBCfg<E>::MINB)
   __shared__ uint32_t s_p;
   __shared__ unsigned long long s_red2[2][KBCfg<E>::W];
   __shared__ unsigned long long s_base;
-  __shared__ uint32_t s_c9, s_qn[2];
+  __shared__ uint32_t s_c9, s_chunk[3], s_qn[3][2];
   __shared__ uint32_t s_bitsw[KBCfg<E>::W][32];
 
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -899,17 +815,23 @@ __global__ void __launch_bounds__(KBCfg<E>::T, KBCfg<E>::MINB)
   uint16_t* sA = reinterpret_cast<uint16_t*>(smem + SL.sA);
   uint16_t* src = reinterpret_cast<uint16_t*>(smem + SL.src);
   uint16_t* slist = reinterpret_cast<uint16_t*>(smem + SL.slist);
+  uint16_t* rlist = reinterpret_cast<uint16_t*>(smem + SL.queue);  // [3][lcap]
   uint8_t* ss = smem + SL.ss;
   uint16_t* sstart = reinterpret_cast<uint16_t*>(smem + SL.sstart);
   uint32_t* soff = reinterpret_cast<uint32_t*>(smem + SL.soff);
   uint8_t* s_t = smem + SL.st;
+  const uint32_t lcap = cap / 2 + 1;
 
   if (tid == 0) {
     s_p = atomicAdd(&stt->ticket, 1u);
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_bar)));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     s_c9 = 0;
-    s_qn[0] = s_qn[1] = 0;
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+      s_chunk[i] = 0;
+      s_qn[i][0] = s_qn[i][1] = 0;
+    }
   }
   if (tid < 33) s_m2[tid] = bp.m2[tid];  // (host-computed: no 64-bit division per CTA)
   for (uint32_t j = tid; j < BP; j += KBCfg<E>::T) soff[j] = 0;  // the histogram
@@ -978,87 +900,123 @@ __global__ void __launch_bounds__(KBCfg<E>::T, KBCfg<E>::MINB)
   HM_TMARK(2);
 
   // ---- exclusive scans of s and s^2 (presum, R1/R2) and of
-  // the class counts; thread t owns buckets [t*CH, t*CH + CH)
+  // the class counts; thread t owns buckets [4t, 4t + 4) (BP = 4T: one 16-byte
+  // load of the four counts) or [t*CH, t*CH + CH) otherwise
   bool huge = false, bfail = false;
   unsigned long long S_p;
+  uint32_t Lall;
   {
     const uint32_t c0 = tid * CH, c1 = min(c0 + CH, nbp);
-    unsigned long long a = 0, b = 0;  // a = s | s^2 << 32, b = #(s=2) | #(s=3..4) << 21 | #(s=5..8) << 42
-    for (uint32_t j = c0; j < c1; j++) {
-      const uint32_t v = soff[j];
-      a += uint64_t(v) | (uint64_t(v * v) << 32);
-      if (uint64_t(v) * v <= bp.bound4n) {  // (a bucket over the bound is never searched: level one redraws)
-        if (v == 2) b += 1;
-        else if (v >= 3 && v <= 4) b += 1ull << 21;
-        else if (v >= 5 && v <= 8) b += 1ull << 42;
+    const bool vec = CH == 4;  // (CTA-uniform; entries past nbp are 0)
+    uint32_t v4[4] = {0, 0, 0, 0};
+    if (vec) {
+      const uint4 q = *reinterpret_cast<const uint4*>(soff + c0);
+      v4[0] = q.x;
+      v4[1] = q.y;
+      v4[2] = q.z;
+      v4[3] = q.w;
+    }
+    // a = s | s^2 << 32; b = #(s=2) | #(s=3..4) << 21 | #(s=5..8) << 42
+    unsigned long long a = 0, b = 0;
+    if (vec) {
+      uint32_t sum = 0, sq = 0, cls = 0;  // cls: the three counts in bytes 0..2
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const uint32_t v = v4[u];
+        sum += v;
+        sq += v * v;
+        cls += (v == 2 ? 1u : 0u) + (v - 3u <= 1u ? 0x100u : 0u) + (v - 5u <= 3u ? 0x10000u : 0u);
+      }
+      a = uint64_t(sum) | (uint64_t(sq) << 32);
+      b = uint64_t(cls & 0xFF) | (uint64_t((cls >> 8) & 0xFF) << 21) | (uint64_t(cls >> 16) << 42);
+    } else {
+      for (uint32_t j = c0; j < c1; j++) {
+        const uint32_t v = soff[j];
+        a += uint64_t(v) | (uint64_t(v * v) << 32);
+        b += v == 2 ? 1ull : (v - 3u <= 1u ? (1ull << 21) : (v - 5u <= 3u ? (1ull << 42) : 0ull));
       }
     }
     unsigned long long ta, tb;
     block_excl_scan2<KBCfg<E>::W>(a, b, &ta, &tb, s_red2);
     S_p = ta >> 32;
-    const uint32_t T4 = uint32_t((tb >> 21) & 0x1FFFFF), T8 = uint32_t(tb >> 42);
+    const uint32_t T2 = uint32_t(tb & 0x1FFFFF), T4 = uint32_t((tb >> 21) & 0x1FFFFF), T8 = uint32_t(tb >> 42);
+    Lall = T2 + T4 + T8;
     uint32_t pos = uint32_t(a), sq = uint32_t(a >> 32);
     // list regions: [s = 5..8 | s = 3..4 | s = 2]
     uint32_t n8 = uint32_t(b >> 42), n4 = T8 + uint32_t((b >> 21) & 0x1FFFFF), n2 = T8 + T4 + uint32_t(b & 0x1FFFFF);
-    for (uint32_t j = c0; j < c1; j++) {
-      const uint32_t v = soff[j];
-      ss[j] = uint8_t(v > 255 ? 255 : v);
-      sstart[j] = uint16_t(pos);
-      soff[j] = sq;
-      if (v != 1) s_t[j] = 0;  // (a singleton keeps its key's tag for the compact directory)
-      pos += v;
-      sq += v * v;
-      if (v >= 2) {
-        if (uint64_t(v) * v > bp.bound4n) bfail = true;  // S > 4n: level one redraws
-        else if (v > 32) huge = true;
-        else if (v == 2) slist[n2++] = uint16_t(j);
-        else if (v <= 4) slist[n4++] = uint16_t(j);
-        else if (v <= 8) slist[n8++] = uint16_t(j);
-        else slist[SL.cls_off[2] + atomicAdd(&s_c9, 1u)] = uint16_t(j);
+    // (a bucket with s^2 > 4n means S > 4n: level one redraws, R7, and this
+    // pass is discarded; s <= 8 buckets are listed all the same — only
+    // reachable with n < 16)
+    auto place = [&](uint32_t j, uint32_t v) {
+      if (v < 2) return;
+      const bool over = uint64_t(v) * v > bp.bound4n;
+      bfail |= over;
+      if (v <= 8) {
+        slist[v == 2 ? n2 : (v <= 4 ? n4 : n8)] = uint16_t(j);
+        n2 += v == 2;
+        n4 += v - 3u <= 1u;
+        n8 += v >= 5;
+      } else if (!over) {
+        if (v <= 32) slist[SL.cls_off[2] + atomicAdd(&s_c9, 1u)] = uint16_t(j);
+        else huge = true;
+      }
+    };
+    if (vec) {
+      uint32_t st4 = *reinterpret_cast<const uint32_t*>(s_t + c0), ss4 = 0, ssk = 0;
+      uint32_t so[4], sp[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const uint32_t v = v4[u];
+        sp[u] = pos;
+        so[u] = sq;
+        ss4 |= (v > 255 ? 255u : v) << (8 * u);
+        if (v == 1) ssk |= 0xFFu << (8 * u);  // (a singleton keeps its key's tag for the compact directory)
+        pos += v;
+        sq += v * v;
+      }
+      *reinterpret_cast<uint4*>(soff + c0) = make_uint4(so[0], so[1], so[2], so[3]);
+      *reinterpret_cast<uint2*>(sstart + c0) = make_uint2(sp[0] | (sp[1] << 16), sp[2] | (sp[3] << 16));
+      *reinterpret_cast<uint32_t*>(ss + c0) = ss4;
+      *reinterpret_cast<uint32_t*>(s_t + c0) = st4 & ssk;
+#pragma unroll
+      for (int u = 0; u < 4; u++) place(c0 + u, v4[u]);
+    } else {
+      for (uint32_t j = c0; j < c1; j++) {
+        const uint32_t v = soff[j];
+        ss[j] = uint8_t(v > 255 ? 255 : v);
+        sstart[j] = uint16_t(pos);
+        soff[j] = sq;
+        if (v != 1) s_t[j] = 0;
+        pos += v;
+        sq += v * v;
+        place(j, v);
       }
     }
     if (huge) atomicOr(&stt->huge, 1u);
     if (bfail) atomicOr(&stt->bound_fail, 1u);
-    if (tid == 0) {
-      s_qn[0] = 0;
-      s_red2[0][0] = tb;  // class counts (read after the next barrier)
-    }
   }
   // publish the partition's aggregate S_p now (decoupled look-back)
   if (tid == 0) st_release(&lbstate[p], (p == 0 ? kFlagInc : kFlagAgg) | (S_p & kValMask));
   __syncthreads();
-  const unsigned long long tcls = s_red2[0][0];
-  const uint32_t Le8 = uint32_t(tcls >> 42), Le4 = Le8 + uint32_t((tcls >> 21) & 0x1FFFFF),
-                 Lall = Le4 + uint32_t(tcls & 0x1FFFFF);
-  // groupby: grouped position of every item
-  for (uint32_t i = tid; i < cnt; i += KBCfg<E>::T) sidx[sstart[lbk[i]] + rk[i]] = uint16_t(i);
+  HM_TMARK(10);
+  // ---- groupby: grouped position of every item; a singleton
+  // (R12: its slot is soff) is mapped right here
+  const bool staged = S_p <= SL.smax && !(bp.flags & HM_FLAG_DIRECT_SLOTS);
+  for (uint32_t i = tid; i < cnt; i += KBCfg<E>::T) {
+    const uint32_t lb = lbk[i];
+    sidx[sstart[lb] + rk[i]] = uint16_t(i);
+    if (staged && ss[lb] == 1) src[soff[lb]] = uint16_t(i);
+  }
   __syncthreads();
   HM_TMARK(3);
 
   // ---- level-2 seed search, map make2 over the multi-key buckets
   // (PAPER.md:286-292); every finished bucket maps its slots to their source
-  // items (bucket_done), the singletons are mapped here (R12: a singleton sits
-  // at soff)
-  const bool staged = S_p <= SL.smax && !(bp.flags & HM_FLAG_DIRECT_SLOTS);
+  // items (bucket_done)
   SearchCtx X{sstart, ss, sidx, soff, sA, s_t, staged ? src : nullptr};
-  uint32_t* q0 = reinterpret_cast<uint32_t*>(smem + SL.queue);
-  uint32_t* q1 = q0 + (cap / 2 + 1);
-  search_warp(bp, skv, X, slist + SL.cls_off[2], s_c9, s_m2, bbase, stt, same, s_bitsw[warp]);
-  HM_TMARK(8);
-  search_round0(bp, skv, X, slist, Le8, Le4, Lall, q0, &s_qn[0], s_m2, bbase, stt, same);
-  HM_TMARK(9);
-  if (staged) {
-    const uint32_t c0 = tid * CH, c1 = min(c0 + CH, nbp);
-    for (uint32_t j = c0; j < c1; j++)
-      if (ss[j] == 1) src[soff[j]] = sidx[sstart[j]];
-  }
-  __syncthreads();
-  HM_TMARK(10);
   // look-back: exclusive prefix of S over the partitions before p (warp 0,
   // lane i inspects partition qb - i: the closest inclusive prefix plus the
-  // aggregates in front of it give the base).  Warp 0 runs it while warps
-  // 1..15 run the first retry round (or right after round 0 when no bucket
-  // needs one).
+  // aggregates in front of it give the base)
   auto look_back = [&]() {
     unsigned long long base = 0;
     if (p > 0) {
@@ -1086,32 +1044,81 @@ __global__ void __launch_bounds__(KBCfg<E>::T, KBCfg<E>::MINB)
       s_base = base;
     }
   };
-  bool looked = false;  // (CTA-uniform)
-  for (uint32_t r = 0;; r++) {
-    const uint32_t L = s_qn[r & 1];
-    if (L == 0) break;
-    if (tid == 0) s_qn[(r + 1) & 1] = 0;
+  // warp 0 takes the look-back first (the partitions before p published their
+  // aggregates right after their scans), then joins the search
+  if (warp == 0) look_back();
+  HM_TMARK(9);
+  search_warp(bp, skv, X, slist + SL.cls_off[2], s_c9, s_m2, bbase, stt, same, s_bitsw[warp]);
+  {
+    uint32_t h[8];
+    // round 0: attempt 0 of every listed bucket, 32-bucket chunks from s_chunk[0]
+    for (;;) {
+      uint32_t c = 0;
+      if (lane == 0) c = atomicAdd(&s_chunk[0], 32u);
+      c = __shfl_sync(0xffffffffu, c, 0);
+      if (c >= Lall) break;
+      const uint32_t i = c + lane;
+      const bool act = i < Lall;
+      const uint32_t lb = act ? slist[i] : 0u;
+      const uint32_t s = act ? ss[lb] : 0u;
+      uint32_t tw;
+      const uint64_t bits = lane_attempt_k<kR0Two>(bp, skv, X, act, lb, s, 0u, s_m2, bbase, true, h, &tw);
+      bool again = act && !bits;
+      if (again && bucket_equal_keys(skv, X, lb, stt, same)) again = false;  // (equal keys: checked once)
+      if (again) s_t[lb] = uint8_t(tw + 1);  // (the next attempt)
+      list_append(again, lb, s, rlist + lcap, lcap, s_qn[1]);
+    }
     __syncthreads();
-    const uint32_t first = r == 0 ? 32u : 0u, lanes = KBCfg<E>::T - first;
-    uint32_t logA = 0;
-    while (logA < HM_RETRY_LOGA && (L << (logA + 1)) <= lanes) logA++;
-    if (tid < first) look_back();
-    else
-      search_round(bp, skv, X, (r & 1) ? q1 : q0, L, logA, (r & 1) ? q0 : q1, &s_qn[(r + 1) & 1], s_m2, bbase, stt,
-                   same, first);
-    looked = true;
-    __syncthreads();
+    HM_TMARK(8);
+    // rounds r >= 1 over the list of round r-1's collisions
+    for (uint32_t r = 1;; r++) {
+      const uint32_t cur = r % 3, nxt = (r + 1) % 3;
+      const uint16_t* cl = rlist + cur * lcap;
+      const uint32_t n3 = s_qn[cur][0], L = n3 + s_qn[cur][1];
 #ifdef HM_PHASE_TIMING
-    if (r == 0) HM_TMARK(11);
-    if (tid == 0) g_hm_phase[(s_p & 65535u) * 16 + 12] = r + 1;  // (the round count)
+      if (tid == 0) g_hm_phase[(s_p & 65535u) * 16 + 12] = r - 1;  // (the retry-round count)
 #endif
+      if (r == 2) HM_TMARK(11);
+      if (L == 0) break;
+      if (tid == 0) {  // (the list two rounds back is not read any more)
+        s_qn[(r + 2) % 3][0] = s_qn[(r + 2) % 3][1] = 0;
+        s_chunk[(r + 2) % 3] = 0;
+      }
+      uint32_t logA = 0;
+      while (logA < HM_RETRY_LOGA && (L << (logA + 1)) <= uint32_t(KBCfg<E>::T)) logA++;
+      const uint32_t A = 1u << logA, W = L << logA;
+      const uint32_t gmask = A == 32 ? 0xffffffffu : (((1u << A) - 1u) << (lane & ~(A - 1u)));
+      for (;;) {
+        uint32_t c = 0;
+        if (lane == 0) c = atomicAdd(&s_chunk[cur], 32u);
+        c = __shfl_sync(0xffffffffu, c, 0);
+        if (c >= W) break;
+        const uint32_t w = c + lane, g = w >> logA, j = w & (A - 1u);
+        const bool act = w < W;
+        const uint32_t lb = act ? (g < n3 ? cl[g] : cl[lcap - 1 - (g - n3)]) : 0u;
+        const uint32_t s = act ? ss[lb] : 0u, tb = act ? s_t[lb] : 0u;
+        uint32_t tw;
+        const uint64_t bits = lane_attempt_k<false>(bp, skv, X, act, lb, s, tb + j, s_m2, bbase, false, h, &tw);
+        const uint32_t om = __ballot_sync(0xffffffffu, bits != 0) & gmask;
+        if (bits && lane == uint32_t(__ffs(om) - 1)) bucket_done_any(X, lb, s, tb + j, h, bits);
+        bool again = false;
+        if (act && j == 0 && om == 0) {
+          if (tb + A >= kT2Cap) {
+            atomicOr(&stt->exhausted, 1u);
+            s_t[lb] = 0;
+          } else {
+            s_t[lb] = uint8_t(tb + A);
+            again = true;
+          }
+        }
+        list_append(again, lb, s, rlist + nxt * lcap, lcap, s_qn[nxt]);
+      }
+      __syncthreads();
+    }
   }
-  if (!looked && warp == 0) look_back();
   HM_TMARK(4);
-
-  __syncthreads();  // (s_base)
-  HM_TMARK(5);
   const unsigned long long base = s_base;
+  HM_TMARK(5);
   if (ovf) {
     if (tid == 0) atomicOr(&stt->part_overflow, 1u);
     return;
@@ -1174,36 +1181,50 @@ __global__ void __launch_bounds__(KBCfg<E>::T, KBCfg<E>::MINB)
     }
   }
   HM_TMARK(6);
-  // directory (coalesced) and compact directory record per 32 buckets (one per
-  // warp iteration)
-  for (uint32_t cb = 0; cb < nbp; cb += KBCfg<E>::T) {
-    const uint32_t lb = cb + tid;
-    uint32_t s = 0, t = 0;
-    uint64_t so = 0;
-    if (lb < nbp) {
-      s = ss[lb];
-      t = s_t[lb];  // (a singleton: its key's tag; t = 0 in the directory, R12)
-      so = base + soff[lb];
-      dir[lb0 + lb] = dir_entry(so, s, s == 1 ? 0u : t);
+  // directory: two buckets per lane, one 16-byte store (lb0 and the pair are
+  // even, so the store is aligned)
+  for (uint32_t q = tid; 2 * q < nbp; q += KBCfg<E>::T) {
+    const uint32_t lb = 2 * q;
+    const uint2 so2 = *reinterpret_cast<const uint2*>(soff + lb);
+    const uint32_t s2 = *reinterpret_cast<const uint16_t*>(ss + lb), t2 = *reinterpret_cast<const uint16_t*>(s_t + lb);
+    const uint32_t sa = s2 & 0xFF, sb = s2 >> 8, ta = sa == 1 ? 0u : (t2 & 0xFF), tb = sb == 1 ? 0u : (t2 >> 8);
+    const uint64_t ea = dir_entry(base + so2.x, sa, ta), eb = dir_entry(base + so2.y, sb, tb);
+    if (lb + 1 < nbp) {
+      *reinterpret_cast<ulonglong2*>(dir + lb0 + lb) = make_ulonglong2(ea, eb);
+    } else {
+      dir[lb0 + lb] = ea;
     }
-    uint32_t pa = __ballot_sync(0xffffffffu, s & 4), pb = __ballot_sync(0xffffffffu, s & 2),
-             pc = __ballot_sync(0xffffffffu, s & 1);
-    const uint32_t t0 = __ballot_sync(0xffffffffu, t & 1), t1 = __ballot_sync(0xffffffffu, t & 2),
-                   t2 = __ballot_sync(0xffffffffu, t & 4), t3 = __ballot_sync(0xffffffffu, t & 8);
-    if (__any_sync(0xffffffffu, s >= kCdirEscS || (s >= 2 && t >= kCdirEscT)) || (bp.flags & HM_FLAG_FULL_DIRECTORY))
-      pa = pb = pc = 0xffffffffu;
-    if (lane == 0 && lb < nbp) {
-      CDir r;
-      r.w[0] = uint32_t(so);
-      r.w[1] = pa;
-      r.w[2] = pb;
-      r.w[3] = pc;
-      r.w[4] = t0;
-      r.w[5] = t1;
-      r.w[6] = t2;
-      r.w[7] = t3;
-      cdir[(lb0 + lb) >> 5] = r;
+  }
+  // compact directory: a lane per 32-bucket record.  Bit i of the four sizes
+  // (or attempts) packed in a word x is gathered with one multiply:
+  // ((x >> i) & 0x01010101) * 0x01020408 puts the four bits at 24..27.
+  for (uint32_t r = tid; 32 * r < nbp; r += KBCfg<E>::T) {
+    const uint32_t* s32 = reinterpret_cast<const uint32_t*>(ss + 32 * r);
+    const uint32_t* t32 = reinterpret_cast<const uint32_t*>(s_t + 32 * r);
+    uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    uint32_t esc = 0;
+    const uint32_t nr = nbp - 32 * r;  // (buckets past nbp count as s = 0, t = 0)
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      const uint32_t vb = nr >= uint32_t(4 * k + 4) ? 4u : (nr > uint32_t(4 * k) ? nr - 4 * k : 0u);
+      const uint32_t bm = vb == 4 ? 0xFFFFFFFFu : ((1u << (8 * vb)) - 1u);
+      const uint32_t x = s32[k] & bm, y = t32[k] & bm;
+      // escapes: any s >= 7, or s >= 2 with t >= 15 (bytes < 128 after the mask: no carries)
+      const uint32_t ge7 = (((x & 0x7F7F7F7Fu) + 0x79797979u) | x) & 0x80808080u;
+      const uint32_t ge2 = (((x & 0x7F7F7F7Fu) + 0x7E7E7E7Eu) | x) & 0x80808080u;
+      const uint32_t t15 = (((y & 0x7F7F7F7Fu) + 0x71717171u) | y) & 0x80808080u;
+      esc |= ge7 | (ge2 & t15);
+#pragma unroll
+      for (int i = 0; i < 3; i++)
+        w[1 + i] |= ((((x >> (2 - i)) & 0x01010101u) * 0x01020408u) >> 24) << (4 * k);
+#pragma unroll
+      for (int i = 0; i < 4; i++) w[4 + i] |= ((((y >> i) & 0x01010101u) * 0x01020408u) >> 24) << (4 * k);
     }
+    if (esc || (bp.flags & HM_FLAG_FULL_DIRECTORY)) w[1] = w[2] = w[3] = 0xffffffffu;
+    w[0] = uint32_t(base + soff[32 * r]);
+    uint4* o = reinterpret_cast<uint4*>(cdir + ((lb0 >> 5) + r));
+    o[0] = make_uint4(w[0], w[1], w[2], w[3]);
+    o[1] = make_uint4(w[4], w[5], w[6], w[7]);
   }
   HM_TMARK(7);
 }
@@ -1345,6 +1366,12 @@ hm_status map_alloc(void** p, size_t bytes, cudaStream_t st) {
     if (!*p) {
       set_error("the user allocator (hm_opts.alloc) returned NULL for " + std::to_string(bytes) + " bytes");
       return HM_ERR_OOM;
+    }
+    if (reinterpret_cast<uintptr_t>(*p) & 31u) {  // (32-byte slot and compact-directory records, 32-B vector loads)
+      tl_user_alloc.free(*p, bytes, reinterpret_cast<void*>(st), tl_user_alloc.ctx);
+      *p = nullptr;
+      set_error("the user allocator (hm_opts.alloc) returned a pointer that is not 32-byte aligned");
+      return HM_ERR_INVALID_ARG;
     }
     return HM_OK;
   }
@@ -1494,7 +1521,7 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
   // kernel configuration
   constexpr int KPT = sizeof(E) == 16 ? 16 : 8;
   const size_t smemA = size_t(pl.np) * 4;
-  const bool smemHist = smemA <= size_t(smem_optin) - 1024 && !getenv("HM_KA_GLOBAL");
+  const bool smemHist = smemA <= size_t(smem_optin) - 1024;
   auto kA_s = k_partition<Src, E, KPT, true>;
   auto kA_g = k_partition<Src, E, KPT, false>;
   auto kB = k_bucket<E, Same>;
@@ -1509,7 +1536,7 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
   const unsigned gridA = unsigned(std::max<uint64_t>(1, std::min<uint64_t>(ntiles, uint64_t(sms) * occA)));
   // large tables: two coalesced radix passes (256- or 512-way) over the
   // partition id instead of one np-way scatter
-  const bool two_pass = pl.np > 1024 && pl.np <= (1u << 18) && !getenv("HM_ONE_PASS");
+  const bool two_pass = pl.np > 1024 && pl.np <= (1u << 18);
   const int sbits = pl.np <= 65536 ? 8 : 9;
   const uint32_t sdig = 1u << sbits;
   uint32_t ncoarse = 0, ccap = 0, tpc = 0;
@@ -1764,28 +1791,23 @@ void launch_fingerprint(const uint8_t* bytes, const uint64_t* offs, uint64_t n, 
   }
 }
 
-hm_status build_bytes_core(const uint8_t* bytes, const uint64_t* offsets, const uint64_t* vals, uint64_t n,
-                           uint64_t seed, uint32_t log2_bp, cudaStream_t st, BuildOut* out, uint32_t* t0_out,
-                           uint64_t* r_out) {
+// The key context's validity (hm.h): offsets non-decreasing (INVALID_ARG) and
+// every key at most 65535 bytes (TOO_LARGE, R23).  Runs before anything reads
+// the bytes (the from_array dedup, the fingerprints).
+hm_status check_offsets(const uint64_t* offsets, uint64_t n, cudaStream_t st) {
   Scratch sc{st};
-  uint64_t* fp = nullptr;
   unsigned int* bad = nullptr;
   hm_status s;
-  if ((s = sc.alloc(WS_FP, &fp, n * 8)) != HM_OK) return s;
   if ((s = sc.alloc(WS_BAD, &bad, 4)) != HM_OK) return s;
   HM_CUDA_TRY(cudaMemsetAsync(bad, 0, 4, st));
+  const unsigned grid = unsigned(std::min<uint64_t>((n + 255) / 256, uint64_t(num_sms()) * 16));
   {
-    const unsigned grid = unsigned(std::min<uint64_t>((n + 255) / 256, uint64_t(num_sms()) * 16));
-    {
-      LaunchScope ls_("k_check_offsets", st);
-      k_check_offsets<<<std::max(grid, 1u), 256, 0, st>>>(offsets, n, bad);
-    }
-    HM_CUDA_TRY(cudaGetLastError());
+    LaunchScope ls_("k_check_offsets", st);
+    k_check_offsets<<<std::max(grid, 1u), 256, 0, st>>>(offsets, n, bad);
   }
+  HM_CUDA_TRY(cudaGetLastError());
   unsigned int hbad = 0;
-  uint64_t off0 = 0;
   HM_CUDA_TRY(cudaMemcpyAsync(&hbad, bad, 4, cudaMemcpyDeviceToHost, st));
-  HM_CUDA_TRY(cudaMemcpyAsync(&off0, offsets, 8, cudaMemcpyDeviceToHost, st));
   HM_CUDA_TRY(cudaStreamSynchronize(st));
   if (hbad & 1u) {
     set_error("offsets are not non-decreasing");
@@ -1795,6 +1817,20 @@ hm_status build_bytes_core(const uint8_t* bytes, const uint64_t* offsets, const 
     set_error("a byte key is longer than 65535 bytes");
     return HM_ERR_TOO_LARGE;
   }
+  return HM_OK;
+}
+
+// (the caller has validated the offsets with check_offsets)
+hm_status build_bytes_core(const uint8_t* bytes, const uint64_t* offsets, const uint64_t* vals, uint64_t n,
+                           uint64_t seed, uint32_t log2_bp, cudaStream_t st, BuildOut* out, uint32_t* t0_out,
+                           uint64_t* r_out) {
+  Scratch sc{st};
+  uint64_t* fp = nullptr;
+  hm_status s;
+  if ((s = sc.alloc(WS_FP, &fp, n * 8)) != HM_OK) return s;
+  uint64_t off0 = 0;
+  HM_CUDA_TRY(cudaMemcpyAsync(&off0, offsets, 8, cudaMemcpyDeviceToHost, st));
+  HM_CUDA_TRY(cudaStreamSynchronize(st));
   const uint64_t smix = seed_mix(seed);
   for (uint32_t t0 = 0; t0 < kT0Cap; t0++) {
     const uint64_t r = derive(smix, 0, 0, t0).a1;

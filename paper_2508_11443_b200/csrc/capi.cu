@@ -305,7 +305,7 @@ hm_status hm_build_u64(const uint64_t* keys, const uint64_t* vals, uint64_t n, c
   }
   BuildOut bo;
   if (opts && (opts->flags & HM_FLAG_ROUNDS)) {
-    s = build_u64_rounds(dk, dv, n, seed, opts->flags, st, &bo);
+    s = build_u64_rounds(dk, dv, n, n, 0, n, -1, seed, opts->flags, st, &bo);
   } else {
     s = build_u64_core(dk, dv, n, n, 0, n, -1, seed, opts ? (opts->log2_bp | (opts->flags << 16)) : 0, st, &bo);
     // a degenerate level-1 distribution within the space bound (a bucket of more
@@ -314,7 +314,7 @@ hm_status hm_build_u64(const uint64_t* keys, const uint64_t* vals, uint64_t n, c
     // handle any bucket size and report equal keys as DUPLICATE_KEY
     if (s == HM_ERR_TOO_LARGE) {
       set_error("");
-      s = build_u64_rounds(dk, dv, n, seed, opts ? opts->flags : 0u, st, &bo);
+      s = build_u64_rounds(dk, dv, n, n, 0, n, -1, seed, opts ? opts->flags : 0u, st, &bo);
     }
   }
   if (uk) {
@@ -378,6 +378,8 @@ hm_status hm_build_bytes(const uint8_t* bytes, const uint64_t* offsets, const ui
       HM_CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(d) + o0, bytes + o0, on - o0, cudaMemcpyHostToDevice, st));
     db = reinterpret_cast<const uint8_t*>(d);
   }
+  // offsets non-decreasing, keys <= 65535 bytes: checked before anything reads the bytes
+  if ((s = check_offsets(doff, n, st)) != HM_OK) return s;
   const uint64_t seed = opts ? opts->seed : 0;
   if (opts && (opts->flags & HM_FLAG_FROM_ARRAY)) {  // from_array: the distinct keys, packed in input order
     uint8_t* pc = nullptr;
@@ -561,7 +563,7 @@ hm_status hm_lookup_u64(const hm_map* map, const uint64_t* q, uint64_t nq, uint6
   if (!map || (!q && nq) || (!out_vals && !out_found) || map->key_kind != 0) return HM_ERR_INVALID_ARG;
   if (nq == 0) return HM_OK;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  if (nq > 2 * kPipeChunk && !is_device_ptr(q) && !getenv("HM_NO_PIPELINE") &&
+  if (nq > 2 * kPipeChunk && !is_device_ptr(q) &&
       (!out_vals || !is_device_ptr(out_vals)) && (!out_found || !is_device_ptr(out_found)))
     return lookup_u64_pipelined(map, q, nq, out_vals, out_found, st);
   Staged sg{st, {}};
@@ -788,6 +790,13 @@ hm_status hm_build_u64_shard(const uint64_t* keys, const uint64_t* vals, uint64_
     return HM_OK;
   }
   s = build_u64_core(keys, vals, n_recv, n_global, b_lo, nb, int(t1), seed, opts ? (opts->log2_bp | (opts->flags << 16)) : 0, st, &bo);
+  // a degenerate level-1 distribution within the bound (as in hm_build_u64):
+  // the flat rounds restricted to the shard's bucket range, any bucket size,
+  // equal keys -> DUPLICATE_KEY
+  if (s == HM_ERR_TOO_LARGE && n_recv) {
+    set_error("");
+    s = build_u64_rounds(keys, vals, n_recv, n_global, b_lo, nb, int(t1), seed, opts ? opts->flags : 0u, st, &bo);
+  }
   if (s != HM_OK) return s;
   hm_map* m = new_map();
   m->is_shard = true;

@@ -152,6 +152,7 @@ hm_status release_workspace();
 hm_status build_u64_core(const uint64_t* keys, const uint64_t* vals, uint64_t n_in, uint64_t n_global,
                          uint64_t b_lo, uint64_t nb, int t1_fixed, uint64_t seed, uint32_t log2_bp,
                          cudaStream_t st, BuildOut* out);
+hm_status check_offsets(const uint64_t* offsets, uint64_t n, cudaStream_t st);
 hm_status build_bytes_core(const uint8_t* bytes, const uint64_t* offsets, const uint64_t* vals, uint64_t n,
                            uint64_t seed, uint32_t log2_bp, cudaStream_t st, BuildOut* out, uint32_t* t0_out,
                            uint64_t* r_out);
@@ -168,8 +169,10 @@ hm_status dedup_partitioned(const uint64_t* keys, const uint64_t* vals, uint64_t
 hm_status dedup_u64(const uint64_t* keys, const uint64_t* vals, uint64_t n, cudaStream_t st, uint64_t** out_keys,
                     uint64_t** out_vals, uint64_t* n_out);
 // rounds.cu: the sortless round-based construction (HM_FLAG_ROUNDS ablation)
-hm_status build_u64_rounds(const uint64_t* keys, const uint64_t* vals, uint64_t n, uint64_t seed, uint32_t flags,
-                           cudaStream_t st, BuildOut* out);
+// (a shard: buckets [b_lo, b_lo + nb) of the level-1 function mod n_global with t1 = t1_fixed >= 0)
+hm_status build_u64_rounds(const uint64_t* keys, const uint64_t* vals, uint64_t n_in, uint64_t n_global,
+                           uint64_t b_lo, uint64_t nb, int t1_fixed, uint64_t seed, uint32_t flags, cudaStream_t st,
+                           BuildOut* out);
 // assemble.cu
 hm_status assemble_cdir_launch(const uint64_t* dir, const void* slots, uint64_t n, uint64_t S, const L1Params& l1,
                                uint32_t full_dir, CDir* cdir, unsigned int* bad, cudaStream_t st);

@@ -40,6 +40,7 @@ constexpr int kRT = 256;
 
 struct RoundsParams {
   uint64_t smix;
+  uint64_t b_lo;  // global id of local bucket 0 (a shard's bucket range; 0 for one table)
   uint64_t m2[33];  // floor((2^64-1) / s^2), s <= 32 (R22)
 };
 
@@ -51,7 +52,7 @@ struct __align__(16) ActKey {  // an active key: the key, its input index, its b
 __device__ __forceinline__ uint32_t level2_slot(const RoundsParams& P, uint64_t b, uint32_t t, uint32_t s,
                                                 uint64_t key) {
   if (s == 1) return 0;  // R12
-  const uint64_t hv = hash64(derive(P.smix, 2, b, t), key);
+  const uint64_t hv = hash64(derive(P.smix, 2, P.b_lo + b, t), key);
   const uint64_t s2 = uint64_t(s) * s;
   if ((s2 & (s2 - 1)) == 0) return uint32_t(hv & (s2 - 1));
   if (s <= 32) {
@@ -64,12 +65,18 @@ __device__ __forceinline__ uint32_t level2_slot(const RoundsParams& P, uint64_t 
 #define HM_GRID_LOOP(i, n) \
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < (n); i += uint64_t(gridDim.x) * blockDim.x)
 
-// make_1: the level-1 bucket of every key and `shape = hist n hashes`.
-__global__ void k_r_l1_hist(const uint64_t* __restrict__ keys, uint64_t n, L1Params l1, uint32_t* __restrict__ kb,
-                            unsigned int* __restrict__ shape) {
+// make_1: the level-1 bucket of every key and `shape = hist n hashes`
+// (local buckets b - b_lo of a shard's range [b_lo, b_lo + nb))
+__global__ void k_r_l1_hist(const uint64_t* __restrict__ keys, uint64_t n, L1Params l1, uint64_t b_lo, uint64_t nb,
+                            uint32_t* __restrict__ kb, unsigned int* __restrict__ shape, unsigned int* __restrict__ bad) {
   HM_GRID_LOOP(i, n) {
-    const uint32_t b = uint32_t(level1_bucket(l1, keys[i]));
-    kb[i] = b;
+    const uint64_t b = level1_bucket(l1, keys[i]) - b_lo;
+    if (b >= nb) {
+      atomicOr(bad, 1u);
+      kb[i] = 0;
+      continue;
+    }
+    kb[i] = uint32_t(b);
     atomicAdd(shape + b, 1u);
   }
 }
@@ -287,64 +294,91 @@ struct Owned {
     name<<<(grid), kRT, 0, st>>>(__VA_ARGS__);             \
   } while (0)
 
-hm_status build_u64_rounds(const uint64_t* keys, const uint64_t* vals, uint64_t n, uint64_t seed, uint32_t flags,
-                           cudaStream_t st, BuildOut* out) {
+hm_status build_u64_rounds(const uint64_t* keys, const uint64_t* vals, uint64_t n_in, uint64_t n_global,
+                           uint64_t b_lo, uint64_t nb, int t1_fixed, uint64_t seed, uint32_t flags, cudaStream_t st,
+                           BuildOut* out) {
   Owned ow{st, {}};
   const uint64_t smix = seed_mix(seed);
   const unsigned gmax = unsigned(num_sms()) * 8;
   auto grid = [&](uint64_t m) { return unsigned(std::max<uint64_t>(1, std::min<uint64_t>((m + kRT - 1) / kRT, gmax))); };
   RoundsParams P{};
   P.smix = smix;
+  P.b_lo = b_lo;
   for (int i = 1; i <= 32; i++) P.m2[i] = ~0ull / (uint64_t(i) * i);
+  const uint64_t n = nb;  // (the bucket count; the keys are n_in)
 
   uint32_t *kb, *A, *A2, *hk, *hkey;
-  unsigned int *shape, *flat;
+  unsigned int *shape, *flat, *bad;
   uint64_t *soff, *rank, *foff, *coll, *sums;
   ActKey *ak, *ak2;
   unsigned long long *fsel, *cursor;
   uint8_t* tb;
   hm_status s;
   const size_t nsums = scan_sums_len(n + 1);
-  if ((s = ralloc(ow.v, &kb, n * 4, st)) || (s = ralloc(ow.v, &shape, n * 4, st)) ||
+  if ((s = ralloc(ow.v, &kb, n_in * 4, st)) || (s = ralloc(ow.v, &shape, n * 4, st)) ||
       (s = ralloc(ow.v, &soff, (n + 1) * 8, st)) || (s = ralloc(ow.v, &rank, (n + 1) * 8, st)) ||
-      (s = ralloc(ow.v, &sums, nsums * 8, st)))
+      (s = ralloc(ow.v, &sums, nsums * 8, st)) || (s = ralloc(ow.v, &bad, 4, st)))
     return s;
 
-  // level one (make_1) with the space bound R7
-  uint32_t t1 = 0;
+  // level one (make_1) with the space bound R7 (a shard: the
+  // caller's t1, the caller checks the global bound)
+  uint32_t t1 = t1_fixed >= 0 ? uint32_t(t1_fixed) : 0u;
   uint64_t S = 0, m = 0;
   for (;; t1++) {
     if (t1 == kT1Cap) {
       set_error("level one exhausted 16 attempts without meeting the space bound S <= 4n");
       return HM_ERR_SEED_EXHAUSTED;
     }
-    const L1Params l1 = make_l1(smix, t1, n);
+    const L1Params l1 = make_l1(smix, t1, n_global);
     HM_CUDA_TRY(cudaMemsetAsync(shape, 0, n * 4, st));
-    HM_RLAUNCH(k_r_l1_hist, grid(n), keys, n, l1, kb, shape);
+    HM_CUDA_TRY(cudaMemsetAsync(bad, 0, 4, st));
+    HM_RLAUNCH(k_r_l1_hist, grid(n_in), keys, n_in, l1, b_lo, nb, kb, shape, bad);
     HM_RLAUNCH(k_r_l1_prep, grid(n + 1), shape, n, soff, rank);
     if ((s = scan_excl(soff, n + 1, sums, st)) != HM_OK) return s;
+    unsigned int hbad = 0;
     HM_CUDA_TRY(cudaMemcpyAsync(&S, soff + n, 8, cudaMemcpyDeviceToHost, st));
+    HM_CUDA_TRY(cudaMemcpyAsync(&hbad, bad, 4, cudaMemcpyDeviceToHost, st));
     HM_CUDA_TRY(cudaStreamSynchronize(st));
-    if (S <= 4 * n) break;
+    if (hbad) {
+      set_error("a routed key does not belong to this shard's bucket range");
+      return HM_ERR_INVALID_ARG;
+    }
+    if (S <= 4 * n_global) break;
+    if (t1_fixed >= 0) {  // a shard over the global bound on its own: the caller redraws level one
+      void* arr[3] = {nullptr, nullptr, nullptr};
+      const size_t bytes[3] = {16, sizeof(CDir), 16};
+      for (int a = 0; a < 3; a++)
+        if ((s = map_alloc(&arr[a], bytes[a], st)) != HM_OK) {
+          for (int b = 0; b < a; b++) map_discard(arr[b], bytes[b], st);
+          return s;
+        }
+      out->dir = static_cast<uint64_t*>(arr[0]);
+      out->cdir = static_cast<CDir*>(arr[1]);
+      out->slots = arr[2];
+      for (int a = 0; a < 3; a++) out->bytes[a] = bytes[a];
+      out->S = S;
+      out->t1 = t1;
+      return HM_OK;
+    }
   }
   if ((s = scan_excl(rank, n + 1, sums, st)) != HM_OK) return s;
   HM_CUDA_TRY(cudaMemcpyAsync(&m, rank + n, 8, cudaMemcpyDeviceToHost, st));
   HM_CUDA_TRY(cudaStreamSynchronize(st));
 
   if ((s = ralloc(ow.v, &A, m * 4, st)) || (s = ralloc(ow.v, &A2, m * 4, st)) ||
-      (s = ralloc(ow.v, &hk, n * 4, st)) || (s = ralloc(ow.v, &hkey, n * 4, st)) ||
+      (s = ralloc(ow.v, &hk, n_in * 4, st)) || (s = ralloc(ow.v, &hkey, n_in * 4, st)) ||
       (s = ralloc(ow.v, &flat, S * 4, st)) || (s = ralloc(ow.v, &foff, (m + 1) * 8, st)) ||
-      (s = ralloc(ow.v, &coll, (m + 1) * 8, st)) || (s = ralloc(ow.v, &ak, n * sizeof(ActKey), st)) ||
-      (s = ralloc(ow.v, &ak2, n * sizeof(ActKey), st)) || (s = ralloc(ow.v, &fsel, n * 8, st)) ||
+      (s = ralloc(ow.v, &coll, (m + 1) * 8, st)) || (s = ralloc(ow.v, &ak, n_in * sizeof(ActKey), st)) ||
+      (s = ralloc(ow.v, &ak2, n_in * sizeof(ActKey), st)) || (s = ralloc(ow.v, &fsel, n * 8, st)) ||
       (s = ralloc(ow.v, &cursor, 8, st)) || (s = ralloc(ow.v, &tb, n, st)))
     return s;
   HM_CUDA_TRY(cudaMemsetAsync(flat, 0, S * 4, st));
   HM_CUDA_TRY(cudaMemsetAsync(tb, 0, n, st));
   HM_RLAUNCH(k_r_init_active, grid(n), shape, rank, n, A);
-  HM_RLAUNCH(k_r_init_keys, grid(n), keys, kb, rank, n, ak);
+  HM_RLAUNCH(k_r_init_keys, grid(n_in), keys, kb, rank, n_in, ak);
 
   // level two: segmake'_2 rounds, round r = attempt t = r
-  uint64_t nk = n;
+  uint64_t nk = n_in;
   uint32_t r = 0;
   for (; m > 0 && r < kT2Cap; r++) {
     HM_RLAUNCH(k_r_seg_sq, grid(m + 1), A, shape, m, foff);
@@ -399,11 +433,11 @@ hm_status build_u64_rounds(const uint64_t* keys, const uint64_t* vals, uint64_t 
   dir = static_cast<uint64_t*>(arr[0]);
   cdir = static_cast<CDir*>(arr[1]);
   slots = static_cast<KV16*>(arr[2]);
-  const L1Params l1 = make_l1(smix, t1, n);
+  const L1Params l1 = make_l1(smix, t1, n_global);
   HM_CUDA_TRY(cudaMemsetAsync(fsel, 0xFF, n * 8, st));
-  HM_RLAUNCH(k_r_fin_min, grid(n), kb, shape, hkey, n, fsel);
+  HM_RLAUNCH(k_r_fin_min, grid(n_in), kb, shape, hkey, n_in, fsel);
   HM_RLAUNCH(k_r_fin_fill, grid(n), shape, soff, fsel, keys, n, slots);
-  HM_RLAUNCH(k_r_fin_members, grid(n), keys, vals, kb, shape, soff, hkey, l1, n, slots, tb);
+  HM_RLAUNCH(k_r_fin_members, grid(n_in), keys, vals, kb, shape, soff, hkey, l1, n_in, slots, tb);
   HM_RLAUNCH(k_r_fin_dir, grid(n), shape, soff, tb, n, flags & HM_FLAG_FULL_DIRECTORY, dir, cdir);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(cuda_fail(e, "rounds build"));

@@ -111,19 +111,36 @@ def _check(code: int):
 
 # ------------------------------------------------------------- marshalling
 
-def _ptr(x):
-    """Pointer + keep-alive for a torch tensor (any device) or numpy array."""
+def _ptr(x, itemsize: int = 0, out: bool = False):
+    """Pointer + keep-alive for a torch tensor (any device) or numpy array.
+
+    itemsize: the element width the C call reads or writes (8 for keys, values,
+    offsets and value outputs, 1 for byte contexts and found flags); a tensor of
+    another width is refused instead of being read as the wrong type.  out: an
+    output the library writes, which must be contiguous (a copy would lose the
+    results)."""
     if x is None:
         return None, None
     try:
         import torch
         if isinstance(x, torch.Tensor):
+            if itemsize and x.element_size() != itemsize:
+                raise TypeError("expected a %d-byte element type, got %s" % (itemsize, x.dtype))
             if not x.is_contiguous():
+                if out:
+                    raise ValueError("output tensors must be contiguous")
                 x = x.contiguous()
             return C.c_void_p(x.data_ptr()), x
     except ImportError:  # pragma: no cover
         pass
-    a = np.ascontiguousarray(x)
+    if out:
+        if not isinstance(x, np.ndarray) or not x.flags.c_contiguous:
+            raise ValueError("output arrays must be contiguous numpy arrays or tensors")
+        a = x
+    else:
+        a = np.ascontiguousarray(x)
+    if itemsize and a.itemsize != itemsize:
+        raise TypeError("expected a %d-byte element type, got %s" % (itemsize, a.dtype))
     return a.ctypes.data_as(C.c_void_p), a
 
 
@@ -199,8 +216,8 @@ class HashMap:
     # -- build
     @classmethod
     def build_u64(cls, keys, vals, seed: int = 0, stream=None, log2_bp: int = 0, flags: int = 0) -> "HashMap":
-        kp, kk = _ptr(keys)
-        vp, vk = _ptr(vals)
+        kp, kk = _ptr(keys, 8)
+        vp, vk = _ptr(vals, 8)
         n = _numel(keys)
         if _numel(vals) != n:
             raise ValueError("keys and vals differ in length")
@@ -224,9 +241,9 @@ class HashMap:
 
     @classmethod
     def build_bytes(cls, ctx, offsets, vals, seed: int = 0, stream=None, log2_bp: int = 0, flags: int = 0) -> "HashMap":
-        cp, ck = _ptr(ctx)
-        op, ok = _ptr(offsets)
-        vp, vk = _ptr(vals)
+        cp, ck = _ptr(ctx, 1)
+        op, ok = _ptr(offsets, 8)
+        vp, vk = _ptr(vals, 8)
         n = _numel(offsets) - 1
         if _numel(vals) != n:
             raise ValueError("offsets and vals disagree on n")
@@ -242,9 +259,9 @@ class HashMap:
         With torch CUDA inputs and no outputs given, allocates device outputs."""
         nq = _numel(q)
         out_vals, out_found = self._outputs(q, nq, out_vals, out_found)
-        qp, qk = _ptr(q)
-        vp, vk = _ptr(out_vals)
-        fp, fk = _ptr(out_found)
+        qp, qk = _ptr(q, 8)
+        vp, vk = _ptr(out_vals, 8, out=True)
+        fp, fk = _ptr(out_found, 1, out=True)
         _check(lib().hm_lookup_u64(self._h, qp, nq, vp, fp, _stream(stream)))
         return out_vals, out_found
 
@@ -252,18 +269,18 @@ class HashMap:
         """Membership only: no value is read or written."""
         nq = _numel(q)
         _, out_found = self._outputs(q, nq, False, out_found)
-        qp, qk = _ptr(q)
-        fp, fk = _ptr(out_found)
+        qp, qk = _ptr(q, 8)
+        fp, fk = _ptr(out_found, 1, out=True)
         _check(lib().hm_lookup_u64(self._h, qp, nq, None, fp, _stream(stream)))
         return out_found
 
     def lookup_bytes(self, qctx, qoffsets, out_vals=None, out_found=None, stream=None):
         nq = _numel(qoffsets) - 1
         out_vals, out_found = self._outputs(qoffsets, nq, out_vals, out_found)
-        cp, ck = _ptr(qctx)
-        op, ok = _ptr(qoffsets)
-        vp, vk = _ptr(out_vals)
-        fp, fk = _ptr(out_found)
+        cp, ck = _ptr(qctx, 1)
+        op, ok = _ptr(qoffsets, 8)
+        vp, vk = _ptr(out_vals, 8, out=True)
+        fp, fk = _ptr(out_found, 1, out=True)
         _check(lib().hm_lookup_bytes(self._h, cp, op, nq, vp, fp, _stream(stream)))
         return out_vals, out_found
 
@@ -271,9 +288,9 @@ class HashMap:
         """Membership of byte-string needles: no value is written."""
         nq = _numel(qoffsets) - 1
         _, out_found = self._outputs(qoffsets, nq, False, out_found)
-        cp, ck = _ptr(qctx)
-        op, ok = _ptr(qoffsets)
-        fp, fk = _ptr(out_found)
+        cp, ck = _ptr(qctx, 1)
+        op, ok = _ptr(qoffsets, 8)
+        fp, fk = _ptr(out_found, 1, out=True)
         _check(lib().hm_lookup_bytes(self._h, cp, op, nq, None, fp, _stream(stream)))
         return out_found
 
@@ -340,8 +357,8 @@ class HashMap:
         """Copy the directory (global soff for a shard) and the slots into
         caller tensors (device or host): dir_out int64[nb], slots_out int64[2*S]
         (u64 keys)."""
-        dp, dk = _ptr(dir_out)
-        sp, sk = _ptr(slots_out)
+        dp, dk = _ptr(dir_out, 8, out=True)
+        sp, sk = _ptr(slots_out, out=True)
         _check(lib().hm_export(self._h, dp, sp, None))
 
     # -- shards (multi-GPU)
@@ -349,26 +366,26 @@ class HashMap:
         _check(lib().hm_shard_set_base(self._h, slot_base))
 
     def route_queries(self, q, world: int, send_q, perm, counts, stream=None):
-        qp, qk = _ptr(q)
-        sp, sk = _ptr(send_q)
-        pp, pk = _ptr(perm)
-        cp, ck = _ptr(counts)
+        qp, qk = _ptr(q, 8)
+        sp, sk = _ptr(send_q, 8, out=True)
+        pp, pk = _ptr(perm, 8, out=True)
+        cp, ck = _ptr(counts, 8, out=True)
         _check(lib().hm_route_queries_u64(self._h, qp, _numel(q), world, sp, pp, cp, _stream(stream)))
 
 
 def route_u64(keys, vals, n_global: int, seed: int, t1: int, world: int, send_keys, send_vals, counts, stream=None):
-    kp, kk = _ptr(keys)
-    vp, vk = _ptr(vals)
-    sk, skk = _ptr(send_keys)
-    sv, svk = _ptr(send_vals)
-    cp, ck = _ptr(counts)
+    kp, kk = _ptr(keys, 8)
+    vp, vk = _ptr(vals, 8)
+    sk, skk = _ptr(send_keys, 8, out=True)
+    sv, svk = _ptr(send_vals, 8, out=True)
+    cp, ck = _ptr(counts, 8, out=True)
     _check(lib().hm_route_u64(kp, vp, _numel(keys), n_global, seed, t1, world, sk, sv, cp, _stream(stream)))
 
 
 def build_u64_shard(keys, vals, n_global: int, b_lo: int, b_hi: int, t1: int, seed: int = 0, stream=None,
                     log2_bp: int = 0):
-    kp, kk = _ptr(keys)
-    vp, vk = _ptr(vals)
+    kp, kk = _ptr(keys, 8)
+    vp, vk = _ptr(vals, 8)
     h = C.c_void_p()
     S = C.c_uint64()
     o = _opts(seed, log2_bp)
@@ -380,8 +397,8 @@ def build_u64_shard(keys, vals, n_global: int, b_lo: int, b_hi: int, t1: int, se
 def build_u64_dist(keys, vals, nccl_comm: int, seed: int = 0, stream=None, log2_bp: int = 0) -> "HashMap":
     """Collective sharded build over an NCCL communicator (hm_build_u64_dist;
     e.g. nccl_comm = the process group's backend ._comm_ptr())."""
-    kp, kk = _ptr(keys)
-    vp, vk = _ptr(vals)
+    kp, kk = _ptr(keys, 8)
+    vp, vk = _ptr(vals, 8)
     h = C.c_void_p()
     o = _opts(seed, log2_bp)
     _check(lib().hm_build_u64_dist(kp, vp, _numel(keys), C.byref(o), _stream(stream), C.c_void_p(int(nccl_comm)),
@@ -393,19 +410,19 @@ def lookup_u64_dist(shard: "HashMap", q, nccl_comm: int, out_vals=None, out_foun
     """Collective routed lookup on the shards of build_u64_dist (hm_lookup_u64_dist)."""
     nq = _numel(q)
     out_vals, out_found = shard._outputs(q, nq, out_vals, out_found)
-    qp, qk = _ptr(q)
-    vp, vk = _ptr(out_vals)
-    fp, fk = _ptr(out_found)
+    qp, qk = _ptr(q, 8)
+    vp, vk = _ptr(out_vals, 8, out=True)
+    fp, fk = _ptr(out_found, 1, out=True)
     _check(lib().hm_lookup_u64_dist(shard._h, qp, nq, vp, fp, _stream(stream), C.c_void_p(int(nccl_comm))))
     return out_vals, out_found
 
 
 def unroute_u64(vals_routed, found_routed, perm, out_vals, out_found, stream=None):
-    a, ak = _ptr(vals_routed)
-    b, bk = _ptr(found_routed)
-    p, pk = _ptr(perm)
-    v, vk = _ptr(out_vals)
-    f, fk = _ptr(out_found)
+    a, ak = _ptr(vals_routed, 8)
+    b, bk = _ptr(found_routed, 1)
+    p, pk = _ptr(perm, 8)
+    v, vk = _ptr(out_vals, 8, out=True)
+    f, fk = _ptr(out_found, 1, out=True)
     _check(lib().hm_unroute_u64(a, b, p, _numel(perm), v, f, _stream(stream)))
 
 

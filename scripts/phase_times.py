@@ -29,10 +29,9 @@ for i in range(len(names) - 1):
 t2 = buf[: 65536 * 16].reshape(65536, 16).astype(np.int64)
 t2 = t2[t2[:, 0] > 0]
 if (t2[:, 8] > 0).all():
-    for a, b, nm in [(3, 8, "search_warp"), (8, 9, "round0 (thread 0)"), (9, 10, "singles+sync"), (10, 4, "retry rounds")]:
-        x = t2[:, b] - t2[:, a]
+    for a, b, nm in [(2, 10, "scan"), (10, 3, "groupby"), (3, 9, "lookback (w0)"), (3, 8, "swarp+round0"), (8, 11, "retry round 1"), (8, 4, "retry rounds")]:
+        ok = (t2[:, b] > 0) & (t2[:, a] > 0)
+        x = (t2[:, b] - t2[:, a])[ok]
         print(f"  search part {nm:18s} mean {x.mean()/1e3:7.2f} us  p50 {np.median(x)/1e3:7.2f}")
     nr = t2[:, 12]
-    x = t2[:, 11] - t2[:, 10]
-    ok = t2[:, 11] > 0
-    print("  rounds per CTA: mean %.2f, dist %s; first retry round mean %.2f us" % (nr.mean(), np.bincount(nr.astype(int))[:6], (x[ok]).mean() / 1e3 if ok.any() else 0))
+    print("  retry rounds per CTA: mean %.2f, dist %s" % (nr.mean(), np.bincount(nr.astype(int))[:8]))
