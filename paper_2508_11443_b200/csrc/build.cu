@@ -54,10 +54,9 @@ struct KBCfg {
   static constexpr int W = T / 32;
   static constexpr int MINB = sizeof(E) == 16 ? HM_KB_MINB : HM_KB_MINB_BYTES;
 };
-#ifndef HM_R0_TWO
-#define HM_R0_TWO 1  // round 0: attempts 0 and 1 per lane (s <= 4)
+#ifndef HM_R0_LOGA
+#define HM_R0_LOGA 1  // round 0: 2^1 adjacent lanes (attempts 0, 1) per bucket
 #endif
-constexpr bool kR0Two = HM_R0_TWO != 0;
 #ifndef HM_RETRY_LOGA
 #define HM_RETRY_LOGA 3  // at most 2^3 lanes (attempts) per queued bucket and round
 #endif
@@ -586,53 +585,31 @@ __device__ __forceinline__ bool bucket_equal_keys(const E* skv, const SearchCtx&
   return bucket_equal_keys_(skv, X.sstart, X.ss, X.sidx, X.s_t, lb, stt, same);
 }
 
-// Attempt t of bucket lb (s keys, K-wide registers) on this lane; with
-// `finish` a success maps the bucket at once.  Returns the occupancy bitmap
-// (0: collision, or no bucket on this lane).  kTwo (round 0, K <= 4):
-// attempts t and t + 1 as two independent chains (the second hides the first
-// one's latency); the lower success wins.  *tw: the successful attempt, else
-// the last one tried.
-template <int K, bool kTwo, class E>
+// Attempt t of bucket lb (s keys, K-wide registers) on this lane.  Returns
+// the occupancy bitmap (0: collision, or no bucket on this lane).
+template <int K, class E>
 __device__ __forceinline__ uint64_t lane_attempt(const BuildParams& bp, const E* skv, const SearchCtx& X, bool act,
                                                  uint32_t lb, uint32_t s, uint32_t t, const uint64_t* s_m2,
-                                                 uint64_t bbase, bool finish, uint32_t* h, uint32_t* tw) {
-  *tw = t;
-  if (!act) return 0;
+                                                 uint64_t bbase, uint32_t* h) {
+  if (!act || t >= kT2Cap) return 0;
   const uint32_t st0 = X.sstart[lb];
   uint64_t k[K];
 #pragma unroll
   for (int j = 0; j < K; j++) k[j] = uint32_t(j) < s ? skv[X.sidx[st0 + j]].key : 0ull;
   FastMod fm{uint64_t(s) * s, 0};
   if (K > 2) fm.m = s_m2[s];
-  constexpr bool kT2 = kTwo && K <= 4;
-  uint64_t bits;
-  if (kT2) {
-    uint32_t h1[K];
-    const Consts c0 = derive(bp.smix, 2, bbase + lb, t), c1 = derive(bp.smix, 2, bbase + lb, t + 1);
-    bits = slots_of<K>(c0, k, s, fm, h);
-    const uint64_t b1 = slots_of<K>(c1, k, s, fm, h1);
-    if (!bits) {  // (*tw: the successful attempt, else the last one tried)
-#pragma unroll
-      for (int j = 0; j < K; j++) h[j] = h1[j];
-      bits = b1;
-      *tw = t + 1;
-    }
-  } else {
-    bits = t < kT2Cap ? slots_of<K>(derive(bp.smix, 2, bbase + lb, t), k, s, fm, h) : 0ull;
-  }
-  if (bits && finish) bucket_done<K>(X, lb, st0, s, *tw, h, bits);
-  return bits;
+  return slots_of<K>(derive(bp.smix, 2, bbase + lb, t), k, s, fm, h);
 }
 
 // The key-register width follows the largest bucket among the warp's lanes.
-template <bool kTwo, class E>
+template <class E>
 __device__ __forceinline__ uint64_t lane_attempt_k(const BuildParams& bp, const E* skv, const SearchCtx& X, bool act,
                                                    uint32_t lb, uint32_t s, uint32_t t, const uint64_t* s_m2,
-                                                   uint64_t bbase, bool finish, uint32_t* h, uint32_t* tw) {
+                                                   uint64_t bbase, uint32_t* h) {
   const uint32_t smax = __reduce_max_sync(0xffffffffu, act ? s : 0u);
-  if (smax <= 2) return lane_attempt<2, kTwo>(bp, skv, X, act, lb, s, t, s_m2, bbase, finish, h, tw);
-  if (smax <= 4) return lane_attempt<4, kTwo>(bp, skv, X, act, lb, s, t, s_m2, bbase, finish, h, tw);
-  return lane_attempt<8, false>(bp, skv, X, act, lb, s, t, s_m2, bbase, finish, h, tw);
+  if (smax <= 2) return lane_attempt<2>(bp, skv, X, act, lb, s, t, s_m2, bbase, h);
+  if (smax <= 4) return lane_attempt<4>(bp, skv, X, act, lb, s, t, s_m2, bbase, h);
+  return lane_attempt<8>(bp, skv, X, act, lb, s, t, s_m2, bbase, h);
 }
 
 __device__ __forceinline__ void bucket_done_any(const SearchCtx& X, uint32_t lb, uint32_t s, uint32_t t,
@@ -1051,41 +1028,28 @@ __global__ void __launch_bounds__(KBCfg<E>::T, KBCfg<E>::MINB)
   search_warp(bp, skv, X, slist + SL.cls_off[2], s_c9, s_m2, bbase, stt, same, s_bitsw[warp]);
   {
     uint32_t h[8];
-    // round 0: attempt 0 of every listed bucket, 32-bucket chunks from s_chunk[0]
-    for (;;) {
-      uint32_t c = 0;
-      if (lane == 0) c = atomicAdd(&s_chunk[0], 32u);
-      c = __shfl_sync(0xffffffffu, c, 0);
-      if (c >= Lall) break;
-      const uint32_t i = c + lane;
-      const bool act = i < Lall;
-      const uint32_t lb = act ? slist[i] : 0u;
-      const uint32_t s = act ? ss[lb] : 0u;
-      uint32_t tw;
-      const uint64_t bits = lane_attempt_k<kR0Two>(bp, skv, X, act, lb, s, 0u, s_m2, bbase, true, h, &tw);
-      bool again = act && !bits;
-      if (again && bucket_equal_keys(skv, X, lb, stt, same)) again = false;  // (equal keys: checked once)
-      if (again) s_t[lb] = uint8_t(tw + 1);  // (the next attempt)
-      list_append(again, lb, s, rlist + lcap, lcap, s_qn[1]);
-    }
-    __syncthreads();
-    HM_TMARK(8);
-    // rounds r >= 1 over the list of round r-1's collisions
-    for (uint32_t r = 1;; r++) {
+    // round r: the list of round r-1's collisions (round 0: every listed
+    // bucket, the class-ordered slist), A adjacent lanes per bucket trying
+    // attempts tb .. tb + A - 1 (tb = s_t[lb]: 0 in round 0), 32-lane chunks
+    // from a shared counter
+    for (uint32_t r = 0;; r++) {
       const uint32_t cur = r % 3, nxt = (r + 1) % 3;
-      const uint16_t* cl = rlist + cur * lcap;
-      const uint32_t n3 = s_qn[cur][0], L = n3 + s_qn[cur][1];
+      const uint16_t* cl = r == 0 ? slist : rlist + cur * lcap;
+      const uint32_t n3 = r == 0 ? Lall : s_qn[cur][0], L = r == 0 ? Lall : n3 + s_qn[cur][1];
 #ifdef HM_PHASE_TIMING
-      if (tid == 0) g_hm_phase[(s_p & 65535u) * 16 + 12] = r - 1;  // (the retry-round count)
-#endif
+      if (tid == 0) g_hm_phase[(s_p & 65535u) * 16 + 12] = r;  // (the round count)
+      if (r == 1) HM_TMARK(8);
       if (r == 2) HM_TMARK(11);
+#endif
       if (L == 0) break;
       if (tid == 0) {  // (the list two rounds back is not read any more)
         s_qn[(r + 2) % 3][0] = s_qn[(r + 2) % 3][1] = 0;
         s_chunk[(r + 2) % 3] = 0;
       }
       uint32_t logA = 0;
-      while (logA < HM_RETRY_LOGA && (L << (logA + 1)) <= uint32_t(KBCfg<E>::T)) logA++;
+      if (r == 0) logA = HM_R0_LOGA;
+      else
+        while (logA < HM_RETRY_LOGA && (L << (logA + 1)) <= uint32_t(KBCfg<E>::T)) logA++;
       const uint32_t A = 1u << logA, W = L << logA;
       const uint32_t gmask = A == 32 ? 0xffffffffu : (((1u << A) - 1u) << (lane & ~(A - 1u)));
       for (;;) {
@@ -1097,13 +1061,14 @@ __global__ void __launch_bounds__(KBCfg<E>::T, KBCfg<E>::MINB)
         const bool act = w < W;
         const uint32_t lb = act ? (g < n3 ? cl[g] : cl[lcap - 1 - (g - n3)]) : 0u;
         const uint32_t s = act ? ss[lb] : 0u, tb = act ? s_t[lb] : 0u;
-        uint32_t tw;
-        const uint64_t bits = lane_attempt_k<false>(bp, skv, X, act, lb, s, tb + j, s_m2, bbase, false, h, &tw);
+        const uint64_t bits = lane_attempt_k(bp, skv, X, act, lb, s, tb + j, s_m2, bbase, h);
         const uint32_t om = __ballot_sync(0xffffffffu, bits != 0) & gmask;
         if (bits && lane == uint32_t(__ffs(om) - 1)) bucket_done_any(X, lb, s, tb + j, h, bits);
         bool again = false;
         if (act && j == 0 && om == 0) {
-          if (tb + A >= kT2Cap) {
+          if (tb == 0 && bucket_equal_keys(skv, X, lb, stt, same)) {
+            // (equal keys collide under every t: retired, checked once)
+          } else if (tb + A >= kT2Cap) {
             atomicOr(&stt->exhausted, 1u);
             s_t[lb] = 0;
           } else {
