@@ -301,6 +301,33 @@ hm_status hm_build_u64_dist(const uint64_t* keys, const uint64_t* vals, uint64_t
 hm_status hm_lookup_u64_dist(const hm_map* shard, const uint64_t* q, uint64_t nq, uint64_t* out_vals,
                              uint8_t* out_found, void* stream, void* nccl_comm);
 
+/* The control decisions of the sharded build, shared by hm_build_u64_dist and
+ * any other orchestration of the per-rank pieces (paper_2508_11443_b200/dist.py
+ * over torch.distributed), so that both take them the same way.  Host-only:
+ * no device is touched.
+ *
+ * hm_dist_bucket_range — [*lo, *hi) of the level-1 buckets rank `rank` of
+ * `world` owns with n = n_global buckets: lo_r = ceil(r n / G).
+ * Returns HM_ERR_INVALID_ARG for world < 1, rank outside [0, world). */
+hm_status hm_dist_bucket_range(uint64_t n_global, int world, int rank, uint64_t* lo, uint64_t* hi);
+
+/* hm_dist_decide — after every rank built its shard with level-1 attempt t1
+ * and the ranks agreed on S_total = sum_r S_r (all-reduce sum) and
+ * max_status = max_r status_r (all-reduce max):
+ *   returns HM_OK when the build is done (max_status 0 and the global space
+ *     bound S_total <= 4 n_global holds, R7);
+ *   returns max_status (nonzero) when some shard failed: every rank reports it;
+ *   otherwise the bound failed: with t1 + 1 < 16, *next_t1 = t1 + 1 and the
+ *     return value is HM_DIST_REDRAW (route again with *next_t1); at t1 = 15,
+ *     HM_ERR_SEED_EXHAUSTED (PAPER.md has no bound; R7, R26). */
+#define HM_DIST_REDRAW 100
+int hm_dist_decide(uint64_t n_global, uint32_t t1, uint64_t S_total, int max_status, uint32_t* next_t1);
+
+/* hm_dist_slot_base — the global slot base of rank `rank`: sum of S_all[q]
+ * for q < rank (the exclusive prefix of the shards' slot counts, from an
+ * all-gather of S_r). */
+uint64_t hm_dist_slot_base(const uint64_t* S_all, int world, int rank);
+
 /* hm_build_u64_shard — build the shard of the global table that holds level-1
  * buckets [b_lo, b_hi) of a table with n_global keys, from exactly the keys
  * routed to it, with level-1 attempt t1 fixed by the caller.  The caller

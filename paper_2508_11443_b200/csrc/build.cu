@@ -1047,7 +1047,7 @@ __global__ void __launch_bounds__(KBCfg<E>::T, KBCfg<E>::MINB)
         s_chunk[(r + 2) % 3] = 0;
       }
       uint32_t logA = 0;
-      if (r == 0) logA = HM_R0_LOGA;
+      if (r == 0) logA = (bp.flags & HM_FLAG_NO_ROUND0_ILP) ? 0u : uint32_t(HM_R0_LOGA);
       else
         while (logA < HM_RETRY_LOGA && (L << (logA + 1)) <= uint32_t(KBCfg<E>::T)) logA++;
       const uint32_t A = 1u << logA, W = L << logA;
@@ -1804,6 +1804,13 @@ hm_status build_bytes_core(const uint8_t* bytes, const uint64_t* offsets, const 
     bool fpc = false;
     s = build_core<SrcBytes, KV32, SameBytes>(SrcBytes{fp, vals, offsets, off0}, SameBytes{bytes, off0}, n, n, 0, n,
                                                -1, seed, log2_bp, st, out, &fpc);
+    if (s == HM_ERR_TOO_LARGE) {
+      // a degenerate level-1 distribution within the space bound (a bucket of
+      // more than 32 keys, an overflowing build partition): the flat rounds
+      // take any bucket size and tell duplicates from fingerprint collisions
+      set_error("");
+      s = build_bytes_rounds(fp, vals, offsets, off0, bytes, n, seed, log2_bp >> 16, st, out, &fpc);
+    }
     if (s != HM_OK) return s;
     if (!fpc) {
       *t0_out = t0;

@@ -400,21 +400,6 @@ hm_status hm_build_bytes(const uint8_t* bytes, const uint64_t* offsets, const ui
   uint32_t t0 = 0;
   uint64_t r = 0;
   s = build_bytes_core(db, doff, dv, n, seed, opts ? (opts->log2_bp | (opts->flags << 16)) : 0, st, &bo, &t0, &r);
-  if (s == HM_ERR_TOO_LARGE && !(opts && (opts->flags & HM_FLAG_FROM_ARRAY))) {
-    // a degenerate level-1 distribution within the bound: equal keys (the
-    // oracle's DUPLICATE_KEY) are found by counting the distinct ones
-    const std::string why = hm_last_error();
-    uint8_t* pc = nullptr;
-    uint64_t *po = nullptr, *pv = nullptr, mdist = 0;
-    if (dedup_bytes(db, doff, dv, n, st, &pc, &po, &pv, &mdist) == HM_OK) {
-      for (void* q : {static_cast<void*>(pc), static_cast<void*>(po), static_cast<void*>(pv)}) cudaFreeAsync(q, st);
-      if (mdist < n) {
-        set_error("duplicate keys in from_array_nodup input");
-        return HM_ERR_DUPLICATE_KEY;
-      }
-    }
-    set_error(why);
-  }
   if (s != HM_OK) return s;
   hm_map* m = new_map();
   m->key_kind = 1;
@@ -817,6 +802,31 @@ hm_status hm_build_u64_shard(const uint64_t* keys, const uint64_t* vals, uint64_
   *S_local = bo.S;
   *out = m;
   return HM_OK;
+}
+
+hm_status hm_dist_bucket_range(uint64_t n_global, int world, int rank, uint64_t* lo, uint64_t* hi) {
+  if (world < 1 || rank < 0 || rank >= world || !lo || !hi) return HM_ERR_INVALID_ARG;
+  const unsigned __int128 n = n_global;
+  *lo = uint64_t((n * uint64_t(rank) + uint64_t(world) - 1) / uint64_t(world));
+  *hi = uint64_t((n * uint64_t(rank + 1) + uint64_t(world) - 1) / uint64_t(world));
+  return HM_OK;
+}
+
+int hm_dist_decide(uint64_t n_global, uint32_t t1, uint64_t S_total, int max_status, uint32_t* next_t1) {
+  if (max_status != 0) return max_status;
+  if (S_total <= 4 * n_global) return HM_OK;  // R7
+  if (t1 + 1 >= kT1Cap) {
+    set_error("level one exhausted 16 attempts without meeting S <= 4n");
+    return HM_ERR_SEED_EXHAUSTED;
+  }
+  if (next_t1) *next_t1 = t1 + 1;
+  return HM_DIST_REDRAW;
+}
+
+uint64_t hm_dist_slot_base(const uint64_t* S_all, int world, int rank) {
+  uint64_t b = 0;
+  for (int q = 0; q < rank && q < world; q++) b += S_all[q];
+  return b;
 }
 
 hm_status hm_shard_set_base(hm_map* map, uint64_t slot_base) {

@@ -114,17 +114,13 @@ hm_status hm_build_u64_dist(const uint64_t* keys, const uint64_t* vals, uint64_t
   HM_CUDA_TRY(cudaStreamSynchronize(st));
   if (n == 0) return HM_ERR_EMPTY;
   if (n > (1ull << 30)) return HM_ERR_TOO_LARGE;
-  const uint64_t lo = (uint64_t(rank) * n + world - 1) / world, hi = (uint64_t(rank + 1) * n + world - 1) / world;
+  uint64_t lo = 0, hi = 0;
+  if ((s = hm_dist_bucket_range(n, world, rank, &lo, &hi)) != HM_OK) return s;
   const uint64_t seed = opts ? opts->seed : 0;
   if ((s = db.get(&sk, n_local)) != HM_OK || (s = db.get(&sv, n_local)) != HM_OK) return s;
   hm_map* m = nullptr;
   uint64_t S_local = 0;
-  uint32_t t1 = 0;
-  for (;; t1++) {
-    if (t1 == kT1Cap) {
-      set_error("level one exhausted 16 attempts without meeting S <= 4n");
-      return HM_ERR_SEED_EXHAUSTED;
-    }
+  for (uint32_t t1 = 0;;) {
     // (2) route, exchange counts and pairs
     if ((s = hm_route_u64(keys, vals, n_local, n, seed, t1, world, sk, sv, d_sc, stream)) != HM_OK) return s;
     std::vector<uint64_t> sc, rc;
@@ -145,12 +141,14 @@ hm_status hm_build_u64_dist(const uint64_t* keys, const uint64_t* vals, uint64_t
     HM_NCCL_TRY(ncclAllReduce(d_small + 1, d_small + 1, 1, ncclUint64, ncclMax, comm, st));
     HM_CUDA_TRY(cudaMemcpyAsync(red, d_small, 16, cudaMemcpyDeviceToHost, st));
     HM_CUDA_TRY(cudaStreamSynchronize(st));
-    if (red[1] == 0 && red[0] <= 4 * n) break;
+    const int d = hm_dist_decide(n, t1, red[0], int(red[1]), &t1);
+    if (d == HM_OK) break;
     hm_free(m);
     m = nullptr;
-    if (red[1] != 0) {
-      set_error(local_err.empty() ? "a shard build failed on another rank (max status over ranks)" : local_err);
-      return hm_status(red[1]);
+    if (d != HM_DIST_REDRAW) {
+      if (red[1] != 0)
+        set_error(local_err.empty() ? "a shard build failed on another rank (max status over ranks)" : local_err);
+      return hm_status(d);
     }
   }
   // (4) the slot base: exclusive prefix of S_r
@@ -159,8 +157,7 @@ hm_status hm_build_u64_dist(const uint64_t* keys, const uint64_t* vals, uint64_t
   std::vector<uint64_t> sall(world);
   HM_CUDA_TRY(cudaMemcpyAsync(sall.data(), d_sall, world * 8, cudaMemcpyDeviceToHost, st));
   HM_CUDA_TRY(cudaStreamSynchronize(st));
-  uint64_t base = 0;
-  for (int r = 0; r < rank; r++) base += sall[r];
+  const uint64_t base = hm_dist_slot_base(sall.data(), world, rank);
   if ((s = hm_shard_set_base(m, base)) != HM_OK) {
     hm_free(m);
     return s;

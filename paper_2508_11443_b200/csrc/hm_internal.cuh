@@ -173,6 +173,9 @@ hm_status dedup_u64(const uint64_t* keys, const uint64_t* vals, uint64_t n, cuda
 hm_status build_u64_rounds(const uint64_t* keys, const uint64_t* vals, uint64_t n_in, uint64_t n_global,
                            uint64_t b_lo, uint64_t nb, int t1_fixed, uint64_t seed, uint32_t flags, cudaStream_t st,
                            BuildOut* out);
+hm_status build_bytes_rounds(const uint64_t* fp, const uint64_t* vals, const uint64_t* offs, uint64_t off0,
+                             const uint8_t* bytes, uint64_t n, uint64_t seed, uint32_t flags, cudaStream_t st,
+                             BuildOut* out, bool* fpcoll);
 // assemble.cu
 hm_status assemble_cdir_launch(const uint64_t* dir, const void* slots, uint64_t n, uint64_t S, const L1Params& l1,
                                uint32_t full_dir, CDir* cdir, unsigned int* bad, cudaStream_t st);

@@ -25,9 +25,29 @@ struct Consts {  // (a1, a2, b)
   uint64_t a1, a2, b;
 };
 
+// z * c mod 2^64.  On the device as three 32-bit multiply-adds (the low
+// product widened, both cross terms added into its high word) where nvcc emits
+// four; on the host the plain product.
+__host__ __device__ __forceinline__ uint64_t mul64_lo(uint64_t z, uint64_t c) {
+#if defined(__CUDA_ARCH__)
+  uint64_t r;
+  asm("{ .reg .u32 wl, wh; .reg .u64 w;\n\t"
+      "mul.wide.u32 w, %1, %3;\n\t"
+      "mov.b64 {wl, wh}, w;\n\t"
+      "mad.lo.u32 wh, %2, %3, wh;\n\t"
+      "mad.lo.u32 wh, %1, %4, wh;\n\t"
+      "mov.b64 %0, {wl, wh}; }"
+      : "=l"(r)
+      : "r"(uint32_t(z)), "r"(uint32_t(z >> 32)), "r"(uint32_t(c)), "r"(uint32_t(c >> 32)));
+  return r;
+#else
+  return z * c;
+#endif
+}
+
 __host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
-  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  z = mul64_lo(z ^ (z >> 30), 0xBF58476D1CE4E5B9ull);
+  z = mul64_lo(z ^ (z >> 27), 0x94D049BB133111EBull);
   return z ^ (z >> 31);
 }
 

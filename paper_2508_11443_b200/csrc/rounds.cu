@@ -62,15 +62,47 @@ __device__ __forceinline__ uint32_t level2_slot(const RoundsParams& P, uint64_t 
   return uint32_t(hv % s2);
 }
 
+// The keys the rounds hash and the slot records they write: u64 keys
+// ({key, value}) or byte keys ({fingerprint, value, ctx_off, len}, the
+// fingerprints of the current t0).
+struct RSrcU64 {
+  const uint64_t* keys;
+  const uint64_t* vals;
+  __device__ __forceinline__ uint64_t key(uint64_t i) const { return keys[i]; }
+  __device__ __forceinline__ KV16 rec(uint64_t i) const {
+    KV16 e;
+    e.key = keys[i];
+    e.value = vals[i];
+    return e;
+  }
+};
+struct RSrcBytes {
+  const uint64_t* fp;
+  const uint64_t* vals;
+  const uint64_t* offs;
+  uint64_t off0;
+  __device__ __forceinline__ uint64_t key(uint64_t i) const { return fp[i]; }
+  __device__ __forceinline__ KV32 rec(uint64_t i) const {
+    KV32 e;
+    e.key = fp[i];
+    e.value = vals[i];
+    e.ctx_off = offs[i] - off0;
+    e.len = uint32_t(offs[i + 1] - offs[i]);
+    e.reserved = 0;
+    return e;
+  }
+};
+
 #define HM_GRID_LOOP(i, n) \
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < (n); i += uint64_t(gridDim.x) * blockDim.x)
 
 // make_1: the level-1 bucket of every key and `shape = hist n hashes`
 // (local buckets b - b_lo of a shard's range [b_lo, b_lo + nb))
-__global__ void k_r_l1_hist(const uint64_t* __restrict__ keys, uint64_t n, L1Params l1, uint64_t b_lo, uint64_t nb,
+template <class Src>
+__global__ void k_r_l1_hist(Src src, uint64_t n, L1Params l1, uint64_t b_lo, uint64_t nb,
                             uint32_t* __restrict__ kb, unsigned int* __restrict__ shape, unsigned int* __restrict__ bad) {
   HM_GRID_LOOP(i, n) {
-    const uint64_t b = level1_bucket(l1, keys[i]) - b_lo;
+    const uint64_t b = level1_bucket(l1, src.key(i)) - b_lo;
     if (b >= nb) {
       atomicOr(bad, 1u);
       kb[i] = 0;
@@ -101,11 +133,12 @@ __global__ void k_r_init_active(const unsigned int* __restrict__ shape, const ui
 }
 
 // okeys = zip koffsets keys
-__global__ void k_r_init_keys(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ kb,
+template <class Src>
+__global__ void k_r_init_keys(Src src, const uint32_t* __restrict__ kb,
                               const uint64_t* __restrict__ rank, uint64_t n, ActKey* __restrict__ ak) {
   HM_GRID_LOOP(i, n) {
     ActKey a;
-    a.key = keys[i];
+    a.key = src.key(i);
     a.idx = uint32_t(i);
     a.o = uint32_t(rank[kb[i]]);
     ak[i] = a;
@@ -199,30 +232,28 @@ __global__ void k_r_fin_min(const uint32_t* __restrict__ kb, const unsigned int*
   }
 }
 
+template <class Src, class E>
 __global__ void k_r_fin_fill(const unsigned int* __restrict__ shape, const uint64_t* __restrict__ soff,
-                             const unsigned long long* __restrict__ fsel, const uint64_t* __restrict__ keys,
-                             uint64_t n, KV16* __restrict__ slots) {
+                             const unsigned long long* __restrict__ fsel, Src src,
+                             uint64_t n, E* __restrict__ slots) {
   HM_GRID_LOOP(b, n) {
     const uint32_t s = shape[b];
     if (s < 2) continue;
-    KV16 f;
-    f.key = keys[uint32_t(fsel[b])];
+    E f = src.rec(uint32_t(fsel[b]));
     f.value = 0;
-    KV16* out = slots + soff[b];
+    E* out = slots + soff[b];
     for (uint32_t x = 0; x < s * s; x++) out[x] = f;
   }
 }
 
-__global__ void k_r_fin_members(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ vals,
-                                const uint32_t* __restrict__ kb, const unsigned int* __restrict__ shape,
+template <class Src, class E>
+__global__ void k_r_fin_members(Src src, const uint32_t* __restrict__ kb, const unsigned int* __restrict__ shape,
                                 const uint64_t* __restrict__ soff, const uint32_t* __restrict__ hkey, L1Params l1,
-                                uint64_t n, KV16* __restrict__ slots, uint8_t* __restrict__ tb) {
+                                uint64_t n, E* __restrict__ slots, uint8_t* __restrict__ tb) {
   HM_GRID_LOOP(i, n) {
     const uint32_t b = kb[i];
-    const uint64_t k = keys[i];
-    KV16 e;
-    e.key = k;
-    e.value = vals[i];
+    const E e = src.rec(i);
+    const uint64_t k = e.key;
     slots[soff[b] + hkey[i]] = e;
     if (shape[b] == 1) tb[b] = uint8_t(tag4_of_hash(hash64(l1.c1, k)));  // the cdir tag of a singleton
   }
@@ -294,9 +325,41 @@ struct Owned {
     name<<<(grid), kRT, 0, st>>>(__VA_ARGS__);             \
   } while (0)
 
-hm_status build_u64_rounds(const uint64_t* keys, const uint64_t* vals, uint64_t n_in, uint64_t n_global,
-                           uint64_t b_lo, uint64_t nb, int t1_fixed, uint64_t seed, uint32_t flags, cudaStream_t st,
-                           BuildOut* out) {
+// Equal keys left in a bucket that exhausted its attempts: u64 keys are
+// duplicates; equal fingerprints of byte keys are duplicates when the bytes are
+// equal too, else a fingerprint collision (the caller redraws t0).
+struct SameHostU64 {
+  hm_status operator()(uint32_t, uint32_t, cudaStream_t, bool* fpcoll) const {
+    *fpcoll = false;
+    return HM_OK;
+  }
+};
+struct SameHostBytes {
+  const uint8_t* bytes;
+  const uint64_t* offs;
+  hm_status operator()(uint32_t i, uint32_t j, cudaStream_t st, bool* fpcoll) const {
+    uint64_t oi[2], oj[2];
+    HM_CUDA_TRY(cudaMemcpyAsync(oi, offs + i, 16, cudaMemcpyDeviceToHost, st));
+    HM_CUDA_TRY(cudaMemcpyAsync(oj, offs + j, 16, cudaMemcpyDeviceToHost, st));
+    HM_CUDA_TRY(cudaStreamSynchronize(st));
+    bool same = oi[1] - oi[0] == oj[1] - oj[0];
+    if (same && oi[1] > oi[0]) {
+      std::vector<uint8_t> a(oi[1] - oi[0]), b(oj[1] - oj[0]);
+      HM_CUDA_TRY(cudaMemcpyAsync(a.data(), bytes + oi[0], a.size(), cudaMemcpyDeviceToHost, st));
+      HM_CUDA_TRY(cudaMemcpyAsync(b.data(), bytes + oj[0], b.size(), cudaMemcpyDeviceToHost, st));
+      HM_CUDA_TRY(cudaStreamSynchronize(st));
+      same = a == b;
+    }
+    *fpcoll = !same;
+    return HM_OK;
+  }
+};
+
+template <class Src, class E, class SameHost>
+static hm_status build_rounds_core(Src src, SameHost same, uint64_t n_in, uint64_t n_global, uint64_t b_lo,
+                                   uint64_t nb, int t1_fixed, uint64_t seed, uint32_t flags, cudaStream_t st,
+                                   BuildOut* out, bool* fpcoll) {
+  *fpcoll = false;
   Owned ow{st, {}};
   const uint64_t smix = seed_mix(seed);
   const unsigned gmax = unsigned(num_sms()) * 8;
@@ -332,7 +395,7 @@ hm_status build_u64_rounds(const uint64_t* keys, const uint64_t* vals, uint64_t 
     const L1Params l1 = make_l1(smix, t1, n_global);
     HM_CUDA_TRY(cudaMemsetAsync(shape, 0, n * 4, st));
     HM_CUDA_TRY(cudaMemsetAsync(bad, 0, 4, st));
-    HM_RLAUNCH(k_r_l1_hist, grid(n_in), keys, n_in, l1, b_lo, nb, kb, shape, bad);
+    HM_RLAUNCH(k_r_l1_hist, grid(n_in), src, n_in, l1, b_lo, nb, kb, shape, bad);
     HM_RLAUNCH(k_r_l1_prep, grid(n + 1), shape, n, soff, rank);
     if ((s = scan_excl(soff, n + 1, sums, st)) != HM_OK) return s;
     unsigned int hbad = 0;
@@ -375,7 +438,7 @@ hm_status build_u64_rounds(const uint64_t* keys, const uint64_t* vals, uint64_t 
   HM_CUDA_TRY(cudaMemsetAsync(flat, 0, S * 4, st));
   HM_CUDA_TRY(cudaMemsetAsync(tb, 0, n, st));
   HM_RLAUNCH(k_r_init_active, grid(n), shape, rank, n, A);
-  HM_RLAUNCH(k_r_init_keys, grid(n_in), keys, kb, rank, n_in, ak);
+  HM_RLAUNCH(k_r_init_keys, grid(n_in), src, kb, rank, n_in, ak);
 
   // level two: segmake'_2 rounds, round r = attempt t = r
   uint64_t nk = n_in;
@@ -403,12 +466,22 @@ hm_status build_u64_rounds(const uint64_t* keys, const uint64_t* vals, uint64_t 
     std::vector<ActKey> h(nk);
     HM_CUDA_TRY(cudaMemcpyAsync(h.data(), ak, nk * sizeof(ActKey), cudaMemcpyDeviceToHost, st));
     HM_CUDA_TRY(cudaStreamSynchronize(st));
-    std::vector<uint64_t> k(nk);
-    for (uint64_t j = 0; j < nk; j++) k[j] = h[j].key;
-    std::sort(k.begin(), k.end());
-    if (std::adjacent_find(k.begin(), k.end()) != k.end()) {
+    std::sort(h.begin(), h.end(), [](const ActKey& a, const ActKey& b) { return a.key < b.key; });
+    bool dup = false, coll = false;
+    for (uint64_t j = 1; j < nk; j++)
+      if (h[j].key == h[j - 1].key) {
+        bool fc = false;
+        hm_status s2 = same(h[j - 1].idx, h[j].idx, st, &fc);
+        if (s2 != HM_OK) return s2;
+        (fc ? coll : dup) = true;
+      }
+    if (dup) {  // (duplicates first, then fingerprint collisions: SURVEY 8(c) step 5)
       set_error("duplicate keys in from_array_nodup input");
       return HM_ERR_DUPLICATE_KEY;
+    }
+    if (coll) {
+      *fpcoll = true;
+      return HM_OK;
     }
     set_error("a level-2 bucket exhausted 256 attempts");
     return HM_ERR_SEED_EXHAUSTED;
@@ -417,9 +490,9 @@ hm_status build_u64_rounds(const uint64_t* keys, const uint64_t* vals, uint64_t 
   // the table
   uint64_t* dir = nullptr;
   CDir* cdir = nullptr;
-  KV16* slots = nullptr;
+  E* slots = nullptr;
   std::vector<void*> res;
-  const size_t bytes_[3] = {n * 8, ((n + 31) / 32) * sizeof(CDir), S * sizeof(KV16)};
+  const size_t bytes_[3] = {n * 8, ((n + 31) / 32) * sizeof(CDir), S * sizeof(E)};
   const size_t* bytes = bytes_;
   auto fail = [&](hm_status code) {
     for (size_t a = 0; a < res.size(); a++) map_discard(res[a], bytes_[a], st);
@@ -432,12 +505,12 @@ hm_status build_u64_rounds(const uint64_t* keys, const uint64_t* vals, uint64_t 
   }
   dir = static_cast<uint64_t*>(arr[0]);
   cdir = static_cast<CDir*>(arr[1]);
-  slots = static_cast<KV16*>(arr[2]);
+  slots = static_cast<E*>(arr[2]);
   const L1Params l1 = make_l1(smix, t1, n_global);
   HM_CUDA_TRY(cudaMemsetAsync(fsel, 0xFF, n * 8, st));
   HM_RLAUNCH(k_r_fin_min, grid(n_in), kb, shape, hkey, n_in, fsel);
-  HM_RLAUNCH(k_r_fin_fill, grid(n), shape, soff, fsel, keys, n, slots);
-  HM_RLAUNCH(k_r_fin_members, grid(n_in), keys, vals, kb, shape, soff, hkey, l1, n_in, slots, tb);
+  HM_RLAUNCH(k_r_fin_fill, grid(n), shape, soff, fsel, src, n, slots);
+  HM_RLAUNCH(k_r_fin_members, grid(n_in), src, kb, shape, soff, hkey, l1, n_in, slots, tb);
   HM_RLAUNCH(k_r_fin_dir, grid(n), shape, soff, tb, n, flags & HM_FLAG_FULL_DIRECTORY, dir, cdir);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(cuda_fail(e, "rounds build"));
@@ -448,6 +521,24 @@ hm_status build_u64_rounds(const uint64_t* keys, const uint64_t* vals, uint64_t 
   out->S = S;
   out->t1 = t1;
   return HM_OK;
+}
+
+hm_status build_u64_rounds(const uint64_t* keys, const uint64_t* vals, uint64_t n_in, uint64_t n_global,
+                           uint64_t b_lo, uint64_t nb, int t1_fixed, uint64_t seed, uint32_t flags, cudaStream_t st,
+                           BuildOut* out) {
+  bool fc = false;
+  return build_rounds_core<RSrcU64, KV16>(RSrcU64{keys, vals}, SameHostU64{}, n_in, n_global, b_lo, nb, t1_fixed,
+                                          seed, flags, st, out, &fc);
+}
+
+// Byte keys (their fingerprints fp[n] under the current t0): any bucket size,
+// the same table as the partitioned build (a fallback for degenerate level-1
+// distributions); *fpcoll: equal fingerprints with different bytes.
+hm_status build_bytes_rounds(const uint64_t* fp, const uint64_t* vals, const uint64_t* offs, uint64_t off0,
+                             const uint8_t* bytes, uint64_t n, uint64_t seed, uint32_t flags, cudaStream_t st,
+                             BuildOut* out, bool* fpcoll) {
+  return build_rounds_core<RSrcBytes, KV32>(RSrcBytes{fp, vals, offs, off0}, SameHostBytes{bytes, offs}, n, n, 0, n,
+                                            -1, seed, flags, st, out, fpcoll);
 }
 
 }  // namespace hm

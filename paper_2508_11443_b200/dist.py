@@ -32,10 +32,9 @@ from . import hm as _hm
 
 
 def bucket_range(rank: int, world: int, n: int):
-    """[lo, hi) of the level-1 buckets owned by `rank` (owner(b) = floor(b*G/n))."""
-    lo = -(-rank * n // world)
-    hi = -(-(rank + 1) * n // world)
-    return lo, hi
+    """[lo, hi) of the level-1 buckets owned by `rank` (owner(b) = floor(b*G/n)),
+    hm_dist_bucket_range."""
+    return _hm.dist_bucket_range(n, world, rank)
 
 
 class GpuOps:
@@ -133,27 +132,29 @@ def build_dist(keys, vals, seed: int = 0, ops=None, group=None) -> DistMap:
     if n == 0:
         raise _hm.HMError(2, "global key set is empty")
     lo, hi = bucket_range(rank, world, n)
-    for t1 in range(16):
+    t1 = 0
+    while True:
         sk, sv, counts = ops.route(keys, vals, n, seed, t1, world)
         in_counts = [int(x) for x in counts.tolist()]
         rk, out_counts = _all_to_all_v(sk, in_counts, group, dev)
         rv, _ = _all_to_all_v(sv, in_counts, group, dev, out_counts)  # (same splits)
         shard, S_local, code = ops.build_shard(rk, rv, n, lo, hi, t1, seed)
-        # agree on the outcome: the space bound is global (R7), errors are global
+        # agree on the outcome: the space bound is global (R7), errors are global;
+        # the decision itself is libhm's (hm_dist_decide, shared with hm_build_u64_dist)
         red = torch.tensor([S_local, code], dtype=torch.int64, device=dev)
         tdist.all_reduce(red[:1], group=group)
         tdist.all_reduce(red[1:], op=tdist.ReduceOp.MAX, group=group)
         S_total, code = int(red[0].item()), int(red[1].item())
-        if code == 0 and S_total <= 4 * n:
+        d, t1_next = _hm.dist_decide(n, t1, S_total, code)
+        if d == 0:
             break
         ops.free(shard)
-        if code != 0:
-            raise _hm.HMError(code, f"shard build failed (max status over ranks) at t1={t1}")
-    else:
-        raise _hm.HMError(4, "level one exhausted 16 attempts without meeting S <= 4n")
+        if d != _hm.DIST_REDRAW:
+            raise _hm.HMError(d, f"sharded build failed at t1={t1} (max status over ranks)")
+        t1 = t1_next
     allS = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(world)]
     tdist.all_gather(allS, torch.tensor([S_local], dtype=torch.int64, device=dev), group=group)
-    base = sum(int(x.item()) for x in allS[:rank])
+    base = _hm.dist_slot_base([int(x.item()) for x in allS], rank)
     ops.set_base(shard, base)
     return DistMap(shard, n, lo, hi, t1, S_local, base, S_total, world, rank, ops, group, seed,
                    tuple(int(x.item()) for x in allS))

@@ -96,6 +96,12 @@ def lib():
         L.hm_assemble_u64.argtypes = [p, p, u64, u64, u64, u32, C.POINTER(_Opts), p, C.POINTER(p)]
         L.hm_build_u64_dist.argtypes = [p, p, u64, C.POINTER(_Opts), p, p, C.POINTER(p)]
         L.hm_lookup_u64_dist.argtypes = [p, p, u64, p, p, p, p]
+        L.hm_dist_bucket_range.argtypes = [u64, i32, i32, C.POINTER(u64), C.POINTER(u64)]
+        L.hm_dist_bucket_range.restype = C.c_int
+        L.hm_dist_decide.argtypes = [u64, u32, u64, i32, C.POINTER(u32)]
+        L.hm_dist_decide.restype = C.c_int
+        L.hm_dist_slot_base.argtypes = [p, i32, i32]
+        L.hm_dist_slot_base.restype = u64
         for f in ("hm_assemble_u64", "hm_build_u64_dist", "hm_lookup_u64_dist", "hm_build_u64", "hm_build_bytes", "hm_lookup_u64", "hm_lookup_bytes", "hm_info", "hm_export",
                   "hm_route_u64", "hm_build_u64_shard", "hm_shard_set_base", "hm_route_queries_u64",
                   "hm_unroute_u64"):
@@ -424,6 +430,29 @@ def unroute_u64(vals_routed, found_routed, perm, out_vals, out_found, stream=Non
     v, vk = _ptr(out_vals, 8, out=True)
     f, fk = _ptr(out_found, 1, out=True)
     _check(lib().hm_unroute_u64(a, b, p, _numel(perm), v, f, _stream(stream)))
+
+
+DIST_REDRAW = 100  # HM_DIST_REDRAW
+
+
+def dist_bucket_range(n_global: int, world: int, rank: int):
+    """[lo, hi) of the level-1 buckets `rank` owns (hm_dist_bucket_range)."""
+    lo, hi = C.c_uint64(), C.c_uint64()
+    _check(lib().hm_dist_bucket_range(n_global, world, rank, C.byref(lo), C.byref(hi)))
+    return int(lo.value), int(hi.value)
+
+
+def dist_decide(n_global: int, t1: int, S_total: int, max_status: int):
+    """(code, next_t1) of hm_dist_decide: 0 done, DIST_REDRAW route again with
+    next_t1, else the status every rank reports."""
+    nt = C.c_uint32(0)
+    code = int(lib().hm_dist_decide(n_global, t1, S_total, max_status, C.byref(nt)))
+    return code, int(nt.value)
+
+
+def dist_slot_base(S_all, rank: int) -> int:
+    a = np.ascontiguousarray(np.asarray(S_all, dtype=np.uint64))
+    return int(lib().hm_dist_slot_base(a.ctypes.data_as(C.c_void_p), len(a), rank))
 
 
 class _KStat(C.Structure):

@@ -89,3 +89,31 @@ def test_shard_build_rejects_single_table_flags():
     for f in (hm.FLAG_FROM_ARRAY, hm.FLAG_ROUNDS):
         o = hm._opts(0, 0, f)
         assert L.hm_build_u64_shard(kp, kp, 4, 8, 0, 4, 0, C.byref(o), None, C.byref(out), C.byref(S)) == 1
+
+
+def test_dist_decisions_need_no_device():
+    """The sharded build's control decisions (hm_dist_*), shared by
+    hm_build_u64_dist and dist.py: the space bound R7 with its 16 level-1
+    draws, the max-status agreement, the bucket ranges owner(b) = floor(bG/n)
+    and the slot bases."""
+    REDRAW = hm.DIST_REDRAW
+    assert hm.dist_decide(100, 0, 400, 0) == (0, 0)          # S = 4n: done
+    assert hm.dist_decide(100, 0, 401, 0) == (REDRAW, 1)     # S > 4n: redraw t1 + 1
+    assert hm.dist_decide(100, 14, 401, 0) == (REDRAW, 15)
+    assert hm.dist_decide(100, 15, 401, 0)[0] == 4           # t1 = 15: SEED_EXHAUSTED (R7 cap)
+    assert hm.dist_decide(100, 3, 10, 3)[0] == 3             # a shard failed: its status everywhere
+    assert hm.dist_decide(100, 3, 10**9, 3)[0] == 3          # (a failure before the bound)
+    for n in (1, 7, 100, 1 << 20, (1 << 30) + 0):
+        for world in (1, 2, 3, 8, 64):
+            prev = 0
+            for r in range(world):
+                lo, hi = hm.dist_bucket_range(n, world, r)
+                assert lo == prev and lo == -(-r * n // world) and hi == -(-(r + 1) * n // world)
+                # every bucket b of the range has owner floor(b*G/n) = r
+                for b in {lo, hi - 1} if hi > lo else ():
+                    assert b * world // n == r
+                prev = hi
+            assert prev == n
+    with __import__("pytest").raises(hm.HMError):
+        hm.dist_bucket_range(10, 2, 2)
+    assert [hm.dist_slot_base([5, 7, 11], r) for r in range(3)] == [0, 5, 12]

@@ -285,9 +285,13 @@ def test_u64_duplicate_heavy_overflow_matches_oracle():
     n = 2_000_000
     keys = gen.u64_keys(n)
     keys[:1500] = keys[11]
+    vals = gen.u64_values(n)
+    with pytest.raises(O.OracleError) as eo:
+        O.build_u64(keys, vals, 0)
     with pytest.raises(hm.HMError) as e:
-        hm.HashMap.build_u64(dev(keys), dev(gen.u64_values(n)))
-    assert e.value.name == "DUPLICATE_KEY"  # (the bound holds: the flat rounds take over and find them)
+        hm.HashMap.build_u64(dev(keys), dev(vals))
+    # (the bound holds: the flat rounds take over and find them, as the oracle's make2 does)
+    assert e.value.name == eo.value.name == "DUPLICATE_KEY"
     # the map and the workspace stay usable after the degenerate builds
     keys, vals = gen.u64_keys(5000), gen.u64_values(5000)
     m = hm.HashMap.build_u64(dev(keys), dev(vals))
@@ -517,6 +521,87 @@ def test_bytes_duplicate_heavy_reports_duplicate_key():
     strs = gen.string_list(*gen.string_keys(2_000_000))
     keys = strs[:1_998_500] + [strs[3]] * 1500
     ctx, offs = gen.pack_bytes_list(keys)
+    vals = gen.u64_values(len(keys))
+    with pytest.raises(O.OracleError) as eo:
+        O.build_bytes(ctx, offs, vals, 0)
     with pytest.raises(hm.HMError) as e:
-        hm.HashMap.build_bytes(torch.from_numpy(ctx).cuda(), dev(offs), dev(gen.u64_values(len(keys))))
-    assert e.value.name == "DUPLICATE_KEY"
+        hm.HashMap.build_bytes(torch.from_numpy(ctx).cuda(), dev(offs), dev(vals))
+    assert e.value.name == eo.value.name == "DUPLICATE_KEY"
+
+
+def _fp_fixture():
+    import os
+    import sys
+    sys.path.insert(0, os.path.dirname(__file__))
+    from test_oracle_fpcoll import load_fixture
+    return load_fixture()
+
+
+@pytest.mark.parametrize("name", ["s2", "s3", "s5", "s9"])
+def test_bytes_fingerprint_collision_redraws_t0(name):
+    """Two different keys with equal fingerprints at (seed 0, t0 0) (the
+    lattice-built fixture, tests/golden/fp_collision_seed0.txt; DESIGN R5,
+    SURVEY 8(c) step 5): the GPU detects them in their level-1 bucket — a
+    2-key bucket in round 0 (s2), 3- and 5-key buckets (s3, s5), a 9-key
+    bucket in the warp-per-bucket search (s9) — redraws t0, and its table is
+    the oracle's (t0 = 1) byte for byte."""
+    hm = _hm()
+    fx = _fp_fixture()
+    strs = fx["sets"][name]
+    ctx, offs = gen.pack_bytes_list(strs)
+    vals = np.arange(100, 100 + len(strs), dtype=np.uint64)
+    ot = O.build_bytes(ctx, offs, vals, 0)
+    assert int(ot.header["t0"]) == 1
+    m = hm.HashMap.build_bytes(torch.from_numpy(ctx).cuda(), dev(offs), dev(vals))
+    assert m.info().t0 == 1
+    assert_table_equal(m, ot)
+    gv, gf = m.lookup_bytes(torch.from_numpy(ctx).cuda(), dev(offs))
+    assert bool(gf.all()) and np.array_equal(host(gv), vals)
+    m.free()
+
+
+def test_bytes_fingerprint_collision_among_many_keys():
+    """The colliding pair among 200 000 generated strings (equal fingerprints
+    share a level-1 bucket at any n): redraw t0, the oracle's table."""
+    hm = _hm()
+    fx = _fp_fixture()
+    a, b = fx["pair"]
+    strs = gen.string_list(*gen.string_keys(200_000))
+    strs[1234] = a
+    strs[150_001] = b
+    assert len(set(strs)) == len(strs)
+    ctx, offs = gen.pack_bytes_list(strs)
+    vals = gen.u64_values(len(strs), lo=9)
+    ot = O.build_bytes(ctx, offs, vals, 0)
+    assert int(ot.header["t0"]) == 1
+    m = hm.HashMap.build_bytes(torch.from_numpy(ctx).cuda(), dev(offs), dev(vals))
+    assert_table_equal(m, ot)
+    m.free()
+
+
+def test_bytes_bucket_over_32_keys_takes_the_flat_rounds():
+    """33 distinct byte keys whose fingerprints share one level-1 bucket, within
+    the space bound: outside the partitioned search (s <= 32), so the byte
+    build falls back to the flat rounds (any s) — the oracle's table, not
+    TOO_LARGE (make2 has no size cap)."""
+    hm = _hm()
+    n, seed = 1024, 0
+    r0 = O.derive(seed, 0, 0, 0)[0]
+    c1 = O.derive(seed, 1, 0, 0)
+    cand = gen.string_list(*gen.string_keys(60_000, lo=5))
+    bucket = [O.hash_(c1, O.fingerprint(x, r0)) % n for x in cand]
+    b0 = bucket[0]
+    same = [x for x, b in zip(cand, bucket) if b == b0][:33]
+    other = [x for x, b in zip(cand, bucket) if b != b0][: n - 33]
+    assert len(same) == 33 and len(other) == n - 33
+    strs = same + other
+    ctx, offs = gen.pack_bytes_list(strs)
+    vals = gen.u64_values(n, lo=1)
+    ot = O.build_bytes(ctx, offs, vals, seed)
+    assert int(ot.header["t0"]) == 0 and int(ot.header["t1"]) == 0
+    assert (ot.dir >> np.uint64(40) & np.uint64(0xFFFF)).max() == 33
+    m = hm.HashMap.build_bytes(torch.from_numpy(ctx).cuda(), dev(offs), dev(vals), seed=seed)
+    assert_table_equal(m, ot)
+    gv, gf = m.lookup_bytes(torch.from_numpy(ctx).cuda(), dev(offs))
+    assert bool(gf.all()) and np.array_equal(host(gv), vals)
+    m.free()
