@@ -54,6 +54,9 @@ struct KBCfg {
   static constexpr int W = T / 32;
   static constexpr int MINB = sizeof(E) == 16 ? HM_KB_MINB : HM_KB_MINB_BYTES;
 };
+#ifndef HM_PF_DIST
+#define HM_PF_DIST 148  // k_bucket: L2 prefetch of partition p + HM_PF_DIST (0: off; 148 measured best)
+#endif
 #ifndef HM_R0_LOGA
 #define HM_R0_LOGA 1  // round 0: 2^1 adjacent lanes (attempts 0, 1) per bucket
 #endif
@@ -316,7 +319,10 @@ __global__ void __launch_bounds__(kAThreads) k_partition(Src src, BuildParams bp
 // (scattered partial-sector stores), a 256-way pass writes runs of ~16
 // elements from a shared-memory staging tile.  Ranking inside the tile uses
 // one shared-memory atomicAdd per element.
-constexpr int kSThreads = 512;
+#ifndef HM_SPLIT_T
+#define HM_SPLIT_T 512  // (>= the digit count 2^BITS: one digit per thread in the scan)
+#endif
+constexpr int kSThreads = HM_SPLIT_T;
 // elements per thread: 8 x 16-byte or 4 x 32-byte records in registers
 #ifndef HM_SPLIT_PT
 #define HM_SPLIT_PT 6
@@ -823,6 +829,17 @@ __global__ void __launch_bounds__(KBCfg<E>::T, KBCfg<E>::MINB)
   const uint64_t bbase = bp.b_lo + lb0;  // global id of the partition's first bucket
 
   // ---- load: one bulk copy (TMA) of the partition's elements into shared memory
+#if HM_PF_DIST
+  // (and an L2 prefetch of the partition a CTA takes about a wave later, so
+  // that its load finds the lines in L2)
+  if (tid == 32 && p + HM_PF_DIST < bp.np) {
+    const uint32_t q = p + HM_PF_DIST, cq = min(pcount[q], cap);
+    const uint32_t qb = (cq * uint32_t(sizeof(E)) + 15u) & ~15u, ql = ((cq + 7) & ~7u) * 2;
+    if (qb)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pbuf + size_t(q) * cap), "r"(qb) : "memory");
+    if (ql) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(plb + size_t(q) * cap), "r"(ql) : "memory");
+  }
+#endif
   if (tid == 0) {
     const uint32_t bytes = cnt * uint32_t(sizeof(E));
     const uint32_t lbytes = ((cnt + 7) & ~7u) * 2;  // (16-byte multiple; cap is a multiple of 32)
