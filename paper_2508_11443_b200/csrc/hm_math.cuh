@@ -368,14 +368,16 @@ __device__ __forceinline__ uint64_t fingerprint_pw64(const uint8_t* bytes, uint6
     const uint32_t rem = L - 4 * i;
     uint32_t w0 = uint32_t(x);
     if (rem < 4) w0 &= (1u << (8 * rem)) - 1u;
-    acc += mul32_p(w0, pw->lo[nw - i], pw->hi[nw - i]);
-    acc = (acc & kP) + (acc >> 61);
+    // two partially reduced terms (< 2^62 + 2^33 each) on acc (< 2^61 + 8) stay
+    // below 2^64: one fold per pair
+    uint64_t t2 = mul32_p(w0, pw->lo[nw - i], pw->hi[nw - i]);
     if (i + 1 < nw) {
       uint32_t w1 = uint32_t(x >> 32);
       if (rem - 4 < 4) w1 &= (1u << (8 * (rem - 4))) - 1u;
-      acc += mul32_p(w1, pw->lo[nw - i - 1], pw->hi[nw - i - 1]);
-      acc = (acc & kP) + (acc >> 61);
+      t2 += mul32_p(w1, pw->lo[nw - i - 1], pw->hi[nw - i - 1]);
     }
+    acc += t2;
+    acc = (acc & kP) + (acc >> 61);
   }
   uint64_t f = acc + len;
   f = (f & kP) + (f >> 61);
@@ -397,14 +399,14 @@ __device__ __forceinline__ uint64_t fingerprint_sm64(const uint64_t* sb, uint32_
     const uint32_t rem = len - 4 * i;
     uint32_t w0 = uint32_t(x);
     if (rem < 4) w0 &= (1u << (8 * rem)) - 1u;
-    acc += mul32_p(w0, pw->lo[nw - i], pw->hi[nw - i]);
-    acc = (acc & kP) + (acc >> 61);
+    uint64_t t2 = mul32_p(w0, pw->lo[nw - i], pw->hi[nw - i]);  // (one fold per pair, as above)
     if (i + 1 < nw) {
       uint32_t w1 = uint32_t(x >> 32);
       if (rem - 4 < 4) w1 &= (1u << (8 * (rem - 4))) - 1u;
-      acc += mul32_p(w1, pw->lo[nw - i - 1], pw->hi[nw - i - 1]);
-      acc = (acc & kP) + (acc >> 61);
+      t2 += mul32_p(w1, pw->lo[nw - i - 1], pw->hi[nw - i - 1]);
     }
+    acc += t2;
+    acc = (acc & kP) + (acc >> 61);
   }
   uint64_t f = acc + len;
   f = (f & kP) + (f >> 61);

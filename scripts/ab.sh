@@ -29,3 +29,5 @@ from paper_2508_11443_b200 import _build
 _build.build_variant('timing', ['HM_PHASE_TIMING'] + [d for d in '${TIMING_DEFS}'.split(',') if d])" >> $OUT/build.log 2>&1
   timeout 300 python scripts/phase_times.py 26 2>&1 | tee $OUT/phases.txt
 fi
+[ -n "$LBYTES" ] && timeout 600 python scripts/lookup_bytes_variants.py $libs 2>&1 | tee $OUT/lookup_bytes_variants.txt
+true
