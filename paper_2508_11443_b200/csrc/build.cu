@@ -57,8 +57,11 @@ struct KBCfg {
 #ifndef HM_PF_DIST
 #define HM_PF_DIST 148  // k_bucket: L2 prefetch of partition p + HM_PF_DIST (0: off; 148 measured best)
 #endif
+#ifndef HM_R0_LOGA2
+#define HM_R0_LOGA2 0  // round 0: 2^0 lanes per s = 2 bucket
+#endif
 #ifndef HM_R0_LOGA
-#define HM_R0_LOGA 1  // round 0: 2^1 adjacent lanes (attempts 0, 1) per bucket
+#define HM_R0_LOGA 2  // round 0: 2^2 adjacent lanes (attempts 0..3) per s >= 3 bucket
 #endif
 #ifndef HM_RETRY_LOGA
 #define HM_RETRY_LOGA 3  // at most 2^3 lanes (attempts) per queued bucket and round
@@ -898,7 +901,7 @@ __global__ void __launch_bounds__(KBCfg<E>::T, KBCfg<E>::MINB)
   // load of the four counts) or [t*CH, t*CH + CH) otherwise
   bool huge = false, bfail = false;
   unsigned long long S_p;
-  uint32_t Lall;
+  uint32_t Lall, L3;  // listed buckets, of them with s >= 3 (at the front)
   {
     const uint32_t c0 = tid * CH, c1 = min(c0 + CH, nbp);
     const bool vec = CH == 4;  // (CTA-uniform; entries past nbp are 0)
@@ -935,6 +938,7 @@ __global__ void __launch_bounds__(KBCfg<E>::T, KBCfg<E>::MINB)
     S_p = ta >> 32;
     const uint32_t T2 = uint32_t(tb & 0x1FFFFF), T4 = uint32_t((tb >> 21) & 0x1FFFFF), T8 = uint32_t(tb >> 42);
     Lall = T2 + T4 + T8;
+    L3 = T4 + T8;
     uint32_t pos = uint32_t(a), sq = uint32_t(a >> 32);
     // list regions: [s = 5..8 | s = 3..4 | s = 2]
     uint32_t n8 = uint32_t(b >> 42), n4 = T8 + uint32_t((b >> 21) & 0x1FFFFF), n2 = T8 + T4 + uint32_t(b & 0x1FFFFF);
@@ -1063,18 +1067,28 @@ __global__ void __launch_bounds__(KBCfg<E>::T, KBCfg<E>::MINB)
         s_qn[(r + 2) % 3][0] = s_qn[(r + 2) % 3][1] = 0;
         s_chunk[(r + 2) % 3] = 0;
       }
-      uint32_t logA = 0;
-      if (r == 0) logA = (bp.flags & HM_FLAG_NO_ROUND0_ILP) ? 0u : uint32_t(HM_R0_LOGA);
-      else
+      // lanes per bucket: round 0 gives the s >= 3 buckets (the front of the
+      // list) 2^HM_R0_LOGA lanes and the s = 2 ones 2^HM_R0_LOGA2; later rounds
+      // A = lanes / list length (at most 2^HM_RETRY_LOGA)
+      uint32_t logA = 0, logA2 = 0, L1 = L;
+      if (r == 0) {
+        const bool one = bp.flags & HM_FLAG_NO_ROUND0_ILP;
+        logA = one ? 0u : uint32_t(HM_R0_LOGA);
+        logA2 = one ? 0u : uint32_t(HM_R0_LOGA2);
+        L1 = L3;
+      } else {
         while (logA < HM_RETRY_LOGA && (L << (logA + 1)) <= uint32_t(KBCfg<E>::T)) logA++;
-      const uint32_t A = 1u << logA, W = L << logA;
-      const uint32_t gmask = A == 32 ? 0xffffffffu : (((1u << A) - 1u) << (lane & ~(A - 1u)));
+      }
+      const uint32_t W1 = L1 << logA, W = W1 + ((L - L1) << logA2);
       for (;;) {
         uint32_t c = 0;
         if (lane == 0) c = atomicAdd(&s_chunk[cur], 32u);
         c = __shfl_sync(0xffffffffu, c, 0);
         if (c >= W) break;
-        const uint32_t w = c + lane, g = w >> logA, j = w & (A - 1u);
+        const uint32_t w = c + lane;
+        const uint32_t lA = w < W1 ? logA : logA2, A = 1u << lA;
+        const uint32_t g = w < W1 ? (w >> logA) : L1 + ((w - W1) >> logA2), j = w & (A - 1u);
+        const uint32_t gmask = A == 32 ? 0xffffffffu : (((1u << A) - 1u) << (lane & ~(A - 1u)));
         const bool act = w < W;
         const uint32_t lb = act ? (g < n3 ? cl[g] : cl[lcap - 1 - (g - n3)]) : 0u;
         const uint32_t s = act ? ss[lb] : 0u, tb = act ? s_t[lb] : 0u;
