@@ -487,17 +487,18 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 
 // make2 for buckets with 2 <= s <= 8, in CTA-wide rounds.
 // One attempt = derive(seed,2,b,t), the s level-2 slots hash mod s^2 and the
-// occupancy bitmap as `collision`.  Round 0 gives every
-// multi-key bucket one lane and attempt t = 0, the list ordered by size class
-// (s = 5..8 | 3..4 | 2) so that the lanes of a warp share one key-register
-// width K; warps take 32-bucket chunks from a shared counter (dynamic
-// balance).  The buckets that collide go to the next round's list (s >= 3 from
-// the front, s = 2 from the back: the order by width again), and round r >= 1
-// tries attempts tb .. tb + A - 1 of each listed bucket on A adjacent lanes
-// (A = lanes / list length, at most 2^HM_RETRY_LOGA); the lowest successful
-// lane wins — the same t as trying them one by one (R13).  Every attempt is
-// one lane's work from start to end, so the instruction count follows the
-// attempts actually made (SASS attribution in profiles/r02/).
+// occupancy bitmap as `collision`.  Every round is a list
+// of buckets with A adjacent lanes per bucket, lane j trying attempt tb + j
+// (tb: the bucket's next attempt, 0 in round 0); the lowest successful lane
+// wins — the same t as trying them one by one (R13).  Round 0 is the class-
+// ordered list (s = 5..8 | 3..4 | 2: the lanes of a warp share one
+// key-register width K) with A = 4 for s >= 3 and A = 1 for s = 2 (success
+// 3/4); the buckets that collide go to the next round's list (s >= 3 from the
+// front, s = 2 from the back: ordered by width again) with A = lanes / list
+// length (at most 2^HM_RETRY_LOGA).  Warps take 32-lane chunks from a shared
+// counter (dynamic balance); one CTA barrier per round.  Every attempt is one
+// lane's work from start to end, so the instruction count follows the attempts
+// made (SASS attribution in profiles/r02/).
 
 // Search state (shared memory).
 struct SearchCtx {
