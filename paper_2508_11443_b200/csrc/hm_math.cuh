@@ -29,7 +29,7 @@ struct Consts {  // (a1, a2, b)
 // product widened, both cross terms added into its high word) where nvcc emits
 // four; on the host the plain product.
 __host__ __device__ __forceinline__ uint64_t mul64_lo(uint64_t z, uint64_t c) {
-#if defined(__CUDA_ARCH__)
+#if defined(__CUDA_ARCH__) && !defined(HM_PLAIN_MUL)
   uint64_t r;
   asm("{ .reg .u32 wl, wh; .reg .u64 w;\n\t"
       "mul.wide.u32 w, %1, %3;\n\t"

@@ -96,12 +96,13 @@ def lib():
         L.hm_assemble_u64.argtypes = [p, p, u64, u64, u64, u32, C.POINTER(_Opts), p, C.POINTER(p)]
         L.hm_build_u64_dist.argtypes = [p, p, u64, C.POINTER(_Opts), p, p, C.POINTER(p)]
         L.hm_lookup_u64_dist.argtypes = [p, p, u64, p, p, p, p]
-        L.hm_dist_bucket_range.argtypes = [u64, i32, i32, C.POINTER(u64), C.POINTER(u64)]
-        L.hm_dist_bucket_range.restype = C.c_int
-        L.hm_dist_decide.argtypes = [u64, u32, u64, i32, C.POINTER(u32)]
-        L.hm_dist_decide.restype = C.c_int
-        L.hm_dist_slot_base.argtypes = [p, i32, i32]
-        L.hm_dist_slot_base.restype = u64
+        if hasattr(L, "hm_dist_decide"):  # (absent only from older debug builds, HM_LIB_PATH)
+            L.hm_dist_bucket_range.argtypes = [u64, i32, i32, C.POINTER(u64), C.POINTER(u64)]
+            L.hm_dist_bucket_range.restype = C.c_int
+            L.hm_dist_decide.argtypes = [u64, u32, u64, i32, C.POINTER(u32)]
+            L.hm_dist_decide.restype = C.c_int
+            L.hm_dist_slot_base.argtypes = [p, i32, i32]
+            L.hm_dist_slot_base.restype = u64
         for f in ("hm_assemble_u64", "hm_build_u64_dist", "hm_lookup_u64_dist", "hm_build_u64", "hm_build_bytes", "hm_lookup_u64", "hm_lookup_bytes", "hm_info", "hm_export",
                   "hm_route_u64", "hm_build_u64_shard", "hm_shard_set_base", "hm_route_queries_u64",
                   "hm_unroute_u64"):

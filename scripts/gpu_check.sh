@@ -10,7 +10,7 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 
 timeout 600 python bench.py > $OUT/bench.json 2> $OUT/bench.err
 timeout 600 python bench.py --impl reference > $OUT/bench_ref.json 2> $OUT/bench_ref.err
 if [ -n "$NCU" ]; then
-timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file $OUT/launches.csv python bench.py --steps 2 --warmup 1 > $OUT/bench_ncu.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file $OUT/launches.csv python bench.py --steps 2 --warmup 1 --no-configs --no-e2e --no-cpu-baseline > $OUT/bench_ncu.log 2>&1
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"k_lookup_u64|k_bucket|k_split" -c 7 -o $OUT/full python scripts/prof_once.py 26 > $OUT/ncu_full.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_lookup_bytes|k_bucket|k_split|k_fingerprint" -c 8 -o $OUT/full_bytes python scripts/prof_once.py 24 bytes > $OUT/ncu_full_bytes.log 2>&1
 fi
