@@ -42,10 +42,10 @@ constexpr int kAThreads = 512;
 #define HM_KB_MINB (1024 / HM_KB_THREADS)  // CTAs per SM the registers must allow
 #endif
 #ifndef HM_KB_THREADS_BYTES
-#define HM_KB_THREADS_BYTES 256  // byte keys: 32-byte records, BP = 2^10, 3 CTAs per SM
+#define HM_KB_THREADS_BYTES 512  // byte keys: only the fingerprints in shared memory, BP = 2^11, 2 CTAs per SM
 #endif
 #ifndef HM_KB_MINB_BYTES
-#define HM_KB_MINB_BYTES 3
+#define HM_KB_MINB_BYTES 2
 #endif
 // k_bucket geometry per record type: threads per CTA, warps, CTAs per SM
 template <class E>
@@ -53,6 +53,31 @@ struct KBCfg {
   static constexpr int T = sizeof(E) == 16 ? HM_KB_THREADS : HM_KB_THREADS_BYTES;
   static constexpr int W = T / 32;
   static constexpr int MINB = sizeof(E) == 16 ? HM_KB_MINB : HM_KB_MINB_BYTES;
+  // bytes per item k_bucket keeps in shared memory: the whole 16-byte record
+  // (key, value); for 32-byte byte-key records only the fingerprint (the out
+  // phase gathers the records from the partition buffer, L2-resident by then)
+  static constexpr int SMEM_ITEM = sizeof(E) == 16 ? 16 : 8;
+};
+
+// The partition's items as k_bucket sees them: keys in shared memory (inside
+// the 16-byte records, or a plain fingerprint array), records from shared
+// memory (16-byte) or from the partition buffer in global memory (32-byte).
+template <class E>
+struct Items {
+  const uint64_t* keys;
+  const E* recs;
+  static constexpr int kStride = sizeof(E) == 16 ? 2 : 1;
+  __device__ __forceinline__ uint64_t key(uint32_t i) const { return keys[size_t(i) * kStride]; }
+  __device__ __forceinline__ E rec(uint32_t i) const {
+    if (sizeof(E) == 16) return recs[i];
+    E e;
+    const uint4* p = reinterpret_cast<const uint4*>(recs + i);
+    const uint4 a = __ldg(p), b = __ldg(p + 1);
+    static_assert(sizeof(E) == 16 || sizeof(E) == 32, "record size");
+    memcpy(&e, &a, 16);
+    memcpy(reinterpret_cast<char*>(&e) + 16, &b, 16);
+    return e;
+  }
 };
 #ifndef HM_PF_DIST
 #define HM_PF_DIST 148  // k_bucket: L2 prefetch of partition p + HM_PF_DIST (0: off; 148 measured best)
@@ -572,7 +597,7 @@ __device__ __forceinline__ void bucket_done(const SearchCtx& X, uint32_t lb, uin
 // Equal keys in a bucket (a duplicate, or equal fingerprints with different
 // bytes) never separate: record which, once, and retire the bucket.
 template <class E, class Same>
-__device__ __noinline__ bool bucket_equal_keys_(const E* skv, const uint16_t* sstart, const uint8_t* ss,
+__device__ __noinline__ bool bucket_equal_keys_(Items<E> skv, const uint16_t* sstart, const uint8_t* ss,
                                                 const uint16_t* sidx, uint8_t* s_t, uint32_t lb, DevStatus* stt,
                                                 Same same) {
   const uint32_t st0 = sstart[lb], s = ss[lb];
@@ -580,8 +605,8 @@ __device__ __noinline__ bool bucket_equal_keys_(const E* skv, const uint16_t* ss
     const uint32_t ii = sidx[st0 + i];
     for (uint32_t j = i + 1; j < s; j++) {
       const uint32_t jj = sidx[st0 + j];
-      if (skv[jj].key == skv[ii].key) {
-        atomicOr(same.same(skv[ii], skv[jj]) ? &stt->dup : &stt->fpcoll, 1u);
+      if (skv.key(jj) == skv.key(ii)) {
+        atomicOr(same.same(skv.rec(ii), skv.rec(jj)) ? &stt->dup : &stt->fpcoll, 1u);
         s_t[lb] = 0;
         return true;
       }
@@ -590,7 +615,7 @@ __device__ __noinline__ bool bucket_equal_keys_(const E* skv, const uint16_t* ss
   return false;
 }
 template <class E, class Same>
-__device__ __forceinline__ bool bucket_equal_keys(const E* skv, const SearchCtx& X, uint32_t lb, DevStatus* stt,
+__device__ __forceinline__ bool bucket_equal_keys(const Items<E>& skv, const SearchCtx& X, uint32_t lb, DevStatus* stt,
                                                   const Same& same) {
   return bucket_equal_keys_(skv, X.sstart, X.ss, X.sidx, X.s_t, lb, stt, same);
 }
@@ -598,14 +623,14 @@ __device__ __forceinline__ bool bucket_equal_keys(const E* skv, const SearchCtx&
 // Attempt t of bucket lb (s keys, K-wide registers) on this lane.  Returns
 // the occupancy bitmap (0: collision, or no bucket on this lane).
 template <int K, class E>
-__device__ __forceinline__ uint64_t lane_attempt(const BuildParams& bp, const E* skv, const SearchCtx& X, bool act,
+__device__ __forceinline__ uint64_t lane_attempt(const BuildParams& bp, const Items<E>& skv, const SearchCtx& X, bool act,
                                                  uint32_t lb, uint32_t s, uint32_t t, const uint64_t* s_m2,
                                                  uint64_t bbase, uint32_t* h) {
   if (!act || t >= kT2Cap) return 0;
   const uint32_t st0 = X.sstart[lb];
   uint64_t k[K];
 #pragma unroll
-  for (int j = 0; j < K; j++) k[j] = uint32_t(j) < s ? skv[X.sidx[st0 + j]].key : 0ull;
+  for (int j = 0; j < K; j++) k[j] = uint32_t(j) < s ? skv.key(X.sidx[st0 + j]) : 0ull;
   FastMod fm{uint64_t(s) * s, 0};
   if (K > 2) fm.m = s_m2[s];
   return slots_of<K>(derive(bp.smix, 2, bbase + lb, t), k, s, fm, h);
@@ -613,7 +638,7 @@ __device__ __forceinline__ uint64_t lane_attempt(const BuildParams& bp, const E*
 
 // The key-register width follows the largest bucket among the warp's lanes.
 template <class E>
-__device__ __forceinline__ uint64_t lane_attempt_k(const BuildParams& bp, const E* skv, const SearchCtx& X, bool act,
+__device__ __forceinline__ uint64_t lane_attempt_k(const BuildParams& bp, const Items<E>& skv, const SearchCtx& X, bool act,
                                                    uint32_t lb, uint32_t s, uint32_t t, const uint64_t* s_m2,
                                                    uint64_t bbase, uint32_t* h) {
   const uint32_t smax = __reduce_max_sync(0xffffffffu, act ? s : 0u);
@@ -653,7 +678,7 @@ __device__ __forceinline__ void list_append(bool want, uint32_t lb, uint32_t s, 
 // __match_any_sync on the level-2 slots as the injectivity test; then the
 // bucket's s^2 slots are mapped as in bucket_done (bitsw: a per-warp bitmap).
 template <class E, class Same>
-__device__ __forceinline__ void search_warp(const BuildParams& bp, const E* skv, const SearchCtx& X,
+__device__ __forceinline__ void search_warp(const BuildParams& bp, const Items<E>& skv, const SearchCtx& X,
                                             const uint16_t* list, uint32_t L, const uint64_t* s_m2, uint64_t bbase,
                                             DevStatus* stt, const Same& same, uint32_t* bitsw) {
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -661,13 +686,13 @@ __device__ __forceinline__ void search_warp(const BuildParams& bp, const E* skv,
     const uint32_t lb = list[idx], st0 = X.sstart[lb], s = X.ss[lb];
     const bool mine = lane < s;
     const uint32_t item = mine ? X.sidx[st0 + lane] : 0u;
-    const uint64_t key = mine ? skv[item].key : 0ull;
+    const uint64_t key = mine ? skv.key(item) : 0ull;
     const uint32_t valid = __ballot_sync(0xffffffffu, mine);
     const uint32_t dm = __match_any_sync(0xffffffffu, key) & valid & ~(1u << lane);
     uint32_t t = 0;
     if (__any_sync(0xffffffffu, mine && dm != 0)) {
       if (mine && dm != 0) {
-        const bool d = same.same(skv[item], skv[X.sidx[st0 + __ffs(dm) - 1]]);
+        const bool d = same.same(skv.rec(item), skv.rec(X.sidx[st0 + __ffs(dm) - 1]));
         atomicOr(d ? &stt->dup : &stt->fpcoll, 1u);
       }
     } else {
@@ -716,7 +741,7 @@ __host__ __device__ __forceinline__ BucketSmem bucket_smem_layout(uint32_t cap, 
   L.cls_off[1] = L.cls_off[0];
   L.cls_off[2] = L.cls_off[1] + cap / 2 + 1;  // s = 9..32: cap/9
   L.cls_off[3] = L.cls_off[2] + cap / 9 + 1;
-  L.skv = 0;                                               // E[cap]: the partition's elements
+  L.skv = 0;                                               // [cap] items: 16-B records or 8-B fingerprints
   L.lbk = L.skv + al16(size_t(cap) * esz);                 // u16[cap]: local bucket of item i
   L.rk = L.lbk + al16(size_t(cap) * 2);                    // u16[cap]: rank of item i in its bucket
   L.sidx = L.rk + al16(size_t(cap) * 2);                   // u16[cap]: grouped position -> item
@@ -795,7 +820,7 @@ __global__ void __launch_bounds__(KBCfg<E>::T, KBCfg<E>::MINB)
   const uint32_t BP = 1u << bp.log2_bp;
   const uint32_t CH = (BP + KBCfg<E>::T - 1) / KBCfg<E>::T;  // buckets per thread in the scans
   const BucketSmem& SL = bp.sl;
-  E* skv = reinterpret_cast<E*>(smem + SL.skv);
+  uint64_t* skey = reinterpret_cast<uint64_t*>(smem + SL.skv);  // (16-byte records, or fingerprints)
   uint16_t* lbk = reinterpret_cast<uint16_t*>(smem + SL.lbk);
   uint16_t* rk = reinterpret_cast<uint16_t*>(smem + SL.rk);
   uint16_t* sidx = reinterpret_cast<uint16_t*>(smem + SL.sidx);
@@ -844,18 +869,20 @@ __global__ void __launch_bounds__(KBCfg<E>::T, KBCfg<E>::MINB)
     if (ql) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(plb + size_t(q) * cap), "r"(ql) : "memory");
   }
 #endif
+  const E* prec = pbuf + size_t(p) * cap;  // (the partition's records in global memory)
   if (tid == 0) {
-    const uint32_t bytes = cnt * uint32_t(sizeof(E));
+    const uint32_t bytes = KBCfg<E>::SMEM_ITEM == int(sizeof(E)) ? cnt * uint32_t(sizeof(E)) : 0u;
     const uint32_t lbytes = ((cnt + 7) & ~7u) * 2;  // (16-byte multiple; cap is a multiple of 32)
-    if (bytes) {
+    if (cnt) {
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&s_bar)),
                    "r"(bytes + lbytes)
                    : "memory");
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-              smem_u32(skv)),
-          "l"(pbuf + size_t(p) * cap), "r"(bytes), "r"(smem_u32(&s_bar))
-          : "memory");
+      if (bytes)
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_u32(skey)),
+            "l"(prec), "r"(bytes), "r"(smem_u32(&s_bar))
+            : "memory");
       asm volatile(
           "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
               smem_u32(lbk)),
@@ -884,6 +911,7 @@ __global__ void __launch_bounds__(KBCfg<E>::T, KBCfg<E>::MINB)
   // k_partition hashed it already); the rank among the items of its bucket
   // comes from the shared-memory counter
   for (uint32_t i = tid; i < cnt; i += KBCfg<E>::T) {
+    if (KBCfg<E>::SMEM_ITEM != int(sizeof(E))) skey[i] = __ldg(reinterpret_cast<const unsigned long long*>(prec + i));
     const uint32_t code = lbk[i];
     uint32_t lb = code & 0xFFFu;
     if (lb >= nbp) {  // cannot happen for a well-routed partition; never index out of range
@@ -1013,6 +1041,7 @@ __global__ void __launch_bounds__(KBCfg<E>::T, KBCfg<E>::MINB)
   // (PAPER.md:286-292); every finished bucket maps its slots to their source
   // items (bucket_done)
   SearchCtx X{sstart, ss, sidx, soff, sA, s_t, staged ? src : nullptr};
+  const Items<E> skv{skey, KBCfg<E>::SMEM_ITEM == int(sizeof(E)) ? reinterpret_cast<const E*>(skey) : prec};
   // look-back: exclusive prefix of S over the partitions before p (warp 0,
   // lane i inspects partition qb - i: the closest inclusive prefix plus the
   // aggregates in front of it give the base)
@@ -1137,7 +1166,7 @@ __global__ void __launch_bounds__(KBCfg<E>::T, KBCfg<E>::MINB)
         const uint32_t x = x0 + j * KBCfg<E>::T + tid;
         if (x < Sp) {
           const uint32_t v = src[x], it = v & 0x7FFFu;
-          e[j] = skv[it < cnt ? it : 0u];  // (an unmapped slot only in a pass that is redone)
+          e[j] = skv.rec(it < cnt ? it : 0u);  // (an unmapped slot only in a pass that is redone)
           if (v & 0x8000u) e[j].value = 0;
         }
       }
@@ -1156,7 +1185,7 @@ __global__ void __launch_bounds__(KBCfg<E>::T, KBCfg<E>::MINB)
       E* out = slots + base + soff[lb];
       const uint32_t st0 = sstart[lb];
       if (s == 1) {
-        out[0] = skv[sidx[st0]];
+        out[0] = skv.rec(sidx[st0]);
         continue;
       }
       const uint32_t s2 = s * s;
@@ -1168,12 +1197,12 @@ __global__ void __launch_bounds__(KBCfg<E>::T, KBCfg<E>::MINB)
           fill = sidx[st0 + j];
         }
       }
-      E f = skv[fill];
+      E f = skv.rec(fill);
       f.value = 0;
       for (uint32_t x = 0; x < s2; x++) out[x] = f;
       for (uint32_t j = 0; j < s; j++) {
         const uint32_t h = sA[st0 + j];
-        if (h < s2) out[h] = skv[sidx[st0 + j]];
+        if (h < s2) out[h] = skv.rec(sidx[st0 + j]);
       }
     }
   }
@@ -1469,7 +1498,7 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
   }
   const uint32_t knob_flags = log2_req >> 16;
   log2_req &= 0xFFFFu;
-  const Plan pl = make_plan(n_in, nb, log2_req, uint32_t(sizeof(E)), size_t(smem_sm) / KBCfg<E>::MINB - 1024 - static_smem_B,
+  const Plan pl = make_plan(n_in, nb, log2_req, uint32_t(KBCfg<E>::SMEM_ITEM), size_t(smem_sm) / KBCfg<E>::MINB - 1024 - static_smem_B,
                             size_t(smem_optin) - static_smem_B);
   if (pl.smemB + static_smem_B > size_t(smem_optin)) {
     set_error("build plan does not fit in shared memory");
@@ -1563,7 +1592,7 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
   bp.np = pl.np;
   bp.cap = pl.cap;
   bp.flags = knob_flags;
-  bp.sl = bucket_smem_layout(pl.cap, 1u << pl.log2_bp, uint32_t(sizeof(E)));
+  bp.sl = bucket_smem_layout(pl.cap, 1u << pl.log2_bp, uint32_t(KBCfg<E>::SMEM_ITEM));
   for (int i = 0; i < 33; i++) bp.m2[i] = i ? ~0ull / (uint64_t(i) * i) : 0ull;
 
   DevStatus hs{};
