@@ -341,6 +341,8 @@ hm_status hm_build_u64(const uint64_t* keys, const uint64_t* vals, uint64_t n, c
   return HM_OK;
 }
 
+static hm_status copy_streams(cudaStream_t* up, cudaStream_t* down);
+
 hm_status hm_build_bytes(const uint8_t* bytes, const uint64_t* offsets, const uint64_t* vals, uint64_t n,
                          const hm_opts* opts, void* stream, hm_map** out) {
   g_last_error.clear();
@@ -396,11 +398,58 @@ hm_status hm_build_bytes(const uint8_t* bytes, const uint64_t* offsets, const ui
     HM_CUDA_TRY(cudaMemcpyAsync(&on, po + m, 8, cudaMemcpyDeviceToHost, st));
     HM_CUDA_TRY(cudaStreamSynchronize(st));
   }
+  // The map's copy of the key context is allocated now and copied
+  // on a library stream while the build kernels run (the copy engine is idle
+  // during the build), joined before the map is returned.
+  const uint64_t ctx_bytes = on - o0;
+  const size_t ctx_alloc = std::max<uint64_t>(ctx_bytes + 16, 16);
+  uint8_t* ctxc = nullptr;
+  {
+    void* c = nullptr;
+    if (tl_user_alloc.alloc) {
+      c = tl_user_alloc.alloc(ctx_alloc, stream, tl_user_alloc.ctx);
+      if (!c) {
+        set_error("the user allocator (hm_opts.alloc) returned NULL for the context copy");
+        return HM_ERR_OOM;
+      }
+    } else {
+      const cudaError_t e = cudaMallocAsync(&c, ctx_alloc, st);
+      if (e != cudaSuccess) return cuda_fail(e, "context copy");
+    }
+    ctxc = reinterpret_cast<uint8_t*>(c);
+  }
+  auto free_ctx = [&]() {
+    if (tl_user_alloc.free) tl_user_alloc.free(ctxc, ctx_alloc, stream, tl_user_alloc.ctx);
+    else cudaFreeAsync(ctxc, st);
+  };
+  cudaEvent_t ev_in = nullptr, ev_copied = nullptr;
+  {
+    cudaStream_t cs, unused;
+    hm_status s2 = copy_streams(&cs, &unused);
+    cudaError_t e = s2 == HM_OK ? cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming) : cudaErrorUnknown;
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_copied, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventRecord(ev_in, st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ev_in, 0);
+    if (e == cudaSuccess && ctx_bytes) e = cudaMemcpyAsync(ctxc, db + o0, ctx_bytes, cudaMemcpyDeviceToDevice, cs);
+    if (e == cudaSuccess) e = cudaEventRecord(ev_copied, cs);
+    if (e != cudaSuccess) {
+      if (ev_in) cudaEventDestroy(ev_in);
+      if (ev_copied) cudaEventDestroy(ev_copied);
+      free_ctx();
+      return cuda_fail(e, "context copy");
+    }
+  }
   BuildOut bo;
   uint32_t t0 = 0;
   uint64_t r = 0;
   s = build_bytes_core(db, doff, dv, n, seed, opts ? (opts->log2_bp | (opts->flags << 16)) : 0, st, &bo, &t0, &r);
-  if (s != HM_OK) return s;
+  cudaStreamWaitEvent(st, ev_copied, 0);  // (the copy has read db before its staging is freed)
+  cudaEventDestroy(ev_in);
+  cudaEventDestroy(ev_copied);
+  if (s != HM_OK) {
+    free_ctx();
+    return s;
+  }
   hm_map* m = new_map();
   m->key_kind = 1;
   m->n_global = n;
@@ -417,33 +466,10 @@ hm_status hm_build_bytes(const uint8_t* bytes, const uint64_t* offsets, const ui
   m->slots = bo.slots;
   for (int a = 0; a < 3; a++) m->abytes[a] = bo.bytes[a];
   adopt_hooks(m);
-  m->ctx_bytes = on - o0;
-  void* c = nullptr;
-  cudaError_t e = cudaSuccess;
-  if (tl_user_alloc.alloc) {
-    m->ctx_alloc = std::max<uint64_t>(m->ctx_bytes + 16, 16);
-    c = tl_user_alloc.alloc(m->ctx_alloc, stream, tl_user_alloc.ctx);
-    if (!c) {
-      hm_free(m);
-      set_error("the user allocator (hm_opts.alloc) returned NULL for the context copy");
-      return HM_ERR_OOM;
-    }
-  } else {
-    e = cudaMallocAsync(&c, std::max<uint64_t>(m->ctx_bytes + 16, 16), st);
-  }
-  if (e != cudaSuccess) {
-    hm_free(m);
-    return cuda_fail(e, "context copy");
-  }
-  m->ctx = reinterpret_cast<uint8_t*>(c);
-  if (m->ctx_bytes) {
-    e = cudaMemcpyAsync(m->ctx, db + o0, m->ctx_bytes, cudaMemcpyDeviceToDevice, st);
-    if (e != cudaSuccess) {
-      hm_free(m);
-      return cuda_fail(e, "context copy");
-    }
-  }
-  e = cudaStreamSynchronize(st);
+  m->ctx_bytes = ctx_bytes;
+  if (tl_user_alloc.alloc) m->ctx_alloc = ctx_alloc;
+  m->ctx = ctxc;
+  const cudaError_t e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) {
     hm_free(m);
     return cuda_fail(e, "build_bytes");
