@@ -406,13 +406,14 @@ def run_ours(args):
     torch.cuda.synchronize()
 
     s_over_n = 2.0  # replaced by the table's actual S / n after the first step
+    dist_flags = hm.FLAG_FUSED_EXCHANGE if args.fused_exchange else 0
 
     def step(ev_b=None):
         nonlocal s_over_n
         if world == 1:
             m = hm.HashMap.build_u64(keys, vals, seed=0)
         else:
-            m = hm.build_u64_dist(keys, vals, comm, seed=0)
+            m = hm.build_u64_dist(keys, vals, comm, seed=0, flags=dist_flags)
         s_over_n = m.info().S / n
         if ev_b is not None:
             ev_b.record()
@@ -553,7 +554,8 @@ def run_ours(args):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
         "data": "synthetic: seeded splitmix64 key stream (workloads/gen.py, generated on device)",
-        "config": config_dict(world),
+        "config": dict(config_dict(world), **({"exchange": "fused route + NVLink window stores"}
+                                              if args.fused_exchange and world > 1 else {})),
         "build_mkeys_s": round(n * world / (build_ms / 1e3) / 1e6, 2),
         "lookup_mq_s": round(n * world / (look_ms / 1e3) / 1e6, 2),
         "build_ms": round(build_ms, 4), "lookup_ms": round(look_ms, 4),
@@ -581,6 +583,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-configs", action="store_true", help="skip the C1/C3/C5 measurements after the timed region")
+    ap.add_argument("--fused-exchange", action="store_true",
+                    help="N > 1: route straight into the owners' NCCL windows (HM_FLAG_FUSED_EXCHANGE, NEXT-2)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -110,6 +110,13 @@ typedef struct {
  * table is identical (R13); only the construction route and its speed
  * differ.  log2_bp is ignored. */
 #define HM_FLAG_ROUNDS 16u
+/* hm_build_u64_dist only: the route kernel stores
+ * every (key, value) straight into its owner's receive window over NVLink (a
+ * symmetric window: ncclMemAlloc + ncclCommWindowRegister, peer pointers from
+ * NCCL 2.28's device API) instead of the grouped ncclSend/ncclRecv all-to-all
+ * after it; the shards are the same.  Needs every rank in one NVLink domain
+ * (a single node).  Other calls: HM_ERR_INVALID_ARG. */
+#define HM_FLAG_FUSED_EXCHANGE 32u
 
 /* Table header, 56 bytes, little-endian (DESIGN.md §4 "Table layout"). */
 typedef struct {

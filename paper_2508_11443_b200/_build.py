@@ -9,7 +9,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libhm.so")
 SOURCES = ["capi.cu", "build.cu", "lookup.cu", "dedup.cu", "rounds.cu", "assemble.cu", "dist.cu"]
-HEADERS = ["hm_internal.cuh", "hm_math.cuh"]
+HEADERS = ["hm_internal.cuh", "hm_math.cuh", "route.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 def _nccl_dir() -> str:
     """The pip NCCL torch loads (same libnccl.so.2 in the process), else the system one."""

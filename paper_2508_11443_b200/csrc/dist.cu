@@ -10,12 +10,14 @@
 // torch's (ProcessGroupNCCL._comm_ptr()): the library links the same
 // libnccl.so.2.
 #include <nccl.h>
+#include <nccl_device.h>  // (NCCL 2.28 device API: window peer pointers)
 
 #include <algorithm>
 #include <string>
 #include <vector>
 
 #include "hm_internal.cuh"
+#include "route.cuh"
 
 namespace hm {
 namespace {
@@ -82,6 +84,103 @@ hm_status all_to_all_v(const void* send, const std::vector<uint64_t>& sc, void* 
   return HM_OK;
 }
 
+// ------------------------------------------- fused route + exchange (NEXT-2)
+// With HM_FLAG_FUSED_EXCHANGE the route kernel stores every (key, value)
+// straight into its owner's receive window (registered with
+// ncclCommWindowRegister, NCCL_WIN_COLL_SYMMETRIC, and mapped over NVLink:
+// ncclGetPeerPointer), at the position the count matrix gives this rank in
+// the owner's buffer — the transfer overlaps the scatter tile by tile instead
+// of following it as an all-to-all.
+struct OutWindow {
+  ncclWindow_t win;
+  size_t vals_off;  // byte offset of the values in every rank's window
+  __device__ __forceinline__ uint64_t* keys(uint32_t d) const {
+    return static_cast<uint64_t*>(ncclGetPeerPointer(win, 0, int(d)));
+  }
+  __device__ __forceinline__ uint64_t* vals(uint32_t d) const {
+    return static_cast<uint64_t*>(ncclGetPeerPointer(win, vals_off, int(d)));
+  }
+};
+__global__ void __launch_bounds__(kRThreads) k_route_scatter_win(const uint64_t* __restrict__ keys,
+                                                                 const uint64_t* __restrict__ vals, uint64_t n,
+                                                                 L1Params l1, int world,
+                                                                 unsigned long long* __restrict__ cursors,
+                                                                 OutWindow out) {
+  route_scatter(keys, vals, n, l1, world, cursors, out, nullptr);
+  __threadfence_system();  // (the peer stores are visible once the exchange's barrier completes)
+}
+
+// The receive window of one build: keys [0, cap) then values [cap, 2 cap), cap
+// the largest count any rank receives (the same size on every rank: a
+// symmetric window).  Registration is collective; so is release().
+struct RecvWindow {
+  void* buf = nullptr;
+  ncclWindow_t win = nullptr;
+  ncclComm_t comm = nullptr;
+  uint64_t cap = 0;
+  hm_status open(ncclComm_t c, uint64_t cap_elems) {
+    comm = c;
+    cap = std::max<uint64_t>(cap_elems, 1);
+    const size_t bytes = (2 * cap * 8 + 4095) & ~size_t(4095);
+    HM_NCCL_TRY(ncclMemAlloc(&buf, bytes));
+    HM_NCCL_TRY(ncclCommWindowRegister(comm, buf, bytes, &win, NCCL_WIN_COLL_SYMMETRIC));
+    return HM_OK;
+  }
+  hm_status release() {
+    if (win) HM_NCCL_TRY(ncclCommWindowDeregister(comm, win));
+    if (buf) HM_NCCL_TRY(ncclMemFree(buf));
+    win = nullptr;
+    buf = nullptr;
+    return HM_OK;
+  }
+};
+
+// Route this rank's pairs into the owners' windows: counts, their all-gather
+// (the G x G matrix C[q][r]), the window, the fused scatter, one barrier.
+// On return rk/rv point into this rank's window (nrecv pairs).
+hm_status fused_exchange(const uint64_t* keys, const uint64_t* vals, uint64_t n_local, const L1Params& l1, int world,
+                         int rank, ncclComm_t comm, cudaStream_t st, uint64_t* d_small, RecvWindow* w,
+                         const uint64_t** rk, const uint64_t** rv, uint64_t* nrecv) {
+  uint64_t* d_c = nullptr;  // [world] own counts, then [world][world] all of them, then [world] cursors
+  const cudaError_t ea = cudaMallocAsync(reinterpret_cast<void**>(&d_c), (size_t(world) * world + 2 * world) * 8, st);
+  if (ea != cudaSuccess) return cuda_fail(ea, "fused exchange");
+  uint64_t* d_all = d_c + world;
+  unsigned long long* d_cur = reinterpret_cast<unsigned long long*>(d_all + size_t(world) * world);
+  hm_status s = route_count_launch(keys, n_local, l1, world, d_c, st);
+  if (s != HM_OK) return s;
+  HM_NCCL_TRY(ncclAllGather(d_c, d_all, world, ncclUint64, comm, st));
+  std::vector<uint64_t> C(size_t(world) * world);
+  HM_CUDA_TRY(cudaMemcpyAsync(C.data(), d_all, C.size() * 8, cudaMemcpyDeviceToHost, st));
+  HM_CUDA_TRY(cudaStreamSynchronize(st));
+  uint64_t cap = 0, mine = 0;
+  std::vector<uint64_t> off(world, 0);  // where this rank's run starts in every owner's buffer
+  for (int r = 0; r < world; r++) {
+    uint64_t tot = 0;
+    for (int q = 0; q < world; q++) {
+      if (q == rank) off[r] = tot;
+      tot += C[size_t(q) * world + r];
+    }
+    cap = std::max(cap, tot);
+    if (r == rank) mine = tot;
+  }
+  if ((s = w->open(comm, cap)) != HM_OK) return s;
+  HM_CUDA_TRY(cudaMemcpyAsync(d_cur, off.data(), size_t(world) * 8, cudaMemcpyHostToDevice, st));
+  if (n_local) {
+    LaunchScope ls_("k_route_scatter_win", st);
+    const unsigned gs =
+        unsigned(std::max<uint64_t>(1, std::min<uint64_t>((n_local + kRTile - 1) / kRTile, uint64_t(num_sms()) * 2)));
+    k_route_scatter_win<<<gs, kRThreads, 0, st>>>(keys, vals, n_local, l1, world, d_cur, OutWindow{w->win, w->cap * 8});
+  }
+  HM_CUDA_TRY(cudaGetLastError());
+  // every rank's stores have landed once every rank's scatter is done
+  HM_NCCL_TRY(ncclAllReduce(d_small + 3, d_small + 3, 1, ncclUint64, ncclSum, comm, st));
+  cudaFreeAsync(d_c, st);
+  *rk = static_cast<const uint64_t*>(w->buf);
+  *rv = static_cast<const uint64_t*>(w->buf) + w->cap;
+  *nrecv = mine;
+  return HM_OK;
+}
+
 }  // namespace
 }  // namespace hm
 
@@ -117,23 +216,46 @@ hm_status hm_build_u64_dist(const uint64_t* keys, const uint64_t* vals, uint64_t
   uint64_t lo = 0, hi = 0;
   if ((s = hm_dist_bucket_range(n, world, rank, &lo, &hi)) != HM_OK) return s;
   const uint64_t seed = opts ? opts->seed : 0;
-  if ((s = db.get(&sk, n_local)) != HM_OK || (s = db.get(&sv, n_local)) != HM_OK) return s;
+  const bool fused = opts && (opts->flags & HM_FLAG_FUSED_EXCHANGE);
+  hm_opts shard_opts{};
+  if (opts) {
+    shard_opts = *opts;
+    shard_opts.flags &= ~uint32_t(HM_FLAG_FUSED_EXCHANGE);
+  }
+  if (!fused && ((s = db.get(&sk, n_local)) != HM_OK || (s = db.get(&sv, n_local)) != HM_OK)) return s;
   hm_map* m = nullptr;
   uint64_t S_local = 0;
+  HM_CUDA_TRY(cudaMemsetAsync(d_small + 3, 0, 8, st));
   for (uint32_t t1 = 0;;) {
-    // (2) route, exchange counts and pairs
-    if ((s = hm_route_u64(keys, vals, n_local, n, seed, t1, world, sk, sv, d_sc, stream)) != HM_OK) return s;
-    std::vector<uint64_t> sc, rc;
-    if ((s = exchange_counts(d_sc, d_rc, sc, rc, world, comm, st)) != HM_OK) return s;
-    uint64_t nrecv = 0;
-    for (uint64_t x : rc) nrecv += x;
+    // (2) route, exchange counts and pairs (fused: straight into the owners' windows)
     DevBufs rb{st, {}};
-    uint64_t *rk, *rv;
-    if ((s = rb.get(&rk, nrecv)) != HM_OK || (s = rb.get(&rv, nrecv)) != HM_OK) return s;
-    if ((s = all_to_all_v(sk, sc, rk, rc, 8, world, comm, st)) != HM_OK) return s;
-    if ((s = all_to_all_v(sv, sc, rv, rc, 8, world, comm, st)) != HM_OK) return s;
+    RecvWindow w;
+    const uint64_t *rk = nullptr, *rv = nullptr;
+    uint64_t nrecv = 0;
+    if (fused) {
+      const L1Params l1 = make_l1(seed_mix(seed), t1, n);
+      if ((s = fused_exchange(keys, vals, n_local, l1, world, rank, comm, st, d_small, &w, &rk, &rv, &nrecv)) !=
+          HM_OK)
+        return s;
+    } else {
+      if ((s = hm_route_u64(keys, vals, n_local, n, seed, t1, world, sk, sv, d_sc, stream)) != HM_OK) return s;
+      std::vector<uint64_t> sc, rc;
+      if ((s = exchange_counts(d_sc, d_rc, sc, rc, world, comm, st)) != HM_OK) return s;
+      for (uint64_t x : rc) nrecv += x;
+      uint64_t *bk, *bv;
+      if ((s = rb.get(&bk, nrecv)) != HM_OK || (s = rb.get(&bv, nrecv)) != HM_OK) return s;
+      if ((s = all_to_all_v(sk, sc, bk, rc, 8, world, comm, st)) != HM_OK) return s;
+      if ((s = all_to_all_v(sv, sc, bv, rc, 8, world, comm, st)) != HM_OK) return s;
+      rk = bk;
+      rv = bv;
+    }
     // (3) the shard, then the global bound and the status, agreed by all ranks
-    const hm_status bs = hm_build_u64_shard(rk, rv, nrecv, n, lo, hi, t1, opts, stream, &m, &S_local);
+    const hm_status bs = hm_build_u64_shard(rk, rv, nrecv, n, lo, hi, t1, opts ? &shard_opts : nullptr, stream, &m,
+                                            &S_local);
+    if (fused) {  // (the shard copied what it needs; collective on every rank)
+      HM_CUDA_TRY(cudaStreamSynchronize(st));
+      if ((s = w.release()) != HM_OK) return s;
+    }
     const std::string local_err = bs != HM_OK ? hm_last_error() : std::string();
     uint64_t red[2] = {bs == HM_OK ? S_local : 0, uint64_t(bs)};
     HM_CUDA_TRY(cudaMemcpyAsync(d_small, red, 16, cudaMemcpyHostToDevice, st));

@@ -185,6 +185,8 @@ hm_status lookup_u64_launch(const hm_map* m, const uint64_t* q, uint64_t nq, uin
                             uint8_t* out_found, cudaStream_t st);
 hm_status lookup_bytes_launch(const hm_map* m, const uint8_t* qb, const uint64_t* qo, uint64_t nq,
                               uint64_t* out_vals, uint8_t* out_found, cudaStream_t st);
+hm_status route_count_launch(const uint64_t* keys, uint64_t n, const L1Params& l1, int world, uint64_t* counts,
+                             cudaStream_t st);
 hm_status route_u64_launch(const uint64_t* keys, const uint64_t* vals, uint64_t n, const L1Params& l1,
                            int world, uint64_t* sk, uint64_t* sv, uint64_t* counts, cudaStream_t st);
 hm_status route_queries_launch(const L1Params& l1, const uint64_t* q, uint64_t nq, int world, uint64_t* sq,

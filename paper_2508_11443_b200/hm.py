@@ -172,6 +172,7 @@ FLAG_DIRECT_SLOTS = 2  # HM_FLAG_DIRECT_SLOTS (testing knob)
 FLAG_NO_ROUND0_ILP = 4  # HM_FLAG_NO_ROUND0_ILP (testing knob)
 FLAG_FROM_ARRAY = 8  # HM_FLAG_FROM_ARRAY: from_array (duplicates allowed, first occurrence kept)
 FLAG_ROUNDS = 16  # HM_FLAG_ROUNDS: the paper's sortless round-based construction (ablation, u64 keys)
+FLAG_FUSED_EXCHANGE = 32  # HM_FLAG_FUSED_EXCHANGE: build_u64_dist routes straight into the owners' NCCL windows
 
 
 _allocator = None  # (alloc, free) ctypes callbacks of set_allocator
@@ -401,13 +402,15 @@ def build_u64_shard(keys, vals, n_global: int, b_lo: int, b_hi: int, t1: int, se
     return HashMap(h.value, 0), int(S.value)
 
 
-def build_u64_dist(keys, vals, nccl_comm: int, seed: int = 0, stream=None, log2_bp: int = 0) -> "HashMap":
+def build_u64_dist(keys, vals, nccl_comm: int, seed: int = 0, stream=None, log2_bp: int = 0,
+                   flags: int = 0) -> "HashMap":
     """Collective sharded build over an NCCL communicator (hm_build_u64_dist;
-    e.g. nccl_comm = the process group's backend ._comm_ptr())."""
+    e.g. nccl_comm = the process group's backend ._comm_ptr()).  flags:
+    FLAG_FUSED_EXCHANGE routes straight into the owners' windows."""
     kp, kk = _ptr(keys, 8)
     vp, vk = _ptr(vals, 8)
     h = C.c_void_p()
-    o = _opts(seed, log2_bp)
+    o = _opts(seed, log2_bp, flags)
     _check(lib().hm_build_u64_dist(kp, vp, _numel(keys), C.byref(o), _stream(stream), C.c_void_p(int(nccl_comm)),
                                    C.byref(h)))
     return HashMap(h.value, 0)

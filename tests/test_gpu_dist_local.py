@@ -192,5 +192,16 @@ def test_dist_build_and_lookup_through_nccl_one_rank():
             hm.build_u64_dist(dev(dup), dev(vals), comm)
         assert e.value.name == "DUPLICATE_KEY"
         m.free()
+        # NEXT-2: the route kernel storing straight into the owner's NCCL
+        # window (here the owner is this rank): the same table
+        m = hm.build_u64_dist(dev(keys), dev(vals), comm, seed=3, flags=hm.FLAG_FUSED_EXCHANGE)
+        d, sl, _ = m.export()
+        assert d.tobytes() == ot.dir.tobytes() and sl.tobytes() == ot.slots.tobytes()
+        v, f = hm.lookup_u64_dist(m, dev(q), comm)
+        assert np.array_equal(host(v), ov) and np.array_equal(host(f), of)
+        m.free()
+        with pytest.raises(hm.HMError) as e:
+            hm.build_u64_dist(dev(dup), dev(vals), comm, flags=hm.FLAG_FUSED_EXCHANGE)
+        assert e.value.name == "DUPLICATE_KEY"
     finally:
         tdist.destroy_process_group()
