@@ -335,6 +335,15 @@ int hm_dist_decide(uint64_t n_global, uint32_t t1, uint64_t S_total, int max_sta
  * all-gather of S_r). */
 uint64_t hm_dist_slot_base(const uint64_t* S_all, int world, int rank);
 
+/* hm_dist_exchange_plan — the fused route + exchange's placement
+ * (HM_FLAG_FUSED_EXCHANGE): from the all-gathered count matrix
+ * C[q * world + r] (pairs rank q routes to owner r), off[r] = where this
+ * rank's run starts in owner r's receive buffer (sum of C[q][r] for q < rank),
+ * *recv = pairs this rank receives (sum of C[q][rank]), *cap = the largest
+ * receive count over the ranks (the symmetric window's size).  Host-only. */
+hm_status hm_dist_exchange_plan(const uint64_t* C, int world, int rank, uint64_t* off, uint64_t* cap,
+                                uint64_t* recv);
+
 /* hm_build_u64_shard — build the shard of the global table that holds level-1
  * buckets [b_lo, b_hi) of a table with n_global keys, from exactly the keys
  * routed to it, with level-1 attempt t1 fixed by the caller.  The caller

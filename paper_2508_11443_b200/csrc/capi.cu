@@ -849,6 +849,23 @@ int hm_dist_decide(uint64_t n_global, uint32_t t1, uint64_t S_total, int max_sta
   return HM_DIST_REDRAW;
 }
 
+hm_status hm_dist_exchange_plan(const uint64_t* C, int world, int rank, uint64_t* off, uint64_t* cap,
+                                uint64_t* recv) {
+  if (!C || !off || !cap || !recv || world < 1 || world > 64 || rank < 0 || rank >= world) return HM_ERR_INVALID_ARG;
+  *cap = 0;
+  *recv = 0;
+  for (int r = 0; r < world; r++) {
+    uint64_t tot = 0;
+    for (int q = 0; q < world; q++) {
+      if (q == rank) off[r] = tot;
+      tot += C[size_t(q) * world + r];
+    }
+    *cap = std::max(*cap, tot);
+    if (r == rank) *recv = tot;
+  }
+  return HM_OK;
+}
+
 uint64_t hm_dist_slot_base(const uint64_t* S_all, int world, int rank) {
   uint64_t b = 0;
   for (int q = 0; q < rank && q < world; q++) b += S_all[q];

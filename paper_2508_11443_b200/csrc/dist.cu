@@ -154,15 +154,7 @@ hm_status fused_exchange(const uint64_t* keys, const uint64_t* vals, uint64_t n_
   HM_CUDA_TRY(cudaStreamSynchronize(st));
   uint64_t cap = 0, mine = 0;
   std::vector<uint64_t> off(world, 0);  // where this rank's run starts in every owner's buffer
-  for (int r = 0; r < world; r++) {
-    uint64_t tot = 0;
-    for (int q = 0; q < world; q++) {
-      if (q == rank) off[r] = tot;
-      tot += C[size_t(q) * world + r];
-    }
-    cap = std::max(cap, tot);
-    if (r == rank) mine = tot;
-  }
+  if ((s = hm_dist_exchange_plan(C.data(), world, rank, off.data(), &cap, &mine)) != HM_OK) return s;
   if ((s = w->open(comm, cap)) != HM_OK) return s;
   HM_CUDA_TRY(cudaMemcpyAsync(d_cur, off.data(), size_t(world) * 8, cudaMemcpyHostToDevice, st));
   if (n_local) {

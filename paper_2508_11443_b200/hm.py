@@ -103,6 +103,8 @@ def lib():
             L.hm_dist_decide.restype = C.c_int
             L.hm_dist_slot_base.argtypes = [p, i32, i32]
             L.hm_dist_slot_base.restype = u64
+            L.hm_dist_exchange_plan.argtypes = [p, i32, i32, p, C.POINTER(u64), C.POINTER(u64)]
+            L.hm_dist_exchange_plan.restype = C.c_int
         for f in ("hm_assemble_u64", "hm_build_u64_dist", "hm_lookup_u64_dist", "hm_build_u64", "hm_build_bytes", "hm_lookup_u64", "hm_lookup_bytes", "hm_info", "hm_export",
                   "hm_route_u64", "hm_build_u64_shard", "hm_shard_set_base", "hm_route_queries_u64",
                   "hm_unroute_u64"):
@@ -457,6 +459,17 @@ def dist_decide(n_global: int, t1: int, S_total: int, max_status: int):
 def dist_slot_base(S_all, rank: int) -> int:
     a = np.ascontiguousarray(np.asarray(S_all, dtype=np.uint64))
     return int(lib().hm_dist_slot_base(a.ctypes.data_as(C.c_void_p), len(a), rank))
+
+
+def dist_exchange_plan(C_matrix, world: int, rank: int):
+    """(off[world], cap, recv) of hm_dist_exchange_plan for the count matrix
+    C_matrix[q][r] (pairs rank q routes to owner r)."""
+    cm = np.ascontiguousarray(np.asarray(C_matrix, dtype=np.uint64).reshape(world, world))
+    off = np.zeros(world, np.uint64)
+    cap, recv = C.c_uint64(), C.c_uint64()
+    _check(lib().hm_dist_exchange_plan(cm.ctypes.data_as(C.c_void_p), world, rank, off.ctypes.data_as(C.c_void_p),
+                                       C.byref(cap), C.byref(recv)))
+    return [int(x) for x in off], int(cap.value), int(recv.value)
 
 
 class _KStat(C.Structure):
