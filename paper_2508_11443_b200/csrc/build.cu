@@ -56,7 +56,11 @@ struct KBCfg {
   // bytes per item k_bucket keeps in shared memory: the whole 16-byte record
   // (key, value); for 32-byte byte-key records only the fingerprint (the out
   // phase gathers the records from the partition buffer, L2-resident by then)
+#ifdef HM_KB_KEYS_ONLY
+  static constexpr int SMEM_ITEM = 8;
+#else
   static constexpr int SMEM_ITEM = sizeof(E) == 16 ? 16 : 8;
+#endif
 };
 
 // The partition's items as k_bucket sees them: keys in shared memory (inside
@@ -66,16 +70,19 @@ template <class E>
 struct Items {
   const uint64_t* keys;
   const E* recs;
-  static constexpr int kStride = sizeof(E) == 16 ? 2 : 1;
+  static constexpr int kStride = KBCfg<E>::SMEM_ITEM / 8;
   __device__ __forceinline__ uint64_t key(uint32_t i) const { return keys[size_t(i) * kStride]; }
   __device__ __forceinline__ E rec(uint32_t i) const {
-    if (sizeof(E) == 16) return recs[i];
+    if (KBCfg<E>::SMEM_ITEM == int(sizeof(E))) return recs[i];
+    static_assert(sizeof(E) == 16 || sizeof(E) == 32, "record size");
     E e;
     const uint4* p = reinterpret_cast<const uint4*>(recs + i);
-    const uint4 a = __ldg(p), b = __ldg(p + 1);
-    static_assert(sizeof(E) == 16 || sizeof(E) == 32, "record size");
+    const uint4 a = __ldg(p);
     memcpy(&e, &a, 16);
-    memcpy(reinterpret_cast<char*>(&e) + 16, &b, 16);
+    if (sizeof(E) == 32) {
+      const uint4 b = __ldg(p + 1);
+      memcpy(reinterpret_cast<char*>(&e) + 16, &b, 16);
+    }
     return e;
   }
 };
