@@ -270,7 +270,7 @@ def frac(units, ms, bpu, peak):
     return round(units * bpu / (ms / 1e3) / 1e9 / peak, 4)
 
 
-def extra_configs(world, rank, dev, comm, peak):
+def extra_configs(world, rank, dev, comm, peak, use_dist):
     """The other BASELINE configs, measured after the timed region (not part of
     `value`): C1 (2^16, launch-bound), C3 (2^24 strings, 4-64 bytes) and C5
     (2^30 lookups on a 2^27-key table; bucket-routed over the ranks for N>1)."""
@@ -341,7 +341,7 @@ def extra_configs(world, rank, dev, comm, peak):
     q, ev, ef = gen_cuda.u64_queries(n_glob, chunk, lo=rank * nq, with_expect=True)
     ov = torch.empty(chunk, dtype=torch.int64, device=dev)
     of = torch.empty(chunk, dtype=torch.uint8, device=dev)
-    if world == 1:
+    if not use_dist:
         m = hm.HashMap.build_u64(k, v)
         look = lambda: [m.lookup(q, ov, of) for _ in range(nq // chunk)]  # noqa: E731
     else:
@@ -353,7 +353,7 @@ def extra_configs(world, rank, dev, comm, peak):
     out["C5"] = {"table_keys": n_glob, "queries": nq_glob, "lookup_ms": round(lms, 4),
                  "lookup_mq_s": round(nq_glob / lms / 1e3, 1),
                  "lookup_roofline_frac_per_gpu": frac(nq, lms, LOOKUP_BYTES_PER_QUERY, peak),
-                 "routing": "bucket-routed all-to-all (hm_lookup_u64_dist)" if world > 1 else "local",
+                 "routing": "bucket-routed all-to-all (hm_lookup_u64_dist)" if use_dist else "local",
                  "correct": ok, "timing": "rank-local CUDA events" if world > 1 else "CUDA events"}
     del k, v, q, ev, ef, ov, of
     torch.cuda.empty_cache()
@@ -380,10 +380,27 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     comm = None
-    if world > 1:
-        tdist.init_process_group("nccl", device_id=dev)
-        tdist.barrier()
-        comm = tdist.distributed_c10d._get_default_group()._get_backend(dev)._comm_ptr()
+    use_dist = world > 1 or args.dist_path  # (--dist-path: the sharded C calls with one rank, a check of this path)
+    if use_dist:
+        if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+            os.environ["NCCL_DEBUG"] = "WARN"  # (no version banner ahead of the JSON line)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", str(_free_port()))
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
+        # (NCCL prints its version banner on stdout when the communicator is
+        # created: sent to stderr, so that stdout carries only the JSON line)
+        sys.stdout.flush()
+        saved = os.dup(1)
+        os.dup2(2, 1)
+        try:
+            tdist.init_process_group("nccl", device_id=dev)
+            tdist.barrier()
+            comm = tdist.distributed_c10d._get_default_group()._get_backend(dev)._comm_ptr()
+            torch.cuda.synchronize()
+        finally:
+            os.dup2(saved, 1)
+            os.close(saved)
 
     def barrier():
         if world > 1:
@@ -410,14 +427,14 @@ def run_ours(args):
 
     def step(ev_b=None):
         nonlocal s_over_n
-        if world == 1:
+        if not use_dist:
             m = hm.HashMap.build_u64(keys, vals, seed=0)
         else:
             m = hm.build_u64_dist(keys, vals, comm, seed=0, flags=dist_flags)
         s_over_n = m.info().S / n
         if ev_b is not None:
             ev_b.record()
-        if world == 1:
+        if not use_dist:
             m.lookup(q, ov, of)
         else:
             hm.lookup_u64_dist(m, q, comm, ov, of)
@@ -502,7 +519,7 @@ def run_ours(args):
         hof = torch.empty(n, dtype=torch.uint8).pin_memory()
 
         def e2e_step():
-            if world == 1:
+            if not use_dist:
                 m = hm.HashMap.build_u64(hk, hv, seed=0)  # host buffers: staged inside the C-ABI
                 m.lookup(hq, hov, hof)  # host in, host out
                 m.free()
@@ -530,7 +547,7 @@ def run_ours(args):
         e2e_ok = bool(torch.equal(hof, ef.cpu())) and bool(torch.equal(hov, ev.cpu()))
         e2e = {"value": round(n * world / (e2e_ms / 1e3) / 1e6, 2), "unit": "Mkeys/s",
                "h2d_bytes_per_step": 24 * n, "d2h_bytes_per_step": 9 * n, "ms_per_step": round(e2e_ms, 3),
-               "correct": e2e_ok, "path": "hm_build_u64/hm_lookup_u64 on pinned host buffers" if world == 1
+               "correct": e2e_ok, "path": "hm_build_u64/hm_lookup_u64 on pinned host buffers" if not use_dist
                else "H2D copy + hm_build_u64_dist/hm_lookup_u64_dist + D2H copy"}
         del hk, hv, hq, hov, hof
 
@@ -538,10 +555,12 @@ def run_ours(args):
     torch.cuda.empty_cache()
     configs = None
     if not args.no_configs:
-        configs = extra_configs(world, rank, dev, comm, peak)
+        configs = extra_configs(world, rank, dev, comm, peak, use_dist)
 
+    if args.fused_exchange and use_dist:
+        hm.dist_release_windows(comm)  # (collective)
     if rank != 0:
-        if world > 1:
+        if use_dist:
             tdist.destroy_process_group()
         return 0
     cpu = None
@@ -555,7 +574,7 @@ def run_ours(args):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
         "data": "synthetic: seeded splitmix64 key stream (workloads/gen.py, generated on device)",
         "config": dict(config_dict(world), **({"exchange": "fused route + NVLink window stores"}
-                                              if args.fused_exchange and world > 1 else {})),
+                                              if args.fused_exchange and use_dist else {})),
         "build_mkeys_s": round(n * world / (build_ms / 1e3) / 1e6, 2),
         "lookup_mq_s": round(n * world / (look_ms / 1e3) / 1e6, 2),
         "build_ms": round(build_ms, 4), "lookup_ms": round(look_ms, 4),
@@ -568,8 +587,10 @@ def run_ours(args):
         "gpu_launches": int(launches),
         "clocks": clocks,
     }
+    if use_dist and world == 1:
+        out["config"]["parallelism"] = "1 GPU through hm_build_u64_dist / hm_lookup_u64_dist (--dist-path)"
     print(json.dumps(out), flush=True)
-    if world > 1:
+    if use_dist:
         tdist.destroy_process_group()
     return 0
 
@@ -583,6 +604,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-configs", action="store_true", help="skip the C1/C3/C5 measurements after the timed region")
+    ap.add_argument("--dist-path", action="store_true",
+                    help="N = 1 through the sharded C calls on a one-rank NCCL group (checks the N > 1 code path)")
     ap.add_argument("--fused-exchange", action="store_true",
                     help="N > 1: route straight into the owners' NCCL windows (HM_FLAG_FUSED_EXCHANGE, NEXT-2)")
     args = ap.parse_args()

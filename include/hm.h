@@ -117,6 +117,9 @@ typedef struct {
  * after it; the shards are the same.  Needs every rank in one NVLink domain
  * (a single node).  Other calls: HM_ERR_INVALID_ARG. */
 #define HM_FLAG_FUSED_EXCHANGE 32u
+/* (The receive windows of HM_FLAG_FUSED_EXCHANGE builds stay registered on
+ * their communicator for the next builds; hm_dist_release_windows, called by
+ * every rank of the communicator — it is collective — frees them.) */
 
 /* Table header, 56 bytes, little-endian (DESIGN.md §4 "Table layout"). */
 typedef struct {
@@ -305,6 +308,8 @@ hm_status hm_build_u64_dist(const uint64_t* keys, const uint64_t* vals, uint64_t
  * routed to the owner of their level-1 bucket, answered there and routed
  * back.  Every rank must call it (nq may be 0).  Synchronous for the count
  * exchange; the results are complete in `stream` order. */
+hm_status hm_dist_release_windows(void* nccl_comm);
+
 hm_status hm_lookup_u64_dist(const hm_map* shard, const uint64_t* q, uint64_t nq, uint64_t* out_vals,
                              uint8_t* out_found, void* stream, void* nccl_comm);
 

@@ -13,6 +13,8 @@
 #include <nccl_device.h>  // (NCCL 2.28 device API: window peer pointers)
 
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -135,12 +137,31 @@ struct RecvWindow {
   }
 };
 
+// Registered windows are kept per communicator and reused while large enough
+// (registration is collective and costs milliseconds); every rank takes the
+// same decision (cap is the global maximum).  hm_dist_release_windows frees
+// them (collective).
+static std::mutex g_win_mu;
+static std::map<ncclComm_t, RecvWindow> g_win;
+
+static hm_status window_for(ncclComm_t comm, uint64_t cap, RecvWindow** out) {
+  std::lock_guard<std::mutex> lk(g_win_mu);
+  RecvWindow& w = g_win[comm];
+  if (!w.win || w.cap < cap) {
+    hm_status s;
+    if ((s = w.release()) != HM_OK) return s;
+    if ((s = w.open(comm, cap + cap / 4 + 1024)) != HM_OK) return s;  // (headroom for the next builds)
+  }
+  *out = &w;
+  return HM_OK;
+}
+
 // Route this rank's pairs into the owners' windows: counts, their all-gather
 // (the G x G matrix C[q][r]), the window, the fused scatter, one barrier.
 // On return rk/rv point into this rank's window (nrecv pairs).
 hm_status fused_exchange(const uint64_t* keys, const uint64_t* vals, uint64_t n_local, const L1Params& l1, int world,
-                         int rank, ncclComm_t comm, cudaStream_t st, uint64_t* d_small, RecvWindow* w,
-                         const uint64_t** rk, const uint64_t** rv, uint64_t* nrecv) {
+                         int rank, ncclComm_t comm, cudaStream_t st, uint64_t* d_small, const uint64_t** rk,
+                         const uint64_t** rv, uint64_t* nrecv) {
   uint64_t* d_c = nullptr;  // [world] own counts, then [world][world] all of them, then [world] cursors
   const cudaError_t ea = cudaMallocAsync(reinterpret_cast<void**>(&d_c), (size_t(world) * world + 2 * world) * 8, st);
   if (ea != cudaSuccess) return cuda_fail(ea, "fused exchange");
@@ -155,7 +176,8 @@ hm_status fused_exchange(const uint64_t* keys, const uint64_t* vals, uint64_t n_
   uint64_t cap = 0, mine = 0;
   std::vector<uint64_t> off(world, 0);  // where this rank's run starts in every owner's buffer
   if ((s = hm_dist_exchange_plan(C.data(), world, rank, off.data(), &cap, &mine)) != HM_OK) return s;
-  if ((s = w->open(comm, cap)) != HM_OK) return s;
+  RecvWindow* w = nullptr;
+  if ((s = window_for(comm, cap, &w)) != HM_OK) return s;
   HM_CUDA_TRY(cudaMemcpyAsync(d_cur, off.data(), size_t(world) * 8, cudaMemcpyHostToDevice, st));
   if (n_local) {
     LaunchScope ls_("k_route_scatter_win", st);
@@ -221,13 +243,11 @@ hm_status hm_build_u64_dist(const uint64_t* keys, const uint64_t* vals, uint64_t
   for (uint32_t t1 = 0;;) {
     // (2) route, exchange counts and pairs (fused: straight into the owners' windows)
     DevBufs rb{st, {}};
-    RecvWindow w;
     const uint64_t *rk = nullptr, *rv = nullptr;
     uint64_t nrecv = 0;
     if (fused) {
       const L1Params l1 = make_l1(seed_mix(seed), t1, n);
-      if ((s = fused_exchange(keys, vals, n_local, l1, world, rank, comm, st, d_small, &w, &rk, &rv, &nrecv)) !=
-          HM_OK)
+      if ((s = fused_exchange(keys, vals, n_local, l1, world, rank, comm, st, d_small, &rk, &rv, &nrecv)) != HM_OK)
         return s;
     } else {
       if ((s = hm_route_u64(keys, vals, n_local, n, seed, t1, world, sk, sv, d_sc, stream)) != HM_OK) return s;
@@ -244,10 +264,8 @@ hm_status hm_build_u64_dist(const uint64_t* keys, const uint64_t* vals, uint64_t
     // (3) the shard, then the global bound and the status, agreed by all ranks
     const hm_status bs = hm_build_u64_shard(rk, rv, nrecv, n, lo, hi, t1, opts ? &shard_opts : nullptr, stream, &m,
                                             &S_local);
-    if (fused) {  // (the shard copied what it needs; collective on every rank)
-      HM_CUDA_TRY(cudaStreamSynchronize(st));
-      if ((s = w.release()) != HM_OK) return s;
-    }
+    // (fused: the shard build has copied the window's pairs; the window stays
+    // registered for the next build)
     const std::string local_err = bs != HM_OK ? hm_last_error() : std::string();
     uint64_t red[2] = {bs == HM_OK ? S_local : 0, uint64_t(bs)};
     HM_CUDA_TRY(cudaMemcpyAsync(d_small, red, 16, cudaMemcpyHostToDevice, st));
@@ -278,6 +296,16 @@ hm_status hm_build_u64_dist(const uint64_t* keys, const uint64_t* vals, uint64_t
   }
   *out = m;
   return HM_OK;
+}
+
+hm_status hm_dist_release_windows(void* nccl_comm) {
+  if (!nccl_comm) return HM_ERR_INVALID_ARG;
+  std::lock_guard<std::mutex> lk(g_win_mu);
+  auto it = g_win.find(static_cast<ncclComm_t>(nccl_comm));
+  if (it == g_win.end()) return HM_OK;
+  const hm_status s = it->second.release();
+  g_win.erase(it);
+  return s;
 }
 
 hm_status hm_lookup_u64_dist(const hm_map* shard, const uint64_t* q, uint64_t nq, uint64_t* out_vals,

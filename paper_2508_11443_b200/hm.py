@@ -418,6 +418,14 @@ def build_u64_dist(keys, vals, nccl_comm: int, seed: int = 0, stream=None, log2_
     return HashMap(h.value, 0)
 
 
+def dist_release_windows(nccl_comm: int) -> None:
+    """Free the receive windows FLAG_FUSED_EXCHANGE builds keep registered on
+    this communicator (hm_dist_release_windows; collective: every rank)."""
+    lib().hm_dist_release_windows.argtypes = [C.c_void_p]
+    lib().hm_dist_release_windows.restype = C.c_int
+    _check(lib().hm_dist_release_windows(C.c_void_p(int(nccl_comm))))
+
+
 def lookup_u64_dist(shard: "HashMap", q, nccl_comm: int, out_vals=None, out_found=None, stream=None):
     """Collective routed lookup on the shards of build_u64_dist (hm_lookup_u64_dist)."""
     nq = _numel(q)
