@@ -423,7 +423,13 @@ def run_ours(args):
     torch.cuda.synchronize()
 
     s_over_n = 2.0  # replaced by the table's actual S / n after the first step
-    dist_flags = hm.FLAG_FUSED_EXCHANGE if args.fused_exchange else 0
+    # N > 1: the fused route + exchange (NEXT-2) unless --no-fused-exchange;
+    # a communicator that cannot register the symmetric window falls back to
+    # route + grouped send/recv (decided on the first warm-up step, every rank
+    # sees the same NCCL error)
+    fused = use_dist and (args.fused_exchange or (world > 1 and not args.no_fused_exchange))
+    dist_flags = hm.FLAG_FUSED_EXCHANGE if fused else 0
+    fused_note = None
 
     def step(ev_b=None):
         nonlocal s_over_n
@@ -440,8 +446,16 @@ def run_ours(args):
             hm.lookup_u64_dist(m, q, comm, ov, of)
         m.free()
 
-    for _ in range(args.warmup):
-        step()
+    for i in range(args.warmup):
+        if i == 0 and fused:
+            try:
+                step()
+            except hm.HMError as e:
+                fused, dist_flags, fused_note = False, 0, f"fused exchange unavailable ({e}); route + send/recv"
+                barrier()
+                step()
+        else:
+            step()
     barrier()
     # ---------------------------------------------------------------- timed
     clk = ClockSampler(local)
@@ -525,7 +539,7 @@ def run_ours(args):
                 m.free()
             else:
                 dk, dv, dq = hk.to(dev, non_blocking=True), hv.to(dev, non_blocking=True), hq.to(dev, non_blocking=True)
-                m = hm.build_u64_dist(dk, dv, comm, seed=0)
+                m = hm.build_u64_dist(dk, dv, comm, seed=0, flags=dist_flags)
                 v, f = hm.lookup_u64_dist(m, dq, comm)
                 hov.copy_(v)
                 hof.copy_(f)
@@ -557,7 +571,7 @@ def run_ours(args):
     if not args.no_configs:
         configs = extra_configs(world, rank, dev, comm, peak, use_dist)
 
-    if args.fused_exchange and use_dist:
+    if fused:
         hm.dist_release_windows(comm)  # (collective)
     if rank != 0:
         if use_dist:
@@ -573,8 +587,9 @@ def run_ours(args):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
         "data": "synthetic: seeded splitmix64 key stream (workloads/gen.py, generated on device)",
-        "config": dict(config_dict(world), **({"exchange": "fused route + NVLink window stores"}
-                                              if args.fused_exchange and use_dist else {})),
+        "config": dict(config_dict(world), **({"exchange": "fused route + NVLink window stores (HM_FLAG_FUSED_EXCHANGE)"}
+                                              if fused else ({"exchange": fused_note or "route + grouped ncclSend/ncclRecv"}
+                                                             if use_dist else {}))),
         "build_mkeys_s": round(n * world / (build_ms / 1e3) / 1e6, 2),
         "lookup_mq_s": round(n * world / (look_ms / 1e3) / 1e6, 2),
         "build_ms": round(build_ms, 4), "lookup_ms": round(look_ms, 4),
@@ -607,7 +622,9 @@ def main():
     ap.add_argument("--dist-path", action="store_true",
                     help="N = 1 through the sharded C calls on a one-rank NCCL group (checks the N > 1 code path)")
     ap.add_argument("--fused-exchange", action="store_true",
-                    help="N > 1: route straight into the owners' NCCL windows (HM_FLAG_FUSED_EXCHANGE, NEXT-2)")
+                    help="with --dist-path at N = 1: route straight into the NCCL window (HM_FLAG_FUSED_EXCHANGE, NEXT-2)")
+    ap.add_argument("--no-fused-exchange", action="store_true",
+                    help="N > 1: route + grouped ncclSend/ncclRecv instead of the fused route + window stores")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
