@@ -86,6 +86,9 @@ struct Items {
     return e;
   }
 };
+#ifndef HM_SMEM_ALIAS
+#define HM_SMEM_ALIAS 0  // k_bucket: alias rk with the rounds' lists and sA with the slot source map
+#endif
 #ifndef HM_PF_DIST
 #define HM_PF_DIST 148  // k_bucket: L2 prefetch of partition p + HM_PF_DIST (0: off; 148 measured best)
 #endif
@@ -715,7 +718,7 @@ __device__ __forceinline__ void search_warp(const BuildParams& bp, const Items<E
         if (lane == 0) atomicOr(&stt->exhausted, 1u);
         t = 0;
       } else {
-        if (mine) X.sA[st0 + lane] = uint16_t(h);
+        if (mine && !X.src) X.sA[st0 + lane] = uint16_t(h);
         if (X.src) {
           uint16_t* o = X.src + X.soff[lb];
           bitsw[lane] = 0;
@@ -750,6 +753,17 @@ __host__ __device__ __forceinline__ BucketSmem bucket_smem_layout(uint32_t cap, 
   L.cls_off[3] = L.cls_off[2] + cap / 9 + 1;
   L.skv = 0;                                               // [cap] items: 16-B records or 8-B fingerprints
   L.lbk = L.skv + al16(size_t(cap) * esz);                 // u16[cap]: local bucket of item i
+#if HM_SMEM_ALIAS
+  // (rk lives from hist to groupby, the rounds' lists from the search on: one
+  // region; sA serves only direct-slot partitions, src only staged ones)
+  L.sidx = L.lbk + al16(size_t(cap) * 2);                  // u16[cap]: grouped position -> item
+  L.src = L.sidx + al16(size_t(cap) * 2);                  // u16[smax]: slot -> item / u16[cap]: sA
+  L.sA = L.src;
+  L.slist = L.src + al16(size_t(L.smax) * 2);              // u16[]: class lists
+  L.queue = L.slist + al16(size_t(L.cls_off[kNCls]) * 2);  // u16[3][cap/2+1]: the rounds' lists / u16[cap]: rk
+  L.rk = L.queue;
+  L.ss = L.queue + al16(std::max(size_t(cap / 2 + 1) * 6, size_t(cap) * 2));
+#else
   L.rk = L.lbk + al16(size_t(cap) * 2);                    // u16[cap]: rank of item i in its bucket
   L.sidx = L.rk + al16(size_t(cap) * 2);                   // u16[cap]: grouped position -> item
   L.sA = L.sidx + al16(size_t(cap) * 2);                   // u16[cap]: level-2 slot of a grouped position
@@ -757,6 +771,7 @@ __host__ __device__ __forceinline__ BucketSmem bucket_smem_layout(uint32_t cap, 
   L.slist = L.src + al16(size_t(L.smax) * 2);              // u16[]: class lists
   L.queue = L.slist + al16(size_t(L.cls_off[kNCls]) * 2);  // u16[3][cap/2+1]: the rounds' lists
   L.ss = L.queue + al16(size_t(cap / 2 + 1) * 6);          // u8[BP]: bucket size s
+#endif
   L.sstart = L.ss + al16(BP);                              // u16[BP]: first grouped position of each bucket
   L.soff = L.sstart + al16(size_t(BP) * 2);                // u32[BP]: histogram, then slot offset in the partition
   L.st = L.soff + al16(size_t(BP) * 4);                    // u8[BP]: attempt t of each bucket
