@@ -228,60 +228,38 @@ __device__ __forceinline__ uint64_t fingerprint_dev(const uint8_t* bytes, uint64
 // The same fingerprint in expanded form.  Unrolling the Horner recurrence
 // acc_{i+1} = (acc_i + w_i) * r gives, exactly (mod P),
 //   acc_nw = sum_{i < nw} w_i * r^(nw - i),
-// so with the powers r^1 .. r^kFpPowMax tabulated once per block every word
-// costs one 32 x 61-bit product (two 32x32->64 multiplies and a fold) instead
-// of a dependent 61 x 61-bit modular multiply, and the words are independent.
+// so with the powers r^1 .. r^kFpPowMax tabulated once per block the words are
+// independent.  Each power is split into 21-bit limbs, r^e = l0 + l1*2^21 +
+// l2*2^42 (l2 < 2^19), and each limb product w*l (< 2^53) is accumulated in
+// its own 64-bit sum with no reduction: a word costs three multiply-adds, and
+// 32 words keep every sum below 2^58.  fp3_finish folds the three sums once.
 // Keys longer than 4*kFpPowMax bytes take the Horner loop above.
-constexpr int kFpPowMax = 16;
+constexpr int kFpPowMax = 32;
 struct FpPow {
-  uint32_t lo[kFpPowMax + 1];
-  uint32_t hi[kFpPowMax + 1];
+  uint4 p[kFpPowMax + 1];  // {l0, l1, l2, 0} of r^e
 };
 // One thread of the block fills the table; the caller synchronises.
 __device__ inline void fp_pow_fill(FpPow* pw, uint64_t r) {
   uint64_t p = 1;
-  pw->lo[0] = 1;
-  pw->hi[0] = 0;
-  for (int e = 1; e <= kFpPowMax; e++) {
+  for (int e = 0; e <= kFpPowMax; e++) {
+    pw->p[e] = make_uint4(uint32_t(p & 0x1FFFFF), uint32_t((p >> 21) & 0x1FFFFF), uint32_t(p >> 42), 0u);
     p = mulmod_p(p, r);
-    pw->lo[e] = uint32_t(p);
-    pw->hi[e] = uint32_t(p >> 32);
   }
 }
 
-// w * R (mod P), partially reduced (< 2^62 + 2^33), for w < 2^32 and R < P
-// given as 32-bit halves R = rh*2^32 + rl (rh < 2^29):  w*rl < 2^64 is folded
-// with 2^61 == 1; t = w*rh < 2^61 and t*2^32 = (t >> 29)*2^61 + (t mod 2^29)*2^32
-// == (t >> 29) + (t mod 2^29)*2^32.
-__device__ __forceinline__ uint64_t mul32_p(uint32_t w, uint32_t rl, uint32_t rh) {
-  const uint64_t x = uint64_t(w) * rl;
-  const uint64_t t = uint64_t(w) * rh;
-  return (x & kP) + (x >> 61) + (t >> 29) + ((t & 0x1FFFFFFFull) << 32);
-}
-
-__device__ __forceinline__ uint64_t fingerprint_pw(const uint8_t* bytes, uint64_t off, uint64_t len, uint64_t r,
-                                                   const FpPow* pw) {
-  if (len == 0) return 0;
-  if (len > 4 * kFpPowMax) return fingerprint_dev(bytes, off, len, r);
-  const uint64_t abase = off & ~uint64_t(3);
-  const uint32_t sh = uint32_t(off & 3) * 8;
-  const uint64_t last_aligned = (off + len - 1) & ~uint64_t(3);
-  const uint32_t nw = uint32_t(len + 3) >> 2;
-  uint64_t acc = 0;  // < 2^61 + 4 after every fold
-  uint32_t cur = ld_u32(bytes + abase);
-  for (uint32_t i = 0; i < nw; i++) {
-    const uint64_t na = abase + 4 * (uint64_t(i) + 1);
-    const uint32_t nxt = na <= last_aligned ? ld_u32(bytes + na) : 0u;
-    uint32_t w = sh ? __funnelshift_r(cur, nxt, sh) : cur;
-    const uint32_t rem = uint32_t(len) - 4 * i;
-    if (rem < 4) w &= (1u << (8 * rem)) - 1u;
-    acc += mul32_p(w, pw->lo[nw - i], pw->hi[nw - i]);
-    acc = (acc & kP) + (acc >> 61);
-    cur = nxt;
-  }
-  uint64_t f = acc + len;
+// (a0 + a1*2^21 + a2*2^42 + len) mod P for a0, a1 < 2^58, a2 < 2^56, using
+// 2^61 == 1: a1*2^21 == (a1 >> 40) + (a1 mod 2^40)*2^21 and a2*2^42 ==
+// (a2 >> 19) + (a2 mod 2^19)*2^42; the sum stays below 2^63.
+__device__ __forceinline__ uint64_t fp3_finish(uint64_t a0, uint64_t a1, uint64_t a2, uint32_t len) {
+  uint64_t f = a0 + (a1 >> 40) + ((a1 & 0xFFFFFFFFFFull) << 21) + (a2 >> 19) + ((a2 & 0x7FFFFull) << 42) + len;
   f = (f & kP) + (f >> 61);
   return f >= kP ? f - kP : f;
+}
+
+__device__ __forceinline__ void fp3_acc(uint64_t& a0, uint64_t& a1, uint64_t& a2, uint32_t w, const uint4& p) {
+  a0 += uint64_t(w) * p.x;
+  a1 += uint64_t(w) * p.y;
+  a2 += uint64_t(w) * p.z;
 }
 
 // Byte equality of two keys of length len at arbitrary alignments: 4-byte
@@ -354,63 +332,56 @@ __device__ __forceinline__ bool bytes_equal64(const uint8_t* a, const uint8_t* b
   return true;
 }
 
-// fingerprint_pw with the words taken two at a time from ChunkStream (the same
-// little-endian 32-bit words, hence the same value).
+// The expanded fingerprint over ChunkStream (8-byte chunks = two words):
+// chunk c holds words 2c and 2c+1, weighted r^(nw-2c) and r^(nw-2c-1); the
+// last chunk is masked to the key's bytes (its second word is then zero when
+// nw is odd, and takes r^0).
 __device__ __forceinline__ uint64_t fingerprint_pw64(const uint8_t* bytes, uint64_t off, uint64_t len, uint64_t r,
                                                      const FpPow* pw) {
   if (len == 0) return 0;
   if (len > 4 * kFpPowMax) return fingerprint_dev(bytes, off, len, r);
-  const uint32_t L = uint32_t(len), nw = (L + 3) >> 2;
+  const uint32_t L = uint32_t(len);
   ChunkStream S(bytes + off, L);
-  uint64_t acc = 0;
-  for (uint32_t i = 0; i < nw; i += 2) {
+  uint64_t a0 = 0, a1 = 0, a2 = 0;
+  uint32_t e = (L + 3) >> 2;
+  for (uint32_t c = 0; c < (L >> 3); c++, e -= 2) {
     const uint64_t x = S.next();
-    const uint32_t rem = L - 4 * i;
-    uint32_t w0 = uint32_t(x);
-    if (rem < 4) w0 &= (1u << (8 * rem)) - 1u;
-    // two partially reduced terms (< 2^62 + 2^33 each) on acc (< 2^61 + 8) stay
-    // below 2^64: one fold per pair
-    uint64_t t2 = mul32_p(w0, pw->lo[nw - i], pw->hi[nw - i]);
-    if (i + 1 < nw) {
-      uint32_t w1 = uint32_t(x >> 32);
-      if (rem - 4 < 4) w1 &= (1u << (8 * (rem - 4))) - 1u;
-      t2 += mul32_p(w1, pw->lo[nw - i - 1], pw->hi[nw - i - 1]);
-    }
-    acc += t2;
-    acc = (acc & kP) + (acc >> 61);
+    fp3_acc(a0, a1, a2, uint32_t(x), pw->p[e]);
+    fp3_acc(a0, a1, a2, uint32_t(x >> 32), pw->p[e - 1]);
   }
-  uint64_t f = acc + len;
-  f = (f & kP) + (f >> 61);
-  return f >= kP ? f - kP : f;
+  if (L & 7) {
+    const uint64_t x = S.next() & ((1ull << (8 * (L & 7))) - 1ull);
+    fp3_acc(a0, a1, a2, uint32_t(x), pw->p[e]);
+    fp3_acc(a0, a1, a2, uint32_t(x >> 32), pw->p[e - 1]);
+  }
+  return fp3_finish(a0, a1, a2, L);
 }
 
-// fingerprint_pw64 over a shared-memory copy: sb holds the 8-byte words of
-// the bytes from an 8-aligned position, the key starts rel bytes in
-// (1 <= len <= 4 * kFpPowMax).
-__device__ __forceinline__ uint64_t fingerprint_sm64(const uint64_t* sb, uint32_t rel, uint32_t len,
-                                                     const FpPow* pw) {
+// The same over a shared-memory copy: u holds the 4-byte words of the bytes
+// from a 4-aligned position (one readable word past the last one), the key
+// starts rel bytes in (1 <= len <= 4 * kFpPowMax); its words are realigned
+// with 32-bit funnel shifts.
+__device__ __forceinline__ uint64_t fingerprint_sm32(const uint32_t* u, uint32_t rel, uint32_t len, const FpPow* pw) {
   if (len == 0) return 0;
-  const uint32_t a0 = rel >> 3, sh = (rel & 7) * 8, last = (rel + len - 1) >> 3, nw = (len + 3) >> 2;
-  uint64_t cur = sb[a0], acc = 0;
-  for (uint32_t i = 0, k = a0 + 1; i < nw; i += 2, k++) {
-    const uint64_t nxt = k <= last ? sb[k] : 0ull;
-    const uint64_t x = sh ? (cur >> sh) | (nxt << (64 - sh)) : cur;
-    cur = nxt;
-    const uint32_t rem = len - 4 * i;
-    uint32_t w0 = uint32_t(x);
-    if (rem < 4) w0 &= (1u << (8 * rem)) - 1u;
-    uint64_t t2 = mul32_p(w0, pw->lo[nw - i], pw->hi[nw - i]);  // (one fold per pair, as above)
-    if (i + 1 < nw) {
-      uint32_t w1 = uint32_t(x >> 32);
-      if (rem - 4 < 4) w1 &= (1u << (8 * (rem - 4))) - 1u;
-      t2 += mul32_p(w1, pw->lo[nw - i - 1], pw->hi[nw - i - 1]);
-    }
-    acc += t2;
-    acc = (acc & kP) + (acc >> 61);
+  const uint32_t sh = (rel & 3) * 8;
+  const uint32_t* q = u + (rel >> 2);
+  uint64_t a0 = 0, a1 = 0, a2 = 0;
+  uint32_t e = (len + 3) >> 2, cur = q[0];
+  for (uint32_t c = 0; c < (len >> 3); c++, e -= 2, q += 2) {
+    const uint32_t m = q[1], n = q[2];
+    fp3_acc(a0, a1, a2, __funnelshift_r(cur, m, sh), pw->p[e]);
+    fp3_acc(a0, a1, a2, __funnelshift_r(m, n, sh), pw->p[e - 1]);
+    cur = n;
   }
-  uint64_t f = acc + len;
-  f = (f & kP) + (f >> 61);
-  return f >= kP ? f - kP : f;
+  if (len & 7) {
+    const uint32_t m = q[1], n = q[2], t = len & 7;
+    uint32_t w0 = __funnelshift_r(cur, m, sh), w1 = __funnelshift_r(m, n, sh);
+    if (t < 4) w0 &= (1u << (8 * t)) - 1u;
+    w1 = t > 4 ? w1 & ((1u << (8 * (t - 4))) - 1u) : 0u;
+    fp3_acc(a0, a1, a2, w0, pw->p[e]);
+    fp3_acc(a0, a1, a2, w1, pw->p[e - 1]);
+  }
+  return fp3_finish(a0, a1, a2, len);
 }
 
 #endif

@@ -220,8 +220,47 @@ hm_status lookup_u64_launch(const hm_map* m, const uint64_t* q, uint64_t nq, uin
 #ifndef HM_LOOKUP_BYTES_QPT
 #define HM_LOOKUP_BYTES_QPT 1
 #endif
+
+// A key of at most 64 bytes as eight little-endian 8-byte chunks (zero past
+// the key), from the at most nine aligned words it touches: every load is
+// issued before the first is used (one memory round trip per key, where a
+// chunk-at-a-time loop pays one per chunk).
+constexpr uint32_t kRegKey = 64;
+__device__ __forceinline__ void key_chunks(const uint8_t* p, uint32_t len, uint64_t (&c)[8]) {
+  const uintptr_t A = reinterpret_cast<uintptr_t>(p);
+  const unsigned long long* w = reinterpret_cast<const unsigned long long*>(A & ~uintptr_t(7));
+  const uint32_t sh = uint32_t(A & 7) * 8, nw = len ? (uint32_t(A & 7) + len + 7) >> 3 : 0u;
+  uint64_t u[9];
+#pragma unroll
+  for (int i = 0; i < 9; i++) u[i] = uint32_t(i) < nw ? __ldg(w + i) : 0ull;
+#pragma unroll
+  for (int i = 0; i < 8; i++) {
+    uint64_t x = sh ? (u[i] >> sh) | (u[i + 1] << (64 - sh)) : u[i];
+    const int rem = int(len) - 8 * i;
+    if (rem < 8) x = rem <= 0 ? 0ull : x & ((1ull << (8 * rem)) - 1ull);
+    c[i] = x;
+  }
+}
+// fingerprint_pw64 of a key held as chunks (len <= 64): chunk i carries words
+// 2i and 2i+1, weighted r^(nw-2i) and r^(nw-2i-1); chunks past the key are 0.
+__device__ __forceinline__ uint64_t fingerprint_chunks(const uint64_t (&c)[8], uint32_t len, const FpPow* pw) {
+  if (len == 0) return 0;
+  const int nw = int(len + 3) >> 2;
+  uint64_t a0 = 0, a1 = 0, a2 = 0;
+#pragma unroll
+  for (int i = 0; i < 8; i++) {
+    if (8 * i < int(len)) {
+      fp3_acc(a0, a1, a2, uint32_t(c[i]), pw->p[nw - 2 * i]);
+      fp3_acc(a0, a1, a2, uint32_t(c[i] >> 32), pw->p[max(nw - 2 * i - 1, 0)]);
+    }
+  }
+  return fp3_finish(a0, a1, a2, len);
+}
+#ifndef HM_LB_MINB
+#define HM_LB_MINB 4  // (64 registers; 1 / 3: 1.01 / 1.00 ms vs 0.87 at C3, 5: spills)
+#endif
 template <int QPT>
-__global__ void __launch_bounds__(kLThreads) k_lookup_bytes(LookupParams lp, const uint8_t* __restrict__ qb,
+__global__ void __launch_bounds__(kLThreads, HM_LB_MINB) k_lookup_bytes(LookupParams lp, const uint8_t* __restrict__ qb,
                                                             const uint64_t* __restrict__ qo, uint64_t nq,
                                                             uint64_t* __restrict__ ov, uint8_t* __restrict__ of) {
   __shared__ uint64_t s_m2[33];
@@ -234,6 +273,7 @@ __global__ void __launch_bounds__(kLThreads) k_lookup_bytes(LookupParams lp, con
   const uint64_t per = uint64_t(kLThreads) * QPT;
   for (uint64_t base = blockIdx.x * per; base < nq; base += uint64_t(gridDim.x) * per) {
     uint64_t fp[QPT], b[QPT], d[QPT], off[QPT], len[QPT];
+    uint64_t kc[QPT][8];  // (keys <= kRegKey bytes: the needle's chunks, kept for the comparison)
     CDir rec[QPT];
 #pragma unroll
     for (int j = 0; j < QPT; j++) {
@@ -244,8 +284,11 @@ __global__ void __launch_bounds__(kLThreads) k_lookup_bytes(LookupParams lp, con
       if (idx < nq) {
         off[j] = qo[idx];
         len[j] = qo[idx + 1] - off[j];
-        fp[j] = fingerprint_pw64(qb, off[j], len[j], lp.r_fp, &s_pw);
       }
+      key_chunks(qb + off[j], len[j] <= kRegKey ? uint32_t(len[j]) : 0u, kc[j]);
+      if (idx < nq)
+        fp[j] = len[j] <= kRegKey ? fingerprint_chunks(kc[j], uint32_t(len[j]), &s_pw)
+                                  : fingerprint_pw64(qb, off[j], len[j], lp.r_fp, &s_pw);
     }
     uint32_t tag[QPT];
 #pragma unroll
@@ -282,7 +325,16 @@ __global__ void __launch_bounds__(kLThreads) k_lookup_bytes(LookupParams lp, con
       bool hit = false;
       uint64_t v = 0;
       if (e[j].key == fp[j] && e[j].len == len[j]) {
-        hit = bytes_equal64(lp.ctx + e[j].ctx_off, qb + off[j], e[j].len);
+        if (len[j] <= kRegKey) {
+          uint64_t mc[8];
+          key_chunks(lp.ctx + e[j].ctx_off, e[j].len, mc);
+          uint64_t diff = 0;
+#pragma unroll
+          for (int i = 0; i < 8; i++) diff |= mc[i] ^ kc[j][i];
+          hit = diff == 0;
+        } else {
+          hit = bytes_equal64(lp.ctx + e[j].ctx_off, qb + off[j], e[j].len);
+        }
         if (hit) v = e[j].value;
       }
       if (ov) ov[idx] = v;

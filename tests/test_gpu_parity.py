@@ -237,6 +237,61 @@ def test_bytes_edge_strings_and_offsets():
     assert e.value.name == "DUPLICATE_KEY"
 
 
+def test_bytes_every_length_and_alignment():
+    """Keys of every length 0..300 at every start alignment (the expanded
+    fingerprint's chunk tails, its 128-byte table limit and the Horner path
+    beyond it; warps whose byte range overflows the shared-memory stage)."""
+    hm = _hm()
+    rng = np.random.default_rng(11)
+    strs = []
+    for L in range(0, 301):
+        for _ in range(3):
+            strs.append(rng.integers(0, 256, size=L, dtype=np.uint8).tobytes() if L else b"")
+    strs = list(dict.fromkeys(strs))  # (distinct; b"" once)
+    strs += [b"\xff" * L for L in (1, 7, 8, 9, 63, 64, 65, 127, 128, 129)]
+    order = rng.permutation(len(strs))
+    strs = [strs[i] for i in order]
+    ctx, offs = gen.pack_bytes_list(strs)
+    vals = np.arange(1, len(strs) + 1, dtype=np.uint64)
+    ot = O.build_bytes(ctx, offs, vals, 4)
+    m = hm.HashMap.build_bytes(torch.from_numpy(ctx).cuda(), dev(offs), dev(vals), seed=4)
+    assert_table_equal(m, ot)
+    needles = strs + [s[:-1] + b"\x01" for s in strs if s] + [b"\xff" * 66]
+    qc, qo = gen.pack_bytes_list(needles)
+    ov, of = O.lookup_bytes(ot, qc, qo)
+    gv, gf = m.lookup_bytes(torch.from_numpy(qc).cuda(), dev(qo))
+    assert np.array_equal(host(gv), ov) and np.array_equal(host(gf), of)
+    m.free()
+
+
+@pytest.mark.parametrize("shift,prefix", [(3, 0), (3, 13), (8, 5), (0, 16), (0, 1)])
+def test_bytes_unaligned_context_pointer(shift, prefix):
+    """A key context that starts at any byte address (a tensor slice) with any
+    first offset: the fingerprint stage aligns by address, and the map's copy
+    of the context is written by the fingerprint kernel exactly when
+    bytes + offsets[0] is 16-aligned, else by a copy."""
+    hm = _hm()
+    ctx, offs = gen.string_keys(5000)
+    ctx2 = np.concatenate([np.full(prefix, 0x5A, np.uint8), ctx])
+    offs2 = offs + np.uint64(prefix)
+    vals = gen.u64_values(5000) + np.uint64(1)
+    base = torch.zeros(shift + len(ctx2) + 32, dtype=torch.uint8, device="cuda")
+    base[shift:shift + len(ctx2)] = torch.from_numpy(ctx2).cuda()
+    t = base[shift:shift + len(ctx2)]
+    ot = O.build_bytes(ctx2, offs2, vals, 2)
+    m = hm.HashMap.build_bytes(t, dev(offs2), dev(vals), seed=2)
+    assert_table_equal(m, ot)
+    base.fill_(0)  # the map holds its own copy
+    qc, qo, f, v = gen.string_queries(5000, 20_000)
+    qbase = torch.zeros(len(qc) + 40, dtype=torch.uint8, device="cuda")
+    qbase[shift + 5:shift + 5 + len(qc)] = torch.from_numpy(qc).cuda()
+    ov, of = O.lookup_bytes(ot, qc, qo)
+    gv, gf = m.lookup_bytes(qbase[shift + 5:shift + 5 + len(qc)], dev(qo))
+    assert np.array_equal(host(gv), ov) and np.array_equal(host(gf), of)
+    assert np.array_equal(host(gf).astype(bool), f)
+    m.free()
+
+
 @pytest.mark.parametrize("flags_name", ["FLAG_DIRECT_SLOTS", "FLAG_NO_ROUND0_ILP", "FLAG_ROUNDS"])
 @pytest.mark.parametrize("n,seed,log2_bp", [(5, 0, 0), (4133, 5, 0), (70_001, 3, 6), (300_007, 1, 0)])
 def test_u64_construction_routes_same_table(flags_name, n, seed, log2_bp):
