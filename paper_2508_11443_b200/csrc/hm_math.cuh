@@ -234,12 +234,14 @@ __device__ __forceinline__ uint64_t fingerprint_dev(const uint8_t* bytes, uint64
 // its own 64-bit sum with no reduction: a word costs three multiply-adds, and
 // 32 words keep every sum below 2^58.  fp3_finish folds the three sums once.
 // Keys longer than 4*kFpPowMax bytes take the Horner loop above.
-constexpr int kFpPowMax = 32;
+constexpr int kFpPowMax = 32, kFpPowPad = 16;
 struct FpPow {
+  uint4 z[kFpPowPad];      // zeros: exponents down to -16 read as 0 (chunks past a key, lookup.cu)
   uint4 p[kFpPowMax + 1];  // {l0, l1, l2, 0} of r^e
 };
 // One thread of the block fills the table; the caller synchronises.
 __device__ inline void fp_pow_fill(FpPow* pw, uint64_t r) {
+  for (int e = 0; e < kFpPowPad; e++) pw->z[e] = make_uint4(0u, 0u, 0u, 0u);
   uint64_t p = 1;
   for (int e = 0; e <= kFpPowMax; e++) {
     pw->p[e] = make_uint4(uint32_t(p & 0x1FFFFF), uint32_t((p >> 21) & 0x1FFFFF), uint32_t(p >> 42), 0u);

@@ -242,17 +242,17 @@ __device__ __forceinline__ void key_chunks(const uint8_t* p, uint32_t len, uint6
   }
 }
 // fingerprint_pw64 of a key held as chunks (len <= 64): chunk i carries words
-// 2i and 2i+1, weighted r^(nw-2i) and r^(nw-2i-1); chunks past the key are 0.
+// 2i and 2i+1, weighted r^(nw-2i) and r^(nw-2i-1).  Branch-free: chunks past
+// the key are 0 and their exponents (down to -15) read the table's zero pad;
+// len = 0 gives 0 as fingerprint_pw64 does.
 __device__ __forceinline__ uint64_t fingerprint_chunks(const uint64_t (&c)[8], uint32_t len, const FpPow* pw) {
-  if (len == 0) return 0;
-  const int nw = int(len + 3) >> 2;
+  // P[-k] = r^(nw-k), 0 below r^0 (the pad: FpPow is one array of uint4)
+  const uint4* P = reinterpret_cast<const uint4*>(pw) + kFpPowPad + ((len + 3) >> 2);
   uint64_t a0 = 0, a1 = 0, a2 = 0;
 #pragma unroll
   for (int i = 0; i < 8; i++) {
-    if (8 * i < int(len)) {
-      fp3_acc(a0, a1, a2, uint32_t(c[i]), pw->p[nw - 2 * i]);
-      fp3_acc(a0, a1, a2, uint32_t(c[i] >> 32), pw->p[max(nw - 2 * i - 1, 0)]);
-    }
+    fp3_acc(a0, a1, a2, uint32_t(c[i]), P[-2 * i]);
+    fp3_acc(a0, a1, a2, uint32_t(c[i] >> 32), P[-2 * i - 1]);
   }
   return fp3_finish(a0, a1, a2, len);
 }
