@@ -516,6 +516,13 @@ __global__ void __launch_bounds__(kSThreads, HM_SPLIT_MINB) k_split(Src src, Bui
 //          and the compact directory.
 constexpr int kNCls = 3;
 
+__device__ __forceinline__ uint4 ld_stream_u4(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -912,6 +919,32 @@ __global__ void __launch_bounds__(KBCfg<E>::T, KBCfg<E>::MINB)
           : "memory");
     } else {
       asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&s_bar)) : "memory");
+    }
+  }
+  if constexpr (sizeof(E) == sizeof(KV32)) {  // (byte-key builds only)
+    if (bp.cp_bytes && warp != 0) {
+      // the side copy (BuildParams::cp_*): this partition's slice, 16-byte
+      // units, HM_CP_UNROLL loads in flight per thread, streaming stores
+#ifndef HM_CP_UNROLL
+#define HM_CP_UNROLL 8
+#endif
+      constexpr int U = HM_CP_UNROLL;
+      const uint64_t a = uint64_t(p) * bp.cp_slice, b = min(a + bp.cp_slice, bp.cp_bytes);
+      const uint32_t nt = KBCfg<E>::T - 32;
+      const uint4* src4 = reinterpret_cast<const uint4*>(bp.cp_src);
+      uint4* dst4 = reinterpret_cast<uint4*>(bp.cp_dst);
+      const uint64_t u0 = a >> 4, u1 = b >> 4;  // (full units; a is 16-aligned)
+      for (uint64_t u = u0 + (tid - 32); u < u1; u += uint64_t(U) * nt) {
+        uint4 v[U];
+#pragma unroll
+        for (int k = 0; k < U; k++)
+          if (u + uint64_t(k) * nt < u1) v[k] = ld_stream_u4(src4 + u + uint64_t(k) * nt);
+#pragma unroll
+        for (int k = 0; k < U; k++)
+          if (u + uint64_t(k) * nt < u1) __stcs(dst4 + u + uint64_t(k) * nt, v[k]);
+      }
+      if (b == bp.cp_bytes && (b & 15) && tid >= 32 && tid < 32 + (b & 15))  // (the last partial unit)
+        bp.cp_dst[(b & ~uint64_t(15)) + (tid - 32)] = bp.cp_src[(b & ~uint64_t(15)) + (tid - 32)];
     }
   }
   if (warp == 0) {  // the other warps wait at the CTA barrier (no issue slots)
@@ -1504,7 +1537,7 @@ hm_status release_workspace() {
 template <class Src, class E, class Same>
 static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global, uint64_t b_lo, uint64_t nb,
                             int t1_fixed, uint64_t seed, uint32_t log2_req, cudaStream_t st, BuildOut* out,
-                            bool* fpcoll) {
+                            bool* fpcoll, SideJob* job = nullptr) {
   *fpcoll = false;
   int dev = 0;
   HM_CUDA_TRY(cudaGetDevice(&dev));
@@ -1651,6 +1684,16 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
         HM_CUDA_TRY(cudaGetLastError());
       }
       run_a = false;
+      bp.cp_bytes = 0;
+      if (job && !job->done && job->kbytes) {
+        bp.cp_src = job->ksrc;
+        bp.cp_dst = job->kdst;
+        bp.cp_bytes = job->kbytes;
+        bp.cp_slice = ((job->kbytes + pl.np - 1) / pl.np + 15) & ~uint64_t(15);
+        job->done = true;
+      } else if (job) {
+        job->run(st);
+      }
       {
         LaunchScope ls_("k_bucket", st);
         kB<<<pl.np, KBCfg<E>::T, pl.smemB, st>>>(bp, pbuf, plb, pcount, lbstate, dir, cdir, slots, dstat, same);
@@ -1924,14 +1967,16 @@ hm_status check_offsets(const uint64_t* offsets, uint64_t n, cudaStream_t st) {
 // (the caller has validated the offsets with check_offsets)
 hm_status build_bytes_core(const uint8_t* bytes, const uint64_t* offsets, const uint64_t* vals, uint64_t n,
                            uint64_t seed, uint32_t log2_bp, cudaStream_t st, BuildOut* out, uint32_t* t0_out,
-                           uint64_t* r_out) {
+                           uint64_t* r_out, SideJob* job, const uint64_t* off0_host) {
   Scratch sc{st};
   uint64_t* fp = nullptr;
   hm_status s;
   if ((s = sc.alloc(WS_FP, &fp, n * 8)) != HM_OK) return s;
-  uint64_t off0 = 0;
-  HM_CUDA_TRY(cudaMemcpyAsync(&off0, offsets, 8, cudaMemcpyDeviceToHost, st));
-  HM_CUDA_TRY(cudaStreamSynchronize(st));
+  uint64_t off0 = off0_host ? *off0_host : 0;
+  if (!off0_host) {
+    HM_CUDA_TRY(cudaMemcpyAsync(&off0, offsets, 8, cudaMemcpyDeviceToHost, st));
+    HM_CUDA_TRY(cudaStreamSynchronize(st));
+  }
   const uint64_t smix = seed_mix(seed);
   for (uint32_t t0 = 0; t0 < kT0Cap; t0++) {
     const uint64_t r = derive(smix, 0, 0, t0).a1;
@@ -1939,7 +1984,7 @@ hm_status build_bytes_core(const uint8_t* bytes, const uint64_t* offsets, const 
     HM_CUDA_TRY(cudaGetLastError());
     bool fpc = false;
     s = build_core<SrcBytes, KV32, SameBytes>(SrcBytes{fp, vals, offsets, off0}, SameBytes{bytes, off0}, n, n, 0, n,
-                                               -1, seed, log2_bp, st, out, &fpc);
+                                               -1, seed, log2_bp, st, out, &fpc, job);
     if (s == HM_ERR_TOO_LARGE) {
       // a degenerate level-1 distribution within the space bound (a bucket of
       // more than 32 keys, an overflowing build partition): the flat rounds

@@ -422,30 +422,69 @@ hm_status hm_build_bytes(const uint8_t* bytes, const uint64_t* offsets, const ui
     if (tl_user_alloc.free) tl_user_alloc.free(ctxc, ctx_alloc, stream, tl_user_alloc.ctx);
     else cudaFreeAsync(ctxc, st);
   };
-  cudaEvent_t ev_in = nullptr, ev_copied = nullptr;
+  // The copy happens inside the first k_bucket launch (its warps copy a slice
+  // each while the partition's bulk load is in flight), or, for a context not
+  // 16-aligned, as a copy on a library stream enqueued right before k_bucket
+  // (SideJob): either way it overlaps the latency-bound k_bucket instead of
+  // competing with the bandwidth-bound fingerprint and radix passes
+  // (DESIGN.md §6.4).
+  struct CtxCopy {
+    uint8_t* dst;
+    const uint8_t* src;
+    uint64_t bytes;
+    cudaStream_t cs;
+    cudaEvent_t ev_in, ev_copied;
+    cudaError_t err;
+  } cc{ctxc, db + o0, ctx_bytes, nullptr, nullptr, nullptr, cudaSuccess};
   {
-    cudaStream_t cs, unused;
-    hm_status s2 = copy_streams(&cs, &unused);
-    cudaError_t e = s2 == HM_OK ? cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming) : cudaErrorUnknown;
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_copied, cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaEventRecord(ev_in, st);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ev_in, 0);
-    if (e == cudaSuccess && ctx_bytes) e = cudaMemcpyAsync(ctxc, db + o0, ctx_bytes, cudaMemcpyDeviceToDevice, cs);
-    if (e == cudaSuccess) e = cudaEventRecord(ev_copied, cs);
+    cudaStream_t unused;
+    hm_status s2 = copy_streams(&cc.cs, &unused);
+    cudaError_t e = s2 == HM_OK ? cudaEventCreateWithFlags(&cc.ev_in, cudaEventDisableTiming) : cudaErrorUnknown;
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&cc.ev_copied, cudaEventDisableTiming);
     if (e != cudaSuccess) {
-      if (ev_in) cudaEventDestroy(ev_in);
-      if (ev_copied) cudaEventDestroy(ev_copied);
+      if (cc.ev_in) cudaEventDestroy(cc.ev_in);
+      if (cc.ev_copied) cudaEventDestroy(cc.ev_copied);
       free_ctx();
       return cuda_fail(e, "context copy");
     }
   }
+  SideJob job;
+  if (ctx_bytes && (reinterpret_cast<uintptr_t>(db + o0) & 15) == 0) {  // (ctxc: 256-aligned)
+    job.ksrc = db + o0;
+    job.kdst = ctxc;
+    job.kbytes = ctx_bytes;
+  }
+  job.ctx = &cc;
+  job.fn = [](void* p, cudaStream_t s_) {
+    CtxCopy* c = static_cast<CtxCopy*>(p);
+    cudaError_t e = cudaEventRecord(c->ev_in, s_);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(c->cs, c->ev_in, 0);
+#ifndef HM_DEBUG_NO_CTX_COPY  // (timing experiments only: the map's context stays unwritten)
+    if (e == cudaSuccess && c->bytes) e = cudaMemcpyAsync(c->dst, c->src, c->bytes, cudaMemcpyDeviceToDevice, c->cs);
+#endif
+    if (e == cudaSuccess) e = cudaEventRecord(c->ev_copied, c->cs);
+    c->err = e;
+  };
   BuildOut bo;
   uint32_t t0 = 0;
   uint64_t r = 0;
-  s = build_bytes_core(db, doff, dv, n, seed, opts ? (opts->log2_bp | (opts->flags << 16)) : 0, st, &bo, &t0, &r);
-  cudaStreamWaitEvent(st, ev_copied, 0);  // (the copy has read db before its staging is freed)
-  cudaEventDestroy(ev_in);
-  cudaEventDestroy(ev_copied);
+  s = build_bytes_core(db, doff, dv, n, seed, opts ? (opts->log2_bp | (opts->flags << 16)) : 0, st, &bo, &t0, &r,
+                       &job, &o0);
+  const bool in_kernel = job.done && job.kbytes;  // (k_bucket copied the context)
+  if (s == HM_OK && !job.done) {  // (a build that never reached k_bucket)
+    job.kbytes = 0;
+    job.run(st);
+  }
+  if (job.done && !in_kernel) cudaStreamWaitEvent(st, cc.ev_copied, 0);  // (the copy read db before its staging is freed)
+  cudaEventDestroy(cc.ev_in);
+  cudaEventDestroy(cc.ev_copied);
+  if (s == HM_OK && cc.err != cudaSuccess) {
+    map_discard(bo.dir, bo.bytes[0], st);
+    map_discard(bo.cdir, bo.bytes[1], st);
+    map_discard(bo.slots, bo.bytes[2], st);
+    free_ctx();
+    return cuda_fail(cc.err, "context copy");
+  }
   if (s != HM_OK) {
     free_ctx();
     return s;

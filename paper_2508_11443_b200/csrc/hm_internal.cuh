@@ -60,6 +60,12 @@ struct BuildParams {
   uint32_t flags;     // HM_FLAG_* (hm.h)
   BucketSmem sl;      // k_bucket shared-memory layout
   uint64_t m2[33];    // floor((2^64 - 1) / s^2) for the exact mod s^2 (R22), s <= 32
+  // a side copy k_bucket does while its first warp waits for the partition's
+  // bulk load (the byte-key context, SideJob): partition p copies bytes
+  // [p*cp_slice, (p+1)*cp_slice) of cp_src to cp_dst (both 16-aligned)
+  const uint8_t* cp_src;
+  uint8_t* cp_dst;
+  uint64_t cp_bytes, cp_slice;
 };
 
 struct LookupParams {
@@ -117,6 +123,24 @@ struct LaunchScope {
 };
 
 // build.cu
+// Work a build enqueues once, on its stream, right before the first k_bucket
+// launch (the radix passes are done): the byte-key build copies the key
+// context then, so that the copy shares DRAM with the latency-bound k_bucket
+// rather than with the bandwidth-bound fingerprint and radix passes.
+struct SideJob {
+  void (*fn)(void* ctx, cudaStream_t st) = nullptr;
+  void* ctx = nullptr;
+  // or, with kbytes set, a copy done inside the first k_bucket launch
+  // (BuildParams::cp_*; 16-aligned pointers)
+  const uint8_t* ksrc = nullptr;
+  uint8_t* kdst = nullptr;
+  uint64_t kbytes = 0;
+  bool done = false;
+  void run(cudaStream_t st) {
+    if (fn && !done) fn(ctx, st);
+    done = true;
+  }
+};
 struct BuildOut {
   uint64_t* dir = nullptr;
   CDir* cdir = nullptr;
@@ -155,7 +179,7 @@ hm_status build_u64_core(const uint64_t* keys, const uint64_t* vals, uint64_t n_
 hm_status check_offsets(const uint64_t* offsets, uint64_t n, cudaStream_t st);
 hm_status build_bytes_core(const uint8_t* bytes, const uint64_t* offsets, const uint64_t* vals, uint64_t n,
                            uint64_t seed, uint32_t log2_bp, cudaStream_t st, BuildOut* out, uint32_t* t0_out,
-                           uint64_t* r_out);
+                           uint64_t* r_out, SideJob* job = nullptr, const uint64_t* off0_host = nullptr);
 hm_status dedup_workspace(void** p, size_t bytes, cudaStream_t st);  // build.cu's cached scratch
 hm_status dedup_partitioned_bytes(const uint8_t* bytes, const uint64_t* offs, const uint64_t* fp,
                                   const uint64_t* vals, uint64_t n, uint64_t off0, cudaStream_t st, uint8_t* keep);
