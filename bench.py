@@ -505,7 +505,7 @@ def run_ours(args):
             units, bpu, what = n * args.steps / launches_dom, LOOKUP_BYTES_PER_QUERY, "queries"
         elif dom in ("k_partition", "k_split1", "k_split2"):
             units, bpu, what = n * args.steps / launches_dom, 32.0, "keys"  # read + write a 16-byte record
-        else:  # k_bucket: read the partition (16), write dir (8) + slots (16 S/n)
+        else:  # k_bucket / k_split2_bucket: read the partition (16), write dir (8) + slots (16 S/n)
             units, bpu, what = n * args.steps / launches_dom, 16.0 + 8.0 + 16.0 * s_over_n, "keys"
         achieved = units * bpu / (avg_ms / 1e3) / 1e9
         traffic = None

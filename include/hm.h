@@ -69,7 +69,7 @@ typedef void (*hm_free_fn)(void* ptr, size_t bytes, void* stream, void* ctx);
 
 typedef struct {
   uint64_t seed;       /* table seed: selects the constant schedule (R6). default 0  */
-  uint32_t log2_bp;    /* 0 = auto. log2 of the level-1 buckets per build partition   */
+  uint32_t log2_bp;    /* 0 = auto. log2 of the level-1 buckets per build partition (5..12; smaller values act as 5) */
   uint32_t flags;      /* 0, or HM_FLAG_* below; other bits -> HM_ERR_INVALID_ARG     */
   /* NULL, NULL: the library's stream-ordered pool (cudaMallocAsync, with freed
    * maps' arrays cached per size, see hm_release_workspace).  Both set: every
@@ -95,6 +95,15 @@ typedef struct {
  * leaves the rest to the lane-parallel rounds. */
 #define HM_FLAG_DIRECT_SLOTS 2u
 #define HM_FLAG_NO_ROUND0_ILP 4u
+/* Alternative route of the u64 construction (same table): radix pass 2 and
+ * the per-partition construction as one pipelined kernel (k_split2_bucket):
+ * a partition job takes its records from L2 right after the pass-2 tiles of
+ * its region wrote them and drops the lines there without write-back (the
+ * build's DRAM traffic falls by ~2 GB per 2^26 keys), but the two job kinds
+ * sharing the SMs issue more slowly than the two kernels (measured 3.05 vs
+ * 2.70 ms at 2^26), so it is not the default.  Byte keys ignore
+ * it. */
+#define HM_FLAG_FUSED_PASS2 64u
 /* from_array: the keys may repeat;
  * the first occurrence (lowest input index) of every key keeps its value, and
  * the map is the one the default build (from_array_nodup) makes from the

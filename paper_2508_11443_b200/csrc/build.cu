@@ -89,6 +89,12 @@ struct Items {
 #ifndef HM_SMEM_ALIAS
 #define HM_SMEM_ALIAS 0  // k_bucket: alias rk with the rounds' lists and sA with the slot source map
 #endif
+#ifndef HM_FUSED_DISCARD
+#define HM_FUSED_DISCARD 1  // k_split2_bucket: drop a consumed partition's L2 lines without write-back
+#endif
+#ifndef HM_FUSED_D
+#define HM_FUSED_D 1  // k_split2_bucket: pass-2 tiles run D coarse regions ahead of the partitions
+#endif
 #ifndef HM_PF_DIST
 #define HM_PF_DIST 148  // k_bucket: L2 prefetch of partition p + HM_PF_DIST (0: off; 148 measured best)
 #endif
@@ -181,6 +187,16 @@ struct SameBytes {
 // ------------------------------------------------------------- primitives
 __device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_u32(const unsigned int* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const unsigned int* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
 }
 __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
   unsigned long long v;
@@ -396,10 +412,11 @@ struct SplitArgs {
   uint16_t* dst_lb;   // pass 2: the record's local bucket | tag4 << 12 for k_bucket (nullptr: none)
 };
 
+// One tile of a radix pass (bid: the tile; pass 2: coarse region bid / tpc,
+// tile bid % tpc of it).  Also a job of the fused pass-2 + k_bucket kernel.
 template <class Src, class E, int PASS, int BITS>
-__global__ void __launch_bounds__(kSThreads, HM_SPLIT_MINB) k_split(Src src, BuildParams bp, SplitArgs a,
-                                                        DevStatus* __restrict__ stt) {
-  extern __shared__ __align__(16) uint8_t smem[];
+__device__ __forceinline__ void split_tile_body(const Src& src, const BuildParams& bp, const SplitArgs& a,
+                                                DevStatus* __restrict__ stt, uint32_t bid, uint8_t* smem) {
   constexpr int kSDigits = 1 << BITS, kSBits = BITS, kSPT = split_pt<E>(), kSTile = split_tile<E>();
   E* stage = reinterpret_cast<E*>(smem);
   uint16_t* sdig = reinterpret_cast<uint16_t*>(smem + size_t(kSTile) * sizeof(E));
@@ -414,11 +431,11 @@ __global__ void __launch_bounds__(kSThreads, HM_SPLIT_MINB) k_split(Src src, Bui
   uint32_t nvalid, coarse = 0;
   const E* cb = reinterpret_cast<const E*>(a.cbuf);
   if (PASS == 1) {
-    base = uint64_t(blockIdx.x) * kSTile;
+    base = uint64_t(bid) * kSTile;
     nvalid = bp.n_in - base < uint64_t(kSTile) ? uint32_t(bp.n_in - base) : uint32_t(kSTile);
   } else {
-    coarse = blockIdx.x / a.tpc;
-    const uint32_t k = blockIdx.x % a.tpc;
+    coarse = bid / a.tpc;
+    const uint32_t k = bid % a.tpc;
     const uint32_t cc = min(a.ccount[coarse], a.ccap);
     base = uint64_t(k) * kSTile;
     nvalid = cc > base ? (cc - base < uint64_t(kSTile) ? uint32_t(cc - base) : uint32_t(kSTile)) : 0u;
@@ -494,6 +511,13 @@ __global__ void __launch_bounds__(kSThreads, HM_SPLIT_MINB) k_split(Src src, Bui
   }
   if (ovf) atomicOr(&stt->part_overflow, 1u);
   if (bad) atomicOr(&stt->pad, 1u);
+}
+
+template <class Src, class E, int PASS, int BITS>
+__global__ void __launch_bounds__(kSThreads, HM_SPLIT_MINB) k_split(Src src, BuildParams bp, SplitArgs a,
+                                                        DevStatus* __restrict__ stt) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  split_tile_body<Src, E, PASS, BITS>(src, bp, a, stt, blockIdx.x, smem);
 }
 
 // ------------------------------------------------------------------ K_B
@@ -829,13 +853,18 @@ __device__ __forceinline__ void block_excl_scan2(unsigned long long& a, unsigned
   b = bb + y - b;
 }
 
-template <class E, class Same>
-__global__ void __launch_bounds__(KBCfg<E>::T, KBCfg<E>::MINB)
-    k_bucket(BuildParams bp, const E* __restrict__ pbuf, const uint16_t* __restrict__ plb,
-             const unsigned int* __restrict__ pcount,
-             unsigned long long* __restrict__ lbstate, uint64_t* __restrict__ dir, CDir* __restrict__ cdir,
-             E* __restrict__ slots, DevStatus* __restrict__ stt, Same same) {
-  extern __shared__ __align__(16) uint8_t smem[];
+// kFused: a job of k_split2_bucket — partition p_given, whose records pass 2
+// is writing in the same kernel: wait until the tiles of its coarse region
+// are all done (*sdone_c == tpc), and drop the partition's L2 lines without
+// write-back once they are in shared memory (discard.global.L2: nothing reads
+// them again).  Otherwise the partition is the next ticket.
+template <class E, class Same, bool kFused>
+__device__ __forceinline__ void bucket_body(const BuildParams& bp, const E* __restrict__ pbuf,
+                                            const uint16_t* __restrict__ plb, const unsigned int* pcount,
+                                            unsigned long long* __restrict__ lbstate, uint64_t* __restrict__ dir,
+                                            CDir* __restrict__ cdir, E* __restrict__ slots,
+                                            DevStatus* __restrict__ stt, const Same& same, uint8_t* smem,
+                                            uint32_t p_given, const unsigned int* sdone_c, uint32_t tpc) {
   __shared__ uint64_t s_m2[33];
   __shared__ __align__(8) unsigned long long s_bar;
   __shared__ uint32_t s_p;
@@ -864,7 +893,16 @@ __global__ void __launch_bounds__(KBCfg<E>::T, KBCfg<E>::MINB)
   const uint32_t lcap = cap / 2 + 1;
 
   if (tid == 0) {
-    s_p = atomicAdd(&stt->ticket, 1u);
+    if (kFused) {
+      s_p = p_given;
+      // the coarse region's pass-2 tiles (release: __threadfence + atomicAdd
+      // after their stores); then the bulk copy (async proxy) may read them
+      uint32_t d;
+      while ((d = ld_acquire_u32(sdone_c)) < tpc) __nanosleep(128);
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+    } else {
+      s_p = atomicAdd(&stt->ticket, 1u);
+    }
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_bar)));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     s_c9 = 0;
@@ -881,7 +919,7 @@ __global__ void __launch_bounds__(KBCfg<E>::T, KBCfg<E>::MINB)
   HM_TMARK(0);
   const uint64_t lb0 = uint64_t(p) << bp.log2_bp;
   const uint32_t nbp = uint32_t(bp.nb - lb0 < uint64_t(BP) ? bp.nb - lb0 : uint64_t(BP));
-  const uint32_t cnt_raw = pcount[p];
+  const uint32_t cnt_raw = kFused ? ld_relaxed_u32(pcount + p) : pcount[p];
   const bool ovf = cnt_raw > cap;
   const uint32_t cnt = ovf ? 0u : cnt_raw;
   const uint64_t bbase = bp.b_lo + lb0;  // global id of the partition's first bucket
@@ -890,7 +928,7 @@ __global__ void __launch_bounds__(KBCfg<E>::T, KBCfg<E>::MINB)
 #if HM_PF_DIST
   // (and an L2 prefetch of the partition a CTA takes about a wave later, so
   // that its load finds the lines in L2)
-  if (tid == 32 && p + HM_PF_DIST < bp.np) {
+  if (!kFused && tid == 32 && p + HM_PF_DIST < bp.np) {
     const uint32_t q = p + HM_PF_DIST, cq = min(pcount[q], cap);
     const uint32_t qb = (cq * uint32_t(sizeof(E)) + 15u) & ~15u, ql = ((cq + 7) & ~7u) * 2;
     if (qb)
@@ -960,6 +998,19 @@ __global__ void __launch_bounds__(KBCfg<E>::T, KBCfg<E>::MINB)
   }
   __syncthreads();
   HM_TMARK(1);
+  if (kFused && HM_FUSED_DISCARD) {
+    // the partition's records and codes are in shared memory: drop their L2
+    // lines (only lines wholly inside this partition's buffer regions)
+    auto drop = [&](const void* b0, size_t region, size_t used) {
+      const uintptr_t a = reinterpret_cast<uintptr_t>(b0);
+      const uintptr_t lo = (a + 127) & ~uintptr_t(127), hi = (a + region) & ~uintptr_t(127);
+      const uintptr_t end = min(hi, (a + used + 127) & ~uintptr_t(127));
+      for (uintptr_t x = lo + uintptr_t(tid) * 128; x < end; x += uintptr_t(KBCfg<E>::T) * 128)
+        asm volatile("discard.global.L2 [%0], 128;" ::"l"(x) : "memory");
+    };
+    drop(prec, size_t(cap) * sizeof(E), size_t(cnt) * sizeof(E));
+    drop(plb + size_t(p) * cap, size_t(cap) * 2, size_t(cnt) * 2);
+  }
 
   // ---- hist: the local bucket of g k and the
   // key's tag came with the record from the partition pass (k_split pass 2 /
@@ -1310,6 +1361,75 @@ __global__ void __launch_bounds__(KBCfg<E>::T, KBCfg<E>::MINB)
   HM_TMARK(7);
 }
 
+template <class E, class Same>
+__global__ void __launch_bounds__(KBCfg<E>::T, KBCfg<E>::MINB)
+    k_bucket(BuildParams bp, const E* __restrict__ pbuf, const uint16_t* __restrict__ plb,
+             const unsigned int* __restrict__ pcount,
+             unsigned long long* __restrict__ lbstate, uint64_t* __restrict__ dir, CDir* __restrict__ cdir,
+             E* __restrict__ slots, DevStatus* __restrict__ stt, Same same) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  bucket_body<E, Same, false>(bp, pbuf, plb, pcount, lbstate, dir, cdir, slots, stt, same, smem, 0, nullptr, 0);
+}
+
+// The fused pass 2 + k_bucket pipeline (u64 keys, HM_FLAG_FUSED_PASS2): one kernel whose CTAs take
+// jobs in ticket order — the pass-2 tiles of coarse region c + D come before the
+// k_bucket partitions of region c — so that a region's partitions are consumed
+// from L2 shortly after pass 2 wrote them (and discarded there), and the
+// bandwidth-bound tiles run beside the issue-bound partitions on the same SMs.
+// A partition job waits for its region's tiles (per-region done counters);
+// every job it can wait for holds an earlier ticket, so the wait always ends.
+struct FuseArgs {
+  unsigned int* sdone;  // per coarse region: pass-2 tiles finished
+  uint32_t R, tpc, sdig, D;
+};
+__device__ __forceinline__ void fused_job(const FuseArgs& f, uint32_t j, bool* split, uint32_t* x) {
+  const uint32_t D = min(f.D, f.R), pre = D * f.tpc;
+  if (j < pre) {
+    *split = true;
+    *x = j;  // region j / tpc, tile j % tpc
+    return;
+  }
+  j -= pre;
+  const uint32_t full = f.R - D, seg = f.tpc + f.sdig;
+  if (j < full * seg) {
+    const uint32_t k = j / seg, r = j % seg;
+    *split = r < f.tpc;
+    *x = *split ? (k + D) * f.tpc + r : k * f.sdig + (r - f.tpc);
+    return;
+  }
+  j -= full * seg;
+  *split = false;
+  *x = (full + j / f.sdig) * f.sdig + j % f.sdig;
+}
+
+template <class Src, class E, class Same, int BITS>
+__global__ void __launch_bounds__(KBCfg<E>::T, KBCfg<E>::MINB)
+    k_split2_bucket(Src src, BuildParams bp, SplitArgs a, FuseArgs f, const E* __restrict__ pbuf,
+                    const uint16_t* __restrict__ plb, const unsigned int* pcount,
+                    unsigned long long* __restrict__ lbstate, uint64_t* __restrict__ dir, CDir* __restrict__ cdir,
+                    E* __restrict__ slots, DevStatus* __restrict__ stt, Same same) {
+  static_assert(KBCfg<E>::T == kSThreads, "one block size for both job kinds");
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ uint32_t s_job;
+  if (threadIdx.x == 0) s_job = atomicAdd(&stt->ticket, 1u);
+  __syncthreads();
+  bool split;
+  uint32_t x;
+  fused_job(f, s_job, &split, &x);
+  if (split) {
+    split_tile_body<Src, E, 2, BITS>(src, bp, a, stt, x, smem);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(&f.sdone[x / f.tpc], 1u);
+    }
+    return;
+  }
+  if (x >= bp.np) return;
+  bucket_body<E, Same, true>(bp, pbuf, plb, pcount, lbstate, dir, cdir, slots, stt, same, smem, x,
+                             f.sdone + x / f.sdig, f.tpc);
+}
+
 // ------------------------------------------------------- overflow check
 // A build partition that overflowed its buffer (a degenerate level-1
 // distribution: many equal keys, or an adversarial key set) lost records, so
@@ -1355,7 +1475,9 @@ static Plan make_plan(uint64_t n_in, uint64_t nb, uint32_t log2_req, uint32_t es
                       size_t smem_one) {
   Plan pl{};
   const int sms = num_sms();
-  uint32_t lg = log2_req ? std::min<uint32_t>(log2_req, 12u) : 12u;
+  // (at least 2^5 buckets: a compact-directory record covers 32 buckets and
+  // is written by the one partition that holds them)
+  uint32_t lg = log2_req ? std::min<uint32_t>(std::max<uint32_t>(log2_req, 5u), 12u) : 12u;
   const size_t limit = log2_req ? smem_one : smem_two;
   if (!log2_req) {
     while (lg > 6 && (nb >> lg) < uint64_t(4 * sms)) lg--;
@@ -1366,7 +1488,7 @@ static Plan make_plan(uint64_t n_in, uint64_t nb, uint32_t log2_req, uint32_t es
     double c = m + 8.0 * std::sqrt(std::max(m, 1.0)) + 64.0;
     uint32_t cap = uint32_t(std::min(16383.0, std::ceil(c / 32.0) * 32.0));
     const size_t sm = bucket_smem_bytes(cap, lg, esz);
-    if ((sm <= limit && c <= 16383.0) || lg <= 1) {
+    if ((sm <= limit && c <= 16383.0) || lg <= 5) {
       pl.log2_bp = lg;
       pl.cap = cap;
       pl.smemB = sm;
@@ -1397,7 +1519,7 @@ static hm_status dmalloc(T** p, size_t bytes, cudaStream_t st) {
 // maps' own arrays), so they stay allocated until hm_release_workspace().
 // Reuse is safe because everything that touches a stream's workspace is
 // ordered on that stream.
-enum WsRole { WS_FP, WS_BAD, WS_PBUF, WS_PLB, WS_PCOUNT, WS_LBSTATE, WS_DSTAT, WS_CBUF, WS_CCOUNT, WS_DEDUP, WS_NROLES };
+enum WsRole { WS_FP, WS_BAD, WS_PBUF, WS_PLB, WS_PCOUNT, WS_LBSTATE, WS_DSTAT, WS_CBUF, WS_CCOUNT, WS_DEDUP, WS_SDONE, WS_NROLES };
 struct Workspace {
   void* p[WS_NROLES] = {};
   size_t bytes[WS_NROLES] = {};
@@ -1550,6 +1672,11 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
     cudaFuncAttributes fa{};
     if (cudaFuncGetAttributes(&fa, k_bucket<E, Same>) == cudaSuccess) static_smem_B = fa.sharedSizeBytes;
     else cudaGetLastError();
+    if constexpr (sizeof(E) == sizeof(KV16)) {  // (the fused kernel holds pass 2's static arrays too)
+      if (cudaFuncGetAttributes(&fa, k_split2_bucket<Src, E, Same, 9>) == cudaSuccess)
+        static_smem_B = std::max<size_t>(static_smem_B, fa.sharedSizeBytes);
+      else cudaGetLastError();
+    }
   }
   const uint32_t knob_flags = log2_req >> 16;
   log2_req &= 0xFFFFu;
@@ -1637,6 +1764,17 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
     HM_CUDA_TRY(cudaFuncSetAttribute(kS1, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smemS)));
     HM_CUDA_TRY(cudaFuncSetAttribute(kS2, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smemS)));
   }
+  // u64 keys: pass 2 and k_bucket as one pipelined kernel (k_split2_bucket)
+  const bool fused = two_pass && sizeof(E) == sizeof(KV16) && !job && (knob_flags & HM_FLAG_FUSED_PASS2);
+  const size_t smemF = std::max(smemS, pl.smemB);
+  unsigned int* sdone = nullptr;
+  if constexpr (sizeof(E) == sizeof(KV16)) {
+    if (fused) {
+      auto kF = sbits == 8 ? k_split2_bucket<Src, E, Same, 8> : k_split2_bucket<Src, E, Same, 9>;
+      if ((s = sc.alloc(WS_SDONE, &sdone, size_t(ncoarse) * 4)) != HM_OK) return fail(s);
+      HM_CUDA_TRY(cudaFuncSetAttribute(kF, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smemF)));
+    }
+  }
   BuildParams bp{};
   bp.smix = smix;
   bp.b_lo = b_lo;
@@ -1669,8 +1807,8 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
           kS1<<<unsigned((n_in + kSTile - 1) / kSTile), kSThreads, smemS, st>>>(src, bp, a1, dstat);
         }
         HM_CUDA_TRY(cudaGetLastError());
-        const SplitArgs a2{cbuf, ccount, ccap, tpc, pbuf, pcount, pl.cap, pl.np, ncoarse, plb};
-        {
+        if (!fused) {
+          const SplitArgs a2{cbuf, ccount, ccap, tpc, pbuf, pcount, pl.cap, pl.np, ncoarse, plb};
           LaunchScope ls_("k_split2", st);
           kS2<<<ncoarse * tpc, kSThreads, smemS, st>>>(src, bp, a2, dstat);
         }
@@ -1694,7 +1832,20 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
       } else if (job) {
         job->run(st);
       }
-      {
+      if (fused) {
+        // (a rerun after a slot overflow repeats pass 2 too: the partitions were
+        // dropped from L2 as they were consumed; the coarse buffer is intact)
+        if (pass > 0) HM_CUDA_TRY(cudaMemsetAsync(pcount, 0, size_t(pl.np) * 4, st));
+        HM_CUDA_TRY(cudaMemsetAsync(sdone, 0, size_t(ncoarse) * 4, st));
+        const SplitArgs a2{cbuf, ccount, ccap, tpc, pbuf, pcount, pl.cap, pl.np, ncoarse, plb};
+        const FuseArgs fa{sdone, ncoarse, tpc, sdig, uint32_t(HM_FUSED_D)};
+        if constexpr (sizeof(E) == sizeof(KV16)) {
+          auto kF = sbits == 8 ? k_split2_bucket<Src, E, Same, 8> : k_split2_bucket<Src, E, Same, 9>;
+          LaunchScope ls_("k_split2_bucket", st);
+          kF<<<ncoarse * (tpc + sdig), KBCfg<E>::T, smemF, st>>>(src, bp, a2, fa, pbuf, plb, pcount, lbstate, dir,
+                                                                  cdir, slots, dstat, same);
+        }
+      } else {
         LaunchScope ls_("k_bucket", st);
         kB<<<pl.np, KBCfg<E>::T, pl.smemB, st>>>(bp, pbuf, plb, pcount, lbstate, dir, cdir, slots, dstat, same);
       }

@@ -283,7 +283,7 @@ hm_status hm_build_u64(const uint64_t* keys, const uint64_t* vals, uint64_t n, c
   if (!keys || !vals) return HM_ERR_INVALID_ARG;
   if (n > (1ull << 30)) return HM_ERR_TOO_LARGE;
   if (opts && (opts->flags & ~uint32_t(HM_FLAG_FULL_DIRECTORY | HM_FLAG_DIRECT_SLOTS | HM_FLAG_NO_ROUND0_ILP |
-                                         HM_FLAG_FROM_ARRAY | HM_FLAG_ROUNDS)))
+                                         HM_FLAG_FROM_ARRAY | HM_FLAG_ROUNDS | HM_FLAG_FUSED_PASS2)))
     return HM_ERR_INVALID_ARG;
   if (!hooks_ok(opts)) return HM_ERR_INVALID_ARG;
   UserAllocScope ua_(opts);
@@ -813,7 +813,8 @@ hm_status hm_build_u64_shard(const uint64_t* keys, const uint64_t* vals, uint64_
   if (n_recv && (!keys || !vals)) return HM_ERR_INVALID_ARG;
   if (!hooks_ok(opts)) return HM_ERR_INVALID_ARG;
   // (from_array and the rounds ablation are single-table paths)
-  if (opts && (opts->flags & ~uint32_t(HM_FLAG_FULL_DIRECTORY | HM_FLAG_DIRECT_SLOTS | HM_FLAG_NO_ROUND0_ILP)))
+  if (opts && (opts->flags & ~uint32_t(HM_FLAG_FULL_DIRECTORY | HM_FLAG_DIRECT_SLOTS | HM_FLAG_NO_ROUND0_ILP |
+                                         HM_FLAG_FUSED_PASS2)))
     return HM_ERR_INVALID_ARG;
   UserAllocScope ua_(opts);
   hm_status s = check_device();

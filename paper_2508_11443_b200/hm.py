@@ -175,6 +175,7 @@ FLAG_NO_ROUND0_ILP = 4  # HM_FLAG_NO_ROUND0_ILP (testing knob)
 FLAG_FROM_ARRAY = 8  # HM_FLAG_FROM_ARRAY: from_array (duplicates allowed, first occurrence kept)
 FLAG_ROUNDS = 16  # HM_FLAG_ROUNDS: the paper's sortless round-based construction (ablation, u64 keys)
 FLAG_FUSED_EXCHANGE = 32  # HM_FLAG_FUSED_EXCHANGE: build_u64_dist routes straight into the owners' NCCL windows
+FLAG_FUSED_PASS2 = 64  # HM_FLAG_FUSED_PASS2: pass 2 + k_bucket as one pipelined kernel (alternative route, same table)
 
 
 _allocator = None  # (alloc, free) ctypes callbacks of set_allocator

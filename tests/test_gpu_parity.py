@@ -292,7 +292,7 @@ def test_bytes_unaligned_context_pointer(shift, prefix):
     m.free()
 
 
-@pytest.mark.parametrize("flags_name", ["FLAG_DIRECT_SLOTS", "FLAG_NO_ROUND0_ILP", "FLAG_ROUNDS"])
+@pytest.mark.parametrize("flags_name", ["FLAG_DIRECT_SLOTS", "FLAG_NO_ROUND0_ILP", "FLAG_ROUNDS", "FLAG_FUSED_PASS2"])
 @pytest.mark.parametrize("n,seed,log2_bp", [(5, 0, 0), (4133, 5, 0), (70_001, 3, 6), (300_007, 1, 0)])
 def test_u64_construction_routes_same_table(flags_name, n, seed, log2_bp):
     """The testing knobs change how k_bucket gets there (direct slot writes
@@ -311,7 +311,36 @@ def test_u64_construction_routes_same_table(flags_name, n, seed, log2_bp):
     m.free()
 
 
-@pytest.mark.parametrize("flags_name", ["FLAG_DIRECT_SLOTS", "FLAG_NO_ROUND0_ILP", "FLAG_ROUNDS"])
+@pytest.mark.parametrize("n,seed,log2_bp", [(70_001, 2, 5), (300_007, 4, 6), (2_200_003, 6, 5), (1 << 20, 8, 5)])
+def test_u64_fused_pipeline_same_table(n, seed, log2_bp):
+    """HM_FLAG_FUSED_PASS2: two-pass builds (more than 1024 partitions) run
+    radix pass 2 and the per-partition construction as one pipelined kernel
+    (k_split2_bucket): a partition job waits for its coarse region's pass-2
+    tiles and drops its L2 lines after loading them.  Ragged last regions (np
+    not a multiple of the 256/512 partitions per region), 8- and 9-bit digits
+    (np > 65536 at 2.2M keys and log2_bp = 5): the oracle's table and lookups,
+    and the same bytes as the default two-kernel route."""
+    hm = _hm()
+    keys, vals = gen.u64_keys(n, lo=n), gen.u64_values(n)
+    ot = O.build_u64(keys, vals, seed)
+    m = hm.HashMap.build_u64(dev(keys), dev(vals), seed=seed, log2_bp=log2_bp, flags=hm.FLAG_FUSED_PASS2)
+    assert_table_equal(m, ot)
+    u = hm.HashMap.build_u64(dev(keys), dev(vals), seed=seed, log2_bp=log2_bp)
+    assert_table_equal(u, ot)
+    q, _, _ = gen.u64_queries(n, n + 1000)
+    ov, of = O.lookup_u64(ot, q)
+    gv, gf = m.lookup(dev(q))
+    assert np.array_equal(host(gv), ov) and np.array_equal(host(gf), of)
+    # back to back on the same stream: the scratch (sdone, pcount) is reset per build
+    for _ in range(3):
+        m2 = hm.HashMap.build_u64(dev(keys), dev(vals), seed=seed, log2_bp=log2_bp, flags=hm.FLAG_FUSED_PASS2)
+        assert_table_equal(m2, ot)
+        m2.free()
+    m.free()
+    u.free()
+
+
+@pytest.mark.parametrize("flags_name", ["FLAG_DIRECT_SLOTS", "FLAG_NO_ROUND0_ILP", "FLAG_ROUNDS", "FLAG_FUSED_PASS2"])
 def test_u64_construction_routes_duplicates(flags_name):
     hm = _hm()
     keys = gen.u64_keys(100_000)
