@@ -770,12 +770,12 @@ __device__ __forceinline__ void search_warp(const BuildParams& bp, const Items<E
   }
 }
 
-__host__ __device__ __forceinline__ size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
+__host__ __device__ constexpr size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
 // Dynamic shared memory of k_bucket (all offsets 16-byte aligned), computed on
 // the host and passed in BuildParams (kernel parameters live in the constant
 // bank: no registers, no recomputation inside the kernel's loops).
-__host__ __device__ __forceinline__ BucketSmem bucket_smem_layout(uint32_t cap, uint32_t BP, uint32_t esz) {
-  BucketSmem L;
+__host__ __device__ constexpr BucketSmem bucket_smem_layout(uint32_t cap, uint32_t BP, uint32_t esz) {
+  BucketSmem L{};
   L.smax = 2 * cap + 256;  // slots of the partition staged in shared memory (S_p is ~2 cnt)
   if (L.smax > 32768u) L.smax = 32768u;
   L.cls_off[0] = 0;                           // s = 2..8 (regions s = 5..8 | 3..4 | 2): at most cap/2 buckets
@@ -793,7 +793,7 @@ __host__ __device__ __forceinline__ BucketSmem bucket_smem_layout(uint32_t cap, 
   L.slist = L.src + al16(size_t(L.smax) * 2);              // u16[]: class lists
   L.queue = L.slist + al16(size_t(L.cls_off[kNCls]) * 2);  // u16[3][cap/2+1]: the rounds' lists / u16[cap]: rk
   L.rk = L.queue;
-  L.ss = L.queue + al16(std::max(size_t(cap / 2 + 1) * 6, size_t(cap) * 2));
+  L.ss = L.queue + al16(size_t(cap / 2 + 1) * 6 > size_t(cap) * 2 ? size_t(cap / 2 + 1) * 6 : size_t(cap) * 2);
 #else
   L.rk = L.lbk + al16(size_t(cap) * 2);                    // u16[cap]: rank of item i in its bucket
   L.sidx = L.rk + al16(size_t(cap) * 2);                   // u16[cap]: grouped position -> item
@@ -858,7 +858,10 @@ __device__ __forceinline__ void block_excl_scan2(unsigned long long& a, unsigned
 // are all done (*sdone_c == tpc), and drop the partition's L2 lines without
 // write-back once they are in shared memory (discard.global.L2: nothing reads
 // them again).  Otherwise the partition is the next ticket.
-template <class E, class Same, bool kFused>
+// kCap != 0: the geometry of every single-table build of 2^16+ keys (2^11
+// buckets per partition, capacity kCap) as compile-time constants, so that
+// shared-memory addresses fold into the instructions' immediate offsets.
+template <class E, class Same, bool kFused, uint32_t kCap>
 __device__ __forceinline__ void bucket_body(const BuildParams& bp, const E* __restrict__ pbuf,
                                             const uint16_t* __restrict__ plb, const unsigned int* pcount,
                                             unsigned long long* __restrict__ lbstate, uint64_t* __restrict__ dir,
@@ -874,22 +877,26 @@ __device__ __forceinline__ void bucket_body(const BuildParams& bp, const E* __re
   __shared__ uint32_t s_bitsw[KBCfg<E>::W][32];
 
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t cap = bp.cap;
-  const uint32_t BP = 1u << bp.log2_bp;
+  constexpr bool kFix = kCap != 0;
+  constexpr uint32_t kFixLog2 = 11;
+  constexpr BucketSmem kSL = bucket_smem_layout(kFix ? kCap : 32u, 1u << kFixLog2, KBCfg<E>::SMEM_ITEM);
+#define HM_SL(f) (kFix ? kSL.f : bp.sl.f)
+  const uint32_t cap = kFix ? kCap : bp.cap;
+  const uint32_t log2bp = kFix ? kFixLog2 : bp.log2_bp;
+  const uint32_t BP = 1u << log2bp;
   const uint32_t CH = (BP + KBCfg<E>::T - 1) / KBCfg<E>::T;  // buckets per thread in the scans
-  const BucketSmem& SL = bp.sl;
-  uint64_t* skey = reinterpret_cast<uint64_t*>(smem + SL.skv);  // (16-byte records, or fingerprints)
-  uint16_t* lbk = reinterpret_cast<uint16_t*>(smem + SL.lbk);
-  uint16_t* rk = reinterpret_cast<uint16_t*>(smem + SL.rk);
-  uint16_t* sidx = reinterpret_cast<uint16_t*>(smem + SL.sidx);
-  uint16_t* sA = reinterpret_cast<uint16_t*>(smem + SL.sA);
-  uint16_t* src = reinterpret_cast<uint16_t*>(smem + SL.src);
-  uint16_t* slist = reinterpret_cast<uint16_t*>(smem + SL.slist);
-  uint16_t* rlist = reinterpret_cast<uint16_t*>(smem + SL.queue);  // [3][lcap]
-  uint8_t* ss = smem + SL.ss;
-  uint16_t* sstart = reinterpret_cast<uint16_t*>(smem + SL.sstart);
-  uint32_t* soff = reinterpret_cast<uint32_t*>(smem + SL.soff);
-  uint8_t* s_t = smem + SL.st;
+  uint64_t* skey = reinterpret_cast<uint64_t*>(smem + HM_SL(skv));  // (16-byte records, or fingerprints)
+  uint16_t* lbk = reinterpret_cast<uint16_t*>(smem + HM_SL(lbk));
+  uint16_t* rk = reinterpret_cast<uint16_t*>(smem + HM_SL(rk));
+  uint16_t* sidx = reinterpret_cast<uint16_t*>(smem + HM_SL(sidx));
+  uint16_t* sA = reinterpret_cast<uint16_t*>(smem + HM_SL(sA));
+  uint16_t* src = reinterpret_cast<uint16_t*>(smem + HM_SL(src));
+  uint16_t* slist = reinterpret_cast<uint16_t*>(smem + HM_SL(slist));
+  uint16_t* rlist = reinterpret_cast<uint16_t*>(smem + HM_SL(queue));  // [3][lcap]
+  uint8_t* ss = smem + HM_SL(ss);
+  uint16_t* sstart = reinterpret_cast<uint16_t*>(smem + HM_SL(sstart));
+  uint32_t* soff = reinterpret_cast<uint32_t*>(smem + HM_SL(soff));
+  uint8_t* s_t = smem + HM_SL(st);
   const uint32_t lcap = cap / 2 + 1;
 
   if (tid == 0) {
@@ -917,7 +924,7 @@ __device__ __forceinline__ void bucket_body(const BuildParams& bp, const E* __re
   __syncthreads();
   const uint32_t p = s_p;
   HM_TMARK(0);
-  const uint64_t lb0 = uint64_t(p) << bp.log2_bp;
+  const uint64_t lb0 = uint64_t(p) << log2bp;
   const uint32_t nbp = uint32_t(bp.nb - lb0 < uint64_t(BP) ? bp.nb - lb0 : uint64_t(BP));
   const uint32_t cnt_raw = kFused ? ld_relaxed_u32(pcount + p) : pcount[p];
   const bool ovf = cnt_raw > cap;
@@ -1090,7 +1097,7 @@ __device__ __forceinline__ void bucket_body(const BuildParams& bp, const E* __re
         n4 += v - 3u <= 1u;
         n8 += v >= 5;
       } else if (!over) {
-        if (v <= 32) slist[SL.cls_off[2] + atomicAdd(&s_c9, 1u)] = uint16_t(j);
+        if (v <= 32) slist[HM_SL(cls_off[2]) + atomicAdd(&s_c9, 1u)] = uint16_t(j);
         else huge = true;
       }
     };
@@ -1134,7 +1141,7 @@ __device__ __forceinline__ void bucket_body(const BuildParams& bp, const E* __re
   HM_TMARK(10);
   // ---- groupby: grouped position of every item; a singleton
   // (R12: its slot is soff) is mapped right here
-  const bool staged = S_p <= SL.smax && !(bp.flags & HM_FLAG_DIRECT_SLOTS);
+  const bool staged = S_p <= HM_SL(smax) && !(bp.flags & HM_FLAG_DIRECT_SLOTS);
   for (uint32_t i = tid; i < cnt; i += KBCfg<E>::T) {
     const uint32_t lb = lbk[i];
     sidx[sstart[lb] + rk[i]] = uint16_t(i);
@@ -1182,7 +1189,7 @@ __device__ __forceinline__ void bucket_body(const BuildParams& bp, const E* __re
   // aggregates right after their scans), then joins the search
   if (warp == 0) look_back();
   HM_TMARK(9);
-  search_warp(bp, skv, X, slist + SL.cls_off[2], s_c9, s_m2, bbase, stt, same, s_bitsw[warp]);
+  search_warp(bp, skv, X, slist + HM_SL(cls_off[2]), s_c9, s_m2, bbase, stt, same, s_bitsw[warp]);
   {
     uint32_t h[8];
     // round r: the list of round r-1's collisions (round 0: every listed
@@ -1213,7 +1220,11 @@ __device__ __forceinline__ void bucket_body(const BuildParams& bp, const E* __re
         logA2 = one ? 0u : uint32_t(HM_R0_LOGA2);
         L1 = L3;
       } else {
-        while (logA < HM_RETRY_LOGA && (L << (logA + 1)) <= uint32_t(KBCfg<E>::T)) logA++;
+        // the largest logA <= HM_RETRY_LOGA with L << logA <= T (T a power of two:
+        // logA = log2 T - ceil(log2 L))
+        static_assert((KBCfg<E>::T & (KBCfg<E>::T - 1)) == 0, "T is a power of two");
+        const int lg = int(__ffs(KBCfg<E>::T) - 1) - (32 - __clz(L - 1));
+        logA = uint32_t(min(max(lg, 0), HM_RETRY_LOGA));
       }
       const uint32_t W1 = L1 << logA, W = W1 + ((L - L1) << logA2);
       for (;;) {
@@ -1359,17 +1370,23 @@ __device__ __forceinline__ void bucket_body(const BuildParams& bp, const E* __re
     o[1] = make_uint4(w[4], w[5], w[6], w[7]);
   }
   HM_TMARK(7);
+#undef HM_SL
 }
 
-template <class E, class Same>
+template <class E, class Same, uint32_t kCap>
 __global__ void __launch_bounds__(KBCfg<E>::T, KBCfg<E>::MINB)
     k_bucket(BuildParams bp, const E* __restrict__ pbuf, const uint16_t* __restrict__ plb,
              const unsigned int* __restrict__ pcount,
              unsigned long long* __restrict__ lbstate, uint64_t* __restrict__ dir, CDir* __restrict__ cdir,
              E* __restrict__ slots, DevStatus* __restrict__ stt, Same same) {
   extern __shared__ __align__(16) uint8_t smem[];
-  bucket_body<E, Same, false>(bp, pbuf, plb, pcount, lbstate, dir, cdir, slots, stt, same, smem, 0, nullptr, 0);
+  bucket_body<E, Same, false, kCap>(bp, pbuf, plb, pcount, lbstate, dir, cdir, slots, stt, same, smem, 0, nullptr,
+                                    0);
 }
+// The geometry of a single-table build of n >= 2^16 keys: 2^11 buckets per
+// partition, m = n BP / nb = 2^11 expected items, cap = ceil((m + 8 sqrt(m) + 64) / 32) * 32
+// (make_plan).
+constexpr uint32_t kCapFix = 2496;
 
 // The fused pass 2 + k_bucket pipeline (u64 keys, HM_FLAG_FUSED_PASS2): one kernel whose CTAs take
 // jobs in ticket order — the pass-2 tiles of coarse region c + D come before the
@@ -1426,7 +1443,7 @@ __global__ void __launch_bounds__(KBCfg<E>::T, KBCfg<E>::MINB)
     return;
   }
   if (x >= bp.np) return;
-  bucket_body<E, Same, true>(bp, pbuf, plb, pcount, lbstate, dir, cdir, slots, stt, same, smem, x,
+  bucket_body<E, Same, true, 0>(bp, pbuf, plb, pcount, lbstate, dir, cdir, slots, stt, same, smem, x,
                              f.sdone + x / f.sdig, f.tpc);
 }
 
@@ -1670,7 +1687,7 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
   size_t static_smem_B = 4096;  // k_bucket's static shared memory (queried below; ~1.5-2.6 KB)
   {
     cudaFuncAttributes fa{};
-    if (cudaFuncGetAttributes(&fa, k_bucket<E, Same>) == cudaSuccess) static_smem_B = fa.sharedSizeBytes;
+    if (cudaFuncGetAttributes(&fa, k_bucket<E, Same, 0>) == cudaSuccess) static_smem_B = fa.sharedSizeBytes;
     else cudaGetLastError();
     if constexpr (sizeof(E) == sizeof(KV16)) {  // (the fused kernel holds pass 2's static arrays too)
       if (cudaFuncGetAttributes(&fa, k_split2_bucket<Src, E, Same, 9>) == cudaSuccess)
@@ -1732,7 +1749,7 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
   const bool smemHist = smemA <= size_t(smem_optin) - 1024;
   auto kA_s = k_partition<Src, E, KPT, true>;
   auto kA_g = k_partition<Src, E, KPT, false>;
-  auto kB = k_bucket<E, Same>;
+  auto kB = pl.log2_bp == 11 && pl.cap == kCapFix ? k_bucket<E, Same, kCapFix> : k_bucket<E, Same, 0>;
   if (smemHist) HM_CUDA_TRY(cudaFuncSetAttribute(kA_s, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smemA)));
   HM_CUDA_TRY(cudaFuncSetAttribute(kB, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smemB)));
   int occA = 1;
