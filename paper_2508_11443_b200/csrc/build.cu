@@ -397,6 +397,10 @@ __host__ __device__ constexpr int split_tile() {
 }
 constexpr int kSWarps = kSThreads / 32;  // BITS-bit digits: up to 2^(2 BITS) partitions in two passes
 
+// Partition capacity of a single-table build (n_in = nb) at 2^11 buckets per
+// partition: m = 2^11 expected items, cap = ceil((m + 8 sqrt(m) + 64) / 32) * 32
+// (make_plan); k_bucket<E, Same, kFixCap> has this geometry built in.
+constexpr uint32_t kFixCap = 2496;
 struct SplitArgs {
   // pass 2 source: the coarse buffer
   const void* cbuf;
@@ -417,6 +421,7 @@ struct SplitArgs {
 template <class Src, class E, int PASS, int BITS>
 __device__ __forceinline__ void split_tile_body(const Src& src, const BuildParams& bp, const SplitArgs& a,
                                                 DevStatus* __restrict__ stt, uint32_t bid, uint8_t* smem) {
+  const uint32_t log2bp = bp.log2_bp, tpc = a.tpc, ccap = a.ccap, dcap = a.dcap;
   constexpr int kSDigits = 1 << BITS, kSBits = BITS, kSPT = split_pt<E>(), kSTile = split_tile<E>();
   E* stage = reinterpret_cast<E*>(smem);
   uint16_t* sdig = reinterpret_cast<uint16_t*>(smem + size_t(kSTile) * sizeof(E));
@@ -434,9 +439,9 @@ __device__ __forceinline__ void split_tile_body(const Src& src, const BuildParam
     base = uint64_t(bid) * kSTile;
     nvalid = bp.n_in - base < uint64_t(kSTile) ? uint32_t(bp.n_in - base) : uint32_t(kSTile);
   } else {
-    coarse = bid / a.tpc;
-    const uint32_t k = bid % a.tpc;
-    const uint32_t cc = min(a.ccount[coarse], a.ccap);
+    coarse = bid / tpc;
+    const uint32_t k = bid % tpc;
+    const uint32_t cc = min(a.ccount[coarse], ccap);
     base = uint64_t(k) * kSTile;
     nvalid = cc > base ? (cc - base < uint64_t(kSTile) ? uint32_t(cc - base) : uint32_t(kSTile)) : 0u;
   }
@@ -448,7 +453,7 @@ __device__ __forceinline__ void split_tile_body(const Src& src, const BuildParam
 #pragma unroll
   for (int j = 0; j < kSPT; j++) {
     const uint32_t i = j * kSThreads + tid;
-    if (i < nvalid) e[j] = PASS == 1 ? src.load(base + i) : cb[size_t(coarse) * a.ccap + base + i];
+    if (i < nvalid) e[j] = PASS == 1 ? src.load(base + i) : cb[size_t(coarse) * ccap + base + i];
   }
 #pragma unroll
   for (int j = 0; j < kSPT; j++) {
@@ -458,9 +463,9 @@ __device__ __forceinline__ void split_tile_body(const Src& src, const BuildParam
       const uint64_t h1 = hash64(bp.l1.c1, e[j].key);
       const uint64_t lb = level1_of_hash(bp.l1, h1) - bp.b_lo;
       if (lb >= bp.nb) bad = true;
-      const uint32_t p = uint32_t(lb >> bp.log2_bp);
+      const uint32_t p = uint32_t(lb >> log2bp);
       dg[j] = PASS == 1 ? ((p >> kSBits) & (kSDigits - 1)) : (p & (kSDigits - 1));
-      lc[j] = uint32_t(lb & ((1u << bp.log2_bp) - 1)) | (tag4_of_hash(h1) << 12);
+      lc[j] = uint32_t(lb & ((1u << log2bp) - 1)) | (tag4_of_hash(h1) << 12);
     }
   }
   // rank of every element among the tile's elements with its digit: one
@@ -502,9 +507,9 @@ __device__ __forceinline__ void split_tile_body(const Src& src, const BuildParam
     const uint32_t d = sdig[i];
     const uint32_t reg = PASS == 1 ? d : coarse * kSDigits + d;
     const uint32_t pos = s_gbase[d] + (i - s_dstart[d]);
-    if (reg < a.nreg && pos < a.dcap) {
-      dst[size_t(reg) * a.dcap + pos] = stage[i];
-      if (PASS == 2 && a.dst_lb) a.dst_lb[size_t(reg) * a.dcap + pos] = slbc[i];
+    if (reg < a.nreg && pos < dcap) {
+      dst[size_t(reg) * dcap + pos] = stage[i];
+      if (PASS == 2 && a.dst_lb) a.dst_lb[size_t(reg) * dcap + pos] = slbc[i];
     } else {
       ovf = true;
     }
@@ -1383,10 +1388,7 @@ __global__ void __launch_bounds__(KBCfg<E>::T, KBCfg<E>::MINB)
   bucket_body<E, Same, false, kCap>(bp, pbuf, plb, pcount, lbstate, dir, cdir, slots, stt, same, smem, 0, nullptr,
                                     0);
 }
-// The geometry of a single-table build of n >= 2^16 keys: 2^11 buckets per
-// partition, m = n BP / nb = 2^11 expected items, cap = ceil((m + 8 sqrt(m) + 64) / 32) * 32
-// (make_plan).
-constexpr uint32_t kCapFix = 2496;
+
 
 // The fused pass 2 + k_bucket pipeline (u64 keys, HM_FLAG_FUSED_PASS2): one kernel whose CTAs take
 // jobs in ticket order — the pass-2 tiles of coarse region c + D come before the
@@ -1749,7 +1751,7 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
   const bool smemHist = smemA <= size_t(smem_optin) - 1024;
   auto kA_s = k_partition<Src, E, KPT, true>;
   auto kA_g = k_partition<Src, E, KPT, false>;
-  auto kB = pl.log2_bp == 11 && pl.cap == kCapFix ? k_bucket<E, Same, kCapFix> : k_bucket<E, Same, 0>;
+  auto kB = pl.log2_bp == 11 && pl.cap == kFixCap ? k_bucket<E, Same, kFixCap> : k_bucket<E, Same, 0>;
   if (smemHist) HM_CUDA_TRY(cudaFuncSetAttribute(kA_s, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smemA)));
   HM_CUDA_TRY(cudaFuncSetAttribute(kB, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smemB)));
   int occA = 1;
@@ -1776,6 +1778,7 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
     const double mc = double(n_in) * double(sdig) * double(uint64_t(1) << pl.log2_bp) / double(nb);
     ccap = uint32_t(mc + 8.0 * std::sqrt(mc + 1.0) + 1024.0);
     tpc = (ccap + kSTile - 1) / kSTile;
+
     if ((s = sc.alloc(WS_CBUF, &cbuf, size_t(ncoarse) * ccap * sizeof(E))) != HM_OK) return fail(s);
     if ((s = sc.alloc(WS_CCOUNT, &ccount, size_t(ncoarse) * 4)) != HM_OK) return fail(s);
     HM_CUDA_TRY(cudaFuncSetAttribute(kS1, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smemS)));
