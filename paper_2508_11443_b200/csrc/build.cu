@@ -418,19 +418,19 @@ struct SplitArgs {
 
 // One tile of a radix pass (bid: the tile; pass 2: coarse region bid / tpc,
 // tile bid % tpc of it).  Also a job of the fused pass-2 + k_bucket kernel.
-template <class Src, class E, int PASS, int BITS>
+template <class Src, class E, int PASS, int BITS, int NT = kSThreads>
 __device__ __forceinline__ void split_tile_body(const Src& src, const BuildParams& bp, const SplitArgs& a,
                                                 DevStatus* __restrict__ stt, uint32_t bid, uint8_t* smem) {
   const uint32_t log2bp = bp.log2_bp, tpc = a.tpc, ccap = a.ccap, dcap = a.dcap;
-  constexpr int kSDigits = 1 << BITS, kSBits = BITS, kSPT = split_pt<E>(), kSTile = split_tile<E>();
+  constexpr int kSDigits = 1 << BITS, kSBits = BITS, kSPT = split_pt<E>(), kSTile = NT * split_pt<E>();
   E* stage = reinterpret_cast<E*>(smem);
   uint16_t* sdig = reinterpret_cast<uint16_t*>(smem + size_t(kSTile) * sizeof(E));
   uint16_t* slbc = sdig + kSTile;  // pass 2: local bucket | tag4 << 12 of the staged record
   __shared__ uint32_t s_cnt[kSDigits], s_dstart[kSDigits], s_gbase[kSDigits];
-  __shared__ unsigned long long s_red[kSWarps];
+  __shared__ unsigned long long s_red[NT / 32];
 
   const uint32_t tid = threadIdx.x;
-  for (uint32_t i = tid; i < kSDigits; i += kSThreads) s_cnt[i] = 0;
+  for (uint32_t i = tid; i < kSDigits; i += NT) s_cnt[i] = 0;
   // this CTA's elements
   uint64_t base;
   uint32_t nvalid, coarse = 0;
@@ -452,12 +452,12 @@ __device__ __forceinline__ void split_tile_body(const Src& src, const BuildParam
   bool bad = false;
 #pragma unroll
   for (int j = 0; j < kSPT; j++) {
-    const uint32_t i = j * kSThreads + tid;
+    const uint32_t i = j * NT + tid;
     if (i < nvalid) e[j] = PASS == 1 ? src.load(base + i) : cb[size_t(coarse) * ccap + base + i];
   }
 #pragma unroll
   for (int j = 0; j < kSPT; j++) {
-    const uint32_t i = j * kSThreads + tid;
+    const uint32_t i = j * NT + tid;
     dg[j] = 0;
     if (i < nvalid) {
       const uint64_t h1 = hash64(bp.l1.c1, e[j].key);
@@ -474,13 +474,13 @@ __device__ __forceinline__ void split_tile_body(const Src& src, const BuildParam
   // (the table is a function of the key set, R13)
 #pragma unroll
   for (int j = 0; j < kSPT; j++)
-    if (j * kSThreads + tid < nvalid) rk[j] = atomicAdd(&s_cnt[dg[j]], 1u);
+    if (j * NT + tid < nvalid) rk[j] = atomicAdd(&s_cnt[dg[j]], 1u);
   __syncthreads();
   // digit-major offsets inside the tile; one global reservation per digit
   {
     const uint32_t tot = tid < kSDigits ? s_cnt[tid] : 0u;
     unsigned long long t_all;
-    const uint32_t ds = uint32_t(block_excl_scan<kSThreads>(tot, &t_all, s_red));
+    const uint32_t ds = uint32_t(block_excl_scan<NT>(tot, &t_all, s_red));
     if (tid < kSDigits) {
       s_dstart[tid] = ds;
       if (tot) {
@@ -492,7 +492,7 @@ __device__ __forceinline__ void split_tile_body(const Src& src, const BuildParam
   __syncthreads();
 #pragma unroll
   for (int j = 0; j < kSPT; j++) {
-    if (j * kSThreads + tid < nvalid) {
+    if (j * NT + tid < nvalid) {
       const uint32_t pos = s_dstart[dg[j]] + rk[j];
       stage[pos] = e[j];
       sdig[pos] = uint16_t(dg[j]);
@@ -503,7 +503,7 @@ __device__ __forceinline__ void split_tile_body(const Src& src, const BuildParam
   // runs of equal digit are contiguous: consecutive threads write consecutive addresses
   E* dst = reinterpret_cast<E*>(a.dst);
   bool ovf = false;
-  for (uint32_t i = tid; i < nvalid; i += kSThreads) {
+  for (uint32_t i = tid; i < nvalid; i += NT) {
     const uint32_t d = sdig[i];
     const uint32_t reg = PASS == 1 ? d : coarse * kSDigits + d;
     const uint32_t pos = s_gbase[d] + (i - s_dstart[d]);
@@ -518,12 +518,15 @@ __device__ __forceinline__ void split_tile_body(const Src& src, const BuildParam
   if (bad) atomicOr(&stt->pad, 1u);
 }
 
-template <class Src, class E, int PASS, int BITS>
-__global__ void __launch_bounds__(kSThreads, HM_SPLIT_MINB) k_split(Src src, BuildParams bp, SplitArgs a,
-                                                        DevStatus* __restrict__ stt) {
+template <class Src, class E, int PASS, int BITS, int NT = kSThreads>
+__global__ void __launch_bounds__(NT, NT == kSThreads ? HM_SPLIT_MINB : 2 * HM_SPLIT_MINB)
+    k_split(Src src, BuildParams bp, SplitArgs a, DevStatus* __restrict__ stt) {
   extern __shared__ __align__(16) uint8_t smem[];
-  split_tile_body<Src, E, PASS, BITS>(src, bp, a, stt, blockIdx.x, smem);
+  split_tile_body<Src, E, PASS, BITS, NT>(src, bp, a, stt, blockIdx.x, smem);
 }
+#ifndef HM_SPLIT1_T
+#define HM_SPLIT1_T 256  // pass 1 of 8-bit digits: 256-thread tiles, twice the CTAs per SM
+#endif
 
 // ------------------------------------------------------------------ K_B
 // One CTA per build partition of BP = 2^log2_bp level-1 buckets; everything
@@ -1771,7 +1774,11 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
   unsigned int* ccount = nullptr;
   constexpr int kSTile = split_tile<E>();
   const size_t smemS = size_t(kSTile) * (sizeof(E) + 4);
-  auto kS1 = sbits == 8 ? k_split<Src, E, 1, 8> : k_split<Src, E, 1, 9>;
+  // pass 1: HM_SPLIT1_T-thread tiles for 8-bit digits (one digit per thread in the scan)
+  auto kS1 = sbits == 8 ? k_split<Src, E, 1, 8, HM_SPLIT1_T> : k_split<Src, E, 1, 9>;
+  const int s1T = sbits == 8 ? HM_SPLIT1_T : kSThreads;
+  const int s1Tile = s1T * split_pt<E>();
+  const size_t smemS1 = size_t(s1Tile) * (sizeof(E) + 4);
   auto kS2 = sbits == 8 ? k_split<Src, E, 2, 8> : k_split<Src, E, 2, 9>;
   if (two_pass) {
     ncoarse = (pl.np + sdig - 1) / sdig;
@@ -1781,7 +1788,7 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
 
     if ((s = sc.alloc(WS_CBUF, &cbuf, size_t(ncoarse) * ccap * sizeof(E))) != HM_OK) return fail(s);
     if ((s = sc.alloc(WS_CCOUNT, &ccount, size_t(ncoarse) * 4)) != HM_OK) return fail(s);
-    HM_CUDA_TRY(cudaFuncSetAttribute(kS1, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smemS)));
+    HM_CUDA_TRY(cudaFuncSetAttribute(kS1, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smemS1)));
     HM_CUDA_TRY(cudaFuncSetAttribute(kS2, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smemS)));
   }
   // u64 keys: pass 2 and k_bucket as one pipelined kernel (k_split2_bucket)
@@ -1824,7 +1831,7 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
         const SplitArgs a1{nullptr, nullptr, 0, 0, cbuf, ccount, ccap, ncoarse, 0};
         {
           LaunchScope ls_("k_split1", st);
-          kS1<<<unsigned((n_in + kSTile - 1) / kSTile), kSThreads, smemS, st>>>(src, bp, a1, dstat);
+          kS1<<<unsigned((n_in + s1Tile - 1) / s1Tile), s1T, smemS1, st>>>(src, bp, a1, dstat);
         }
         HM_CUDA_TRY(cudaGetLastError());
         if (!fused) {
