@@ -1204,8 +1204,8 @@ __device__ __forceinline__ void bucket_body(const BuildParams& bp, const E* __re
     // bucket, the class-ordered slist), A adjacent lanes per bucket trying
     // attempts tb .. tb + A - 1 (tb = s_t[lb]: 0 in round 0), 32-lane chunks
     // from a shared counter
+    uint32_t cur = 0, nxt = 1, prv = 2;  // (the three lists rotate: r % 3, (r + 1) % 3, (r + 2) % 3)
     for (uint32_t r = 0;; r++) {
-      const uint32_t cur = r % 3, nxt = (r + 1) % 3;
       const uint16_t* cl = r == 0 ? slist : rlist + cur * lcap;
       const uint32_t n3 = r == 0 ? Lall : s_qn[cur][0], L = r == 0 ? Lall : n3 + s_qn[cur][1];
 #ifdef HM_PHASE_TIMING
@@ -1215,8 +1215,8 @@ __device__ __forceinline__ void bucket_body(const BuildParams& bp, const E* __re
 #endif
       if (L == 0) break;
       if (tid == 0) {  // (the list two rounds back is not read any more)
-        s_qn[(r + 2) % 3][0] = s_qn[(r + 2) % 3][1] = 0;
-        s_chunk[(r + 2) % 3] = 0;
+        s_qn[prv][0] = s_qn[prv][1] = 0;
+        s_chunk[prv] = 0;
       }
       // lanes per bucket: round 0 gives the s >= 3 buckets (the front of the
       // list) 2^HM_R0_LOGA lanes and the s = 2 ones 2^HM_R0_LOGA2; later rounds
@@ -1265,6 +1265,10 @@ __device__ __forceinline__ void bucket_body(const BuildParams& bp, const E* __re
         list_append(again, lb, s, rlist + nxt * lcap, lcap, s_qn[nxt]);
       }
       __syncthreads();
+      const uint32_t t3 = prv;
+      prv = cur;
+      cur = nxt;
+      nxt = t3;
     }
   }
   HM_TMARK(4);
@@ -1291,7 +1295,7 @@ __device__ __forceinline__ void bucket_body(const BuildParams& bp, const E* __re
         const uint32_t x = x0 + j * KBCfg<E>::T + tid;
         if (x < Sp) {
           const uint32_t v = src[x], it = v & 0x7FFFu;
-          e[j] = skv.rec(it < cnt ? it : 0u);  // (an unmapped slot only in a pass that is redone)
+          e[j] = skv.rec(min(it, cnt - 1u));  // (an unmapped slot only in a pass that is redone; Sp > 0: cnt > 0)
           if (v & 0x8000u) e[j].value = 0;
         }
       }
