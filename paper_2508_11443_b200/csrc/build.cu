@@ -26,6 +26,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <map>
+#include <tuple>
 #include <mutex>
 #include <type_traits>
 #include <vector>
@@ -1487,6 +1488,62 @@ static size_t bucket_smem_bytes(uint32_t cap, uint32_t log2_bp, uint32_t esz) {
   return bucket_smem_layout(cap, 1u << log2_bp, esz).total;
 }
 
+// Per-device caches of the host-side launch configuration.
+static std::mutex g_attr_mu;
+static std::map<std::pair<int, const void*>, int> g_smem_set;                    // dynamic smem limit set
+static std::map<std::tuple<int, const void*, int, size_t>, int> g_occ;           // blocks per SM
+static cudaError_t device_smem(int* optin, int* per_sm) {
+  static int c_optin[64] = {}, c_sm[64] = {};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 64 || !c_optin[dev]) {
+    if ((e = cudaDeviceGetAttribute(optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess) return e;
+    if ((e = cudaDeviceGetAttribute(per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev)) != cudaSuccess) return e;
+    if (dev >= 0 && dev < 64) {
+      c_sm[dev] = *per_sm;
+      c_optin[dev] = *optin;
+    }
+    return cudaSuccess;
+  }
+  *optin = c_optin[dev];
+  *per_sm = c_sm[dev];
+  return cudaSuccess;
+}
+static cudaError_t ensure_smem(const void* fn, int bytes) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  {
+    std::lock_guard<std::mutex> g(g_attr_mu);
+    auto it = g_smem_set.find({dev, fn});
+    if (it != g_smem_set.end() && it->second >= bytes) return cudaSuccess;
+  }
+  if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes)) != cudaSuccess) return e;
+  std::lock_guard<std::mutex> g(g_attr_mu);
+  int& v = g_smem_set[{dev, fn}];
+  v = std::max(v, bytes);
+  return cudaSuccess;
+}
+static cudaError_t occupancy(int* blocks, const void* fn, int threads, size_t smem) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const auto key = std::make_tuple(dev, fn, threads, smem);
+  {
+    std::lock_guard<std::mutex> g(g_attr_mu);
+    auto it = g_occ.find(key);
+    if (it != g_occ.end()) {
+      *blocks = it->second;
+      return cudaSuccess;
+    }
+  }
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, fn, threads, smem)) != cudaSuccess) return e;
+  std::lock_guard<std::mutex> g(g_attr_mu);
+  g_occ[key] = *blocks;
+  return cudaSuccess;
+}
+
 struct Plan {
   uint32_t log2_bp, np, cap;
   size_t smemB;
@@ -1545,7 +1602,7 @@ static hm_status dmalloc(T** p, size_t bytes, cudaStream_t st) {
 // maps' own arrays), so they stay allocated until hm_release_workspace().
 // Reuse is safe because everything that touches a stream's workspace is
 // ordered on that stream.
-enum WsRole { WS_FP, WS_BAD, WS_PBUF, WS_PLB, WS_PCOUNT, WS_LBSTATE, WS_DSTAT, WS_CBUF, WS_CCOUNT, WS_DEDUP, WS_SDONE, WS_NROLES };
+enum WsRole { WS_FP, WS_BAD, WS_PBUF, WS_PLB, WS_PCOUNT, WS_LBSTATE, WS_DSTAT, WS_CBUF, WS_CCOUNT, WS_DEDUP, WS_SDONE, WS_ZERO, WS_NROLES };
 struct Workspace {
   void* p[WS_NROLES] = {};
   size_t bytes[WS_NROLES] = {};
@@ -1687,22 +1744,23 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
                             int t1_fixed, uint64_t seed, uint32_t log2_req, cudaStream_t st, BuildOut* out,
                             bool* fpcoll, SideJob* job = nullptr) {
   *fpcoll = false;
-  int dev = 0;
-  HM_CUDA_TRY(cudaGetDevice(&dev));
-  int smem_optin = 0;
-  HM_CUDA_TRY(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-  int smem_sm = 0;
-  HM_CUDA_TRY(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
-  size_t static_smem_B = 4096;  // k_bucket's static shared memory (queried below; ~1.5-2.6 KB)
-  {
+  // (device attributes, the kernels' static shared memory, their dynamic
+  // shared-memory limits and occupancies are queried once per device: a
+  // build's fixed cost is its launches, not these host calls)
+  int smem_optin = 0, smem_sm = 0;
+  HM_CUDA_TRY(device_smem(&smem_optin, &smem_sm));
+  static size_t static_smem_B = 0;  // k_bucket's static shared memory (~2.6 KB; the same binary on every device)
+  if (!static_smem_B) {
+    size_t v = 4096;
     cudaFuncAttributes fa{};
-    if (cudaFuncGetAttributes(&fa, k_bucket<E, Same, 0>) == cudaSuccess) static_smem_B = fa.sharedSizeBytes;
+    if (cudaFuncGetAttributes(&fa, k_bucket<E, Same, 0>) == cudaSuccess) v = fa.sharedSizeBytes;
     else cudaGetLastError();
     if constexpr (sizeof(E) == sizeof(KV16)) {  // (the fused kernel holds pass 2's static arrays too)
       if (cudaFuncGetAttributes(&fa, k_split2_bucket<Src, E, Same, 9>) == cudaSuccess)
-        static_smem_B = std::max<size_t>(static_smem_B, fa.sharedSizeBytes);
+        v = std::max<size_t>(v, fa.sharedSizeBytes);
       else cudaGetLastError();
     }
+    static_smem_B = v;
   }
   const uint32_t knob_flags = log2_req >> 16;
   log2_req &= 0xFFFFu;
@@ -1724,9 +1782,16 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
   if ((s = sc.alloc(WS_PBUF, &pbuf, size_t(pl.np) * pl.cap * sizeof(E))) != HM_OK) return s;
   uint16_t* plb = nullptr;
   if ((s = sc.alloc(WS_PLB, &plb, size_t(pl.np) * pl.cap * 2)) != HM_OK) return s;
-  if ((s = sc.alloc(WS_PCOUNT, &pcount, size_t(pl.np) * 4)) != HM_OK) return s;
-  if ((s = sc.alloc(WS_LBSTATE, &lbstate, size_t(pl.np) * 8)) != HM_OK) return s;
-  if ((s = sc.alloc(WS_DSTAT, &dstat, sizeof(DevStatus))) != HM_OK) return s;
+  // the counters a pass starts from zero, one block (one memset per level-1
+  // draw): status | look-back words | partition counts | coarse counts
+  const size_t z_lb = 256, z_pc = z_lb + size_t(pl.np) * 8, z_cc = z_pc + al16(size_t(pl.np) * 4),
+               z_end = z_cc + al16(size_t(pl.np / 256 + 2) * 4);
+  static_assert(sizeof(DevStatus) <= 256, "status block");
+  uint8_t* zblk = nullptr;
+  if ((s = sc.alloc(WS_ZERO, &zblk, z_end)) != HM_OK) return s;
+  dstat = reinterpret_cast<DevStatus*>(zblk);
+  lbstate = reinterpret_cast<unsigned long long*>(zblk + z_lb);
+  pcount = reinterpret_cast<unsigned int*>(zblk + z_pc);
 
   uint64_t* dir = nullptr;
   E* slots = nullptr;
@@ -1759,11 +1824,11 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
   auto kA_s = k_partition<Src, E, KPT, true>;
   auto kA_g = k_partition<Src, E, KPT, false>;
   auto kB = pl.log2_bp == 11 && pl.cap == kFixCap ? k_bucket<E, Same, kFixCap> : k_bucket<E, Same, 0>;
-  if (smemHist) HM_CUDA_TRY(cudaFuncSetAttribute(kA_s, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smemA)));
-  HM_CUDA_TRY(cudaFuncSetAttribute(kB, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smemB)));
+  if (smemHist) HM_CUDA_TRY(ensure_smem(reinterpret_cast<const void*>(kA_s), int(smemA)));
+  HM_CUDA_TRY(ensure_smem(reinterpret_cast<const void*>(kB), int(pl.smemB)));
   int occA = 1;
-  if (smemHist) HM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occA, kA_s, kAThreads, smemA));
-  else HM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occA, kA_g, kAThreads, 0));
+  if (smemHist) HM_CUDA_TRY(occupancy(&occA, reinterpret_cast<const void*>(kA_s), kAThreads, smemA));
+  else HM_CUDA_TRY(occupancy(&occA, reinterpret_cast<const void*>(kA_g), kAThreads, 0));
   occA = std::max(occA, 1);
   const uint64_t T = uint64_t(kAThreads) * KPT;
   const uint64_t ntiles = (n_in + T - 1) / T;
@@ -1791,9 +1856,9 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
     tpc = (ccap + kSTile - 1) / kSTile;
 
     if ((s = sc.alloc(WS_CBUF, &cbuf, size_t(ncoarse) * ccap * sizeof(E))) != HM_OK) return fail(s);
-    if ((s = sc.alloc(WS_CCOUNT, &ccount, size_t(ncoarse) * 4)) != HM_OK) return fail(s);
-    HM_CUDA_TRY(cudaFuncSetAttribute(kS1, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smemS1)));
-    HM_CUDA_TRY(cudaFuncSetAttribute(kS2, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smemS)));
+    ccount = reinterpret_cast<unsigned int*>(zblk + z_cc);  // (ncoarse <= np / 256 + 1)
+    HM_CUDA_TRY(ensure_smem(reinterpret_cast<const void*>(kS1), int(smemS1)));
+    HM_CUDA_TRY(ensure_smem(reinterpret_cast<const void*>(kS2), int(smemS)));
   }
   // u64 keys: pass 2 and k_bucket as one pipelined kernel (k_split2_bucket)
   const bool fused = two_pass && sizeof(E) == sizeof(KV16) && !job && (knob_flags & HM_FLAG_FUSED_PASS2);
@@ -1803,7 +1868,7 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
     if (fused) {
       auto kF = sbits == 8 ? k_split2_bucket<Src, E, Same, 8> : k_split2_bucket<Src, E, Same, 9>;
       if ((s = sc.alloc(WS_SDONE, &sdone, size_t(ncoarse) * 4)) != HM_OK) return fail(s);
-      HM_CUDA_TRY(cudaFuncSetAttribute(kF, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smemF)));
+      HM_CUDA_TRY(ensure_smem(reinterpret_cast<const void*>(kF), int(smemF)));
     }
   }
   BuildParams bp{};
@@ -1825,13 +1890,11 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
   for (uint32_t t1 = t1_lo; t1 < t1_hi; t1++) {
     bp.l1 = make_l1(smix, t1, n_global);
     bp.slot_cap = slot_cap;
-    HM_CUDA_TRY(cudaMemsetAsync(pcount, 0, size_t(pl.np) * 4, st));
+    HM_CUDA_TRY(cudaMemsetAsync(zblk, 0, z_end, st));
     bool run_a = true;
     for (int pass = 0; pass < 3; pass++) {
-      HM_CUDA_TRY(cudaMemsetAsync(lbstate, 0, size_t(pl.np) * 8, st));
-      HM_CUDA_TRY(cudaMemsetAsync(dstat, 0, sizeof(DevStatus), st));
+      if (pass > 0) HM_CUDA_TRY(cudaMemsetAsync(zblk, 0, z_pc, st));  // (a rerun: status and look-back words)
       if (run_a && ntiles > 0 && two_pass) {
-        HM_CUDA_TRY(cudaMemsetAsync(ccount, 0, size_t(ncoarse) * 4, st));
         const SplitArgs a1{nullptr, nullptr, 0, 0, cbuf, ccount, ccap, ncoarse, 0};
         {
           LaunchScope ls_("k_split1", st);
