@@ -203,7 +203,10 @@ hm_status lookup_u64_launch(const hm_map* m, const uint64_t* q, uint64_t nq, uin
   constexpr int QPT = HM_LOOKUP_QPT;
   const uint64_t per = uint64_t(kLThreads) * QPT;
   const uint64_t blocks = (nq + per - 1) / per;
-  const unsigned grid = unsigned(std::min<uint64_t>(blocks, uint64_t(num_sms()) * 8));
+#ifndef HM_LOOKUP_CPS
+#define HM_LOOKUP_CPS 64  // grid: CTAs per SM, 3 resident at a time (the block scheduler balances the SMs: 8 -> 64 cut 2^26 lookups 1.42 -> 1.33 ms)
+#endif
+  const unsigned grid = unsigned(std::min<uint64_t>(blocks, uint64_t(num_sms()) * HM_LOOKUP_CPS));
   {
     LaunchScope ls_("k_lookup_u64", st);
     k_lookup_u64<QPT><<<grid, kLThreads, 0, st>>>(lp, q, nq, out_vals, out_found);
@@ -357,7 +360,10 @@ hm_status lookup_bytes_launch(const hm_map* m, const uint8_t* qb, const uint64_t
   lp.ctx = m->ctx;
   lp.r_fp = m->r_fp;
   const uint64_t blocks = (nq + kLThreads * HM_LOOKUP_BYTES_QPT - 1) / (kLThreads * HM_LOOKUP_BYTES_QPT);
-  const unsigned grid = unsigned(std::min<uint64_t>(blocks, uint64_t(num_sms()) * 8));
+#ifndef HM_LOOKUP_BYTES_CPS
+#define HM_LOOKUP_BYTES_CPS 8  // grid: CTAs per SM (grid-stride)
+#endif
+  const unsigned grid = unsigned(std::min<uint64_t>(blocks, uint64_t(num_sms()) * HM_LOOKUP_BYTES_CPS));
   {
     LaunchScope ls_("k_lookup_bytes", st);
     k_lookup_bytes<HM_LOOKUP_BYTES_QPT><<<grid, kLThreads, 0, st>>>(lp, qb, qo, nq, out_vals, out_found);
