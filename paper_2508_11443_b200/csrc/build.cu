@@ -1090,9 +1090,9 @@ __device__ __forceinline__ void bucket_body(const BuildParams& bp, const E* __re
     const uint32_t T2 = uint32_t(tb & 0x1FFFFF), T4 = uint32_t((tb >> 21) & 0x1FFFFF), T8 = uint32_t(tb >> 42);
     Lall = T2 + T4 + T8;
     L3 = T4 + T8;
-    uint32_t pos = uint32_t(a), sq = uint32_t(a >> 32);
     // list regions: [s = 5..8 | s = 3..4 | s = 2]
     uint32_t n8 = uint32_t(b >> 42), n4 = T8 + uint32_t((b >> 21) & 0x1FFFFF), n2 = T8 + T4 + uint32_t(b & 0x1FFFFF);
+    uint32_t pos = uint32_t(a), sq = uint32_t(a >> 32);
     // (a bucket with s^2 > 4n means S > 4n: level one redraws, R7, and this
     // pass is discarded; s <= 8 buckets are listed all the same — only
     // reachable with n < 16)
@@ -2158,12 +2158,22 @@ __global__ void __launch_bounds__(kFpThreads, HM_FP_MINB) k_fingerprint(const ui
   asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
+// (four keys per thread and iteration: eight loads in flight)
 __global__ void k_check_offsets(const uint64_t* __restrict__ offs, uint64_t n, unsigned int* bad) {
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
-    const uint64_t o = offs[i], o1 = offs[i + 1];
-    if (o1 < o) atomicOr(bad, 1u);
-    else if (o1 - o > 65535) atomicOr(bad, 2u);
+  const uint64_t T = uint64_t(gridDim.x) * blockDim.x;
+  uint32_t f = 0;
+  for (uint64_t i0 = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i0 < n; i0 += 4 * T) {
+    uint64_t o[4], o1[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const uint64_t i = i0 + u * T;
+      o[u] = i < n ? __ldg(offs + i) : 0;
+      o1[u] = i < n ? __ldg(offs + i + 1) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; u++) f |= o1[u] < o[u] ? 1u : (o1[u] - o[u] > 65535 ? 2u : 0u);
   }
+  if (f) atomicOr(bad, f);
 }
 
 void launch_fingerprint(const uint8_t* bytes, const uint64_t* offs, uint64_t n, uint64_t r, uint64_t* fp,
