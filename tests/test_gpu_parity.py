@@ -48,6 +48,9 @@ U64_CASES = [
     (1 << 14, 0, 0), (50_000, 7, 0), (1 << 16, 0, 0), (1 << 16, 11, 0),
     # forced small partitions: many CTAs, long look-back chains, ragged last partition
     (70_001, 3, 6), (1 << 17, 4, 9), (300_007, 0, 12),
+    # requests below 2^5 buckets per partition act as 2^5 (a compact-directory
+    # record is one partition's): a two-pass build at this size
+    (100_003, 2, 2),
 ]
 
 
