@@ -928,8 +928,10 @@ __device__ __forceinline__ void bucket_body(const BuildParams& bp, const E* __re
       s_qn[i][0] = s_qn[i][1] = 0;
     }
   }
-  if (tid < 33) s_m2[tid] = bp.m2[tid];  // (host-computed: no 64-bit division per CTA)
-  for (uint32_t j = tid; j < BP; j += KBCfg<E>::T) soff[j] = 0;  // the histogram
+  if (tid < 33) s_m2[tid] = g_m2.v[tid];  // (a compile-time table: no 64-bit division per CTA)
+  if (BP == 4u * KBCfg<E>::T) reinterpret_cast<uint4*>(soff)[tid] = make_uint4(0u, 0u, 0u, 0u);  // the histogram
+  else
+    for (uint32_t j = tid; j < BP; j += KBCfg<E>::T) soff[j] = 0;
   __syncthreads();
   const uint32_t p = s_p;
   HM_TMARK(0);

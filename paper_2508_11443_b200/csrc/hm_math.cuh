@@ -141,6 +141,22 @@ __host__ __device__ __forceinline__ uint64_t fastmod(uint64_t x, const FastMod& 
   return r >= f.d ? r - f.d : r;
 }
 
+// floor((2^64 - 1) / s^2) for s = 1..32 (index 0 unused): the reciprocals of
+// the level-2 moduli (R22), a compile-time table in global memory, so that a
+// kernel copies it into shared memory with one coalesced load instead of 33
+// 64-bit divisions (or constant-bank loads at 33 distinct addresses).
+struct M2Table {
+  uint64_t v[33];
+};
+__host__ __device__ constexpr M2Table make_m2_table() {
+  M2Table t{};
+  for (int i = 1; i <= 32; i++) t.v[i] = ~0ull / (uint64_t(i) * uint64_t(i));
+  return t;
+}
+#if defined(__CUDACC__)
+static __device__ const M2Table g_m2 = make_m2_table();
+#endif
+
 // Level-one range reduction `mod n`: mask when n is a power of
 // two (all benchmark configs), reciprocal otherwise.
 struct L1Params {
