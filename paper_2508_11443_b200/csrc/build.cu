@@ -52,6 +52,10 @@ constexpr int kAThreads = 512;
 template <class E>
 struct KBCfg {
   static constexpr int T = sizeof(E) == 16 ? HM_KB_THREADS : HM_KB_THREADS_BYTES;
+  // the single-table geometry k_bucket<E, Same, FIX_CAP> has built in: 4 buckets
+  // per thread, cap = ceil((m + 8 sqrt(m) + 64) / 32) * 32 for m = 2^FIX_LOG2 (make_plan)
+  static constexpr uint32_t FIX_LOG2 = T == 512 ? 11u : 10u;
+  static constexpr uint32_t FIX_CAP = FIX_LOG2 == 11 ? 2496u : 1344u;
   static constexpr int W = T / 32;
   static constexpr int MINB = sizeof(E) == 16 ? HM_KB_MINB : HM_KB_MINB_BYTES;
   // bytes per item k_bucket keeps in shared memory: the whole 16-byte record
@@ -398,10 +402,6 @@ __host__ __device__ constexpr int split_tile() {
 }
 constexpr int kSWarps = kSThreads / 32;  // BITS-bit digits: up to 2^(2 BITS) partitions in two passes
 
-// Partition capacity of a single-table build (n_in = nb) at 2^11 buckets per
-// partition: m = 2^11 expected items, cap = ceil((m + 8 sqrt(m) + 64) / 32) * 32
-// (make_plan); k_bucket<E, Same, kFixCap> has this geometry built in.
-constexpr uint32_t kFixCap = 2496;
 struct SplitArgs {
   // pass 2 source: the coarse buffer
   const void* cbuf;
@@ -887,7 +887,7 @@ __device__ __forceinline__ void bucket_body(const BuildParams& bp, const E* __re
 
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr bool kFix = kCap != 0;
-  constexpr uint32_t kFixLog2 = 11;
+  constexpr uint32_t kFixLog2 = KBCfg<E>::FIX_LOG2;
   constexpr BucketSmem kSL = bucket_smem_layout(kFix ? kCap : 32u, 1u << kFixLog2, KBCfg<E>::SMEM_ITEM);
 #define HM_SL(f) (kFix ? kSL.f : bp.sl.f)
   const uint32_t cap = kFix ? kCap : bp.cap;
@@ -1437,26 +1437,29 @@ __global__ void __launch_bounds__(KBCfg<E>::T, KBCfg<E>::MINB)
                     const uint16_t* __restrict__ plb, const unsigned int* pcount,
                     unsigned long long* __restrict__ lbstate, uint64_t* __restrict__ dir, CDir* __restrict__ cdir,
                     E* __restrict__ slots, DevStatus* __restrict__ stt, Same same) {
-  static_assert(KBCfg<E>::T == kSThreads, "one block size for both job kinds");
   extern __shared__ __align__(16) uint8_t smem[];
-  __shared__ uint32_t s_job;
-  if (threadIdx.x == 0) s_job = atomicAdd(&stt->ticket, 1u);
-  __syncthreads();
-  bool split;
-  uint32_t x;
-  fused_job(f, s_job, &split, &x);
-  if (split) {
-    split_tile_body<Src, E, 2, BITS>(src, bp, a, stt, x, smem);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();
-      atomicAdd(&f.sdone[x / f.tpc], 1u);
-    }
+  if constexpr (KBCfg<E>::T != kSThreads) {  // (one block size for both job kinds; the host checks)
     return;
+  } else {
+    __shared__ uint32_t s_job;
+    if (threadIdx.x == 0) s_job = atomicAdd(&stt->ticket, 1u);
+    __syncthreads();
+    bool split;
+    uint32_t x;
+    fused_job(f, s_job, &split, &x);
+    if (split) {
+      split_tile_body<Src, E, 2, BITS>(src, bp, a, stt, x, smem);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(&f.sdone[x / f.tpc], 1u);
+      }
+      return;
+    }
+    if (x >= bp.np) return;
+    bucket_body<E, Same, true, 0>(bp, pbuf, plb, pcount, lbstate, dir, cdir, slots, stt, same, smem, x,
+                               f.sdone + x / f.sdig, f.tpc);
   }
-  if (x >= bp.np) return;
-  bucket_body<E, Same, true, 0>(bp, pbuf, plb, pcount, lbstate, dir, cdir, slots, stt, same, smem, x,
-                             f.sdone + x / f.sdig, f.tpc);
 }
 
 // ------------------------------------------------------- overflow check
@@ -1825,7 +1828,8 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
   const bool smemHist = smemA <= size_t(smem_optin) - 1024;
   auto kA_s = k_partition<Src, E, KPT, true>;
   auto kA_g = k_partition<Src, E, KPT, false>;
-  auto kB = pl.log2_bp == 11 && pl.cap == kFixCap ? k_bucket<E, Same, kFixCap> : k_bucket<E, Same, 0>;
+  auto kB = pl.log2_bp == KBCfg<E>::FIX_LOG2 && pl.cap == KBCfg<E>::FIX_CAP ? k_bucket<E, Same, KBCfg<E>::FIX_CAP>
+                                                                              : k_bucket<E, Same, 0>;
   if (smemHist) HM_CUDA_TRY(ensure_smem(reinterpret_cast<const void*>(kA_s), int(smemA)));
   HM_CUDA_TRY(ensure_smem(reinterpret_cast<const void*>(kB), int(pl.smemB)));
   int occA = 1;
@@ -1863,7 +1867,8 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
     HM_CUDA_TRY(ensure_smem(reinterpret_cast<const void*>(kS2), int(smemS)));
   }
   // u64 keys: pass 2 and k_bucket as one pipelined kernel (k_split2_bucket)
-  const bool fused = two_pass && sizeof(E) == sizeof(KV16) && !job && (knob_flags & HM_FLAG_FUSED_PASS2);
+  const bool fused = two_pass && sizeof(E) == sizeof(KV16) && !job && (knob_flags & HM_FLAG_FUSED_PASS2) &&
+                     KBCfg<E>::T == kSThreads;
   const size_t smemF = std::max(smemS, pl.smemB);
   unsigned int* sdone = nullptr;
   if constexpr (sizeof(E) == sizeof(KV16)) {
