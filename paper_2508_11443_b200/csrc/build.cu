@@ -1866,7 +1866,7 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
     HM_CUDA_TRY(ensure_smem(reinterpret_cast<const void*>(kS1), int(smemS1)));
     HM_CUDA_TRY(ensure_smem(reinterpret_cast<const void*>(kS2), int(smemS)));
   }
-  // u64 keys: pass 2 and k_bucket as one pipelined kernel (k_split2_bucket)
+  // HM_FLAG_FUSED_PASS2 (u64 keys, opt-in): pass 2 and k_bucket as one pipelined kernel (k_split2_bucket)
   const bool fused = two_pass && sizeof(E) == sizeof(KV16) && !job && (knob_flags & HM_FLAG_FUSED_PASS2) &&
                      KBCfg<E>::T == kSThreads;
   const size_t smemF = std::max(smemS, pl.smemB);
