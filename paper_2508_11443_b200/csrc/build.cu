@@ -23,6 +23,7 @@
 // One host synchronisation per attempt reads the device status (total S for
 // the space bound R7, duplicate / exhaustion flags).
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <map>
@@ -1498,21 +1499,23 @@ static std::mutex g_attr_mu;
 static std::map<std::pair<int, const void*>, int> g_smem_set;                    // dynamic smem limit set
 static std::map<std::tuple<int, const void*, int, size_t>, int> g_occ;           // blocks per SM
 static cudaError_t device_smem(int* optin, int* per_sm) {
-  static int c_optin[64] = {}, c_sm[64] = {};
+  static std::map<int, std::pair<int, int>> cache;  // device -> (opt-in per block, per SM)
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
-  if (dev < 0 || dev >= 64 || !c_optin[dev]) {
-    if ((e = cudaDeviceGetAttribute(optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess) return e;
-    if ((e = cudaDeviceGetAttribute(per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev)) != cudaSuccess) return e;
-    if (dev >= 0 && dev < 64) {
-      c_sm[dev] = *per_sm;
-      c_optin[dev] = *optin;
+  {
+    std::lock_guard<std::mutex> g(g_attr_mu);
+    auto it = cache.find(dev);
+    if (it != cache.end()) {
+      *optin = it->second.first;
+      *per_sm = it->second.second;
+      return cudaSuccess;
     }
-    return cudaSuccess;
   }
-  *optin = c_optin[dev];
-  *per_sm = c_sm[dev];
+  if ((e = cudaDeviceGetAttribute(optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess) return e;
+  if ((e = cudaDeviceGetAttribute(per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev)) != cudaSuccess) return e;
+  std::lock_guard<std::mutex> g(g_attr_mu);
+  cache[dev] = {*optin, *per_sm};
   return cudaSuccess;
 }
 static cudaError_t ensure_smem(const void* fn, int bytes) {
@@ -1754,7 +1757,8 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
   // build's fixed cost is its launches, not these host calls)
   int smem_optin = 0, smem_sm = 0;
   HM_CUDA_TRY(device_smem(&smem_optin, &smem_sm));
-  static size_t static_smem_B = 0;  // k_bucket's static shared memory (~2.6 KB; the same binary on every device)
+  static std::atomic<size_t> static_smem_cache{0};  // k_bucket's static shared memory (~2.6 KB; one binary)
+  size_t static_smem_B = static_smem_cache.load();
   if (!static_smem_B) {
     size_t v = 4096;
     cudaFuncAttributes fa{};
@@ -1766,6 +1770,7 @@ static hm_status build_core(Src src, Same same, uint64_t n_in, uint64_t n_global
       else cudaGetLastError();
     }
     static_smem_B = v;
+    static_smem_cache.store(v);
   }
   const uint32_t knob_flags = log2_req >> 16;
   log2_req &= 0xFFFFu;
