@@ -95,6 +95,9 @@ struct Items {
 #ifndef HM_SMEM_ALIAS
 #define HM_SMEM_ALIAS 0  // k_bucket: alias rk with the rounds' lists and sA with the slot source map
 #endif
+#ifndef HM_LATE_RECORDS
+#define HM_LATE_RECORDS 1  // k_bucket: the record copy completes its own barrier, waited for only before the search
+#endif
 #ifndef HM_FUSED_DISCARD
 #define HM_FUSED_DISCARD 1  // k_split2_bucket: drop a consumed partition's L2 lines without write-back
 #endif
@@ -879,7 +882,7 @@ __device__ __forceinline__ void bucket_body(const BuildParams& bp, const E* __re
                                             DevStatus* __restrict__ stt, const Same& same, uint8_t* smem,
                                             uint32_t p_given, const unsigned int* sdone_c, uint32_t tpc) {
   __shared__ uint64_t s_m2[33];
-  __shared__ __align__(8) unsigned long long s_bar;
+  __shared__ __align__(8) unsigned long long s_bar[2];  // bulk loads: [0] the codes, [1] the records
   __shared__ uint32_t s_p;
   __shared__ unsigned long long s_red2[2][KBCfg<E>::W];
   __shared__ unsigned long long s_base;
@@ -920,7 +923,8 @@ __device__ __forceinline__ void bucket_body(const BuildParams& bp, const E* __re
     } else {
       s_p = atomicAdd(&stt->ticket, 1u);
     }
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_bar)));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_bar[0])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_bar[1])));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     s_c9 = 0;
 #pragma unroll
@@ -959,23 +963,34 @@ __device__ __forceinline__ void bucket_body(const BuildParams& bp, const E* __re
   if (tid == 0) {
     const uint32_t bytes = KBCfg<E>::SMEM_ITEM == int(sizeof(E)) ? cnt * uint32_t(sizeof(E)) : 0u;
     const uint32_t lbytes = ((cnt + 7) & ~7u) * 2;  // (16-byte multiple; cap is a multiple of 32)
+    // the codes (all that hist, scan and groupby read) complete barrier 0, the
+    // records (first read by the search) barrier 1: the record copy overlaps
+    // hist, scan and groupby
+    const uint32_t b0 = smem_u32(&s_bar[0]), b1 = smem_u32(&s_bar[HM_LATE_RECORDS ? 1 : 0]);
     if (cnt) {
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&s_bar)),
-                   "r"(bytes + lbytes)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b0),
+                   "r"(lbytes + (HM_LATE_RECORDS ? 0u : bytes))
                    : "memory");
+      if (HM_LATE_RECORDS) {
+        if (bytes)
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b1), "r"(bytes) : "memory");
+        else
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(b1) : "memory");
+      }
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_u32(lbk)),
+          "l"(plb + size_t(p) * cap), "r"(lbytes), "r"(b0)
+          : "memory");
       if (bytes)
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                 smem_u32(skey)),
-            "l"(prec), "r"(bytes), "r"(smem_u32(&s_bar))
+            "l"(prec), "r"(bytes), "r"(b1)
             : "memory");
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-              smem_u32(lbk)),
-          "l"(plb + size_t(p) * cap), "r"(lbytes), "r"(smem_u32(&s_bar))
-          : "memory");
     } else {
-      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&s_bar)) : "memory");
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(b0) : "memory");
+      if (HM_LATE_RECORDS) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(b1) : "memory");
     }
   }
   if constexpr (sizeof(E) == sizeof(KV32)) {  // (byte-key builds only)
@@ -1004,32 +1019,21 @@ __device__ __forceinline__ void bucket_body(const BuildParams& bp, const E* __re
         bp.cp_dst[(b & ~uint64_t(15)) + (tid - 32)] = bp.cp_src[(b & ~uint64_t(15)) + (tid - 32)];
     }
   }
-  if (warp == 0) {  // the other warps wait at the CTA barrier (no issue slots)
+  // (warp 0 waits; the other warps wait at the CTA barrier that follows, with no issue slots)
+  auto bulk_wait = [&](const unsigned long long* bar) {
     uint32_t done = 0;
     do {
       asm volatile(
           "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
           : "=r"(done)
-          : "r"(smem_u32(&s_bar))
+          : "r"(smem_u32(bar))
           : "memory");
       if (!done) __nanosleep(64);
     } while (!done);
-  }
+  };
+  if (warp == 0) bulk_wait(&s_bar[0]);
   __syncthreads();
   HM_TMARK(1);
-  if (kFused && HM_FUSED_DISCARD) {
-    // the partition's records and codes are in shared memory: drop their L2
-    // lines (only lines wholly inside this partition's buffer regions)
-    auto drop = [&](const void* b0, size_t region, size_t used) {
-      const uintptr_t a = reinterpret_cast<uintptr_t>(b0);
-      const uintptr_t lo = (a + 127) & ~uintptr_t(127), hi = (a + region) & ~uintptr_t(127);
-      const uintptr_t end = min(hi, (a + used + 127) & ~uintptr_t(127));
-      for (uintptr_t x = lo + uintptr_t(tid) * 128; x < end; x += uintptr_t(KBCfg<E>::T) * 128)
-        asm volatile("discard.global.L2 [%0], 128;" ::"l"(x) : "memory");
-    };
-    drop(prec, size_t(cap) * sizeof(E), size_t(cnt) * sizeof(E));
-    drop(plb + size_t(p) * cap, size_t(cap) * 2, size_t(cnt) * 2);
-  }
 
   // ---- hist: the local bucket of g k and the
   // key's tag came with the record from the partition pass (k_split pass 2 /
@@ -1159,8 +1163,22 @@ __device__ __forceinline__ void bucket_body(const BuildParams& bp, const E* __re
     sidx[sstart[lb] + rk[i]] = uint16_t(i);
     if (staged && ss[lb] == 1) src[soff[lb]] = uint16_t(i);
   }
+  if (HM_LATE_RECORDS && warp == 0) bulk_wait(&s_bar[1]);  // (the records, for the search)
   __syncthreads();
   HM_TMARK(3);
+  if (kFused && HM_FUSED_DISCARD) {
+    // the partition's records and codes are in shared memory: drop their L2
+    // lines (only lines wholly inside this partition's buffer regions)
+    auto drop = [&](const void* b0, size_t region, size_t used) {
+      const uintptr_t a = reinterpret_cast<uintptr_t>(b0);
+      const uintptr_t lo = (a + 127) & ~uintptr_t(127), hi = (a + region) & ~uintptr_t(127);
+      const uintptr_t end = min(hi, (a + used + 127) & ~uintptr_t(127));
+      for (uintptr_t x = lo + uintptr_t(tid) * 128; x < end; x += uintptr_t(KBCfg<E>::T) * 128)
+        asm volatile("discard.global.L2 [%0], 128;" ::"l"(x) : "memory");
+    };
+    drop(prec, size_t(cap) * sizeof(E), size_t(cnt) * sizeof(E));
+    drop(plb + size_t(p) * cap, size_t(cap) * 2, size_t(cnt) * 2);
+  }
 
   // ---- level-2 seed search, map make2 over the multi-key buckets
   // (PAPER.md:286-292); every finished bucket maps its slots to their source
