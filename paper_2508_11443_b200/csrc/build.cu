@@ -404,7 +404,6 @@ template <class E>
 __host__ __device__ constexpr int split_tile() {
   return kSThreads * split_pt<E>();
 }
-constexpr int kSWarps = kSThreads / 32;  // BITS-bit digits: up to 2^(2 BITS) partitions in two passes
 
 struct SplitArgs {
   // pass 2 source: the coarse buffer
