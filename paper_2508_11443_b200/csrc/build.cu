@@ -95,6 +95,9 @@ struct Items {
 #ifndef HM_SMEM_ALIAS
 #define HM_SMEM_ALIAS 0  // k_bucket: alias rk with the rounds' lists and sA with the slot source map
 #endif
+#ifndef HM_PRED_ATOM
+#define HM_PRED_ATOM 1  // k_bucket: the search's chunk and list counters bumped by predicated atomics
+#endif
 #ifndef HM_LATE_RECORDS
 #define HM_LATE_RECORDS 1  // k_bucket: the record copy completes its own barrier, waited for only before the search
 #endif
@@ -562,6 +565,16 @@ __device__ __forceinline__ uint4 ld_stream_u4(const uint4* p) {
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+// atomicAdd on a shared counter by the lanes with `pred` only, as one
+// predicated instruction (no divergent branch around it); other lanes get 0
+__device__ __forceinline__ uint32_t atom_add_if(bool pred, uint32_t saddr, uint32_t v) {
+  uint32_t r = 0;
+  asm volatile("{ .reg .pred p; setp.ne.u32 p, %1, 0; @p atom.shared::cta.add.u32 %0, [%2], %3; }"
+               : "+r"(r)
+               : "r"(uint32_t(pred)), "r"(saddr), "r"(v)
+               : "memory");
+  return r;
+}
 
 // make2 for buckets with 2 <= s <= 8, in CTA-wide rounds.
 // One attempt = derive(seed,2,b,t), the s level-2 slots hash mod s^2 and the
@@ -719,8 +732,12 @@ __device__ __forceinline__ void list_append(bool want, uint32_t lb, uint32_t s, 
     const uint32_t m = __ballot_sync(0xffffffffu, mine);
     if (m) {
       const uint32_t leader = __ffs(m) - 1;
+#if HM_PRED_ATOM
+      uint32_t b = atom_add_if(lane == leader, smem_u32(&ncnt[side]), uint32_t(__popc(m)));
+#else
       uint32_t b = 0;
       if (lane == leader) b = atomicAdd(&ncnt[side], uint32_t(__popc(m)));
+#endif
       b = __shfl_sync(0xffffffffu, b, leader) + __popc(m & lt);
       if (mine) nl[side == 0 ? b : lcap - 1 - b] = uint16_t(lb);
     }
@@ -1256,9 +1273,16 @@ __device__ __forceinline__ void bucket_body(const BuildParams& bp, const E* __re
         logA = uint32_t(min(max(lg, 0), HM_RETRY_LOGA));
       }
       const uint32_t W1 = L1 << logA, W = W1 + ((L - L1) << logA2);
+#if HM_PRED_ATOM
+      const uint32_t chunk_sa = smem_u32(&s_chunk[cur]);
+#endif
       for (;;) {
+#if HM_PRED_ATOM
+        uint32_t c = atom_add_if(lane == 0, chunk_sa, 32u);
+#else
         uint32_t c = 0;
         if (lane == 0) c = atomicAdd(&s_chunk[cur], 32u);
+#endif
         c = __shfl_sync(0xffffffffu, c, 0);
         if (c >= W) break;
         const uint32_t w = c + lane;
