@@ -95,6 +95,9 @@ struct Items {
 #ifndef HM_SMEM_ALIAS
 #define HM_SMEM_ALIAS 0  // k_bucket: alias rk with the rounds' lists and sA with the slot source map
 #endif
+#ifndef HM_EQ_INLINE2
+#define HM_EQ_INLINE2 1  // k_bucket: the duplicate check of an s = 2 bucket inline (no call)
+#endif
 #ifndef HM_PRED_ATOM
 #define HM_PRED_ATOM 1  // k_bucket: the search's chunk and list counters bumped by predicated atomics
 #endif
@@ -683,6 +686,14 @@ __device__ __noinline__ bool bucket_equal_keys_(Items<E> skv, const uint16_t* ss
 template <class E, class Same>
 __device__ __forceinline__ bool bucket_equal_keys(const Items<E>& skv, const SearchCtx& X, uint32_t lb, DevStatus* stt,
                                                   const Same& same) {
+#if HM_EQ_INLINE2
+  // (the common case inline: a pair of distinct keys; the call only for s > 2
+  // or an equal pair)
+  if (X.ss[lb] == 2) {
+    const uint32_t st0 = X.sstart[lb];
+    if (skv.key(X.sidx[st0]) != skv.key(X.sidx[st0 + 1])) return false;
+  }
+#endif
   return bucket_equal_keys_(skv, X.sstart, X.ss, X.sidx, X.s_t, lb, stt, same);
 }
 
