@@ -95,6 +95,9 @@ struct Items {
 #ifndef HM_SMEM_ALIAS
 #define HM_SMEM_ALIAS 0  // k_bucket: alias rk with the rounds' lists and sA with the slot source map
 #endif
+#ifndef HM_PLACE_FLAT
+#define HM_PLACE_FLAT 1  // k_bucket scan: class-list placement without a branch per bucket
+#endif
 #ifndef HM_EQ_INLINE2
 #define HM_EQ_INLINE2 1  // k_bucket: the duplicate check of an s = 2 bucket inline (no call)
 #endif
@@ -1131,6 +1134,23 @@ __device__ __forceinline__ void bucket_body(const BuildParams& bp, const E* __re
     // pass is discarded; s <= 8 buckets are listed all the same — only
     // reachable with n < 16)
     auto place = [&](uint32_t j, uint32_t v) {
+#if HM_PLACE_FLAT
+      // s = 2..8 branch-free (a predicated store); s >= 5 — the only sizes the
+      // space bound can reject (s <= n) and the warp-per-bucket list — apart
+      const uint32_t pos = v == 2 ? n2 : (v <= 4 ? n4 : n8);
+      if (v - 2u <= 6u) slist[pos] = uint16_t(j);
+      n2 += v == 2;
+      n4 += v - 3u <= 1u;
+      n8 += v - 5u <= 3u;
+      if (v >= 5) {
+        const bool over = uint64_t(v) * v > bp.bound4n;
+        bfail |= over;
+        if (v >= 9 && !over) {
+          if (v <= 32) slist[HM_SL(cls_off[2]) + atomicAdd(&s_c9, 1u)] = uint16_t(j);
+          else huge = true;
+        }
+      }
+#else
       if (v < 2) return;
       const bool over = uint64_t(v) * v > bp.bound4n;
       bfail |= over;
@@ -1143,6 +1163,7 @@ __device__ __forceinline__ void bucket_body(const BuildParams& bp, const E* __re
         if (v <= 32) slist[HM_SL(cls_off[2]) + atomicAdd(&s_c9, 1u)] = uint16_t(j);
         else huge = true;
       }
+#endif
     };
     if (vec) {
       uint32_t st4 = *reinterpret_cast<const uint32_t*>(s_t + c0), ss4 = 0, ssk = 0;
