@@ -738,7 +738,7 @@ __device__ __forceinline__ void bucket_done_any(const SearchCtx& X, uint32_t lb,
 // Append lb to the next round's list (s >= 3 at the front, s = 2 at the back),
 // warp-aggregated: one shared atomic per warp and side.
 __device__ __forceinline__ void list_append(bool want, uint32_t lb, uint32_t s, uint16_t* nl, uint32_t lcap,
-                                            uint32_t* ncnt) {
+                                            uint32_t* ncnt, uint32_t ncnt_sa) {
   const uint32_t lane = threadIdx.x & 31, lt = (1u << lane) - 1u;
 #pragma unroll
   for (int side = 0; side < 2; side++) {
@@ -747,7 +747,7 @@ __device__ __forceinline__ void list_append(bool want, uint32_t lb, uint32_t s, 
     if (m) {
       const uint32_t leader = __ffs(m) - 1;
 #if HM_PRED_ATOM
-      uint32_t b = atom_add_if(lane == leader, smem_u32(&ncnt[side]), uint32_t(__popc(m)));
+      uint32_t b = atom_add_if(lane == leader, ncnt_sa + 4u * side, uint32_t(__popc(m)));  // (ncnt_sa: &ncnt[0])
 #else
       uint32_t b = 0;
       if (lane == leader) b = atomicAdd(&ncnt[side], uint32_t(__popc(m)));
@@ -1306,7 +1306,9 @@ __device__ __forceinline__ void bucket_body(const BuildParams& bp, const E* __re
       }
       const uint32_t W1 = L1 << logA, W = W1 + ((L - L1) << logA2);
 #if HM_PRED_ATOM
-      const uint32_t chunk_sa = smem_u32(&s_chunk[cur]);
+      const uint32_t chunk_sa = smem_u32(&s_chunk[cur]), qn_sa = smem_u32(&s_qn[nxt][0]);
+#else
+      const uint32_t qn_sa = 0;
 #endif
       for (;;) {
 #if HM_PRED_ATOM
@@ -1339,7 +1341,7 @@ __device__ __forceinline__ void bucket_body(const BuildParams& bp, const E* __re
             again = true;
           }
         }
-        list_append(again, lb, s, rlist + nxt * lcap, lcap, s_qn[nxt]);
+        list_append(again, lb, s, rlist + nxt * lcap, lcap, s_qn[nxt], qn_sa);
       }
       __syncthreads();
       const uint32_t t3 = prv;
