@@ -56,13 +56,27 @@ __device__ __forceinline__ uint64_t mod_s2(uint64_t h, uint32_t s, const uint64_
 }
 
 // probe-2 slot index of key k in bucket b (global id) with directory entry d
+#ifndef HM_SLOT_FLAT
+#define HM_SLOT_FLAT 1  // lookups: the level-2 hash computed for every lane, the singleton case selected (no branch)
+#endif
 __device__ __forceinline__ uint64_t slot_index(uint64_t smix, uint64_t b, uint64_t d, uint64_t k,
                                                const uint64_t* s_m2) {
   const uint32_t s = uint32_t((d >> 40) & 0xFFFF);
   const uint64_t soff = d & kMask40;
+#if HM_SLOT_FLAT
+  // (a warp's queries mix singletons and multi-key buckets, so the level-2
+  // hash costs the warp the same either way; without the branch the four
+  // queries of a thread interleave)
+  const Consts c = derive(smix, 2, b, uint32_t(d >> 56));
+  const uint64_t hv = hash64(c, k);
+  if (s > 32) return s <= 1 ? soff : soff + hv % (uint64_t(s) * s);  // (never for distinct keys; R22)
+  const FastMod fm{uint64_t(s) * s, s_m2[s]};
+  return s <= 1 ? soff : soff + fastmod(hv, fm);  // R12: a singleton's slot is soff
+#else
   if (s <= 1) return soff;  // R12
   const Consts c = derive(smix, 2, b, uint32_t(d >> 56));
   return soff + mod_s2(hash64(c, k), s, s_m2);
+#endif
 }
 
 // L2 cache policies: the compact directory should stay resident (evict_last);
