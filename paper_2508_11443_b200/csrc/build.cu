@@ -95,6 +95,9 @@ struct Items {
 #ifndef HM_SMEM_ALIAS
 #define HM_SMEM_ALIAS 0  // k_bucket: alias rk with the rounds' lists and sA with the slot source map
 #endif
+#ifndef HM_MOD_ALWAYS
+#define HM_MOD_ALWAYS 1  // k_bucket search: mod s^2 by the reciprocal for every s in K > 2 chunks
+#endif
 #ifndef HM_PLACE_FLAT
 #define HM_PLACE_FLAT 1  // k_bucket scan: class-list placement without a branch per bucket
 #endif
@@ -622,7 +625,12 @@ __device__ __forceinline__ uint64_t slots_of(const Consts& c, const uint64_t* k,
     h[j] = 0;
     if (uint32_t(j) < s) {
       const uint64_t hv = hash64(c, k[j]);
+#if HM_MOD_ALWAYS
+      // (K > 2: the reciprocal for every s, exact for s = 4 and 8 too — no per-lane select)
+      h[j] = K == 2 ? uint32_t(hv) & (s * s - 1) : uint32_t(fastmod(hv, fm));
+#else
       h[j] = (K == 2 || (s & (s - 1)) == 0) ? uint32_t(hv) & (s * s - 1) : uint32_t(fastmod(hv, fm));
+#endif
       const B bit = B(1) << h[j];
       coll |= (bits & bit) != 0;
       bits |= bit;
