@@ -434,50 +434,38 @@ struct SplitArgs {
 
 // One tile of a radix pass (bid: the tile; pass 2: coarse region bid / tpc,
 // tile bid % tpc of it).  Also a job of the fused pass-2 + k_bucket kernel.
-template <class Src, class E, int PASS, int BITS, int NT = kSThreads>
-__device__ __forceinline__ void split_tile_body(const Src& src, const BuildParams& bp, const SplitArgs& a,
-                                                DevStatus* __restrict__ stt, uint32_t bid, uint8_t* smem) {
-  const uint32_t log2bp = bp.log2_bp, tpc = a.tpc, ccap = a.ccap, dcap = a.dcap;
+// The tile's work after its extent is known.  FULL: a whole tile (no
+// per-record bounds checks); POW2: n is a power of two (level-one reduction
+// by a mask) — both compile-time, so that the per-record loops carry no
+// branches.
+template <class Src, class E, int PASS, int BITS, int NT, bool FULL, bool POW2>
+__device__ __forceinline__ void split_tile_rest(const Src& src, const BuildParams& bp, const SplitArgs& a,
+                                                DevStatus* __restrict__ stt, uint8_t* smem, uint64_t base,
+                                                uint32_t nvalid, uint32_t coarse, uint32_t* s_cnt,
+                                                uint32_t* s_dstart, uint32_t* s_gbase, unsigned long long* s_red) {
+  const uint32_t log2bp = bp.log2_bp, ccap = a.ccap, dcap = a.dcap;
   constexpr int kSDigits = 1 << BITS, kSBits = BITS, kSPT = split_pt<E>(), kSTile = NT * split_pt<E>();
   E* stage = reinterpret_cast<E*>(smem);
   uint16_t* sdig = reinterpret_cast<uint16_t*>(smem + size_t(kSTile) * sizeof(E));
   uint16_t* slbc = sdig + kSTile;  // pass 2: local bucket | tag4 << 12 of the staged record
-  __shared__ uint32_t s_cnt[kSDigits], s_dstart[kSDigits], s_gbase[kSDigits];
-  __shared__ unsigned long long s_red[NT / 32];
-
   const uint32_t tid = threadIdx.x;
-  for (uint32_t i = tid; i < kSDigits; i += NT) s_cnt[i] = 0;
-  // this CTA's elements
-  uint64_t base;
-  uint32_t nvalid, coarse = 0;
   const E* cb = reinterpret_cast<const E*>(a.cbuf);
-  if (PASS == 1) {
-    base = uint64_t(bid) * kSTile;
-    nvalid = bp.n_in - base < uint64_t(kSTile) ? uint32_t(bp.n_in - base) : uint32_t(kSTile);
-  } else {
-    coarse = bid / tpc;
-    const uint32_t k = bid % tpc;
-    const uint32_t cc = min(a.ccount[coarse], ccap);
-    base = uint64_t(k) * kSTile;
-    nvalid = cc > base ? (cc - base < uint64_t(kSTile) ? uint32_t(cc - base) : uint32_t(kSTile)) : 0u;
-  }
-  __syncthreads();
-  if (nvalid == 0) return;
+  if (FULL) nvalid = kSTile;
   E e[kSPT];
   uint32_t dg[kSPT], rk[kSPT], lc[kSPT];
   bool bad = false;
 #pragma unroll
   for (int j = 0; j < kSPT; j++) {
     const uint32_t i = j * NT + tid;
-    if (i < nvalid) e[j] = PASS == 1 ? src.load(base + i) : cb[size_t(coarse) * ccap + base + i];
+    if (FULL || i < nvalid) e[j] = PASS == 1 ? src.load(base + i) : cb[size_t(coarse) * ccap + base + i];
   }
 #pragma unroll
   for (int j = 0; j < kSPT; j++) {
     const uint32_t i = j * NT + tid;
     dg[j] = 0;
-    if (i < nvalid) {
+    if (FULL || i < nvalid) {
       const uint64_t h1 = hash64(bp.l1.c1, e[j].key);
-      const uint64_t lb = level1_of_hash(bp.l1, h1) - bp.b_lo;
+      const uint64_t lb = (POW2 ? (h1 & bp.l1.mask) : level1_of_hash(bp.l1, h1)) - bp.b_lo;
       if (lb >= bp.nb) bad = true;
       const uint32_t p = uint32_t(lb >> log2bp);
       dg[j] = PASS == 1 ? ((p >> kSBits) & (kSDigits - 1)) : (p & (kSDigits - 1));
@@ -490,7 +478,7 @@ __device__ __forceinline__ void split_tile_body(const Src& src, const BuildParam
   // (the table is a function of the key set, R13)
 #pragma unroll
   for (int j = 0; j < kSPT; j++)
-    if (j * NT + tid < nvalid) rk[j] = atomicAdd(&s_cnt[dg[j]], 1u);
+    if (FULL || j * NT + tid < nvalid) rk[j] = atomicAdd(&s_cnt[dg[j]], 1u);
   __syncthreads();
   // digit-major offsets inside the tile; one global reservation per digit
   {
@@ -508,7 +496,7 @@ __device__ __forceinline__ void split_tile_body(const Src& src, const BuildParam
   __syncthreads();
 #pragma unroll
   for (int j = 0; j < kSPT; j++) {
-    if (j * NT + tid < nvalid) {
+    if (FULL || j * NT + tid < nvalid) {
       const uint32_t pos = s_dstart[dg[j]] + rk[j];
       stage[pos] = e[j];
       sdig[pos] = uint16_t(dg[j]);
@@ -532,6 +520,45 @@ __device__ __forceinline__ void split_tile_body(const Src& src, const BuildParam
   }
   if (ovf) atomicOr(&stt->part_overflow, 1u);
   if (bad) atomicOr(&stt->pad, 1u);
+}
+
+template <class Src, class E, int PASS, int BITS, int NT = kSThreads>
+__device__ __forceinline__ void split_tile_body(const Src& src, const BuildParams& bp, const SplitArgs& a,
+                                                DevStatus* __restrict__ stt, uint32_t bid, uint8_t* smem) {
+  const uint32_t tpc = a.tpc, ccap = a.ccap;
+  constexpr int kSDigits = 1 << BITS, kSTile = NT * split_pt<E>();
+  __shared__ uint32_t s_cnt[kSDigits], s_dstart[kSDigits], s_gbase[kSDigits];
+  __shared__ unsigned long long s_red[NT / 32];
+
+  const uint32_t tid = threadIdx.x;
+  for (uint32_t i = tid; i < kSDigits; i += NT) s_cnt[i] = 0;
+  // this CTA's elements
+  uint64_t base;
+  uint32_t nvalid, coarse = 0;
+  if (PASS == 1) {
+    base = uint64_t(bid) * kSTile;
+    nvalid = bp.n_in - base < uint64_t(kSTile) ? uint32_t(bp.n_in - base) : uint32_t(kSTile);
+  } else {
+    coarse = bid / tpc;
+    const uint32_t k = bid % tpc;
+    const uint32_t cc = min(a.ccount[coarse], ccap);
+    base = uint64_t(k) * kSTile;
+    nvalid = cc > base ? (cc - base < uint64_t(kSTile) ? uint32_t(cc - base) : uint32_t(kSTile)) : 0u;
+  }
+  __syncthreads();
+  if (nvalid == 0) return;
+  // (the tile's remaining work with its bounds and level-one reduction fixed at compile time)
+  if (nvalid == uint32_t(kSTile)) {
+    if (bp.l1.pow2)
+      split_tile_rest<Src, E, PASS, BITS, NT, true, true>(src, bp, a, stt, smem, base, nvalid, coarse, s_cnt,
+                                                          s_dstart, s_gbase, s_red);
+    else
+      split_tile_rest<Src, E, PASS, BITS, NT, true, false>(src, bp, a, stt, smem, base, nvalid, coarse, s_cnt,
+                                                           s_dstart, s_gbase, s_red);
+  } else {
+    split_tile_rest<Src, E, PASS, BITS, NT, false, false>(src, bp, a, stt, smem, base, nvalid, coarse, s_cnt,
+                                                          s_dstart, s_gbase, s_red);
+  }
 }
 
 template <class Src, class E, int PASS, int BITS, int NT = kSThreads>
