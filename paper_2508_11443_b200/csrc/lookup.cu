@@ -140,7 +140,9 @@ __device__ __forceinline__ uint64_t cdir_entry(const CDir& r, uint64_t lb, const
 
 // u64 lookup: probe 1 reads the L2-resident compact directory, probe 2 the
 // slot (the one DRAM line a query needs); 4 queries in flight per thread.
-template <int QPT>
+// POW2: the table's n is a power of two (level-one reduction by a mask, no
+// per-query branch; every benchmark configuration)
+template <int QPT, bool POW2>
 __global__ void __launch_bounds__(kLThreads) k_lookup_u64(LookupParams lp, const uint64_t* __restrict__ q,
                                                           uint64_t nq, uint64_t* __restrict__ ov,
                                                           uint8_t* __restrict__ of) {
@@ -165,7 +167,7 @@ __global__ void __launch_bounds__(kLThreads) k_lookup_u64(LookupParams lp, const
     for (int j = 0; j < QPT; j++) {
       const uint64_t idx = base + uint64_t(j) * kLThreads + threadIdx.x;
       const uint64_t h1 = hash64(lp.l1.c1, key[j]);
-      b[j] = level1_of_hash(lp.l1, h1) - lp.b_lo;
+      b[j] = (POW2 ? (h1 & lp.l1.mask) : level1_of_hash(lp.l1, h1)) - lp.b_lo;
       tag[j] = tag4_of_hash(h1);
       const bool ok = idx < nq && b[j] < lp.nb;
       if (!ok) b[j] = 0;
@@ -224,7 +226,11 @@ hm_status lookup_u64_launch(const hm_map* m, const uint64_t* q, uint64_t nq, uin
   const unsigned grid = unsigned(std::min<uint64_t>(blocks, uint64_t(num_sms()) * HM_LOOKUP_CPS));
   {
     LaunchScope ls_("k_lookup_u64", st);
-    k_lookup_u64<QPT><<<grid, kLThreads, 0, st>>>(lp, q, nq, out_vals, out_found);
+#ifndef HM_LOOKUP_POW2
+#define HM_LOOKUP_POW2 1
+#endif
+    if (HM_LOOKUP_POW2 && lp.l1.pow2) k_lookup_u64<QPT, true><<<grid, kLThreads, 0, st>>>(lp, q, nq, out_vals, out_found);
+    else k_lookup_u64<QPT, false><<<grid, kLThreads, 0, st>>>(lp, q, nq, out_vals, out_found);
   }
   HM_CUDA_TRY(cudaGetLastError());
   return HM_OK;
@@ -277,7 +283,7 @@ __device__ __forceinline__ uint64_t fingerprint_chunks(const uint64_t (&c)[8], u
 #ifndef HM_LB_MINB
 #define HM_LB_MINB 4  // (64 registers; 1 / 3: 1.01 / 1.00 ms vs 0.87 at C3, 5: spills)
 #endif
-template <int QPT>
+template <int QPT, bool POW2>
 __global__ void __launch_bounds__(kLThreads, HM_LB_MINB) k_lookup_bytes(LookupParams lp, const uint8_t* __restrict__ qb,
                                                             const uint64_t* __restrict__ qo, uint64_t nq,
                                                             uint64_t* __restrict__ ov, uint8_t* __restrict__ of) {
@@ -314,7 +320,7 @@ __global__ void __launch_bounds__(kLThreads, HM_LB_MINB) k_lookup_bytes(LookupPa
     for (int j = 0; j < QPT; j++) {
       const uint64_t idx = base + uint64_t(j) * kLThreads + threadIdx.x;
       const uint64_t h1 = hash64(lp.l1.c1, fp[j]);
-      b[j] = level1_of_hash(lp.l1, h1) - lp.b_lo;
+      b[j] = (POW2 ? (h1 & lp.l1.mask) : level1_of_hash(lp.l1, h1)) - lp.b_lo;
       tag[j] = tag4_of_hash(h1);
       const bool ok = idx < nq && b[j] < lp.nb;
       if (!ok) b[j] = 0;
@@ -382,7 +388,10 @@ hm_status lookup_bytes_launch(const hm_map* m, const uint8_t* qb, const uint64_t
   const unsigned grid = unsigned(std::min<uint64_t>(blocks, uint64_t(num_sms()) * HM_LOOKUP_BYTES_CPS));
   {
     LaunchScope ls_("k_lookup_bytes", st);
-    k_lookup_bytes<HM_LOOKUP_BYTES_QPT><<<grid, kLThreads, 0, st>>>(lp, qb, qo, nq, out_vals, out_found);
+    if (HM_LOOKUP_POW2 && lp.l1.pow2)
+      k_lookup_bytes<HM_LOOKUP_BYTES_QPT, true><<<grid, kLThreads, 0, st>>>(lp, qb, qo, nq, out_vals, out_found);
+    else
+      k_lookup_bytes<HM_LOOKUP_BYTES_QPT, false><<<grid, kLThreads, 0, st>>>(lp, qb, qo, nq, out_vals, out_found);
   }
   HM_CUDA_TRY(cudaGetLastError());
   return HM_OK;
