@@ -95,6 +95,9 @@ struct Items {
 #ifndef HM_SMEM_ALIAS
 #define HM_SMEM_ALIAS 0  // k_bucket: alias rk with the rounds' lists and sA with the slot source map
 #endif
+#ifndef HM_DIR_V4
+#define HM_DIR_V4 1  // k_bucket: a whole partition's directory as one 32-byte store per thread
+#endif
 #ifndef HM_MOD_ALWAYS
 #define HM_MOD_ALWAYS 1  // k_bucket search: mod s^2 by the reciprocal for every s in K > 2 chunks
 #endif
@@ -1452,6 +1455,24 @@ __device__ __forceinline__ void bucket_body(const BuildParams& bp, const E* __re
   HM_TMARK(6);
   // directory: two buckets per lane, one 16-byte store (lb0 and the pair are
   // even, so the store is aligned)
+#if HM_DIR_V4
+  if (BP == 4u * KBCfg<E>::T && nbp == BP) {
+    // a whole partition: four buckets per thread, one 32-byte store
+    const uint32_t lb = 4 * tid;
+    const uint4 so4 = *reinterpret_cast<const uint4*>(soff + lb);
+    const uint32_t s4 = *reinterpret_cast<const uint32_t*>(ss + lb), t4 = *reinterpret_cast<const uint32_t*>(s_t + lb);
+    uint64_t e[4];
+    const uint32_t sov[4] = {so4.x, so4.y, so4.z, so4.w};
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const uint32_t su = (s4 >> (8 * u)) & 0xFF, tu = su == 1 ? 0u : (t4 >> (8 * u)) & 0xFF;
+      e[u] = dir_entry(base + sov[u], su, tu);
+    }
+    asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(dir + lb0 + lb), "l"(e[0]), "l"(e[1]), "l"(e[2]),
+                 "l"(e[3])
+                 : "memory");
+  } else
+#endif
   for (uint32_t q = tid; 2 * q < nbp; q += KBCfg<E>::T) {
     const uint32_t lb = 2 * q;
     const uint2 so2 = *reinterpret_cast<const uint2*>(soff + lb);
