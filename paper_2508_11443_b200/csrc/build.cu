@@ -95,6 +95,9 @@ struct Items {
 #ifndef HM_SMEM_ALIAS
 #define HM_SMEM_ALIAS 0  // k_bucket: alias rk with the rounds' lists and sA with the slot source map
 #endif
+#ifndef HM_FP_BATCH
+#define HM_FP_BATCH 1  // k_bucket (byte keys): the fingerprints loaded five per thread at a time
+#endif
 #ifndef HM_OUT_FULL
 #define HM_OUT_FULL 1  // k_bucket out phase: whole groups of slots without per-slot bounds checks
 #endif
@@ -1110,8 +1113,29 @@ __device__ __forceinline__ void bucket_body(const BuildParams& bp, const E* __re
   // key's tag came with the record from the partition pass (k_split pass 2 /
   // k_partition hashed it already); the rank among the items of its bucket
   // comes from the shared-memory counter
+#if HM_FP_BATCH
+  if constexpr (KBCfg<E>::SMEM_ITEM != int(sizeof(E))) {
+    // byte keys: the fingerprints from the partition buffer, five loads in
+    // flight per thread (the search reads them from shared memory)
+    constexpr int U = 5;
+    for (uint32_t i0 = tid; i0 < cnt; i0 += U * KBCfg<E>::T) {
+      uint64_t f[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const uint32_t i = i0 + u * KBCfg<E>::T;
+        f[u] = i < cnt ? __ldg(reinterpret_cast<const unsigned long long*>(prec + i)) : 0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const uint32_t i = i0 + u * KBCfg<E>::T;
+        if (i < cnt) skey[i] = f[u];
+      }
+    }
+  }
+#endif
   for (uint32_t i = tid; i < cnt; i += KBCfg<E>::T) {
-    if (KBCfg<E>::SMEM_ITEM != int(sizeof(E))) skey[i] = __ldg(reinterpret_cast<const unsigned long long*>(prec + i));
+    if (!HM_FP_BATCH && KBCfg<E>::SMEM_ITEM != int(sizeof(E)))
+      skey[i] = __ldg(reinterpret_cast<const unsigned long long*>(prec + i));
     const uint32_t code = lbk[i];
     uint32_t lb = code & 0xFFFu;
     if (lb >= nbp) {  // cannot happen for a well-routed partition; never index out of range
