@@ -221,7 +221,7 @@ hm_status lookup_u64_launch(const hm_map* m, const uint64_t* q, uint64_t nq, uin
   const uint64_t per = uint64_t(kLThreads) * QPT;
   const uint64_t blocks = (nq + per - 1) / per;
 #ifndef HM_LOOKUP_CPS
-#define HM_LOOKUP_CPS 64  // grid: CTAs per SM, 3 resident at a time (the block scheduler balances the SMs: 8 -> 64 cut 2^26 lookups 1.42 -> 1.33 ms)
+#define HM_LOOKUP_CPS 96  // grid: CTAs per SM, 3-4 resident at a time (the block scheduler balances the SMs: 8 -> 64 cut 2^26 lookups 1.42 -> 1.33 ms; 96: 2^28 on 2^27 -1 %)
 #endif
   const unsigned grid = unsigned(std::min<uint64_t>(blocks, uint64_t(num_sms()) * HM_LOOKUP_CPS));
   {
